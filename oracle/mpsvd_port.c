@@ -1,0 +1,1033 @@
+/* TEST INFRASTRUCTURE ONLY — see mpsvd_port.h. CPU restatement of the
+ * reference hot path (mp_thin_svd, TwoSidedJacobi branch) plus the
+ * double-double extension, in plain C. Built by oracle/Makefile with
+ * -ffp-contract=off so every multiply/add rounds exactly where the source
+ * says (the reference's x86-64 build has no FMA either: proj/CMakeLists.txt:14
+ * sets no -march). Where this file calls fma() it does so on purpose, to
+ * restate the device kernels' arithmetic (PORT_SEM_DEVICE).
+ */
+#define _GNU_SOURCE
+#include "mpsvd_port.h"
+
+#include <float.h>
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+enum {
+  ST_OK = 0,
+  ST_INVALID = 1,
+  ST_NPD = 2,
+  ST_NOCONV = 3,
+  ST_ZERO_DIVISOR = 5,
+  ST_TINY_SV = 7,
+  ST_INTERNAL = 10
+};
+
+static int set_err(port_error* e, int status, int64_t index, double value) {
+  if (e) {
+    e->status = status;
+    e->index = index;
+    e->value = value;
+  }
+  return status;
+}
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+/* ======================================================================== */
+/* Schedules                                                                */
+/* ======================================================================== */
+
+static int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+/* make_partition_plan (proj/src/parallel_gram.cpp:243-263): contiguous,
+ * balanced row ranges, the first m%blocks blocks one row longer. */
+int port_partition_plan(int64_t m, int workers, int64_t blocks, int64_t* ranges,
+                        int64_t* nblocks) {
+  if (m < 1) return ST_INVALID;
+  if (workers < 1 || (int64_t)workers > m) return ST_INVALID;
+  if (blocks == 0) blocks = workers == 1 ? 1 : (m < next_pow2(2 * (int64_t)workers) ? m : next_pow2(2 * (int64_t)workers));
+  if (blocks < 1 || blocks > m) return ST_INVALID;
+  const int64_t base = m / blocks, extra = m % blocks;
+  int64_t row = 0;
+  for (int64_t b = 0; b < blocks; ++b) {
+    const int64_t len = base + (b < extra ? 1 : 0);
+    if (ranges) {
+      ranges[2 * b] = row;
+      ranges[2 * b + 1] = row + len;
+    }
+    row += len;
+  }
+  if (nblocks) *nblocks = blocks;
+  return ST_OK;
+}
+
+/* Parallel round-robin ("circle method") schedule used by the device Jacobi:
+ * N = n rounded up to even; player N-1 is fixed and meets `round`, the rest
+ * rotate. Round r in [0, N-2], slot k in [0, N/2-1]; every unordered pair
+ * meets exactly once per sweep. q == n marks the bye of an odd n. */
+void port_rr_pair(int64_t n, int64_t round, int64_t k, int64_t* p, int64_t* q) {
+  const int64_t N = n + (n & 1);
+  int64_t a, b;
+  if (k == 0) {
+    a = N - 1;
+    b = round;
+  } else {
+    a = (round + k) % (N - 1);
+    b = (round - k + (N - 1)) % (N - 1);
+  }
+  *p = a < b ? a : b;
+  *q = a < b ? b : a;
+}
+
+/* ======================================================================== */
+/* Gram (proj/src/parallel_gram.cpp:20-32, 265-298)                         */
+/* ======================================================================== */
+
+/* block_gram: upper triangle by ascending-k dots from 0, mirrored. */
+static void block_gram_f64(const double* a, int64_t m, int64_t n, int64_t r0, int64_t r1,
+                           double* out) {
+  for (int64_t j = 0; j < n; ++j) {
+    const double* cj = a + j * m;
+    for (int64_t i = 0; i <= j; ++i) {
+      const double* ci = a + i * m;
+      double s = 0.0;
+      for (int64_t k = r0; k < r1; ++k) s += ci[k] * cj[k];
+      out[j * n + i] = s;
+      out[i * n + j] = s;
+    }
+  }
+}
+
+typedef struct {
+  const double* a;
+  int64_t m, n, nb, first, stride;
+  const int64_t* ranges;
+  double* slots;
+} gram_job;
+
+static void* gram_worker(void* arg) {
+  gram_job* j = (gram_job*)arg;
+  for (int64_t b = j->first; b < j->nb; b += j->stride)
+    block_gram_f64(j->a, j->m, j->n, j->ranges[2 * b], j->ranges[2 * b + 1],
+                   j->slots + b * j->n * j->n);
+  return NULL;
+}
+
+int port_partitioned_gram_f64(const double* a, int64_t m, int64_t n, int64_t blocks,
+                              double* out) {
+  if (n < 1) return ST_INVALID;
+  int64_t nb = 0;
+  if (port_partition_plan(m, 1, blocks, NULL, &nb) != ST_OK) return ST_INVALID;
+  int64_t* ranges = (int64_t*)malloc(sizeof(int64_t) * 2 * nb);
+  port_partition_plan(m, 1, blocks, ranges, &nb);
+  double* slots = (double*)calloc((size_t)(nb * n * n), sizeof(double));
+  if (!slots || !ranges) return ST_INTERNAL;
+  /* Blocks run on up to 16 threads; every block's bits are independent of
+   * which thread computes it (parallel_gram.cpp:220-239). */
+  int nthreads = (int)(nb < 16 ? nb : 16);
+  pthread_t th[16];
+  gram_job jobs[16];
+  for (int t = 0; t < nthreads; ++t) {
+    jobs[t] = (gram_job){a, m, n, nb, t, nthreads, ranges, slots};
+    pthread_create(&th[t], NULL, gram_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  /* Fixed binary tree over block indices: (0,1),(2,3),... then width x2. */
+  for (int64_t width = 1; width < nb; width *= 2)
+    for (int64_t i = 0; i + width < nb; i += 2 * width) {
+      double* dst = slots + i * n * n;
+      const double* src = slots + (i + width) * n * n;
+      for (int64_t k = 0; k < n * n; ++k) dst[k] += src[k];
+    }
+  memcpy(out, slots, sizeof(double) * (size_t)(n * n));
+  free(slots);
+  free(ranges);
+  return ST_OK;
+}
+
+int port_partitioned_gram_f32(const float* a, int64_t m, int64_t n, int64_t blocks,
+                              double* out) {
+  /* cast(A, Higher) (proj/src/dense.cpp:156-161): exact widening. */
+  double* ah = (double*)malloc(sizeof(double) * (size_t)(m * n));
+  if (!ah) return ST_INTERNAL;
+  for (int64_t k = 0; k < m * n; ++k) ah[k] = (double)a[k];
+  int st = port_partitioned_gram_f64(ah, m, n, blocks, out);
+  free(ah);
+  return st;
+}
+
+/* ======================================================================== */
+/* Two-sided Jacobi, fp64 (proj/src/jacobi.cpp:493-616)                     */
+/* ======================================================================== */
+
+/* Stable descending permutation (jacobi.cpp:425-434): insertion sort keeps
+ * equal keys in input order. */
+static void descending_perm_f64(const double* vals, int64_t n, int64_t* perm) {
+  for (int64_t i = 0; i < n; ++i) perm[i] = i;
+  for (int64_t i = 1; i < n; ++i) {
+    int64_t x = perm[i];
+    int64_t j = i - 1;
+    while (j >= 0 && vals[x] > vals[perm[j]]) {
+      perm[j + 1] = perm[j];
+      --j;
+    }
+    perm[j + 1] = x;
+  }
+}
+
+/* Device-semantics helpers: the exact expressions the CUDA kernels evaluate. */
+static inline double dev_hyp1(double z) {
+  const double az = fabs(z);
+  return az < 0x1p500 ? sqrt(fma(z, z, 1.0)) : az;
+}
+static inline double rot_lo(double c, double s, double x, double y) { return fma(c, x, -(s * y)); }
+static inline double rot_hi(double c, double s, double x, double y) { return fma(s, x, c * y); }
+
+/* finish (jacobi.cpp:585-609): sort by eigenvalue, sign from V's first
+ * largest-magnitude entry. */
+static void finish_f64(const double* a, const double* v, int64_t n, double* lambda,
+                       double* vout) {
+  double* lam = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) lam[i] = a[i * n + i];
+  descending_perm_f64(lam, n, perm);
+  for (int64_t jj = 0; jj < n; ++jj) {
+    const int64_t src = perm[jj];
+    const double* vc = v + src * n;
+    int64_t imax = 0;
+    double amax = -1.0;
+    for (int64_t i = 0; i < n; ++i)
+      if (fabs(vc[i]) > amax) {
+        amax = fabs(vc[i]);
+        imax = i;
+      }
+    const double flip = vc[imax] < 0.0 ? -1.0 : 1.0;
+    for (int64_t i = 0; i < n; ++i) vout[jj * n + i] = flip * vc[i];
+    lambda[jj] = lam[src];
+  }
+  free(lam);
+  free(perm);
+}
+
+/* twosided_impl restated (jacobi.cpp:493-569): cyclic by rows. */
+static int jacobi_cyclic_f64(double* A, double* V, int64_t n, double tol, int max_sweeps,
+                             port_jacobi_stats* st, port_error* err) {
+#define AE(i, j) A[(j) * n + (i)]
+  const double reltol = tol;
+  double worst = 0.0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    worst = 0.0;
+    for (int64_t i = 0; i < n - 1; ++i) {
+      for (int64_t j = i + 1; j < n; ++j) {
+        const double aii = AE(i, i), ajj = AE(j, j), aij = AE(i, j);
+        const double thresh = reltol * sqrt(aii) * sqrt(ajj);
+        const double ratio = fabs(aij) / sqrt(aii * ajj);
+        if (worst < ratio) worst = ratio;
+        if (fabs(aij) <= thresh) continue;
+        const double zeta = (ajj - aii) / (2.0 * aij);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+        const double cs = 1.0 / hypot(1.0, t);
+        const double sn = cs * t;
+        for (int64_t k = 0; k < n; ++k) {
+          if (k == i || k == j) continue;
+          const double aki = AE(k, i), akj = AE(k, j);
+          const double ni = cs * aki - sn * akj;
+          const double nj = sn * aki + cs * akj;
+          AE(k, i) = ni;
+          AE(i, k) = ni;
+          AE(k, j) = nj;
+          AE(j, k) = nj;
+        }
+        AE(i, i) = aii - t * aij;
+        AE(j, j) = ajj + t * aij;
+        AE(i, j) = 0.0;
+        AE(j, i) = 0.0;
+        if (!(AE(i, i) > 0.0)) return set_err(err, ST_NPD, i + 1, AE(i, i));
+        if (!(AE(j, j) > 0.0)) return set_err(err, ST_NPD, j + 1, AE(j, j));
+        double* vi = V + i * n;
+        double* vj = V + j * n;
+        for (int64_t k = 0; k < n; ++k) {
+          const double t1 = vi[k], t2 = vj[k];
+          vi[k] = cs * t1 - sn * t2;
+          vj[k] = sn * t1 + cs * t2;
+        }
+        rotated = 1;
+        if (st) ++st->rotations;
+      }
+    }
+    if (st) ++st->sweeps;
+    if (!rotated) return ST_OK;
+  }
+  return set_err(err, ST_NOCONV, max_sweeps, worst);
+#undef AE
+}
+
+/* Device semantics: parallel round-robin rounds. All rotations of a round
+ * are computed from the matrix at the start of the round; every 2x2 block
+ * between two pairs a<b gets the column rotation of b first, then the row
+ * rotation of a; diagonal blocks take the t*a_pq update (jacobi.cpp:541-546)
+ * with fma; V columns are rotated with the same fma forms. */
+static int jacobi_rr_f64(double* A, double* V, int64_t n, double tol, int max_sweeps,
+                         port_jacobi_stats* st, port_error* err) {
+#define AE(i, j) A[(j) * n + (i)]
+  const int64_t N = n + (n & 1), np = N / 2;
+  int64_t* P = (int64_t*)malloc(sizeof(int64_t) * (size_t)np);
+  int64_t* Q = (int64_t*)malloc(sizeof(int64_t) * (size_t)np);
+  double* C = (double*)malloc(sizeof(double) * (size_t)np);
+  double* S = (double*)malloc(sizeof(double) * (size_t)np);
+  double* T = (double*)malloc(sizeof(double) * (size_t)np);
+  int* act = (int*)malloc(sizeof(int) * (size_t)np);
+  double worst = 0.0;
+  int status = ST_NOCONV;
+  for (int sweep = 0; sweep < max_sweeps && status == ST_NOCONV; ++sweep) {
+    int64_t rot_in_sweep = 0;
+    worst = 0.0;
+    for (int64_t r = 0; r < N - 1; ++r) {
+      for (int64_t k = 0; k < np; ++k) {
+        port_rr_pair(n, r, k, &P[k], &Q[k]);
+        act[k] = 0;
+        C[k] = 1.0;
+        S[k] = 0.0;
+        T[k] = 0.0;
+        if (Q[k] >= n) continue;
+        const double aii = AE(P[k], P[k]), ajj = AE(Q[k], Q[k]), aij = AE(P[k], Q[k]);
+        const double thresh = tol * sqrt(aii) * sqrt(ajj);
+        const double ratio = fabs(aij) / sqrt(aii * ajj);
+        if (worst < ratio) worst = ratio;
+        if (fabs(aij) <= thresh) continue;
+        const double zeta = (ajj - aii) / (2.0 * aij);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + dev_hyp1(zeta));
+        const double c = 1.0 / dev_hyp1(t);
+        C[k] = c;
+        S[k] = c * t;
+        T[k] = t;
+        act[k] = 1;
+        ++rot_in_sweep;
+      }
+      /* off-diagonal 2x2 blocks */
+      for (int64_t a = 0; a < np; ++a) {
+        for (int64_t b = a + 1; b < np; ++b) {
+          if (!act[a] && !act[b]) continue;
+          const int64_t rows[2] = {P[a], Q[a]}, cols[2] = {P[b], Q[b]};
+          const int nr = Q[a] < n ? 2 : 1, nc = Q[b] < n ? 2 : 1;
+          double x[2][2] = {{0, 0}, {0, 0}};
+          for (int u = 0; u < nr; ++u)
+            for (int w = 0; w < nc; ++w) x[u][w] = AE(rows[u], cols[w]);
+          if (act[b])
+            for (int u = 0; u < nr; ++u) {
+              const double x0 = x[u][0], x1 = x[u][1];
+              x[u][0] = rot_lo(C[b], S[b], x0, x1);
+              x[u][1] = rot_hi(C[b], S[b], x0, x1);
+            }
+          if (act[a])
+            for (int w = 0; w < nc; ++w) {
+              const double y0 = x[0][w], y1 = x[1][w];
+              x[0][w] = rot_lo(C[a], S[a], y0, y1);
+              x[1][w] = rot_hi(C[a], S[a], y0, y1);
+            }
+          for (int u = 0; u < nr; ++u)
+            for (int w = 0; w < nc; ++w) {
+              AE(rows[u], cols[w]) = x[u][w];
+              AE(cols[w], rows[u]) = x[u][w];
+            }
+        }
+      }
+      /* diagonal blocks + positive-definiteness check (first failing index) */
+      int64_t bad_idx = 0;
+      double bad_val = 0.0;
+      for (int64_t k = 0; k < np; ++k) {
+        if (!act[k]) continue;
+        const int64_t p = P[k], q = Q[k];
+        const double apq = AE(p, q);
+        const double app = fma(-T[k], apq, AE(p, p));
+        const double aqq = fma(T[k], apq, AE(q, q));
+        AE(p, p) = app;
+        AE(q, q) = aqq;
+        AE(p, q) = 0.0;
+        AE(q, p) = 0.0;
+        if (!(app > 0.0) && (bad_idx == 0 || p + 1 < bad_idx)) {
+          bad_idx = p + 1;
+          bad_val = app;
+        }
+        if (!(aqq > 0.0) && (bad_idx == 0 || q + 1 < bad_idx)) {
+          bad_idx = q + 1;
+          bad_val = aqq;
+        }
+      }
+      if (bad_idx) {
+        status = set_err(err, ST_NPD, bad_idx, bad_val);
+        break;
+      }
+      for (int64_t k = 0; k < np; ++k) {
+        if (!act[k]) continue;
+        double* vp = V + P[k] * n;
+        double* vq = V + Q[k] * n;
+        for (int64_t x = 0; x < n; ++x) {
+          const double t1 = vp[x], t2 = vq[x];
+          vp[x] = rot_lo(C[k], S[k], t1, t2);
+          vq[x] = rot_hi(C[k], S[k], t1, t2);
+        }
+      }
+    }
+    if (status != ST_NOCONV) break;
+    if (st) {
+      ++st->sweeps;
+      st->rotations += rot_in_sweep;
+    }
+    if (rot_in_sweep == 0) status = ST_OK;
+  }
+  if (status == ST_NOCONV) set_err(err, ST_NOCONV, max_sweeps, worst);
+  free(P);
+  free(Q);
+  free(C);
+  free(S);
+  free(T);
+  free(act);
+  return status;
+#undef AE
+}
+
+int port_twosided_jacobi_f64(const double* mtx, int64_t n, double tol, int max_sweeps,
+                             int sem, double* lambda, double* v,
+                             port_jacobi_stats* stats, port_error* err) {
+  set_err(err, ST_OK, 0, 0.0);
+  if (n < 1 || max_sweeps < 1) return set_err(err, ST_INVALID, 0, 0.0);
+  if (!(tol > 0.0)) tol = (double)n * 0x1p-53; /* jacobi.cpp:579-580 */
+  if (stats) {
+    stats->sweeps = 0;
+    stats->rotations = 0;
+    stats->pairs_per_sweep = n * (n - 1) / 2;
+  }
+  double* A = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  double* V = (double*)calloc((size_t)(n * n), sizeof(double));
+  memcpy(A, mtx, sizeof(double) * (size_t)(n * n));
+  for (int64_t i = 0; i < n; ++i) V[i * n + i] = 1.0;
+  int st = ST_OK;
+  for (int64_t k = 0; k < n; ++k)
+    if (!(A[k * n + k] > 0.0)) {
+      st = set_err(err, ST_NPD, k + 1, A[k * n + k]);
+      break;
+    }
+  if (st == ST_OK)
+    st = sem == PORT_SEM_REFERENCE ? jacobi_cyclic_f64(A, V, n, tol, max_sweeps, stats, err)
+                                   : jacobi_rr_f64(A, V, n, tol, max_sweeps, stats, err);
+  if (st == ST_OK) finish_f64(A, V, n, lambda, v);
+  free(A);
+  free(V);
+  return st;
+}
+
+/* ======================================================================== */
+/* fp32 thin SVD (proj/src/thinsvd.cpp:49-123)                              */
+/* ======================================================================== */
+
+typedef struct {
+  const float* a;
+  const float* w;
+  float* u;
+  int64_t m, n, j0, j1;
+  int fma_chain;
+} av_job;
+
+/* matmul_impl (dense.cpp:83-96), jli order, f32; device semantics use one
+ * fmaf chain per output entry over ascending l (same order). */
+static void* av_worker(void* arg) {
+  av_job* j = (av_job*)arg;
+  const int64_t m = j->m, n = j->n;
+  for (int64_t c = j->j0; c < j->j1; ++c) {
+    float* uc = j->u + c * m;
+    for (int64_t i = 0; i < m; ++i) uc[i] = 0.0f;
+    for (int64_t l = 0; l < n; ++l) {
+      const float blj = j->w[c * n + l];
+      const float* al = j->a + l * m;
+      if (j->fma_chain)
+        for (int64_t i = 0; i < m; ++i) uc[i] = fmaf(al[i], blj, uc[i]);
+      else
+        for (int64_t i = 0; i < m; ++i) uc[i] += al[i] * blj;
+    }
+  }
+  return NULL;
+}
+
+int port_thin_svd_f32(const float* a, int64_t m, int64_t n, int threads, int sem,
+                      float* u, double* sigma, float* v, double* times5,
+                      port_error* err) {
+  const double t0 = now_s();
+  set_err(err, ST_OK, 0, 0.0);
+  if (m < n || n < 1) return set_err(err, ST_INVALID, 0, 0.0);
+  if (threads < 1) return set_err(err, ST_INVALID, 0, 0.0);
+  const int64_t blocks = m < 16 ? m : 16; /* thinsvd.cpp:66 */
+  double* mh = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  const double tg = now_s();
+  int st = port_partitioned_gram_f32(a, m, n, blocks, mh);
+  const double t_gram = now_s() - tg;
+  if (st != ST_OK) {
+    free(mh);
+    return set_err(err, st, 0, 0.0);
+  }
+  const double te = now_s();
+  double* lam = (double*)malloc(sizeof(double) * (size_t)n);
+  double* vh = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  st = port_twosided_jacobi_f64(mh, n, 0.0, 30, sem, lam, vh, NULL, err);
+  free(mh);
+  if (st != ST_OK) {
+    free(lam);
+    free(vh);
+    return st;
+  }
+  for (int64_t i = 0; i < n; ++i) sigma[i] = (double)(float)sqrt(lam[i]);
+  for (int64_t k = 0; k < n * n; ++k) v[k] = (float)vh[k];
+  free(lam);
+  free(vh);
+  for (int64_t i = 0; i < n; ++i) /* check_sigma_normal, thinsvd.cpp:22-26 */
+    if ((float)sigma[i] < FLT_MIN) return set_err(err, ST_TINY_SV, i + 1, sigma[i]);
+  const double t_eig = now_s() - te;
+  const double tu = now_s();
+  /* scale_columns(v, sigma, invert) (dense.cpp:220-232): true f32 division */
+  float* w = (float*)malloc(sizeof(float) * (size_t)(n * n));
+  for (int64_t j = 0; j < n; ++j) {
+    const float sj = (float)sigma[j];
+    if (sj == 0.0f) {
+      free(w);
+      return set_err(err, ST_ZERO_DIVISOR, j + 1, 0.0);
+    }
+    for (int64_t i = 0; i < n; ++i) w[j * n + i] = v[j * n + i] / sj;
+  }
+  /* the reference's matmul is single-threaded; threading over output
+   * columns does not change any bit (each entry's order is fixed). */
+  int nt = threads < (int)n ? threads : (int)n;
+  if (nt > 64) nt = 64;
+  pthread_t th[64];
+  av_job jobs[64];
+  for (int t = 0; t < nt; ++t) {
+    jobs[t] = (av_job){a, w, u, m, n, n * t / nt, n * (t + 1) / nt, sem == PORT_SEM_DEVICE};
+    pthread_create(&th[t], NULL, av_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  free(w);
+  const double t_u = now_s() - tu;
+  if (times5) {
+    times5[0] = t_gram;
+    times5[1] = t_eig;
+    times5[2] = t_u;
+    times5[4] = now_s() - t0;
+    times5[3] = times5[4] - t_gram - t_eig - t_u;
+  }
+  return ST_OK;
+}
+
+/* ======================================================================== */
+/* Double-double (proj/tests/support/dd.cpp:10-65)                          */
+/* ======================================================================== */
+
+typedef struct {
+  double hi, lo;
+} dd;
+
+static inline dd two_sum(double a, double b) {
+  const double s = a + b;
+  const double bb = s - a;
+  const double e = (a - (s - bb)) + (b - bb);
+  return (dd){s, e};
+}
+static inline dd quick_two_sum(double a, double b) {
+  const double s = a + b;
+  return (dd){s, b - (s - a)};
+}
+static inline dd two_prod(double a, double b) {
+  const double p = a * b;
+  return (dd){p, fma(a, b, -p)};
+}
+static inline dd dd_from(double x) { return (dd){x, 0.0}; }
+static inline dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  s.lo += a.lo + b.lo;
+  return quick_two_sum(s.hi, s.lo);
+}
+static inline dd dd_neg(dd a) { return (dd){-a.hi, -a.lo}; }
+static inline dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
+static inline dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo += a.hi * b.lo + a.lo * b.hi;
+  return quick_two_sum(p.hi, p.lo);
+}
+static inline dd dd_div(dd a, dd b) {
+  const double q1 = a.hi / b.hi;
+  dd r = dd_sub(a, dd_mul(dd_from(q1), b));
+  const double q2 = r.hi / b.hi;
+  r = dd_sub(r, dd_mul(dd_from(q2), b));
+  const double q3 = r.hi / b.hi;
+  return dd_add(quick_two_sum(q1, q2), dd_from(q3));
+}
+static inline dd dd_sqrt(dd a) {
+  if (a.hi == 0.0 && a.lo == 0.0) return (dd){0.0, 0.0};
+  const double s = sqrt(a.hi);
+  const dd e = dd_sub(a, two_prod(s, s));
+  const double corr = e.hi / (2.0 * s);
+  return quick_two_sum(s, corr);
+}
+static inline dd dd_abs(dd a) { return a.hi < 0.0 ? dd_neg(a) : a; }
+static inline int dd_le(dd a, dd b) { return a.hi < b.hi || (a.hi == b.hi && a.lo <= b.lo); }
+static inline int dd_gt0(dd a) { return a.hi > 0.0 || (a.hi == 0.0 && a.lo > 0.0); }
+static inline dd dd_scale2(dd a) { return (dd){2.0 * a.hi, 2.0 * a.lo}; }
+/* sqrt(1 + z^2) in double-double; z^2 stays finite below 2^500. */
+static inline dd dd_hyp1(dd z) {
+  const dd az = dd_abs(z);
+  if (az.hi >= 0x1p500) return az;
+  return dd_sqrt(dd_add(dd_mul(z, z), dd_from(1.0)));
+}
+
+void port_dd_add(double ah, double al, double bh, double bl, double* rh, double* rl) {
+  dd r = dd_add((dd){ah, al}, (dd){bh, bl});
+  *rh = r.hi;
+  *rl = r.lo;
+}
+void port_dd_mul(double ah, double al, double bh, double bl, double* rh, double* rl) {
+  dd r = dd_mul((dd){ah, al}, (dd){bh, bl});
+  *rh = r.hi;
+  *rl = r.lo;
+}
+void port_dd_div(double ah, double al, double bh, double bl, double* rh, double* rl) {
+  dd r = dd_div((dd){ah, al}, (dd){bh, bl});
+  *rh = r.hi;
+  *rl = r.lo;
+}
+void port_dd_sqrt(double ah, double al, double* rh, double* rl) {
+  dd r = dd_sqrt((dd){ah, al});
+  *rh = r.hi;
+  *rl = r.lo;
+}
+
+/* dd_gram (dd.cpp:75-88): acc = dd_add(acc, two_prod(a_ki, a_kj)), k
+ * ascending, upper triangle mirrored. Threads split the columns j. */
+typedef struct {
+  const double* a;
+  int64_t m, n;
+  int tid, nt;
+  double *hi, *lo;
+} ddg_job;
+
+static void* ddg_worker(void* arg) {
+  ddg_job* J = (ddg_job*)arg;
+  const int64_t m = J->m, n = J->n;
+  /* interleave columns so threads get balanced triangles */
+  for (int64_t j = J->tid; j < n; j += J->nt) {
+    const double* cj = J->a + j * m;
+    for (int64_t i = 0; i <= j; ++i) {
+      const double* ci = J->a + i * m;
+      dd acc = {0.0, 0.0};
+      for (int64_t k = 0; k < m; ++k) acc = dd_add(acc, two_prod(ci[k], cj[k]));
+      J->hi[j * n + i] = acc.hi;
+      J->lo[j * n + i] = acc.lo;
+      J->hi[i * n + j] = acc.hi;
+      J->lo[i * n + j] = acc.lo;
+    }
+  }
+  return NULL;
+}
+
+int port_dd_gram(const double* a, int64_t m, int64_t n, int threads, double* hi,
+                 double* lo) {
+  if (m < 1 || n < 1) return ST_INVALID;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  ddg_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (ddg_job){a, m, n, t, threads, hi, lo};
+    pthread_create(&th[t], NULL, ddg_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  return ST_OK;
+}
+
+static void finish_dd(const dd* A, const dd* V, int64_t n, double* lam_hi, double* lam_lo,
+                      double* vhi, double* vlo) {
+  /* sort keys: dd values compared lexicographically (hi, lo); stable. */
+  int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) perm[i] = i;
+  for (int64_t i = 1; i < n; ++i) {
+    const int64_t x = perm[i];
+    const dd kx = A[x * n + x];
+    int64_t j = i - 1;
+    while (j >= 0) {
+      const dd kj = A[perm[j] * n + perm[j]];
+      if (!(kx.hi > kj.hi || (kx.hi == kj.hi && kx.lo > kj.lo))) break;
+      perm[j + 1] = perm[j];
+      --j;
+    }
+    perm[j + 1] = x;
+  }
+  for (int64_t jj = 0; jj < n; ++jj) {
+    const int64_t src = perm[jj];
+    const dd* vc = V + src * n;
+    int64_t imax = 0;
+    dd amax = {-1.0, 0.0};
+    for (int64_t i = 0; i < n; ++i) {
+      const dd av = dd_abs(vc[i]);
+      if (av.hi > amax.hi || (av.hi == amax.hi && av.lo > amax.lo)) {
+        amax = av;
+        imax = i;
+      }
+    }
+    const int flip = vc[imax].hi < 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      const dd x = flip ? dd_neg(vc[i]) : vc[i];
+      vhi[jj * n + i] = x.hi;
+      vlo[jj * n + i] = x.lo;
+    }
+    lam_hi[jj] = A[src * n + src].hi;
+    lam_lo[jj] = A[src * n + src].lo;
+  }
+  free(perm);
+}
+
+typedef struct {
+  dd c, s, t;
+  int act;
+} dd_rot;
+
+/* One rotation from the 2x2 diagonal block, jacobi.cpp:516-529 in dd. */
+static int dd_make_rotation(dd aii, dd ajj, dd aij, dd tol, double* worst, dd_rot* r) {
+  const dd thresh = dd_mul(dd_mul(tol, dd_sqrt(aii)), dd_sqrt(ajj));
+  const double ratio = fabs(aij.hi) / sqrt(aii.hi * ajj.hi);
+  if (*worst < ratio) *worst = ratio;
+  r->act = 0;
+  r->c = dd_from(1.0);
+  r->s = dd_from(0.0);
+  r->t = dd_from(0.0);
+  if (dd_le(dd_abs(aij), thresh)) return 0;
+  const dd zeta = dd_div(dd_sub(ajj, aii), dd_scale2(aij));
+  const dd t = dd_div(dd_from(zeta.hi >= 0.0 ? 1.0 : -1.0), dd_add(dd_abs(zeta), dd_hyp1(zeta)));
+  const dd c = dd_div(dd_from(1.0), dd_hyp1(t));
+  r->c = c;
+  r->s = dd_mul(c, t);
+  r->t = t;
+  r->act = 1;
+  return 1;
+}
+
+static inline dd ddrot_lo(dd c, dd s, dd x, dd y) { return dd_sub(dd_mul(c, x), dd_mul(s, y)); }
+static inline dd ddrot_hi(dd c, dd s, dd x, dd y) { return dd_add(dd_mul(s, x), dd_mul(c, y)); }
+
+static int jacobi_cyclic_dd(dd* A, dd* V, int64_t n, dd tol, int max_sweeps,
+                            port_jacobi_stats* st, port_error* err) {
+#define AE(i, j) A[(j) * n + (i)]
+  double worst = 0.0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    worst = 0.0;
+    for (int64_t i = 0; i < n - 1; ++i)
+      for (int64_t j = i + 1; j < n; ++j) {
+        const dd aii = AE(i, i), ajj = AE(j, j), aij = AE(i, j);
+        dd_rot r;
+        if (!dd_make_rotation(aii, ajj, aij, tol, &worst, &r)) continue;
+        for (int64_t k = 0; k < n; ++k) {
+          if (k == i || k == j) continue;
+          const dd aki = AE(k, i), akj = AE(k, j);
+          const dd ni = ddrot_lo(r.c, r.s, aki, akj), nj = ddrot_hi(r.c, r.s, aki, akj);
+          AE(k, i) = ni;
+          AE(i, k) = ni;
+          AE(k, j) = nj;
+          AE(j, k) = nj;
+        }
+        AE(i, i) = dd_sub(aii, dd_mul(r.t, aij));
+        AE(j, j) = dd_add(ajj, dd_mul(r.t, aij));
+        AE(i, j) = dd_from(0.0);
+        AE(j, i) = dd_from(0.0);
+        if (!dd_gt0(AE(i, i))) return set_err(err, ST_NPD, i + 1, AE(i, i).hi);
+        if (!dd_gt0(AE(j, j))) return set_err(err, ST_NPD, j + 1, AE(j, j).hi);
+        dd* vi = V + i * n;
+        dd* vj = V + j * n;
+        for (int64_t k = 0; k < n; ++k) {
+          const dd t1 = vi[k], t2 = vj[k];
+          vi[k] = ddrot_lo(r.c, r.s, t1, t2);
+          vj[k] = ddrot_hi(r.c, r.s, t1, t2);
+        }
+        rotated = 1;
+        if (st) ++st->rotations;
+      }
+    if (st) ++st->sweeps;
+    if (!rotated) return ST_OK;
+  }
+  return set_err(err, ST_NOCONV, max_sweeps, worst);
+#undef AE
+}
+
+static int jacobi_rr_dd(dd* A, dd* V, int64_t n, dd tol, int max_sweeps,
+                        port_jacobi_stats* st, port_error* err) {
+#define AE(i, j) A[(j) * n + (i)]
+  const int64_t N = n + (n & 1), np = N / 2;
+  int64_t* P = (int64_t*)malloc(sizeof(int64_t) * (size_t)np);
+  int64_t* Q = (int64_t*)malloc(sizeof(int64_t) * (size_t)np);
+  dd_rot* R = (dd_rot*)malloc(sizeof(dd_rot) * (size_t)np);
+  double worst = 0.0;
+  int status = ST_NOCONV;
+  for (int sweep = 0; sweep < max_sweeps && status == ST_NOCONV; ++sweep) {
+    int64_t rot_in_sweep = 0;
+    worst = 0.0;
+    for (int64_t r = 0; r < N - 1; ++r) {
+      for (int64_t k = 0; k < np; ++k) {
+        port_rr_pair(n, r, k, &P[k], &Q[k]);
+        R[k].act = 0;
+        if (Q[k] >= n) continue;
+        rot_in_sweep += dd_make_rotation(AE(P[k], P[k]), AE(Q[k], Q[k]), AE(P[k], Q[k]), tol,
+                                         &worst, &R[k]);
+      }
+      for (int64_t a = 0; a < np; ++a)
+        for (int64_t b = a + 1; b < np; ++b) {
+          if (!R[a].act && !R[b].act) continue;
+          const int64_t rows[2] = {P[a], Q[a]}, cols[2] = {P[b], Q[b]};
+          const int nr = Q[a] < n ? 2 : 1, nc = Q[b] < n ? 2 : 1;
+          dd x[2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
+          for (int u = 0; u < nr; ++u)
+            for (int w = 0; w < nc; ++w) x[u][w] = AE(rows[u], cols[w]);
+          if (R[b].act)
+            for (int u = 0; u < nr; ++u) {
+              const dd x0 = x[u][0], x1 = x[u][1];
+              x[u][0] = ddrot_lo(R[b].c, R[b].s, x0, x1);
+              x[u][1] = ddrot_hi(R[b].c, R[b].s, x0, x1);
+            }
+          if (R[a].act)
+            for (int w = 0; w < nc; ++w) {
+              const dd y0 = x[0][w], y1 = x[1][w];
+              x[0][w] = ddrot_lo(R[a].c, R[a].s, y0, y1);
+              x[1][w] = ddrot_hi(R[a].c, R[a].s, y0, y1);
+            }
+          for (int u = 0; u < nr; ++u)
+            for (int w = 0; w < nc; ++w) {
+              AE(rows[u], cols[w]) = x[u][w];
+              AE(cols[w], rows[u]) = x[u][w];
+            }
+        }
+      int64_t bad_idx = 0;
+      double bad_val = 0.0;
+      for (int64_t k = 0; k < np; ++k) {
+        if (!R[k].act) continue;
+        const int64_t p = P[k], q = Q[k];
+        const dd tapq = dd_mul(R[k].t, AE(p, q));
+        const dd app = dd_sub(AE(p, p), tapq);
+        const dd aqq = dd_add(AE(q, q), tapq);
+        AE(p, p) = app;
+        AE(q, q) = aqq;
+        AE(p, q) = dd_from(0.0);
+        AE(q, p) = dd_from(0.0);
+        if (!dd_gt0(app) && (bad_idx == 0 || p + 1 < bad_idx)) {
+          bad_idx = p + 1;
+          bad_val = app.hi;
+        }
+        if (!dd_gt0(aqq) && (bad_idx == 0 || q + 1 < bad_idx)) {
+          bad_idx = q + 1;
+          bad_val = aqq.hi;
+        }
+      }
+      if (bad_idx) {
+        status = set_err(err, ST_NPD, bad_idx, bad_val);
+        break;
+      }
+      for (int64_t k = 0; k < np; ++k) {
+        if (!R[k].act) continue;
+        dd* vp = V + P[k] * n;
+        dd* vq = V + Q[k] * n;
+        for (int64_t x = 0; x < n; ++x) {
+          const dd t1 = vp[x], t2 = vq[x];
+          vp[x] = ddrot_lo(R[k].c, R[k].s, t1, t2);
+          vq[x] = ddrot_hi(R[k].c, R[k].s, t1, t2);
+        }
+      }
+    }
+    if (status != ST_NOCONV) break;
+    if (st) {
+      ++st->sweeps;
+      st->rotations += rot_in_sweep;
+    }
+    if (rot_in_sweep == 0) status = ST_OK;
+  }
+  if (status == ST_NOCONV) set_err(err, ST_NOCONV, max_sweeps, worst);
+  free(P);
+  free(Q);
+  free(R);
+  return status;
+#undef AE
+}
+
+int port_twosided_jacobi_dd(const double* mhi, const double* mlo, int64_t n, double tol,
+                            int max_sweeps, int sem, double* lam_hi, double* lam_lo,
+                            double* vhi, double* vlo, port_jacobi_stats* stats,
+                            port_error* err) {
+  set_err(err, ST_OK, 0, 0.0);
+  if (n < 1 || max_sweeps < 1) return set_err(err, ST_INVALID, 0, 0.0);
+  if (!(tol > 0.0)) tol = (double)n * 0x1p-104; /* u_dd = 2^-104 */
+  if (stats) {
+    stats->sweeps = 0;
+    stats->rotations = 0;
+    stats->pairs_per_sweep = n * (n - 1) / 2;
+  }
+  dd* A = (dd*)malloc(sizeof(dd) * (size_t)(n * n));
+  dd* V = (dd*)calloc((size_t)(n * n), sizeof(dd));
+  for (int64_t k = 0; k < n * n; ++k) A[k] = (dd){mhi[k], mlo ? mlo[k] : 0.0};
+  for (int64_t i = 0; i < n; ++i) V[i * n + i] = dd_from(1.0);
+  int st = ST_OK;
+  for (int64_t k = 0; k < n; ++k)
+    if (!dd_gt0(A[k * n + k])) {
+      st = set_err(err, ST_NPD, k + 1, A[k * n + k].hi);
+      break;
+    }
+  if (st == ST_OK)
+    st = sem == PORT_SEM_REFERENCE ? jacobi_cyclic_dd(A, V, n, dd_from(tol), max_sweeps, stats, err)
+                                   : jacobi_rr_dd(A, V, n, dd_from(tol), max_sweeps, stats, err);
+  if (st == ST_OK) finish_dd(A, V, n, lam_hi, lam_lo, vhi, vlo);
+  free(A);
+  free(V);
+  return st;
+}
+
+typedef struct {
+  const double* a;
+  const double* w;
+  double* u;
+  int64_t m, n, j0, j1;
+} av64_job;
+
+/* U = A*W in fp64, one fma chain per entry over ascending l. */
+static void* av64_worker(void* arg) {
+  av64_job* j = (av64_job*)arg;
+  const int64_t m = j->m, n = j->n;
+  for (int64_t c = j->j0; c < j->j1; ++c) {
+    double* uc = j->u + c * m;
+    for (int64_t i = 0; i < m; ++i) uc[i] = 0.0;
+    for (int64_t l = 0; l < n; ++l) {
+      const double blj = j->w[c * n + l];
+      const double* al = j->a + l * m;
+      for (int64_t i = 0; i < m; ++i) uc[i] = fma(al[i], blj, uc[i]);
+    }
+  }
+  return NULL;
+}
+
+int port_thin_svd_f64dd(const double* a, int64_t m, int64_t n, int threads, int sem,
+                        double* u, double* sigma, double* v, double* times5,
+                        port_error* err) {
+  const double t0 = now_s();
+  set_err(err, ST_OK, 0, 0.0);
+  if (m < n || n < 1 || threads < 1) return set_err(err, ST_INVALID, 0, 0.0);
+  double* ghi = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  double* glo = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  const double tg = now_s();
+  port_dd_gram(a, m, n, threads, ghi, glo);
+  const double t_gram = now_s() - tg;
+  const double te = now_s();
+  double* lh = (double*)malloc(sizeof(double) * (size_t)n);
+  double* ll = (double*)malloc(sizeof(double) * (size_t)n);
+  double* vl = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  int st = port_twosided_jacobi_dd(ghi, glo, n, 0.0, 30, sem, lh, ll, v, vl, NULL, err);
+  free(ghi);
+  free(glo);
+  free(vl);
+  if (st != ST_OK) {
+    free(lh);
+    free(ll);
+    return st;
+  }
+  for (int64_t i = 0; i < n; ++i) sigma[i] = dd_sqrt((dd){lh[i], ll[i]}).hi;
+  free(lh);
+  free(ll);
+  for (int64_t i = 0; i < n; ++i)
+    if (sigma[i] < DBL_MIN) return set_err(err, ST_TINY_SV, i + 1, sigma[i]);
+  const double t_eig = now_s() - te;
+  const double tu = now_s();
+  double* w = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < n; ++i) w[j * n + i] = v[j * n + i] / sigma[j];
+  int nt = threads < (int)n ? threads : (int)n;
+  if (nt > 64) nt = 64;
+  pthread_t th[64];
+  av64_job jobs[64];
+  for (int t = 0; t < nt; ++t) {
+    jobs[t] = (av64_job){a, w, u, m, n, n * t / nt, n * (t + 1) / nt};
+    pthread_create(&th[t], NULL, av64_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  free(w);
+  const double t_u = now_s() - tu;
+  if (times5) {
+    times5[0] = t_gram;
+    times5[1] = t_eig;
+    times5[2] = t_u;
+    times5[4] = now_s() - t0;
+    times5[3] = times5[4] - t_gram - t_eig - t_u;
+  }
+  return ST_OK;
+}
+
+/* ======================================================================== */
+/* orth_error (proj/src/dense.cpp:250-272), threaded over columns j         */
+/* ======================================================================== */
+
+typedef struct {
+  const float* qf;
+  const double* qd;
+  int64_t m, n;
+  int tid, nt;
+  double sum;
+} orth_job;
+
+static void* orth_worker(void* arg) {
+  orth_job* J = (orth_job*)arg;
+  const int64_t m = J->m, n = J->n;
+  double sum = 0.0;
+  for (int64_t j = J->tid; j < n; j += J->nt)
+    for (int64_t i = 0; i <= j; ++i) {
+      double dot = 0.0;
+      if (J->qf) {
+        const float* ci = J->qf + i * m;
+        const float* cj = J->qf + j * m;
+        for (int64_t k = 0; k < m; ++k) dot += (double)ci[k] * (double)cj[k];
+      } else {
+        const double* ci = J->qd + i * m;
+        const double* cj = J->qd + j * m;
+        for (int64_t k = 0; k < m; ++k) dot += ci[k] * cj[k];
+      }
+      const double d = dot - (i == j ? 1.0 : 0.0);
+      sum += (i == j) ? d * d : 2.0 * d * d;
+    }
+  J->sum = sum;
+  return NULL;
+}
+
+static double orth_run(const float* qf, const double* qd, int64_t m, int64_t n, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  orth_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (orth_job){qf, qd, m, n, t, threads, 0.0};
+    pthread_create(&th[t], NULL, orth_worker, &jobs[t]);
+  }
+  double sum = 0.0;
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(th[t], NULL);
+    sum += jobs[t].sum;
+  }
+  return sqrt(sum);
+}
+
+double port_orth_error_f32(const float* q, int64_t m, int64_t n, int threads) {
+  return orth_run(q, NULL, m, n, threads);
+}
+double port_orth_error_f64(const double* q, int64_t m, int64_t n, int threads) {
+  return orth_run(NULL, q, m, n, threads);
+}
