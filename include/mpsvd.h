@@ -1,0 +1,145 @@
+/* mpsvd-b200 — C ABI of the B200 (sm_100a) Gram-based thin SVD.
+ *
+ * Drop-in for the thin-SVD surface of the reference's C header
+ * (proj/include/mpsvd.h): same type names, enum values, function names,
+ * argument meaning, ownership rules (caller-owned handles released with
+ * *_destroy; accessors borrow) and thread-local diagnostics. Each declaration
+ * below cites the reference line it replaces. Declarations marked ADDITIVE do
+ * not exist in the reference: the double-double fp64 path, the device-pointer
+ * plan API used for benchmarking and multi-GPU, and stage-level entry points
+ * used by the parity tests. No declaration exposes a C++ or torch type.
+ */
+#ifndef MPSVD_B200_H
+#define MPSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* proj/include/mpsvd.h:25-37 */
+typedef enum mpsvd_status {
+  MPSVD_OK = 0,
+  MPSVD_ERR_INVALID_ARGUMENT = 1,
+  MPSVD_ERR_NOT_POSITIVE_DEFINITE = 2,
+  MPSVD_ERR_NO_CONVERGENCE = 3,
+  MPSVD_ERR_ZERO_COLUMN = 4,
+  MPSVD_ERR_ZERO_DIVISOR = 5,
+  MPSVD_ERR_CAST_OVERFLOW = 6,
+  MPSVD_ERR_TINY_SINGULAR_VALUE = 7,
+  MPSVD_ERR_INFEASIBLE = 8,
+  MPSVD_ERR_IO = 9,
+  MPSVD_ERR_INTERNAL = 10
+} mpsvd_status;
+
+/* proj/include/mpsvd.h:39-42 */
+typedef enum mpsvd_precision { MPSVD_PRECISION_WORKING = 0, MPSVD_PRECISION_HIGHER = 1 } mpsvd_precision;
+
+/* proj/include/mpsvd.h:44-48 (only TWOSIDED_JACOBI runs on the GPU path) */
+typedef enum mpsvd_eigensolver {
+  MPSVD_EIG_TWOSIDED_JACOBI = 0,
+  MPSVD_EIG_GRAM_CHOL_SVD = 1,
+  MPSVD_EIG_ONESIDED_JACOBI_GRAM = 2
+} mpsvd_eigensolver;
+
+typedef struct mpsvd_matrix mpsvd_matrix;         /* proj/include/mpsvd.h:50 */
+typedef struct mpsvd_svd_result mpsvd_svd_result; /* proj/include/mpsvd.h:52 */
+
+/* ---- diagnostics --------------------------------------------------------- */
+const char* mpsvd_last_error_message(void); /* proj/include/mpsvd.h:57 */
+int64_t mpsvd_last_error_index(void);       /* proj/include/mpsvd.h:60 */
+
+/* ---- matrices (host, column-major) --------------------------------------- */
+mpsvd_status mpsvd_matrix_create(int64_t rows, int64_t cols, mpsvd_precision prec,
+                                 mpsvd_matrix** out);                        /* mpsvd.h:64-65 */
+void mpsvd_matrix_destroy(mpsvd_matrix* a);                                  /* mpsvd.h:66 */
+int64_t mpsvd_matrix_rows(const mpsvd_matrix* a);                            /* mpsvd.h:68 */
+int64_t mpsvd_matrix_cols(const mpsvd_matrix* a);                            /* mpsvd.h:69 */
+mpsvd_precision mpsvd_matrix_precision(const mpsvd_matrix* a);               /* mpsvd.h:70 */
+mpsvd_status mpsvd_matrix_set(mpsvd_matrix* a, int64_t row, int64_t col, double value); /* :72 */
+mpsvd_status mpsvd_matrix_get(const mpsvd_matrix* a, int64_t row, int64_t col,
+                              double* value);                                /* mpsvd.h:73-74 */
+int mpsvd_matrix_bitwise_equal(const mpsvd_matrix* a, const mpsvd_matrix* b); /* mpsvd.h:77 */
+/* ADDITIVE: borrowed pointer to the column-major storage (float* or double*),
+ * page-locked when possible; lets a binding fill/read a matrix in one copy. */
+void* mpsvd_matrix_data(mpsvd_matrix* a);
+/* ||A^T A - I||_F in binary64 (mpsvd.h:85), A^T A formed on the GPU. */
+mpsvd_status mpsvd_orth_error(const mpsvd_matrix* a, double* out);
+
+/* ---- thin SVD -------------------------------------------------------------- */
+/* proj/include/mpsvd.h:116-117: f32 A (m >= n >= 1), Gram + Jacobi in fp64,
+ * U in f32. `threads` must be >= 1 (it does not change any bit). */
+mpsvd_status mpsvd_thin_svd(const mpsvd_matrix* a, mpsvd_eigensolver eig, int threads,
+                            mpsvd_svd_result** out);
+/* ADDITIVE: f64 A, Gram + Jacobi in double-double, U in f64. */
+mpsvd_status mpsvd_thin_svd_f64(const mpsvd_matrix* a, int threads, mpsvd_svd_result** out);
+
+void mpsvd_svd_destroy(mpsvd_svd_result* r);                                 /* mpsvd.h:122 */
+const mpsvd_matrix* mpsvd_svd_u(const mpsvd_svd_result* r);                  /* mpsvd.h:124 */
+const mpsvd_matrix* mpsvd_svd_v(const mpsvd_svd_result* r);                  /* mpsvd.h:125 */
+const double* mpsvd_svd_sigma(const mpsvd_svd_result* r, int64_t* count);    /* mpsvd.h:126 */
+void mpsvd_svd_times(const mpsvd_svd_result* r, double times[5]);            /* mpsvd.h:131 */
+int mpsvd_svd_sync_events(const mpsvd_svd_result* r);                        /* mpsvd.h:132 */
+int64_t mpsvd_svd_gram_blocks(const mpsvd_svd_result* r);                    /* mpsvd.h:133 */
+int mpsvd_svd_is_qr_baseline(const mpsvd_svd_result* r);                     /* mpsvd.h:134 */
+/* ADDITIVE: Jacobi sweeps / rotations of the solve. */
+void mpsvd_svd_jacobi_stats(const mpsvd_svd_result* r, int* sweeps, int64_t* rotations);
+
+/* ---- ADDITIVE: device-resident plans (bench / multi-GPU) ------------------ */
+/* One plan per (rows, cols, precision, rank): owns every device workspace so
+ * mpsvd_plan_execute allocates nothing. Pointers are device pointers on the
+ * plan's device; `stream` is a cudaStream_t (NULL = the plan's own stream).
+ * m_local rows of A live on this rank; the Gram partials of all ranks are
+ * combined by NCCL (all-reduce for fp64, all-gather + compensated sum for
+ * double-double) through `comm` (NULL: single GPU). */
+typedef struct mpsvd_comm mpsvd_comm;
+typedef struct mpsvd_plan mpsvd_plan;
+
+typedef struct mpsvd_exec_info {
+  int status;          /* mpsvd_status of the device pipeline */
+  int64_t error_index; /* 1-based index of the failure (0: none) */
+  double error_value;
+  int sweeps;
+  int64_t rotations;
+  double ms_gram, ms_eigen, ms_compute_u; /* CUDA-event device times */
+  int kernel_launches; /* kernels of this library launched by one execute */
+} mpsvd_exec_info;
+
+mpsvd_status mpsvd_comm_unique_id(unsigned char id[128]);
+mpsvd_status mpsvd_comm_init(const unsigned char id[128], int nranks, int rank, mpsvd_comm** out);
+void mpsvd_comm_destroy(mpsvd_comm* c);
+
+mpsvd_status mpsvd_plan_create(int64_t m_local, int64_t n, mpsvd_precision working, mpsvd_comm* comm,
+                               mpsvd_plan** out);
+/* d_a: m_local x n column-major (lda >= m_local); d_u: m_local x n (ldu);
+ * d_sigma: n doubles (device); d_v: n x n working precision (device).
+ * Asynchronous; completes on `stream`. */
+mpsvd_status mpsvd_plan_execute(mpsvd_plan* p, const void* d_a, int64_t lda, void* d_u, int64_t ldu,
+                                void* d_sigma, void* d_v, void* stream);
+/* Blocks until the last execute finished; reports the device status. */
+mpsvd_status mpsvd_plan_wait(mpsvd_plan* p, mpsvd_exec_info* info);
+/* Timed region helpers for the dominant kernels (CUDA events, ms). */
+void mpsvd_plan_destroy(mpsvd_plan* p);
+
+/* ---- ADDITIVE: stage entry points (host buffers; parity tests) ------------- */
+/* M = A^T A: prec WORKING -> f32 A, fp64 M (m_hi); HIGHER -> f64 A,
+ * double-double M (m_hi + m_lo). */
+mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, int64_t n, double* m_hi,
+                              double* m_lo);
+/* Two-sided Jacobi on the GPU: dd = 0 fp64 (m_lo ignored), 1 double-double.
+ * Outputs sorted/sign-fixed eigenpairs in the higher precision. */
+mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, int64_t n, double tol,
+                                int max_sweeps, double* lam_hi, double* lam_lo, double* v_hi,
+                                double* v_lo, int* sweeps, int64_t* rotations);
+
+/* ---- ADDITIVE: measured device peaks (roofline denominators) --------------- */
+double mpsvd_fp64_peak_tflops(int device);
+/* 1 if a CUDA device is usable by this library. */
+int mpsvd_device_available(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPSVD_B200_H */

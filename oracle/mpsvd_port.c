@@ -462,6 +462,21 @@ static void* av_worker(void* arg) {
   return NULL;
 }
 
+/* U = A W alone (w: n x n column-major), device semantics (fmaf chain). */
+int port_av_f32(const float* a, int64_t m, int64_t n, const float* w, float* u, int threads) {
+  int nt = threads < (int)n ? threads : (int)n;
+  if (nt < 1) nt = 1;
+  if (nt > 64) nt = 64;
+  pthread_t th[64];
+  av_job jobs[64];
+  for (int t = 0; t < nt; ++t) {
+    jobs[t] = (av_job){a, w, u, m, n, n * t / nt, n * (t + 1) / nt, 1};
+    pthread_create(&th[t], NULL, av_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+  return ST_OK;
+}
+
 int port_thin_svd_f32(const float* a, int64_t m, int64_t n, int threads, int sem,
                       float* u, double* sigma, float* v, double* times5,
                       port_error* err) {

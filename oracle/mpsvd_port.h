@@ -65,6 +65,8 @@ int port_thin_svd_f32(const float* a, int64_t m, int64_t n, int threads, int sem
                       float* u, double* sigma, float* v, double* times5,
                       port_error* err);
 
+int port_av_f32(const float* a, int64_t m, int64_t n, const float* w, float* u, int threads);
+
 /* ---- double-double ------------------------------------------------------- */
 void port_dd_add(double ah, double al, double bh, double bl, double* rh, double* rl);
 void port_dd_mul(double ah, double al, double bh, double bl, double* rh, double* rl);

@@ -290,6 +290,14 @@ class Port:
         self._raise(st, err)
         return SvdOut(u, s, v, t, 1, min(16, m))
 
+    def av_f32(self, a, w, threads=8):
+        a = _fcol(a, np.float32)
+        w = _fcol(w, np.float32)
+        m, n = a.shape
+        u = np.zeros((m, n), np.float32, order="F")
+        self.lib.port_av_f32(_f(a), _i64(m), _i64(n), _f(w), _f(u), C.c_int(threads))
+        return u
+
     def dd_op(self, op, a, b=(0.0, 0.0)):
         rh, rl = C.c_double(0), C.c_double(0)
         f = getattr(self.lib, "port_dd_" + op)

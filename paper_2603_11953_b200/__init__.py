@@ -1,0 +1,32 @@
+"""B200-native (sm_100a) mixed-precision Gram-based thin SVD (arXiv 2603.11953).
+
+Drop-in for the reference's ``mp_thin_svd`` / ``mpsvd_thin_svd`` path: the
+C-ABI library ``libmpsvd_b200.so`` (include/mpsvd.h) runs the Gram (DMMA /
+double-double SYRK), the two-sided Jacobi, and U = A V Sigma^-1 on the GPU.
+"""
+from .api import (  # noqa: F401
+    CastOverflowError,
+    Comm,
+    EigensolverChoice,
+    InternalError,
+    InvalidArgument,
+    Matrix,
+    MpsvdError,
+    NoConvergenceError,
+    NotPositiveDefiniteError,
+    PhaseTimes,
+    Plan,
+    Precision,
+    ThinSvdResult,
+    TinySingularValueError,
+    ZeroColumnError,
+    ZeroDivisorError,
+    device_available,
+    fp64_peak_tflops,
+    gram,
+    mp_thin_svd,
+    mp_thin_svd_f64,
+    orth_error,
+    twosided_jacobi_eig,
+)
+from ._lib import LIB_PATH  # noqa: F401

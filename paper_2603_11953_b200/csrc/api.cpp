@@ -1,0 +1,666 @@
+// Public C++ API (include/mpsvd/*.hpp) and C ABI (include/mpsvd.h) of the
+// B200 thin SVD. The C ABI wraps the C++ API exactly like the reference's
+// capi.cpp wraps its core (proj/src/capi.cpp:50-81,245-252): every entry runs
+// inside `guarded`, which maps the exception hierarchy to mpsvd_status codes
+// and keeps the message and the 1-based index thread-locally.
+//
+// The compute entry points run only on the GPU: with no usable CUDA device
+// they fail with MPSVD_ERR_INTERNAL ("no CUDA device"); there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "engine.h"
+#include "mpsvd.h"
+#include "mpsvd/thinsvd.hpp"
+#include "mpsvd/types.hpp"
+
+namespace mpsvd {
+
+// ---------------------------------------------------------------------------
+// errors
+NotPositiveDefiniteError::NotPositiveDefiniteError(index_t p, double v)
+    : Error("matrix not positive definite at pivot " + std::to_string(p) + " (value " + std::to_string(v) +
+            "); condition number too large for chosen higher precision"),
+      pivot(p),
+      value(v) {}
+NoConvergenceError::NoConvergenceError(int s, double w)
+    : Error("Jacobi iteration did not converge in " + std::to_string(s) +
+            " sweeps; final max normalized off-diagonal " + std::to_string(w)),
+      sweeps(s),
+      max_offdiag(w) {}
+ZeroColumnError::ZeroColumnError(index_t c) : Error("column " + std::to_string(c) + " has zero norm"), column(c) {}
+ZeroDivisorError::ZeroDivisorError(index_t i) : Error("zero scale entry at index " + std::to_string(i)), index(i) {}
+CastOverflowError::CastOverflowError(index_t r, index_t c, double v)
+    : Error("entry (" + std::to_string(r) + "," + std::to_string(c) + ") overflows the working precision"),
+      row(r),
+      col(c),
+      value(v) {}
+TinySingularValueError::TinySingularValueError(index_t i, double v)
+    : Error("singular value " + std::to_string(i) + " = " + std::to_string(v) +
+            " underflows the working precision normal range"),
+      index(i),
+      value(v) {}
+
+// ---------------------------------------------------------------------------
+// host buffers: page-locked for sizes worth pinning, plain heap otherwise
+namespace detail {
+static constexpr std::size_t kPinThreshold = 1u << 20;
+
+HostBuffer::HostBuffer(std::size_t bytes) : bytes_(bytes) {
+  if (bytes == 0) return;
+  if (bytes >= kPinThreshold && engine::device_available()) {
+    if (cudaMallocHost(&ptr_, bytes) == cudaSuccess) {
+      pinned_ = true;
+      std::memset(ptr_, 0, bytes);
+      return;
+    }
+    cudaGetLastError();
+    ptr_ = nullptr;
+  }
+  ptr_ = std::calloc(bytes, 1);
+  if (!ptr_) throw std::bad_alloc();
+}
+HostBuffer::HostBuffer(const HostBuffer& o) : HostBuffer(o.bytes_) {
+  if (bytes_) std::memcpy(ptr_, o.ptr_, bytes_);
+}
+HostBuffer& HostBuffer::operator=(const HostBuffer& o) {
+  if (this != &o) {
+    HostBuffer t(o);
+    *this = std::move(t);
+  }
+  return *this;
+}
+HostBuffer::HostBuffer(HostBuffer&& o) noexcept : ptr_(o.ptr_), bytes_(o.bytes_), pinned_(o.pinned_) {
+  o.ptr_ = nullptr;
+  o.bytes_ = 0;
+  o.pinned_ = false;
+}
+HostBuffer& HostBuffer::operator=(HostBuffer&& o) noexcept {
+  if (this != &o) {
+    release();
+    ptr_ = o.ptr_;
+    bytes_ = o.bytes_;
+    pinned_ = o.pinned_;
+    o.ptr_ = nullptr;
+    o.bytes_ = 0;
+    o.pinned_ = false;
+  }
+  return *this;
+}
+HostBuffer::~HostBuffer() { release(); }
+void HostBuffer::release() {
+  if (!ptr_) return;
+  if (pinned_)
+    cudaFreeHost(ptr_);
+  else
+    std::free(ptr_);
+  ptr_ = nullptr;
+}
+}  // namespace detail
+
+DenseMatrix::DenseMatrix(index_t rows, index_t cols, Precision prec)
+    : rows_(rows), cols_(cols), prec_(prec) {
+  if (rows < 0 || cols < 0) throw InvalidArgument("negative matrix dimension");
+  const std::size_t elt = prec == Precision::Working ? sizeof(float) : sizeof(double);
+  buf_ = detail::HostBuffer(static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols) * elt);
+}
+
+DenseMatrix DenseMatrix::identity(index_t n, Precision prec) {
+  DenseMatrix a(n, n, prec);
+  for (index_t i = 0; i < n; ++i) a.set(i, i, 1.0);
+  return a;
+}
+
+double DenseMatrix::get(index_t i, index_t j) const {
+  const std::size_t k = static_cast<std::size_t>(j) * rows_ + i;
+  return prec_ == Precision::Working ? static_cast<double>(fptr()[k]) : dptr()[k];
+}
+
+void DenseMatrix::set(index_t i, index_t j, double v) {
+  const std::size_t k = static_cast<std::size_t>(j) * rows_ + i;
+  if (prec_ == Precision::Working)
+    fptr()[k] = static_cast<float>(v);
+  else
+    dptr()[k] = v;
+}
+
+bool DenseMatrix::bitwise_equal(const DenseMatrix& o) const {
+  if (rows_ != o.rows_ || cols_ != o.cols_ || prec_ != o.prec_) return false;
+  const std::size_t bytes = static_cast<std::size_t>(size()) * (prec_ == Precision::Working ? 4 : 8);
+  return bytes == 0 || std::memcmp(buf_.data(), o.buf_.data(), bytes) == 0;
+}
+
+// ---------------------------------------------------------------------------
+// Per-thread device resources: calls on distinct threads never share a plan
+// or a stream, which keeps mp_thin_svd reentrant.
+namespace {
+
+struct Bundle {
+  std::unique_ptr<engine::Plan> plan;
+  void* d_a = nullptr;
+  void* d_u = nullptr;
+  double* d_sigma = nullptr;
+  void* d_v = nullptr;
+  ~Bundle() {
+    cudaFree(d_a);
+    cudaFree(d_u);
+    cudaFree(d_sigma);
+    cudaFree(d_v);
+  }
+};
+
+using Key = std::tuple<long long, long long, bool>;
+
+Bundle& bundle_for(long long m, long long n, bool f64) {
+  thread_local std::map<Key, std::unique_ptr<Bundle>> cache;
+  const Key key{m, n, f64};
+  auto it = cache.find(key);
+  if (it != cache.end()) return *it->second;
+  if (cache.size() >= 4) cache.clear();  // bounded: large plans hold GBs
+  auto b = std::make_unique<Bundle>();
+  b->plan = std::make_unique<engine::Plan>(m, n, f64, nullptr);
+  const std::size_t elt = f64 ? 8 : 4;
+  engine::check(cudaMalloc(&b->d_a, std::max<std::size_t>(1, m * n * elt)), "cudaMalloc A");
+  engine::check(cudaMalloc(&b->d_u, std::max<std::size_t>(1, m * n * elt)), "cudaMalloc U");
+  engine::check(cudaMalloc((void**)&b->d_sigma, n * sizeof(double)), "cudaMalloc sigma");
+  engine::check(cudaMalloc(&b->d_v, n * n * elt), "cudaMalloc V");
+  auto& ref = *b;
+  cache.emplace(key, std::move(b));
+  return ref;
+}
+
+void require_device() {
+  if (!engine::device_available()) throw std::runtime_error("no CUDA device: the mpsvd GPU path cannot run");
+}
+
+void raise_device_status(const mpsvd_exec_info& info, int max_sweeps) {
+  switch (info.status) {
+    case 0:
+      return;
+    case 2:
+      throw NotPositiveDefiniteError(info.error_index, info.error_value);
+    case 3:
+      throw NoConvergenceError(max_sweeps, info.error_value);
+    case 7:
+      throw TinySingularValueError(info.error_index, info.error_value);
+    default:
+      throw std::runtime_error("device pipeline failed with status " + std::to_string(info.status));
+  }
+}
+
+using Clock = std::chrono::steady_clock;
+
+ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f64) {
+  const auto t0 = Clock::now();
+  const long long m = a.rows(), n = a.cols();
+  if (cfg.max_sweeps < 1) throw InvalidArgument("max_sweeps must be >= 1");
+  require_device();
+  Bundle& b = bundle_for(m, n, f64);
+  engine::Plan& p = *b.plan;
+  p.set_jacobi(cfg.tol, cfg.max_sweeps);
+  const std::size_t elt = f64 ? 8 : 4;
+  cudaStream_t st = p.own_stream;
+  engine::check(cudaMemcpyAsync(b.d_a, a.raw(), m * n * elt, cudaMemcpyHostToDevice, st), "H2D A");
+  p.execute(b.d_a, m, b.d_u, m, b.d_sigma, b.d_v, st);
+  const Precision wp = f64 ? Precision::Higher : Precision::Working;
+  ThinSvdResult out;
+  out.factors.u = DenseMatrix(m, n, wp);
+  out.factors.v = DenseMatrix(n, n, wp);
+  out.factors.sigma.assign(n, 0.0);
+  out.factors.precision = wp;
+  engine::check(cudaMemcpyAsync(out.factors.u.raw(), b.d_u, m * n * elt, cudaMemcpyDeviceToHost, st), "D2H U");
+  engine::check(cudaMemcpyAsync(out.factors.v.raw(), b.d_v, n * n * elt, cudaMemcpyDeviceToHost, st), "D2H V");
+  engine::check(cudaMemcpyAsync(out.factors.sigma.data(), b.d_sigma, n * sizeof(double), cudaMemcpyDeviceToHost, st),
+                "D2H sigma");
+  const mpsvd_exec_info info = p.wait();
+  raise_device_status(info, cfg.max_sweeps);
+  out.eigensolver = EigensolverChoice::TwoSidedJacobi;
+  out.gram_sync_events = 1;  // one global combine of the partial Grams
+  out.gram_blocks = p.nblocks;
+  out.jacobi_sweeps = info.sweeps;
+  out.jacobi_rotations = (long)info.rotations;
+  out.times.gram = info.ms_gram * 1e-3;
+  out.times.eigen = info.ms_eigen * 1e-3;
+  out.times.compute_u = info.ms_compute_u * 1e-3;
+  out.times.total = std::chrono::duration<double>(Clock::now() - t0).count();
+  out.times.overlap = out.times.total - out.times.gram - out.times.eigen - out.times.compute_u;
+  if (out.times.overlap < 0.0) {  // event clocks vs host clock granularity
+    out.times.total -= out.times.overlap;
+    out.times.overlap = 0.0;
+  }
+  return out;
+}
+
+}  // namespace
+
+ThinSvdResult mp_thin_svd(const DenseMatrix& a, EigensolverChoice choice, const JacobiConfig& cfg, int threads) {
+  // validation order of proj/src/thinsvd.cpp:52-56
+  if (a.precision() != Precision::Working) throw InvalidArgument("mp_thin_svd expects a Working-precision matrix");
+  if (a.rows() < a.cols() || a.cols() < 1) throw InvalidArgument("mp_thin_svd: need m >= n >= 1");
+  if (threads < 1) throw InvalidArgument("mp_thin_svd: thread count must be positive");
+  if (choice != EigensolverChoice::TwoSidedJacobi)
+    throw InvalidArgument("mp_thin_svd: only EigensolverChoice::TwoSidedJacobi runs on the GPU path");
+  return run_thin_svd(a, cfg, false);
+}
+
+ThinSvdResult mp_thin_svd_f64(const DenseMatrix& a, const JacobiConfig& cfg, int threads) {
+  if (a.precision() != Precision::Higher) throw InvalidArgument("mp_thin_svd_f64 expects a Higher-precision matrix");
+  if (a.rows() < a.cols() || a.cols() < 1) throw InvalidArgument("mp_thin_svd_f64: need m >= n >= 1");
+  if (threads < 1) throw InvalidArgument("mp_thin_svd_f64: thread count must be positive");
+  return run_thin_svd(a, cfg, true);
+}
+
+namespace {
+// Jacobi on an uploaded symmetric M (fp64, or double-double as hi/lo);
+// outputs sorted, sign-fixed eigenpairs. Used by twosided_jacobi_eig and the
+// stage entry point.
+void gpu_jacobi(bool dd, const double* m_hi, const double* m_lo, long long n, double tol, int max_sweeps,
+                double* lam_hi, double* lam_lo, double* v_hi, double* v_lo, int* sweeps, long long* rotations) {
+  require_device();
+  if (n < 1) throw InvalidArgument("twosided_jacobi_eig: empty matrix");
+  if (max_sweeps < 1) throw InvalidArgument("max_sweeps must be >= 1");
+  engine::Plan p(0, n, dd, nullptr);
+  p.set_jacobi(tol, max_sweeps);
+  cudaStream_t st = p.own_stream;
+  const std::size_t nn = (std::size_t)n * n;
+  std::vector<double> inter;
+  if (dd) {
+    inter.resize(2 * nn);
+    for (std::size_t k = 0; k < nn; ++k) {
+      inter[2 * k] = m_hi[k];
+      inter[2 * k + 1] = m_lo ? m_lo[k] : 0.0;
+    }
+    engine::check(cudaMemcpyAsync(p.d_m, inter.data(), 2 * nn * 8, cudaMemcpyHostToDevice, st), "H2D M");
+  } else {
+    engine::check(cudaMemcpyAsync(p.d_m, m_hi, nn * 8, cudaMemcpyHostToDevice, st), "H2D M");
+  }
+  void* d_vfull = nullptr;
+  engine::check(cudaMalloc(&d_vfull, nn * 8 * (dd ? 2 : 1)), "cudaMalloc V");
+  p.reset_status(st);
+  p.eigen(st);
+  engine::check(dev::launch_finish(dd, (int)n, p.jws, p.d_perm, p.d_lam_hi, p.d_lam_lo, p.d_sigma_tmp, nullptr,
+                                   nullptr, 1, st, d_vfull),
+                "finish");
+  p.fetch_status(st);
+  std::vector<double> vbuf(nn * (dd ? 2 : 1));
+  engine::check(cudaMemcpyAsync(vbuf.data(), d_vfull, vbuf.size() * 8, cudaMemcpyDeviceToHost, st), "D2H V");
+  engine::check(cudaMemcpyAsync(lam_hi, p.d_lam_hi, n * 8, cudaMemcpyDeviceToHost, st), "D2H lambda");
+  std::vector<double> lo(n);
+  engine::check(cudaMemcpyAsync(lo.data(), p.d_lam_lo, n * 8, cudaMemcpyDeviceToHost, st), "D2H lambda lo");
+  const mpsvd_exec_info info = p.wait();
+  cudaFree(d_vfull);
+  raise_device_status(info, max_sweeps);
+  if (lam_lo) std::memcpy(lam_lo, lo.data(), n * 8);
+  if (dd) {
+    for (std::size_t k = 0; k < nn; ++k) {
+      v_hi[k] = vbuf[2 * k];
+      if (v_lo) v_lo[k] = vbuf[2 * k + 1];
+    }
+  } else {
+    std::memcpy(v_hi, vbuf.data(), nn * 8);
+    if (v_lo) std::memset(v_lo, 0, nn * 8);
+  }
+  if (sweeps) *sweeps = info.sweeps;
+  if (rotations) *rotations = info.rotations;
+}
+
+void gpu_gram(bool f64, const void* a, long long m, long long n, double* m_hi, double* m_lo) {
+  require_device();
+  if (m < 1 || n < 1) throw InvalidArgument("gram: need m >= 1, n >= 1");
+  engine::Plan p(m, n, f64, nullptr);
+  cudaStream_t st = p.own_stream;
+  const std::size_t elt = f64 ? 8 : 4;
+  void* d_a = nullptr;
+  engine::check(cudaMalloc(&d_a, m * n * elt), "cudaMalloc A");
+  engine::check(cudaMemcpyAsync(d_a, a, m * n * elt, cudaMemcpyHostToDevice, st), "H2D A");
+  p.launches = 0;
+  p.gram(d_a, m, st);
+  const std::size_t nn = (std::size_t)n * n;
+  std::vector<double> buf(nn * (f64 ? 2 : 1));
+  engine::check(cudaMemcpyAsync(buf.data(), p.d_m, buf.size() * 8, cudaMemcpyDeviceToHost, st), "D2H M");
+  engine::check(cudaStreamSynchronize(st), "sync");
+  cudaFree(d_a);
+  if (f64) {
+    for (std::size_t k = 0; k < nn; ++k) {
+      m_hi[k] = buf[2 * k];
+      if (m_lo) m_lo[k] = buf[2 * k + 1];
+    }
+  } else {
+    std::memcpy(m_hi, buf.data(), nn * 8);
+    if (m_lo) std::memset(m_lo, 0, nn * 8);
+  }
+}
+}  // namespace
+
+EigFactors twosided_jacobi_eig(const DenseMatrix& m, const JacobiConfig& cfg, JacobiStats* stats) {
+  const index_t n = m.rows();
+  if (m.cols() != n) throw InvalidArgument("twosided_jacobi_eig: not square");
+  if (n < 1) throw InvalidArgument("twosided_jacobi_eig: empty matrix");
+  if (cfg.max_sweeps < 1) throw InvalidArgument("max_sweeps must be >= 1");
+  if (m.precision() != Precision::Higher)
+    throw InvalidArgument("twosided_jacobi_eig: the GPU path takes a Higher-precision matrix");
+  EigFactors out;
+  out.precision = Precision::Higher;
+  out.lambda.assign(n, 0.0);
+  out.v = DenseMatrix(n, n, Precision::Higher);
+  int sw = 0;
+  long long rot = 0;
+  gpu_jacobi(false, m.dptr(), nullptr, n, cfg.tol, cfg.max_sweeps, out.lambda.data(), nullptr, out.v.dptr(),
+             nullptr, &sw, &rot);
+  if (stats) {
+    stats->sweeps = sw;
+    stats->rotations = (long)rot;
+    stats->pairs_per_sweep = (long)(n * (n - 1) / 2);
+  }
+  return out;
+}
+
+double orth_error(const DenseMatrix& q) {
+  const index_t m = q.rows(), n = q.cols();
+  if (m < n) throw InvalidArgument("orth_error: rows < cols");
+  std::vector<double> g((std::size_t)n * n);
+  gpu_gram(q.precision() == Precision::Higher, q.raw(), m, n, g.data(), nullptr);
+  double sum = 0.0;
+  for (index_t j = 0; j < n; ++j)
+    for (index_t i = 0; i <= j; ++i) {
+      const double d = g[(std::size_t)j * n + i] - (i == j ? 1.0 : 0.0);
+      sum += (i == j) ? d * d : 2.0 * d * d;
+    }
+  return std::sqrt(sum);
+}
+
+// entry points for the C ABI below
+void raise_device_status_public(const mpsvd_exec_info& info, int max_sweeps) {
+  raise_device_status(info, max_sweeps);
+}
+void gpu_gram_public(bool f64, const void* a, long long m, long long n, double* m_hi, double* m_lo) {
+  gpu_gram(f64, a, m, n, m_hi, m_lo);
+}
+void gpu_jacobi_public(bool dd, const double* m_hi, const double* m_lo, long long n, double tol, int max_sweeps,
+                       double* lam_hi, double* lam_lo, double* v_hi, double* v_lo, int* sweeps,
+                       long long* rotations) {
+  gpu_jacobi(dd, m_hi, m_lo, n, tol, max_sweeps, lam_hi, lam_lo, v_hi, v_lo, sweeps, rotations);
+}
+
+}  // namespace mpsvd
+
+// =============================================================================
+// C ABI
+// =============================================================================
+struct mpsvd_matrix {
+  mpsvd::DenseMatrix m;
+};
+
+struct mpsvd_svd_result {
+  mpsvd_matrix u, v;
+  std::vector<double> sigma;
+  double times[5] = {0, 0, 0, 0, 0};
+  int sync_events = 0;
+  int64_t gram_blocks = 0;
+  int qr_baseline = 0;
+  int sweeps = 0;
+  int64_t rotations = 0;
+};
+
+struct mpsvd_comm {
+  mpsvd::engine::Comm* c = nullptr;
+};
+
+struct mpsvd_plan {
+  std::unique_ptr<mpsvd::engine::Plan> p;
+};
+
+namespace {
+
+thread_local std::string t_message;
+thread_local int64_t t_index = 0;
+
+mpsvd_status fail(mpsvd_status s, const char* msg, int64_t index = 0) {
+  t_message = msg;
+  t_index = index;
+  return s;
+}
+
+template <typename F>
+mpsvd_status guarded(F&& body) noexcept {
+  using namespace mpsvd;
+  try {
+    t_message.clear();
+    t_index = 0;
+    body();
+    return MPSVD_OK;
+  } catch (const InvalidArgument& e) {
+    return fail(MPSVD_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const NotPositiveDefiniteError& e) {
+    return fail(MPSVD_ERR_NOT_POSITIVE_DEFINITE, e.what(), e.pivot);
+  } catch (const NoConvergenceError& e) {
+    return fail(MPSVD_ERR_NO_CONVERGENCE, e.what());
+  } catch (const ZeroColumnError& e) {
+    return fail(MPSVD_ERR_ZERO_COLUMN, e.what(), e.column);
+  } catch (const ZeroDivisorError& e) {
+    return fail(MPSVD_ERR_ZERO_DIVISOR, e.what(), e.index);
+  } catch (const CastOverflowError& e) {
+    return fail(MPSVD_ERR_CAST_OVERFLOW, e.what());
+  } catch (const TinySingularValueError& e) {
+    return fail(MPSVD_ERR_TINY_SINGULAR_VALUE, e.what(), e.index);
+  } catch (const InfeasibleError& e) {
+    return fail(MPSVD_ERR_INFEASIBLE, e.what());
+  } catch (const IoError& e) {
+    return fail(MPSVD_ERR_IO, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(MPSVD_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const std::exception& e) {
+    return fail(MPSVD_ERR_INTERNAL, e.what());
+  } catch (...) {
+    return fail(MPSVD_ERR_INTERNAL, "unknown error");
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw mpsvd::InvalidArgument(msg);
+}
+
+mpsvd_svd_result* wrap(mpsvd::ThinSvdResult&& r) {
+  auto* out = new mpsvd_svd_result;
+  out->u.m = std::move(r.factors.u);
+  out->v.m = std::move(r.factors.v);
+  out->sigma = std::move(r.factors.sigma);
+  out->times[0] = r.times.gram;
+  out->times[1] = r.times.eigen;
+  out->times[2] = r.times.compute_u;
+  out->times[3] = r.times.overlap;
+  out->times[4] = r.times.total;
+  out->sync_events = r.gram_sync_events;
+  out->gram_blocks = r.gram_blocks;
+  out->qr_baseline = r.qr_baseline ? 1 : 0;
+  out->sweeps = r.jacobi_sweeps;
+  out->rotations = r.jacobi_rotations;
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpsvd_last_error_message(void) { return t_message.c_str(); }
+int64_t mpsvd_last_error_index(void) { return t_index; }
+
+mpsvd_status mpsvd_matrix_create(int64_t rows, int64_t cols, mpsvd_precision prec, mpsvd_matrix** out) {
+  return guarded([&] {
+    require(out != nullptr, "out is null");
+    require(rows >= 0 && cols >= 0, "negative dimension");
+    require(prec == MPSVD_PRECISION_WORKING || prec == MPSVD_PRECISION_HIGHER, "unknown precision value");
+    *out = new mpsvd_matrix{mpsvd::DenseMatrix(
+        rows, cols, prec == MPSVD_PRECISION_WORKING ? mpsvd::Precision::Working : mpsvd::Precision::Higher)};
+  });
+}
+
+void mpsvd_matrix_destroy(mpsvd_matrix* a) { delete a; }
+int64_t mpsvd_matrix_rows(const mpsvd_matrix* a) { return a ? a->m.rows() : 0; }
+int64_t mpsvd_matrix_cols(const mpsvd_matrix* a) { return a ? a->m.cols() : 0; }
+mpsvd_precision mpsvd_matrix_precision(const mpsvd_matrix* a) {
+  return (a && a->m.precision() == mpsvd::Precision::Higher) ? MPSVD_PRECISION_HIGHER : MPSVD_PRECISION_WORKING;
+}
+
+mpsvd_status mpsvd_matrix_set(mpsvd_matrix* a, int64_t row, int64_t col, double value) {
+  return guarded([&] {
+    require(a != nullptr, "matrix is null");
+    require(row >= 0 && row < a->m.rows() && col >= 0 && col < a->m.cols(), "index out of range");
+    a->m.set(row, col, value);
+  });
+}
+
+mpsvd_status mpsvd_matrix_get(const mpsvd_matrix* a, int64_t row, int64_t col, double* value) {
+  return guarded([&] {
+    require(a != nullptr && value != nullptr, "null argument");
+    require(row >= 0 && row < a->m.rows() && col >= 0 && col < a->m.cols(), "index out of range");
+    *value = a->m.get(row, col);
+  });
+}
+
+int mpsvd_matrix_bitwise_equal(const mpsvd_matrix* a, const mpsvd_matrix* b) {
+  if (!a || !b) return 0;
+  return a->m.bitwise_equal(b->m) ? 1 : 0;
+}
+
+void* mpsvd_matrix_data(mpsvd_matrix* a) { return a ? a->m.raw() : nullptr; }
+
+mpsvd_status mpsvd_orth_error(const mpsvd_matrix* a, double* out) {
+  return guarded([&] {
+    require(a != nullptr && out != nullptr, "null argument");
+    *out = mpsvd::orth_error(a->m);
+  });
+}
+
+mpsvd_status mpsvd_thin_svd(const mpsvd_matrix* a, mpsvd_eigensolver eig, int threads, mpsvd_svd_result** out) {
+  return guarded([&] {
+    require(a != nullptr && out != nullptr, "null argument");
+    require(eig == MPSVD_EIG_TWOSIDED_JACOBI || eig == MPSVD_EIG_GRAM_CHOL_SVD || eig == MPSVD_EIG_ONESIDED_JACOBI_GRAM,
+            "unknown eigensolver value");
+    auto choice = eig == MPSVD_EIG_TWOSIDED_JACOBI ? mpsvd::EigensolverChoice::TwoSidedJacobi
+                  : eig == MPSVD_EIG_GRAM_CHOL_SVD ? mpsvd::EigensolverChoice::GramCholSvd
+                                                   : mpsvd::EigensolverChoice::OneSidedJacobiOnGram;
+    *out = wrap(mpsvd::mp_thin_svd(a->m, choice, {}, threads));
+  });
+}
+
+mpsvd_status mpsvd_thin_svd_f64(const mpsvd_matrix* a, int threads, mpsvd_svd_result** out) {
+  return guarded([&] {
+    require(a != nullptr && out != nullptr, "null argument");
+    *out = wrap(mpsvd::mp_thin_svd_f64(a->m, {}, threads));
+  });
+}
+
+void mpsvd_svd_destroy(mpsvd_svd_result* r) { delete r; }
+const mpsvd_matrix* mpsvd_svd_u(const mpsvd_svd_result* r) { return r ? &r->u : nullptr; }
+const mpsvd_matrix* mpsvd_svd_v(const mpsvd_svd_result* r) { return r ? &r->v : nullptr; }
+const double* mpsvd_svd_sigma(const mpsvd_svd_result* r, int64_t* count) {
+  if (count) *count = r ? (int64_t)r->sigma.size() : 0;
+  return r ? r->sigma.data() : nullptr;
+}
+void mpsvd_svd_times(const mpsvd_svd_result* r, double times[5]) {
+  if (r && times) std::memcpy(times, r->times, sizeof(r->times));
+}
+int mpsvd_svd_sync_events(const mpsvd_svd_result* r) { return r ? r->sync_events : 0; }
+int64_t mpsvd_svd_gram_blocks(const mpsvd_svd_result* r) { return r ? r->gram_blocks : 0; }
+int mpsvd_svd_is_qr_baseline(const mpsvd_svd_result* r) { return r ? r->qr_baseline : 0; }
+void mpsvd_svd_jacobi_stats(const mpsvd_svd_result* r, int* sweeps, int64_t* rotations) {
+  if (sweeps) *sweeps = r ? r->sweeps : 0;
+  if (rotations) *rotations = r ? r->rotations : 0;
+}
+
+mpsvd_status mpsvd_comm_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    require(id != nullptr, "null argument");
+    mpsvd::engine::comm_unique_id(id);
+  });
+}
+
+mpsvd_status mpsvd_comm_init(const unsigned char id[128], int nranks, int rank, mpsvd_comm** out) {
+  return guarded([&] {
+    require(id != nullptr && out != nullptr, "null argument");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    auto* c = new mpsvd_comm;
+    c->c = mpsvd::engine::comm_init(id, nranks, rank);
+    *out = c;
+  });
+}
+
+void mpsvd_comm_destroy(mpsvd_comm* c) {
+  if (!c) return;
+  mpsvd::engine::comm_destroy(c->c);
+  delete c;
+}
+
+mpsvd_status mpsvd_plan_create(int64_t m_local, int64_t n, mpsvd_precision working, mpsvd_comm* comm,
+                               mpsvd_plan** out) {
+  return guarded([&] {
+    require(out != nullptr, "null argument");
+    require(n >= 1 && m_local >= 0, "need n >= 1 and m_local >= 0");
+    if (!mpsvd::engine::device_available()) throw std::runtime_error("no CUDA device");
+    auto* p = new mpsvd_plan;
+    p->p = std::make_unique<mpsvd::engine::Plan>(m_local, n, working == MPSVD_PRECISION_HIGHER,
+                                                 comm ? comm->c : nullptr);
+    *out = p;
+  });
+}
+
+mpsvd_status mpsvd_plan_execute(mpsvd_plan* p, const void* d_a, int64_t lda, void* d_u, int64_t ldu, void* d_sigma,
+                                void* d_v, void* stream) {
+  return guarded([&] {
+    require(p != nullptr && p->p, "null plan");
+    require(lda >= p->p->m && (d_u == nullptr || ldu >= p->p->m), "leading dimension too small");
+    p->p->execute(d_a, lda, d_u, ldu, d_sigma, d_v, (cudaStream_t)stream);
+  });
+}
+
+mpsvd_status mpsvd_plan_wait(mpsvd_plan* p, mpsvd_exec_info* info) {
+  mpsvd_exec_info local;
+  std::memset(&local, 0, sizeof(local));
+  const mpsvd_status s = guarded([&] {
+    require(p != nullptr && p->p, "null plan");
+    local = p->p->wait();
+    mpsvd::raise_device_status_public(local, p->p->max_sweeps);
+  });
+  if (info) *info = local;
+  return s;
+}
+
+void mpsvd_plan_destroy(mpsvd_plan* p) { delete p; }
+
+mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, int64_t n, double* m_hi, double* m_lo) {
+  return guarded([&] {
+    require(a != nullptr && m_hi != nullptr, "null argument");
+    mpsvd::gpu_gram_public(prec == MPSVD_PRECISION_HIGHER, a, m, n, m_hi, m_lo);
+  });
+}
+
+mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, int64_t n, double tol, int max_sweeps,
+                                double* lam_hi, double* lam_lo, double* v_hi, double* v_lo, int* sweeps,
+                                int64_t* rotations) {
+  return guarded([&] {
+    require(m_hi != nullptr && lam_hi != nullptr && v_hi != nullptr, "null argument");
+    long long rot = 0;
+    mpsvd::gpu_jacobi_public(dd != 0, m_hi, m_lo, n, tol, max_sweeps, lam_hi, lam_lo, v_hi, v_lo, sweeps, &rot);
+    if (rotations) *rotations = rot;
+  });
+}
+
+double mpsvd_fp64_peak_tflops(int device) {
+  if (!mpsvd::engine::device_available()) return 0.0;
+  cudaSetDevice(device);
+  return mpsvd::dev::measure_fp64_peak_tflops(device);
+}
+
+int mpsvd_device_available(void) { return mpsvd::engine::device_available() ? 1 : 0; }
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+// Host orchestrator of the B200 thin SVD (host code; compiled by nvcc only
+// because it includes the device status layout).
+//
+// One Plan = every device workspace for one (rows, cols, precision, rank),
+// so executing the pipeline allocates nothing:
+//
+//   K1/K2 gram (split-K over rows, 16 logical blocks x S splits)
+//     -> gram_combine (splits in order, blocks along the reference tree)
+//     -> [N > 1: NCCL all-reduce (fp64) | all-gather + compensated rank sum (dd)]
+//     -> K4/K5 jacobi (persistent, one barrier per round)
+//     -> jacobi_replay (V) -> finish (sort, sign, sigma, V, W = V / sigma)
+//     -> K7 av (U = A W)
+//
+// all on one stream, with CUDA events between the phases for PhaseTimes.
+// NCCL is resolved with dlopen on first multi-rank use, so the library loads
+// (and its single-GPU path runs) without it.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.h"
+#include "kernels.h"
+
+namespace mpsvd {
+namespace engine {
+
+using dev::DevStatus;
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool device_available() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return count > 0;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL through dlopen (minimal ABI subset; types from nccl.h 2.x).
+namespace nccl {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+enum { ncclSuccess = 0 };
+enum { ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+struct Api {
+  int (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool ok = false;
+};
+Api& api() {
+  static Api a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    a.GetUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+    a.AllReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+    a.AllGather = (int (*)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllGather");
+    a.CommDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+    a.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.AllGather && a.CommDestroy;
+  });
+  return a;
+}
+void check(int r, const char* what) {
+  if (r != ncclSuccess) {
+    const char* s = api().GetErrorString ? api().GetErrorString(r) : "?";
+    throw std::runtime_error(std::string("NCCL ") + what + ": " + s);
+  }
+}
+}  // namespace nccl
+
+struct Comm {
+  nccl::ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+void comm_unique_id(unsigned char id[128]) {
+  auto& a = nccl::api();
+  if (!a.ok) throw std::runtime_error("NCCL (libnccl.so.2) not loadable");
+  nccl::ncclUniqueId u;
+  nccl::check(a.GetUniqueId(&u), "GetUniqueId");
+  std::memcpy(id, u.internal, 128);
+}
+
+Comm* comm_init(const unsigned char id[128], int nranks, int rank) {
+  auto& a = nccl::api();
+  if (!a.ok) throw std::runtime_error("NCCL (libnccl.so.2) not loadable");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank/nranks");
+  nccl::ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  auto* c = new Comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  nccl::check(a.CommInitRank(&c->comm, nranks, u, rank), "CommInitRank");
+  return c;
+}
+
+void comm_destroy(Comm* c) {
+  if (!c) return;
+  if (c->comm && nccl::api().CommDestroy) nccl::api().CommDestroy(c->comm);
+  delete c;
+}
+
+// ---------------------------------------------------------------------------
+// Gram schedule: logical blocks over the local rows (reference plan,
+// parallel_gram.cpp:243-263, 16 blocks as thinsvd.cpp:66), each cut into
+// S splits sized so (tile pairs x splits) fills one wave of resident CTAs.
+static void build_schedule(Plan& p) {
+  const long long m = p.m, n = p.n;
+  const int T = (int)((n + 63) / 64);
+  p.tiles.clear();
+  for (int ti = 0; ti < T; ++ti)
+    for (int tj = ti; tj < T; ++tj) p.tiles.push_back(make_int2(ti, tj));
+  p.ntp = (int)p.tiles.size();
+  p.nblocks = (int)(m < 16 ? m : 16);
+  p.splits.clear();
+  p.block_split_begin.assign(1, 0);
+  if (p.nblocks == 0) return;
+  const int slots = p.sm_count * p.gram_occupancy;
+  int per_block = slots / (p.nblocks * p.ntp);
+  if (per_block < 1) per_block = 1;
+  const long long base = m / p.nblocks, extra = m % p.nblocks;
+  long long row = 0;
+  for (int b = 0; b < p.nblocks; ++b) {
+    const long long len = base + (b < extra ? 1 : 0);
+    long long s = per_block;
+    const long long max_s = (len + 31) / 32;
+    if (s > max_s) s = max_s;
+    if (s < 1) s = 1;
+    // piece length rounded up to whole 32-row chunks
+    long long piece = (len + s - 1) / s;
+    piece = (piece + 31) / 32 * 32;
+    for (long long r = row; r < row + len; r += piece) {
+      longlong2 sp;
+      sp.x = r;
+      sp.y = r + piece < row + len ? r + piece : row + len;
+      p.splits.push_back(sp);
+    }
+    p.block_split_begin.push_back((int)p.splits.size());
+    row += len;
+  }
+}
+
+template <typename T>
+static T* dalloc(size_t count, std::vector<void*>& owned) {
+  void* ptr = nullptr;
+  if (count == 0) count = 1;
+  check(cudaMalloc(&ptr, count * sizeof(T)), "cudaMalloc");
+  owned.push_back(ptr);
+  return static_cast<T*>(ptr);
+}
+
+Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
+    : m(m_local), n(n_cols), dd(f64_working), comm(c) {
+  if (n < 1 || m < 0) throw std::invalid_argument("plan: need n >= 1, m >= 0");
+  if (!device_available()) throw std::runtime_error("no CUDA device available");
+  check(cudaGetDevice(&device), "cudaGetDevice");
+  check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
+  gram_occupancy = dd ? 1 : 2;
+  build_schedule(*this);
+  const size_t nn = (size_t)n * n;
+  const size_t esz = dd ? 2 : 1;  // doubles per element of the higher precision
+  const int N = (int)(n + (n & 1)), np = N / 2;
+
+  d_tiles = dalloc<int2>(tiles.size(), owned);
+  d_splits = dalloc<longlong2>(splits.size(), owned);
+  d_bsb = dalloc<int>(block_split_begin.size(), owned);
+  check(cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice), "H2D tiles");
+  if (!splits.empty())
+    check(cudaMemcpy(d_splits, splits.data(), splits.size() * sizeof(longlong2), cudaMemcpyHostToDevice),
+          "H2D splits");
+  check(cudaMemcpy(d_bsb, block_split_begin.data(), block_split_begin.size() * sizeof(int),
+                   cudaMemcpyHostToDevice),
+        "H2D bsb");
+  d_partials = dalloc<double>(splits.size() * tiles.size() * 64 * 64 * esz, owned);
+  d_m = dalloc<double>(nn * esz, owned);
+  const int nranks = comm ? comm->nranks : 1;
+  if (nranks > 1) {
+    d_mloc = dalloc<double>(nn * esz, owned);
+    if (dd) d_gather = dalloc<double>(nn * esz * nranks, owned);
+  }
+  jws.a = d_m;
+  jws.diagbuf = dalloc<double>((size_t)2 * np * 3 * esz, owned);
+  jws.log = dalloc<double>(dev::jacobi_log_elems((int)n, max_sweeps_cap) * esz, owned);
+  jws.v = dalloc<double>(nn * esz, owned);
+  jws.status = dalloc<DevStatus>(1, owned);
+  d_perm = dalloc<int>(n, owned);
+  d_lam_hi = dalloc<double>(n, owned);
+  d_lam_lo = dalloc<double>(n, owned);
+  d_sigma_tmp = dalloc<double>(n, owned);
+  d_w = dalloc<double>(nn, owned);  // W^T in working precision (<= 8 bytes/elt)
+  d_vwork_tmp = dalloc<double>(nn, owned);
+  check(cudaMallocHost(&h_status, sizeof(DevStatus)), "cudaMallocHost status");
+  check(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "stream");
+  for (auto& e : ev) check(cudaEventCreate(&e), "event");
+}
+
+Plan::~Plan() {
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (own_stream) cudaStreamDestroy(own_stream);
+  if (h_status) cudaFreeHost(h_status);
+  for (void* p : owned) cudaFree(p);
+}
+
+void Plan::set_jacobi(double t, int sweeps) {
+  if (sweeps < 1) throw std::invalid_argument("max_sweeps must be >= 1");
+  if (sweeps > max_sweeps_cap) throw std::invalid_argument("max_sweeps above the plan's log capacity (30)");
+  tol = t;
+  max_sweeps = sweeps;
+}
+
+double Plan::effective_tol() const {
+  if (tol > 0.0) return tol;
+  return (double)n * (dd ? 0x1p-104 : 0x1p-53);  // jacobi.cpp:579-580; u_dd = 2^-104
+}
+
+void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
+  const int nranks = comm ? comm->nranks : 1;
+  void* target = nranks > 1 ? d_mloc : d_m;
+  if (nblocks == 0) {
+    check(cudaMemsetAsync(target, 0, (size_t)n * n * sizeof(double) * (dd ? 2 : 1), st), "memset M");
+  } else if (dd) {
+    check(dev::launch_gram_dd((const double*)d_a, lda, (int)n, d_tiles, ntp, d_splits, (int)splits.size(),
+                              (double2*)d_partials, st),
+          "gram_dd");
+    check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, d_bsb, nblocks,
+                                      (double2*)target, nullptr, st),
+          "gram_combine_dd");
+    launches += 2;
+  } else {
+    check(dev::launch_gram_f32((const float*)d_a, lda, (int)n, d_tiles, ntp, d_splits, (int)splits.size(),
+                               (double*)d_partials, st),
+          "gram_f32");
+    check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks, (double*)target,
+                                       nullptr, st),
+          "gram_combine_f64");
+    launches += 2;
+  }
+  if (nranks > 1) {
+    auto& a = nccl::api();
+    const size_t nn = (size_t)n * n;
+    if (!dd) {
+      // fp64: one all-reduce of the partial Grams (north_star (4)); the
+      // result is re-symmetrised because a ring reduction may order the two
+      // triangles' additions differently.
+      nccl::check(a.AllReduce(d_mloc, d_m, nn, nccl::ncclFloat64, nccl::ncclSum, comm->comm, st), "AllReduce");
+      check(dev::launch_mirror_upper((double*)d_m, (int)n, st), "mirror");
+      launches += 1;
+    } else {
+      // double-double: a plain NCCL sum would drop the lo words; gather every
+      // rank's (hi, lo) partial and add them in rank order with dd_add.
+      nccl::check(a.AllGather(d_mloc, d_gather, nn * 2, nccl::ncclFloat64, comm->comm, st), "AllGather");
+      check(dev::launch_block_tree(d_gather, comm->nranks, (int)n, d_m, true, st), "rank combine");
+      launches += 1;
+    }
+  }
+}
+
+void Plan::eigen(cudaStream_t st) {
+  check(dev::launch_jacobi(dd, (int)n, effective_tol(), max_sweeps, jws, sm_count, st), "jacobi");
+  check(dev::launch_jacobi_replay(dd, (int)n, jws, st), "jacobi_replay");
+  launches += 2;
+}
+
+void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
+                   cudaStream_t st) {
+  if (!st) st = own_stream;
+  last_stream = st;
+  launches = 0;
+  check(cudaMemsetAsync(jws.status, 0, sizeof(DevStatus), st), "status reset");
+  check(cudaEventRecord(ev[0], st), "event");
+  gram(d_a, lda, st);
+  check(cudaEventRecord(ev[1], st), "event");
+  eigen(st);
+  double* sig = d_sigma ? (double*)d_sigma : d_sigma_tmp;
+  void* vw = d_v ? d_v : d_vwork_tmp;
+  check(dev::launch_finish(dd, (int)n, jws, d_perm, d_lam_hi, d_lam_lo, sig, vw, d_w, dd ? 1 : 0, st),
+        "finish");
+  launches += 2;
+  check(cudaEventRecord(ev[2], st), "event");
+  if (d_u && m > 0) {
+    if (dd)
+      check(dev::launch_av_f64((const double*)d_a, lda, m, (int)n, (const double*)d_w, (double*)d_u, ldu,
+                               jws.status, st),
+            "av_f64");
+    else
+      check(dev::launch_av_f32((const float*)d_a, lda, m, (int)n, (const float*)d_w, (float*)d_u, ldu,
+                               jws.status, st),
+            "av_f32");
+    launches += 1;
+  }
+  check(cudaEventRecord(ev[3], st), "event");
+  events_recorded = true;
+  check(cudaMemcpyAsync(h_status, jws.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status D2H");
+}
+
+void Plan::reset_status(cudaStream_t st) {
+  last_stream = st;
+  events_recorded = false;
+  check(cudaMemsetAsync(jws.status, 0, sizeof(DevStatus), st), "status reset");
+}
+
+void Plan::fetch_status(cudaStream_t st) {
+  check(cudaMemcpyAsync(h_status, jws.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status D2H");
+}
+
+mpsvd_exec_info Plan::wait() {
+  check(cudaStreamSynchronize(last_stream ? last_stream : own_stream), "stream sync");
+  mpsvd_exec_info info;
+  std::memset(&info, 0, sizeof(info));
+  info.status = h_status->status;
+  info.error_index = h_status->index;
+  info.error_value = h_status->value;
+  info.sweeps = h_status->sweeps;
+  info.rotations = h_status->rotations;
+  if (events_recorded) {
+    float ms = 0;
+    check(cudaEventElapsedTime(&ms, ev[0], ev[1]), "event time");
+    info.ms_gram = ms;
+    check(cudaEventElapsedTime(&ms, ev[1], ev[2]), "event time");
+    info.ms_eigen = ms;
+    check(cudaEventElapsedTime(&ms, ev[2], ev[3]), "event time");
+    info.ms_compute_u = ms;
+  }
+  info.kernel_launches = launches;
+  return info;
+}
+
+}  // namespace engine
+}  // namespace mpsvd

@@ -1,0 +1,77 @@
+// Host orchestrator interface (engine.cu); used by api.cpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "kernels.h"
+#include "mpsvd.h"
+
+namespace mpsvd {
+namespace engine {
+
+struct Comm;
+
+void check(cudaError_t e, const char* what);
+bool device_available();
+void comm_unique_id(unsigned char id[128]);
+Comm* comm_init(const unsigned char id[128], int nranks, int rank);
+void comm_destroy(Comm* c);
+
+class Plan {
+ public:
+  Plan(long long m_local, long long n, bool f64_working, Comm* comm);
+  ~Plan();
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  void set_jacobi(double tol, int max_sweeps);
+  // Enqueue the whole pipeline on `st` (nullptr: the plan's stream).
+  void execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
+               cudaStream_t st);
+  mpsvd_exec_info wait();
+  // status word handling around hand-assembled stage sequences
+  void reset_status(cudaStream_t st);
+  void fetch_status(cudaStream_t st);
+
+  // stages (used by execute and by the stage-level entry points)
+  void gram(const void* d_a, long long lda, cudaStream_t st);
+  void eigen(cudaStream_t st);
+  double effective_tol() const;
+
+  long long m, n;
+  bool dd;
+  Comm* comm;
+  int device = 0, sm_count = 148, gram_occupancy = 3;
+  double tol = 0.0;
+  int max_sweeps = 30;
+  static constexpr int max_sweeps_cap = 30;
+
+  std::vector<int2> tiles;
+  std::vector<longlong2> splits;
+  std::vector<int> block_split_begin;
+  int ntp = 0, nblocks = 0;
+
+  int2* d_tiles = nullptr;
+  longlong2* d_splits = nullptr;
+  int* d_bsb = nullptr;
+  double* d_partials = nullptr;
+  double* d_m = nullptr;       // n x n higher precision (f64 or dd as double2)
+  double* d_mloc = nullptr;    // rank-local partial (N > 1)
+  double* d_gather = nullptr;  // all-gathered partials (dd, N > 1)
+  dev::JacobiWorkspace jws{};
+  int* d_perm = nullptr;
+  double *d_lam_hi = nullptr, *d_lam_lo = nullptr, *d_sigma_tmp = nullptr;
+  double* d_w = nullptr;
+  double* d_vwork_tmp = nullptr;
+  dev::DevStatus* h_status = nullptr;
+  cudaStream_t own_stream = nullptr, last_stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int launches = 0;
+  bool events_recorded = false;
+  std::vector<void*> owned;
+};
+
+}  // namespace engine
+}  // namespace mpsvd

@@ -1,0 +1,62 @@
+// Launchers of the sm_100a kernels (host-callable; implemented in *.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace mpsvd {
+namespace dev {
+
+struct DevStatus;
+
+// gram.cu --------------------------------------------------------------------
+size_t gram_smem_bytes(bool dd);
+cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* tiles, int ntp,
+                            const longlong2* splits, int nsplit, double* partials,
+                            cudaStream_t st);
+cudaError_t launch_gram_dd(const double* a, long long lda, int n, const int2* tiles, int ntp,
+                           const longlong2* splits, int nsplit, double2* partials,
+                           cudaStream_t st);
+cudaError_t launch_gram_combine_f64(const double* partials, int ntp, int n,
+                                    const int* block_split_begin, int nblocks, double* m_out,
+                                    double* block_out, cudaStream_t st);
+cudaError_t launch_gram_combine_dd(const double2* partials, int ntp, int n,
+                                   const int* block_split_begin, int nblocks, double2* m_out,
+                                   double2* block_out, cudaStream_t st);
+cudaError_t launch_mirror_upper(double* m, int n, cudaStream_t st);
+cudaError_t launch_block_tree(const void* blocks, int nblocks, int n, void* m_out, bool dd,
+                              cudaStream_t st);
+
+// jacobi.cu ------------------------------------------------------------------
+// A (n x n, full symmetric, column-major; f64 or dd=double2) is overwritten:
+// on success its diagonal holds the eigenvalues. The rotation log receives
+// (c, s) per pair per round; V is rebuilt from it by launch_jacobi_replay.
+struct JacobiWorkspace {
+  void* a;            // n*n elements of T
+  void* diagbuf;      // 2 * np * 3 elements of T
+  void* log;          // max_sweeps * (N-1) * np * 2 elements of T
+  void* v;            // n*n elements of T (replay output)
+  DevStatus* status;
+};
+size_t jacobi_log_elems(int n, int max_sweeps);
+cudaError_t launch_jacobi(bool dd, int n, double tol, int max_sweeps, const JacobiWorkspace& ws,
+                          int sm_count, cudaStream_t st);
+cudaError_t launch_jacobi_replay(bool dd, int n, const JacobiWorkspace& ws, cudaStream_t st);
+
+// finish: sort, sign, sigma, V in working precision, W = V / sigma.
+// working: 0 = fp32 (sigma = fl32(sqrt(lambda))), 1 = fp64 (sigma = fl64(sqrt_dd(lambda))).
+cudaError_t launch_finish(bool dd, int n, const JacobiWorkspace& ws, int* perm, double* lambda_hi,
+                          double* lambda_lo, double* sigma, void* v_work, void* w_work,
+                          int working_f64, cudaStream_t st, void* v_full = nullptr);
+
+// compute_u.cu ----------------------------------------------------------------
+cudaError_t launch_av_f32(const float* a, long long lda, long long m, int n, const float* w,
+                          float* u, long long ldu, const DevStatus* status, cudaStream_t st);
+cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w,
+                          double* u, long long ldu, const DevStatus* status, cudaStream_t st);
+
+// microbench.cu ---------------------------------------------------------------
+double measure_fp64_peak_tflops(int device);
+
+}  // namespace dev
+}  // namespace mpsvd

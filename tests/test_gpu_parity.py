@@ -1,0 +1,216 @@
+"""GPU parity tests: every call goes through the C-ABI library
+(libmpsvd_b200.so) on the B200 and is checked against the CPU oracles
+(oracle/_port restatement, pinned to the reference; oracle/_ref, the
+reference itself, when present)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import U32, U64, UDD, dd_diff, kappa_b, max_rel, north_star_gates, orth_err, rowwise_backward, stacked_diag
+
+pytestmark = pytest.mark.gpu
+
+M = pytest.importorskip("paper_2603_11953_b200")
+from paper_2603_11953_b200 import inputs  # noqa: E402
+
+if not M.device_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import pyoracle  # noqa: E402
+
+SEM_DEVICE = pyoracle.SEM_DEVICE
+
+
+def rng_matrix(m, n, seed, dtype=np.float32, scale_decades=0.0):
+    r = np.random.default_rng(seed)
+    a = r.uniform(-1.0, 1.0, size=(n, m))
+    if scale_decades:
+        a *= 10.0 ** (-scale_decades * np.arange(n) / max(n - 1, 1))[:, None]
+    return np.asfortranarray(a.T.astype(dtype))
+
+
+# ---------------------------------------------------------------------------
+# K1: fp32 -> fp64 Gram
+@pytest.mark.parametrize("m,n", [(1, 1), (7, 3), (37, 5), (300, 24), (1024, 64), (5000, 100), (4096, 128),
+                                 (2000, 200), (65, 65)])
+def test_gram_f32_matches_reference(port, m, n):
+    a = rng_matrix(m, n, seed=m + n)
+    g = M.gram(a)
+    ref = port.partitioned_gram_f32(a, blocks=min(16, m))
+    # exact symmetry by construction (parallel_gram.cpp:28-29)
+    assert np.array_equal(g, g.T)
+    # test_parallel_gram.cpp:74-86 criterion
+    assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 10.0 * m * U64
+    # entrywise: both sums are within m*u_h*||a_i|| ||a_j|| of the exact one
+    d = np.sqrt(np.diag(ref))
+    assert np.all(np.abs(g - ref) <= 2.0 * m * U64 * np.outer(d, d) + 1e-300)
+
+
+def test_gram_f32_large_rows(port):
+    a = inputs.make(inputs.CONFIGS["c1"], seed=3)  # 20000 x 32 graded
+    g = M.gram(a)
+    ref = port.partitioned_gram_f32(a, blocks=16)
+    d = np.sqrt(np.diag(ref))
+    assert np.all(np.abs(g - ref) <= 2.0 * a.shape[0] * U64 * np.outer(d, d))
+    assert np.array_equal(g, g.T)
+
+
+# K2: fp64 -> double-double Gram
+@pytest.mark.parametrize("m,n", [(1, 1), (9, 4), (300, 24), (2048, 64), (3000, 130)])
+def test_gram_dd_matches_oracle(port, m, n):
+    a = rng_matrix(m, n, seed=7 * m + n, dtype=np.float64, scale_decades=6.0)
+    hi, lo = M.gram(a)
+    rh, rl = port.dd_gram(a)
+    assert np.array_equal(hi, hi.T) and np.array_equal(lo, lo.T)
+    an = np.sqrt(np.einsum("ij,ij->j", a, a))
+    # Dot2 / dd_add accumulation: error <= ~(m u)^2 * sum|a_i a_j| <= (m u)^2 ||a_i|| ||a_j||
+    bound = 4.0 * (m * U64) ** 2 * np.outer(an, an) + 8.0 * UDD * np.abs(rh)
+    assert np.all(dd_diff(hi, lo, rh, rl) <= bound)
+
+
+# ---------------------------------------------------------------------------
+# K4: fp64 Jacobi — bitwise against the device-semantics restatement
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 24, 64, 101, 128, 129, 200, 256])
+def test_jacobi_f64_bitwise_vs_restatement(port, n):
+    a = rng_matrix(3 * n + 5, n, seed=n, dtype=np.float64, scale_decades=3.0)
+    g = a.T @ a
+    g = (g + g.T) / 2
+    lam, v, sw, rot = M.twosided_jacobi_eig(g)
+    plam, pv, psw, prot = port.twosided_jacobi(g, sem=SEM_DEVICE)
+    assert (sw, rot) == (psw, prot)
+    assert np.array_equal(lam, plam)
+    assert np.array_equal(v, pv)
+    # and within rounding of the reference's cyclic order
+    rlam, rv, _, _ = port.twosided_jacobi(g)
+    assert max_rel(lam, rlam) <= 1e3 * n * U64 * np.linalg.cond(a) ** 2
+
+
+def test_jacobi_golden_examples():
+    # proj/tests/test_jacobi.cpp:184-207
+    lam, v, _, _ = M.twosided_jacobi_eig(np.diag([4.0, 1.0]))
+    assert list(lam) == [4.0, 1.0] and v[0, 0] == 1.0 and v[1, 1] == 1.0
+    lam, v, _, _ = M.twosided_jacobi_eig(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    isq = 1.0 / np.sqrt(2.0)
+    assert lam[0] == pytest.approx(3.0, rel=1e-15) and lam[1] == pytest.approx(1.0, rel=1e-15)
+    assert v[0, 0] == pytest.approx(isq, rel=1e-15) and v[1, 0] == pytest.approx(isq, rel=1e-15)
+    assert v[0, 1] == pytest.approx(isq, rel=1e-15) and v[1, 1] == pytest.approx(-isq, rel=1e-15)
+
+
+def test_jacobi_hilbert_vs_dd_bisection(ref):
+    # proj/tests/test_jacobi.cpp:209-227
+    h = np.array([[1.0 / (i + j + 1) for j in range(4)] for i in range(4)])
+    lam, _, _, _ = M.twosided_jacobi_eig(h)
+    oracle = ref.dd_oracle_eigenvalues(h)
+    bh = h / np.sqrt(np.outer(np.diag(h), np.diag(h)))
+    bl = ref.dd_oracle_eigenvalues(bh)
+    assert max_rel(lam, oracle) <= 1e3 * U64 * bl[0] / bl[-1]
+
+
+def test_jacobi_errors():
+    # NPD paths (test_jacobi.cpp:245-262)
+    with pytest.raises(M.NotPositiveDefiniteError) as e:
+        M.twosided_jacobi_eig(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    assert e.value.index == 1
+    with pytest.raises(M.NotPositiveDefiniteError):
+        M.twosided_jacobi_eig(np.array([[-1.0]]))
+    with pytest.raises(M.NoConvergenceError):
+        g = rng_matrix(40, 20, 1, np.float64)
+        M.twosided_jacobi_eig(g.T @ g, max_sweeps=1)
+
+
+# K5: double-double Jacobi — bitwise against the restatement
+@pytest.mark.parametrize("n", [2, 7, 32, 90, 120])
+def test_jacobi_dd_bitwise_vs_restatement(port, n):
+    a = rng_matrix(2 * n + 3, n, seed=100 + n, dtype=np.float64, scale_decades=8.0)
+    hi, lo = port.dd_gram(a)
+    (lh, ll), (vh, vl), sw, rot = M.twosided_jacobi_eig(hi, lo, dd=True)
+    (plh, pll), (pvh, pvl), psw, prot = port.twosided_jacobi_dd(hi, lo, sem=SEM_DEVICE)
+    assert (sw, rot) == (psw, prot)
+    assert np.array_equal(lh, plh) and np.array_equal(ll, pll)
+    assert np.array_equal(vh, pvh) and np.array_equal(vl, pvl)
+
+
+# ---------------------------------------------------------------------------
+# Full pipeline through mpsvd_thin_svd
+def test_thin_svd_stacked_diagonal_exact():
+    # proj/tests/test_thinsvd.cpp:70-84, proj/tests/test_capi.cpp:164-188
+    a = stacked_diag(4, [5.0, 3.0])
+    r = M.mp_thin_svd(a)
+    assert list(r.sigma) == [5.0, 3.0]
+    assert np.array_equal(r.v, np.eye(2, dtype=np.float32))
+    assert np.array_equal(r.u, stacked_diag(4, [1.0, 1.0]))
+    assert r.gram_sync_events == 1
+    t = r.times
+    assert min(t.gram, t.eigen, t.compute_u, t.overlap) >= 0.0
+    assert abs(t.gram + t.eigen + t.compute_u + t.overlap - t.total) <= 1e-9 + 1e-6 * t.total
+
+
+def test_thin_svd_graded_suite_instance(ref):
+    # proj/tests/test_thinsvd.cpp:103-132 (build_problem {1024,64,1e8,1e3,3,5})
+    a, _, kb = ref.build_problem(1024, 64, 1e8, 1e3, 3, 5)
+    oracle = ref.reference_svd(a)
+    r = M.mp_thin_svd(a)
+    high_acc = 100.0 * (U32 + U64 * kb * kb)
+    assert max_rel(r.sigma, oracle) <= high_acc
+    assert rowwise_backward(a, r.u, r.sigma, r.v) <= 100.0 * 8.0 * U32
+    assert orth_err(r.u) <= 100.0 * (8.0 * U32 + 64.0 * high_acc)
+    assert orth_err(r.v) <= 100.0 * 64.0 * U64 + 64.0 * U32
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_thin_svd_config_c1(port, seed):
+    cfg = inputs.CONFIGS["c1"]
+    a = inputs.make(cfg, seed=seed)
+    r = M.mp_thin_svd(a)
+    o = port.thin_svd(a, threads=8)
+    kb = kappa_b(a)
+    g_sigma, g_orth = north_star_gates(cfg.n, U32, kb)
+    assert max_rel(r.sigma, o.sigma) <= g_sigma
+    assert orth_err(r.v) <= g_orth
+    assert orth_err(r.u) <= g_orth
+    assert rowwise_backward(a, r.u, r.sigma, r.v) <= 100.0 * np.sqrt(cfg.n) * U32
+
+
+def test_thin_svd_tiny_sigma():
+    # proj/tests/test_thinsvd.cpp:244-264; test_capi.cpp:220-225
+    a = stacked_diag(2, [1.0, 1e-39])
+    with pytest.raises(M.TinySingularValueError) as e:
+        M.mp_thin_svd(a)
+    assert e.value.index == 2
+
+
+def test_thin_svd_argument_validation():
+    # proj/tests/test_thinsvd.cpp:266-276
+    with pytest.raises(M.InvalidArgument):
+        M.mp_thin_svd(np.eye(2))  # f64 input rejected
+    with pytest.raises(M.InvalidArgument):
+        M.mp_thin_svd(np.zeros((2, 3), np.float32))
+    with pytest.raises(M.InvalidArgument):
+        M.mp_thin_svd(np.eye(2, dtype=np.float32), threads=0)
+
+
+def test_thin_svd_device_semantics_bitwise(port):
+    """Given the device's own Gram, the whole downstream pipeline (Jacobi,
+    sort/sign, sigma, W, U) is bit-identical to the restatement."""
+    a = inputs.make(inputs.CONFIGS["c1"], seed=5, m=4096)
+    r = M.mp_thin_svd(a)
+    g = M.gram(a)
+    lam, v, _, _ = port.twosided_jacobi(g, sem=SEM_DEVICE)
+    sigma = np.sqrt(lam).astype(np.float32).astype(np.float64)
+    assert np.array_equal(r.sigma, sigma)
+    assert np.array_equal(r.v, v.astype(np.float32))
+    w = v.astype(np.float32) / sigma.astype(np.float32)[None, :]
+    assert np.array_equal(r.u, port.av_f32(a, w))
+
+
+def test_thin_svd_f64_dd_small(port):
+    cfg = inputs.CONFIGS["c3"]
+    a = inputs.make(cfg, seed=2, m=4096)[:, :64].copy(order="F")
+    r = M.mp_thin_svd_f64(a)
+    o = port.thin_svd_f64dd(a, threads=8)
+    kb = kappa_b(a)
+    g_sigma, g_orth = north_star_gates(64, U64, kb)
+    assert max_rel(r.sigma, o.sigma) <= g_sigma
+    assert orth_err(r.v) <= g_orth
+    assert orth_err(r.u) <= g_orth
