@@ -196,8 +196,13 @@ def run_ours(args, cfg):
     sig_t = torch.empty(n, dtype=torch.float64, device=dev)
     v_t = torch.empty((n, n), dtype=a_t.dtype, device=dev)
     plan = M.Plan(m_local, n, working, comm)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-legacy) stream: the plan enqueues every kernel on it and
+    # the CUDA events below are recorded on the same stream
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
+    torch.cuda.synchronize()
 
     def step():
         plan.execute(a_t.data_ptr(), m_local, u_t.data_ptr(), m_local, sig_t.data_ptr(), v_t.data_ptr(), sptr)

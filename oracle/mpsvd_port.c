@@ -188,10 +188,6 @@ static void descending_perm_f64(const double* vals, int64_t n, int64_t* perm) {
 }
 
 /* Device-semantics helpers: the exact expressions the CUDA kernels evaluate. */
-static inline double dev_hyp1(double z) {
-  const double az = fabs(z);
-  return az < 0x1p500 ? sqrt(fma(z, z, 1.0)) : az;
-}
 static inline double rot_lo(double c, double s, double x, double y) { return fma(c, x, -(s * y)); }
 static inline double rot_hi(double c, double s, double x, double y) { return fma(s, x, c * y); }
 
@@ -304,13 +300,28 @@ static int jacobi_rr_f64(double* A, double* V, int64_t n, double tol, int max_sw
         T[k] = 0.0;
         if (Q[k] >= n) continue;
         const double aii = AE(P[k], P[k]), ajj = AE(Q[k], Q[k]), aij = AE(P[k], Q[k]);
-        const double thresh = tol * sqrt(aii) * sqrt(ajj);
-        const double ratio = fabs(aij) / sqrt(aii * ajj);
-        if (worst < ratio) worst = ratio;
+        /* device formula (jacobi.cu Arith<double>::rotation) */
+        const double pr = aii * ajj;
+        const double thresh = (pr > 0x1p-1000 && pr < 0x1p1000) ? tol * sqrt(pr) : tol * sqrt(aii) * sqrt(ajj);
+        if (sweep + 1 == max_sweeps) {
+          const double ratio = fabs(aij) / sqrt(pr);
+          if (worst < ratio) worst = ratio;
+        }
         if (fabs(aij) <= thresh) continue;
-        const double zeta = (ajj - aii) / (2.0 * aij);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + dev_hyp1(zeta));
-        const double c = 1.0 / dev_hyp1(t);
+        const double x = ajj - aii, y = 2.0 * aij, ax = fabs(x);
+        const double big = fmax(ax, fabs(y));
+        double r;
+        if (big < 0x1p500 && big > 0x1p-500) {
+          r = sqrt(fma(x, x, y * y));
+        } else {
+          int e;
+          frexp(big, &e);
+          const double xs = ldexp(x, -e), ys = ldexp(y, -e);
+          r = ldexp(sqrt(fma(xs, xs, ys * ys)), e);
+        }
+        const double den = ax + r;
+        const double t = x == 0.0 ? 1.0 : (x > 0.0 ? y : -y) / den;
+        const double c = sqrt(den / (2.0 * r));
         C[k] = c;
         S[k] = c * t;
         T[k] = t;
@@ -735,6 +746,44 @@ static int dd_make_rotation(dd aii, dd ajj, dd aij, dd tol, double* worst, dd_ro
   return 1;
 }
 
+/* Device formula (jacobi.cu Arith<double2>::rotation). */
+static int dd_make_rotation_dev(dd aii, dd ajj, dd aij, double tol, double* worst, int want_ratio,
+                                dd_rot* r) {
+  const double pr = aii.hi * ajj.hi;
+  const double thresh = (pr > 0x1p-1000 && pr < 0x1p1000) ? tol * sqrt(pr) : tol * sqrt(aii.hi) * sqrt(ajj.hi);
+  if (want_ratio) {
+    const double ratio = fabs(aij.hi) / sqrt(pr);
+    if (*worst < ratio) *worst = ratio;
+  }
+  r->act = 0;
+  r->c = dd_from(1.0);
+  r->s = dd_from(0.0);
+  r->t = dd_from(0.0);
+  if (fabs(aij.hi) <= thresh) return 0;
+  const dd x = dd_sub(ajj, aii), y = dd_scale2(aij), ax = dd_abs(x);
+  const double big = fmax(ax.hi, fabs(y.hi));
+  dd rr;
+  if (big < 0x1p250 && big > 0x1p-250) {
+    rr = dd_sqrt(dd_add(dd_mul(x, x), dd_mul(y, y)));
+  } else {
+    int e;
+    frexp(big, &e);
+    const dd xs = {ldexp(x.hi, -e), ldexp(x.lo, -e)};
+    const dd ys = {ldexp(y.hi, -e), ldexp(y.lo, -e)};
+    const dd rs = dd_sqrt(dd_add(dd_mul(xs, xs), dd_mul(ys, ys)));
+    rr = (dd){ldexp(rs.hi, e), ldexp(rs.lo, e)};
+  }
+  const dd den = dd_add(ax, rr);
+  const dd t = x.hi == 0.0 ? dd_from(1.0) : dd_div(x.hi > 0.0 ? y : dd_neg(y), den);
+  const dd c = dd_sqrt(dd_div(den, dd_scale2(rr)));
+  r->c = c;
+  r->s = dd_mul(c, t);
+  r->t = t;
+  r->act = 1;
+  return 1;
+}
+
+
 static inline dd ddrot_lo(dd c, dd s, dd x, dd y) { return dd_sub(dd_mul(c, x), dd_mul(s, y)); }
 static inline dd ddrot_hi(dd c, dd s, dd x, dd y) { return dd_add(dd_mul(s, x), dd_mul(c, y)); }
 
@@ -799,8 +848,8 @@ static int jacobi_rr_dd(dd* A, dd* V, int64_t n, dd tol, int max_sweeps,
         port_rr_pair(n, r, k, &P[k], &Q[k]);
         R[k].act = 0;
         if (Q[k] >= n) continue;
-        rot_in_sweep += dd_make_rotation(AE(P[k], P[k]), AE(Q[k], Q[k]), AE(P[k], Q[k]), tol,
-                                         &worst, &R[k]);
+        rot_in_sweep += dd_make_rotation_dev(AE(P[k], P[k]), AE(Q[k], Q[k]), AE(P[k], Q[k]), tol.hi,
+                                             &worst, sweep + 1 == max_sweeps, &R[k]);
       }
       for (int64_t a = 0; a < np; ++a)
         for (int64_t b = a + 1; b < np; ++b) {

@@ -2,70 +2,90 @@
 //
 // Reference semantics: matmul(a, scale_columns(v, sigma, invert))
 // (proj/src/thinsvd.cpp:110-113, proj/src/dense.cpp:83-96,214-232): W is
-// formed first (true division, done by finish_columns in jacobi.cu, stored
-// row-major "W^T" so every CTA stages it with straight coalesced copies),
-// then every U entry accumulates A(i,l)*W(l,j) over ascending l. Here each
-// entry is one fma chain over ascending l (the reference's x86 build rounds
-// the product and the sum separately; both are the same order).
+// formed first (true division, done by finish_columns in jacobi.cu and stored
+// row-major "W^T" with a 16-byte aligned leading dimension), then every U
+// entry accumulates A(i,l)*W(l,j) over ascending l. Here each entry is one
+// fma chain over ascending l (the reference's x86 build rounds the product
+// and the sum separately; same order).
 //
-// Tiling: a CTA owns BM=128 rows x NB output columns; A and W^T are staged
-// through shared memory in BK=32 slices with a register prefetch of the next
-// slice; each thread keeps a TM x TN register tile. A is streamed exactly
-// once per column block (once in total for n <= NB) and U written once.
+// Tiling: a CTA owns BM rows x NB output columns (NB >= n for n <= 128, so A
+// is streamed from HBM exactly once and U written once); A and W^T slices of
+// BK columns are staged into shared memory by cp.async (16-byte LDGSTS,
+// zero-filled at the matrix edges) in a two-stage pipeline; each thread keeps
+// a TM x TN register tile and reads its operands with 128-bit shared loads.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace mpsvd {
 namespace dev {
 
-constexpr int kBM = 128;
-constexpr int kBK = 32;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
-template <typename T, int NB, int TM, int TN>
+template <typename T, int NB, int TM, int TN, int BK>
+struct AvShape {
+  static constexpr int CG = NB / TN;  // column groups
+  static constexpr int RG = 256 / CG; // row groups
+  static constexpr int BM = RG * TM;  // rows per CTA
+  static constexpr int V = 16 / sizeof(T);
+  static constexpr size_t smem = 2 * (size_t)BK * (BM + NB) * sizeof(T);
+};
+
+// kAsync: 16-byte cp.async staging (needs lda % V == 0 and a 16-byte aligned A).
+template <typename T, int NB, int TM, int TN, int BK, bool kAsync>
 __global__ void __launch_bounds__(256)
-av_kernel(const T* __restrict__ a, long long lda, long long m, int n, const T* __restrict__ wt,
+av_kernel(const T* __restrict__ a, long long lda, long long m, int n, const T* __restrict__ wt, int ldw,
           T* __restrict__ u, long long ldu, const DevStatus* __restrict__ status) {
-  static_assert((kBM / TM) * (NB / TN) == 256, "256 threads");
+  using S = AvShape<T, NB, TM, TN, BK>;
+  constexpr int BM = S::BM, V = S::V;
   if (status && status->status != kOk) return;
   extern __shared__ __align__(16) unsigned char avsm[];
-  T* as = reinterpret_cast<T*>(avsm);  // [2][kBK][kBM]
-  T* ws = as + 2 * kBK * kBM;          // [2][kBK][NB]
+  T* as = reinterpret_cast<T*>(avsm);  // [2][BK][BM]
+  T* ws = as + 2 * BK * BM;            // [2][BK][NB]
   const int tid = threadIdx.x;
-  const int tx = tid % (NB / TN), ty = tid / (NB / TN);
-  const long long r0 = (long long)blockIdx.x * kBM;
+  const int tx = tid % S::CG, ty = tid / S::CG;
+  const long long r0 = (long long)blockIdx.x * BM;
   const int c0 = blockIdx.y * NB;
 
-  constexpr int kAPer = kBK * kBM / 256;  // 16
-  constexpr int kWPer = kBK * NB / 256;   // NB/8
-  T pa[kAPer], pw[kWPer];
-  auto load = [&](int l0) {
-#pragma unroll
-    for (int it = 0; it < kAPer; ++it) {
-      const int e = it * 256 + tid;
-      const int kk = e / kBM, i = e % kBM;
-      const long long row = r0 + i;
-      const int l = l0 + kk;
-      pa[it] = (row < m && l < n) ? a[(long long)l * lda + row] : T(0);
+  auto issue = [&](int l0, int buf) {
+    T* ad = as + buf * BK * BM;
+    T* wd = ws + buf * BK * NB;
+    if (kAsync) {
+      constexpr int AV = BK * BM / V;  // 16-byte vectors of the A slice
+      for (int e = tid; e < AV; e += 256) {
+        const int kk = e / (BM / V), iv = e - kk * (BM / V);
+        const long long row = r0 + (long long)iv * V;
+        const int l = l0 + kk;
+        long long rem = (m - row) * (long long)sizeof(T);
+        int bytes = (l < n && rem > 0) ? (rem >= 16 ? 16 : (int)rem) : 0;
+        const T* src = bytes ? a + (long long)l * lda + row : a;
+        cp_async16(ad + kk * BM + iv * V, src, bytes);
+      }
+    } else {
+      for (int e = tid; e < BK * BM; e += 256) {
+        const int kk = e / BM, i = e - kk * BM;
+        const long long row = r0 + i;
+        const int l = l0 + kk;
+        ad[kk * BM + i] = (l < n && row < m) ? a[(long long)l * lda + row] : T(0);
+      }
     }
-#pragma unroll
-    for (int it = 0; it < kWPer; ++it) {
-      const int e = it * 256 + tid;
-      const int kk = e / NB, j = e % NB;
-      const int l = l0 + kk, col = c0 + j;
-      pw[it] = (l < n && col < n) ? wt[(long long)l * n + col] : T(0);
+    constexpr int WV = BK * NB / V;
+    for (int e = tid; e < WV; e += 256) {
+      const int kk = e / (NB / V), jv = e - kk * (NB / V);
+      const int l = l0 + kk, col = c0 + jv * V;
+      const int rem = (n - col) * (int)sizeof(T);
+      const int bytes = (l < n && rem > 0) ? (rem >= 16 ? 16 : rem) : 0;
+      const T* src = bytes ? wt + (long long)l * ldw + col : wt;
+      cp_async16(wd + kk * NB + jv * V, src, bytes);
     }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int it = 0; it < kAPer; ++it) {
-      const int e = it * 256 + tid;
-      as[buf * kBK * kBM + e] = pa[it];
-    }
-#pragma unroll
-    for (int it = 0; it < kWPer; ++it) {
-      const int e = it * 256 + tid;
-      ws[buf * kBK * NB + e] = pw[it];
-    }
+    cp_async_commit();
   };
 
   T acc[TM][TN];
@@ -74,67 +94,92 @@ av_kernel(const T* __restrict__ a, long long lda, long long m, int n, const T* _
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
 
-  const int nchunks = (n + kBK - 1) / kBK;
-  load(0);
-  store(0);
-  __syncthreads();
+  const int nchunks = (n + BK - 1) / BK;
+  issue(0, 0);
   for (int ch = 0; ch < nchunks; ++ch) {
     const int cur = ch & 1;
-    const bool more = ch + 1 < nchunks;
-    if (more) load((ch + 1) * kBK);
-    const T* ac = as + cur * kBK * kBM;
-    const T* wc = ws + cur * kBK * NB;
-    const int kmax = min(kBK, n - ch * kBK);
+    if (ch + 1 < nchunks) {
+      issue((ch + 1) * BK, cur ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const T* ac = as + cur * BK * BM + ty * TM;
+    const T* wc = ws + cur * BK * NB + tx * TN;
+    const int kmax = min(BK, n - ch * BK);
+#pragma unroll 4
     for (int k = 0; k < kmax; ++k) {
       T av[TM], wv[TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) av[i] = ac[k * kBM + ty * TM + i];
+      for (int i = 0; i < TM; i += V) *reinterpret_cast<float4*>(&av[i]) = *reinterpret_cast<const float4*>(ac + k * BM + i);
 #pragma unroll
-      for (int j = 0; j < TN; ++j) wv[j] = wc[k * NB + tx * TN + j];
+      for (int j = 0; j < TN; j += V) *reinterpret_cast<float4*>(&wv[j]) = *reinterpret_cast<const float4*>(wc + k * NB + j);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], wv[j], acc[i][j]);
     }
-    if (more) store(cur ^ 1);
     __syncthreads();
   }
+  const long long rbase = r0 + (long long)ty * TM;
+  const bool vec_ok = kAsync && (ldu % V == 0) && (rbase + TM <= m);
 #pragma unroll
   for (int j = 0; j < TN; ++j) {
     const int col = c0 + tx * TN + j;
     if (col >= n) continue;
+    T* dst = u + (long long)col * ldu + rbase;
+    if (vec_ok) {
 #pragma unroll
-    for (int i = 0; i < TM; ++i) {
-      const long long row = r0 + ty * TM + i;
-      if (row < m) u[(long long)col * ldu + row] = acc[i][j];
+      for (int i = 0; i < TM; i += V) {
+        T tmp[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) tmp[q] = acc[i + q][j];
+        *reinterpret_cast<float4*>(dst + i) = *reinterpret_cast<const float4*>(tmp);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+        if (rbase + i < m) dst[i] = acc[i][j];
     }
   }
 }
 
-template <typename T, int NB, int TM, int TN>
-static cudaError_t launch_av_t(const T* a, long long lda, long long m, int n, const T* w, T* u,
+template <typename T, int NB, int TM, int TN, int BK>
+static cudaError_t launch_av_t(const T* a, long long lda, long long m, int n, const T* w, int ldw, T* u,
                                long long ldu, const DevStatus* status, cudaStream_t st) {
-  auto k = av_kernel<T, NB, TM, TN>;
-  const size_t smem = 2 * (size_t)kBK * (kBM + NB) * sizeof(T);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)((m + kBM - 1) / kBM), (unsigned)((n + NB - 1) / NB));
-  k<<<grid, 256, smem, st>>>(a, lda, m, n, w, u, ldu, status);
+  using S = AvShape<T, NB, TM, TN, BK>;
+  const bool async_ok = (lda % S::V == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0);
+  dim3 grid((unsigned)((m + S::BM - 1) / S::BM), (unsigned)((n + NB - 1) / NB));
+  if (async_ok) {
+    auto k = av_kernel<T, NB, TM, TN, BK, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
+    k<<<grid, 256, S::smem, st>>>(a, lda, m, n, w, ldw, u, ldu, status);
+  } else {
+    auto k = av_kernel<T, NB, TM, TN, BK, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem);
+    k<<<grid, 256, S::smem, st>>>(a, lda, m, n, w, ldw, u, ldu, status);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_av_f32(const float* a, long long lda, long long m, int n, const float* w,
-                          float* u, long long ldu, const DevStatus* status, cudaStream_t st) {
+
+
+cudaError_t launch_av_f32(const float* a, long long lda, long long m, int n, const float* w, float* u,
+                          long long ldu, const DevStatus* status, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  if (n <= 32) return launch_av_t<float, 32, 4, 4>(a, lda, m, n, w, u, ldu, status, st);
-  if (n <= 64) return launch_av_t<float, 64, 8, 4>(a, lda, m, n, w, u, ldu, status, st);
-  return launch_av_t<float, 128, 8, 8>(a, lda, m, n, w, u, ldu, status, st);
+  const int ldw = av_ldw(n);
+  if (n <= 32) return launch_av_t<float, 32, 8, 8, 16>(a, lda, m, n, w, ldw, u, ldu, status, st);
+  if (n <= 64) return launch_av_t<float, 64, 8, 8, 32>(a, lda, m, n, w, ldw, u, ldu, status, st);
+  return launch_av_t<float, 128, 8, 8, 32>(a, lda, m, n, w, ldw, u, ldu, status, st);
 }
 
-cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w,
-                          double* u, long long ldu, const DevStatus* status, cudaStream_t st) {
+cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w, double* u,
+                          long long ldu, const DevStatus* status, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  if (n <= 32) return launch_av_t<double, 32, 4, 4>(a, lda, m, n, w, u, ldu, status, st);
-  return launch_av_t<double, 64, 8, 4>(a, lda, m, n, w, u, ldu, status, st);
+  const int ldw = av_ldw(n);
+  if (n <= 32) return launch_av_t<double, 32, 8, 4, 16>(a, lda, m, n, w, ldw, u, ldu, status, st);
+  return launch_av_t<double, 64, 8, 4, 32>(a, lda, m, n, w, ldw, u, ldu, status, st);
 }
 
 }  // namespace dev

@@ -193,6 +193,7 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
                    cudaMemcpyHostToDevice),
         "H2D bsb");
   d_partials = dalloc<double>(splits.size() * tiles.size() * 64 * 64 * esz, owned);
+  d_bsums = dalloc<double>((size_t)(nblocks > 0 ? nblocks : 1) * tiles.size() * 64 * 64 * esz, owned);
   d_m = dalloc<double>(nn * esz, owned);
   const int nranks = comm ? comm->nranks : 1;
   if (nranks > 1) {
@@ -200,7 +201,7 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     if (dd) d_gather = dalloc<double>(nn * esz * nranks, owned);
   }
   jws.a = d_m;
-  jws.diagbuf = dalloc<double>((size_t)2 * np * 3 * esz, owned);
+  jws.diagbuf = dalloc<double>((size_t)2 * np * 3 * esz + 2, owned);  // + sweep flags
   jws.log = dalloc<double>(dev::jacobi_log_elems((int)n, max_sweeps_cap) * esz, owned);
   jws.v = dalloc<double>(nn * esz, owned);
   jws.status = dalloc<DevStatus>(1, owned);
@@ -208,7 +209,8 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   d_lam_hi = dalloc<double>(n, owned);
   d_lam_lo = dalloc<double>(n, owned);
   d_sigma_tmp = dalloc<double>(n, owned);
-  d_w = dalloc<double>(nn, owned);  // W^T in working precision (<= 8 bytes/elt)
+  d_w = dalloc<double>((size_t)n * dev::av_ldw((int)n), owned);  // W^T, working precision
+  check(cudaMemset(d_w, 0, (size_t)n * dev::av_ldw((int)n) * sizeof(double)), "memset W");
   d_vwork_tmp = dalloc<double>(nn, owned);
   check(cudaMallocHost(&h_status, sizeof(DevStatus)), "cudaMallocHost status");
   check(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "stream");
@@ -245,17 +247,17 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
                               (double2*)d_partials, st),
           "gram_dd");
     check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, d_bsb, nblocks,
-                                      (double2*)target, nullptr, st),
+                                      (double2*)d_bsums, (double2*)target, st),
           "gram_combine_dd");
-    launches += 2;
+    launches += 3;
   } else {
     check(dev::launch_gram_f32((const float*)d_a, lda, (int)n, d_tiles, ntp, d_splits, (int)splits.size(),
                                (double*)d_partials, st),
           "gram_f32");
-    check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks, (double*)target,
-                                       nullptr, st),
+    check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks,
+                                       (double*)d_bsums, (double*)target, st),
           "gram_combine_f64");
-    launches += 2;
+    launches += 3;
   }
   if (nranks > 1) {
     auto& a = nccl::api();

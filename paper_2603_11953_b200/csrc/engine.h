@@ -57,6 +57,7 @@ class Plan {
   longlong2* d_splits = nullptr;
   int* d_bsb = nullptr;
   double* d_partials = nullptr;
+  double* d_bsums = nullptr;   // per-logical-block sums (combine pass 1)
   double* d_m = nullptr;       // n x n higher precision (f64 or dd as double2)
   double* d_mloc = nullptr;    // rank-local partial (N > 1)
   double* d_gather = nullptr;  // all-gathered partials (dd, N > 1)

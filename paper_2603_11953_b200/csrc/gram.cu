@@ -229,72 +229,63 @@ gram_f64_dd(const double* __restrict__ a, long long lda, int n, const int2* __re
 }
 
 // ---------------------------------------------------------------------------
-// Combine: block sums over their splits (ascending), then the reference's
-// fixed tree over blocks (parallel_gram.cpp:93-102), then mirror.
+// Combine, two coalesced passes:
+//   gram_block_sums: for every (tile pair, tile element, logical block) the
+//                    block's splits summed in ascending order;
+//   gram_tree:       the reference's fixed tree over the block sums
+//                    (parallel_gram.cpp:93-102), written to both triangles.
+template <typename ST>
+__device__ __forceinline__ ST st_add(ST a, ST b);
+template <>
+__device__ __forceinline__ double st_add<double>(double a, double b) { return a + b; }
+template <>
+__device__ __forceinline__ double2 st_add<double2>(double2 a, double2 b) {
+  const dd r = dd_add(dd_make(a.x, a.y), dd_make(b.x, b.y));
+  return make_double2(r.hi, r.lo);
+}
+template <typename ST>
+__device__ __forceinline__ ST st_zero();
+template <>
+__device__ __forceinline__ double st_zero<double>() { return 0.0; }
+template <>
+__device__ __forceinline__ double2 st_zero<double2>() { return make_double2(0.0, 0.0); }
+
+template <typename ST>
+__global__ void __launch_bounds__(256)
+gram_block_sums(const ST* __restrict__ partials, int ntp, const int* __restrict__ block_split_begin,
+                ST* __restrict__ sums) {
+  const int tp = blockIdx.x, b = blockIdx.z;
+  const int e = blockIdx.y * 256 + threadIdx.x;  // tile element, 16 x 256 = 64 x 64
+  const int s0 = block_split_begin[b], s1 = block_split_begin[b + 1];
+  ST acc = st_zero<ST>();
+  for (int sidx = s0; sidx < s1; ++sidx)
+    acc = st_add<ST>(acc, partials[((long long)sidx * ntp + tp) * (kTile * kTile) + e]);
+  sums[((long long)b * ntp + tp) * (kTile * kTile) + e] = acc;
+}
+
 __device__ __forceinline__ int tile_pair_index(int ti, int tj, int T) {
   return ti * T - (ti * (ti - 1)) / 2 + (tj - ti);
 }
 
-__global__ void gram_combine_f64(const double* __restrict__ partials, int ntp, int n,
-                                 const int* __restrict__ block_split_begin, int nblocks,
-                                 double* __restrict__ m_out, double* __restrict__ block_out) {
+template <typename ST>
+__global__ void __launch_bounds__(256)
+gram_tree(const ST* __restrict__ sums, int ntp, int n, int nblocks, ST* __restrict__ m_out) {
   const int T = (n + kTile - 1) / kTile;
-  const long long npairs = (long long)n * (n + 1) / 2;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < npairs;
+  const long long nn = (long long)n * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn;
        e += (long long)gridDim.x * blockDim.x) {
-    // e -> (i, j), i <= j, column-major upper-triangle enumeration
-    int j = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-    while ((long long)j * (j + 1) / 2 > e) --j;
-    while ((long long)(j + 1) * (j + 2) / 2 <= e) ++j;
-    const int i = (int)(e - (long long)j * (j + 1) / 2);
+    const int i = (int)(e / n), j = (int)(e - (long long)i * n);  // row-major walk: coalesced reads
+    if (i > j) continue;
     const int ti = i / kTile, tj = j / kTile;
-    const int tp = tile_pair_index(ti, tj, T);
     const int off = (i - ti * kTile) * kTile + (j - tj * kTile);
-    double slot[16];
-    for (int b = 0; b < nblocks; ++b) {
-      double sum = 0.0;
-      for (int sidx = block_split_begin[b]; sidx < block_split_begin[b + 1]; ++sidx)
-        sum += partials[((long long)sidx * ntp + tp) * (kTile * kTile) + off];
-      slot[b] = sum;
-      if (block_out) block_out[(long long)b * n * n + (long long)j * n + i] = sum;
-    }
+    const long long base = (long long)tile_pair_index(ti, tj, T) * (kTile * kTile) + off;
+    const long long bstride = (long long)ntp * kTile * kTile;
+    ST slot[16];
+    for (int b = 0; b < nblocks; ++b) slot[b] = sums[b * bstride + base];
     for (int width = 1; width < nblocks; width *= 2)
-      for (int b = 0; b + width < nblocks; b += 2 * width) slot[b] += slot[b + width];
+      for (int b = 0; b + width < nblocks; b += 2 * width) slot[b] = st_add<ST>(slot[b], slot[b + width]);
     m_out[(long long)j * n + i] = slot[0];
     m_out[(long long)i * n + j] = slot[0];
-  }
-}
-
-__global__ void gram_combine_dd(const double2* __restrict__ partials, int ntp, int n,
-                                const int* __restrict__ block_split_begin, int nblocks,
-                                double2* __restrict__ m_out, double2* __restrict__ block_out) {
-  const int T = (n + kTile - 1) / kTile;
-  const long long npairs = (long long)n * (n + 1) / 2;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < npairs;
-       e += (long long)gridDim.x * blockDim.x) {
-    int j = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-    while ((long long)j * (j + 1) / 2 > e) --j;
-    while ((long long)(j + 1) * (j + 2) / 2 <= e) ++j;
-    const int i = (int)(e - (long long)j * (j + 1) / 2);
-    const int ti = i / kTile, tj = j / kTile;
-    const int tp = tile_pair_index(ti, tj, T);
-    const int off = (i - ti * kTile) * kTile + (j - tj * kTile);
-    dd slot[16];
-    for (int b = 0; b < nblocks; ++b) {
-      dd sum = dd_from(0.0);
-      for (int sidx = block_split_begin[b]; sidx < block_split_begin[b + 1]; ++sidx) {
-        const double2 v = partials[((long long)sidx * ntp + tp) * (kTile * kTile) + off];
-        sum = dd_add(sum, dd_make(v.x, v.y));
-      }
-      slot[b] = sum;
-      if (block_out)
-        block_out[(long long)b * n * n + (long long)j * n + i] = make_double2(sum.hi, sum.lo);
-    }
-    for (int width = 1; width < nblocks; width *= 2)
-      for (int b = 0; b + width < nblocks; b += 2 * width) slot[b] = dd_add(slot[b], slot[b + width]);
-    const double2 r = make_double2(slot[0].hi, slot[0].lo);
-    m_out[(long long)j * n + i] = r;
-    m_out[(long long)i * n + j] = r;
   }
 }
 
@@ -380,26 +371,26 @@ cudaError_t launch_gram_dd(const double* a, long long lda, int n, const int2* ti
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_combine_f64(const double* partials, int ntp, int n,
-                                    const int* block_split_begin, int nblocks, double* m_out,
-                                    double* block_out, cudaStream_t st) {
-  const long long npairs = (long long)n * (n + 1) / 2;
-  int blocks = (int)((npairs + 255) / 256);
-  if (blocks > 4 * 148) blocks = 4 * 148;
-  gram_combine_f64<<<blocks, 256, 0, st>>>(partials, ntp, n, block_split_begin, nblocks, m_out,
-                                           block_out);
+template <typename ST>
+static cudaError_t combine_t(const ST* partials, int ntp, int n, const int* block_split_begin, int nblocks,
+                             ST* sums, ST* m_out, cudaStream_t st) {
+  dim3 g1(ntp, (kTile * kTile) / 256, nblocks);
+  gram_block_sums<ST><<<g1, 256, 0, st>>>(partials, ntp, block_split_begin, sums);
+  const long long nn = (long long)n * n;
+  int grid = (int)((nn + 255) / 256);
+  if (grid > 8 * 148) grid = 8 * 148;
+  gram_tree<ST><<<grid, 256, 0, st>>>(sums, ntp, n, nblocks, m_out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_combine_dd(const double2* partials, int ntp, int n,
-                                   const int* block_split_begin, int nblocks, double2* m_out,
-                                   double2* block_out, cudaStream_t st) {
-  const long long npairs = (long long)n * (n + 1) / 2;
-  int blocks = (int)((npairs + 255) / 256);
-  if (blocks > 4 * 148) blocks = 4 * 148;
-  gram_combine_dd<<<blocks, 256, 0, st>>>(partials, ntp, n, block_split_begin, nblocks, m_out,
-                                          block_out);
-  return cudaGetLastError();
+cudaError_t launch_gram_combine_f64(const double* partials, int ntp, int n, const int* block_split_begin,
+                                    int nblocks, double* sums, double* m_out, cudaStream_t st) {
+  return combine_t<double>(partials, ntp, n, block_split_begin, nblocks, sums, m_out, st);
+}
+
+cudaError_t launch_gram_combine_dd(const double2* partials, int ntp, int n, const int* block_split_begin,
+                                   int nblocks, double2* sums, double2* m_out, cudaStream_t st) {
+  return combine_t<double2>(partials, ntp, n, block_split_begin, nblocks, sums, m_out, st);
 }
 
 cudaError_t launch_block_tree(const void* blocks, int nblocks, int n, void* m_out, bool dd,

@@ -52,28 +52,39 @@ struct Arith<double> {
   static __device__ __forceinline__ bool is_identity(AT c, AT s) { return s == 0.0 && c == 1.0; }
   static __device__ __forceinline__ AT rot_lo(AT c, AT s, AT x, AT y) { return fma(c, x, -(s * y)); }
   static __device__ __forceinline__ AT rot_hi(AT c, AT s, AT x, AT y) { return fma(s, x, c * y); }
-  static __device__ __forceinline__ AT hyp1(AT z) {
-    const double az = fabs(z);
-    return az < 0x1p500 ? sqrt(fma(z, z, 1.0)) : az;
+  // Stop test of jacobi.cpp:516-522, |a_pq| <= tol sqrt(a_pp) sqrt(a_qq), with
+  // one square root of the product; the two-root form only when the product
+  // leaves the normal range (the reference's reason for it).
+  static __device__ __forceinline__ bool active(AT app, AT aqq, AT apq, double tol) {
+    const double pr = app * aqq;
+    const double thresh = (pr > 0x1p-1000 && pr < 0x1p1000) ? tol * sqrt(pr) : tol * sqrt(app) * sqrt(aqq);
+    return !(fabs(apq) <= thresh);
   }
-  // returns active; fills c, s, t, new diagonal entries; ratio for NoConvergence payload
-  static __device__ __forceinline__ bool rotation(AT app, AT aqq, AT apq, double tol, AT& c, AT& s,
-                                                  AT& t, AT& npp, AT& nqq, double& ratio) {
-    const double thresh = tol * sqrt(app) * sqrt(aqq);
-    ratio = fabs(apq) / sqrt(app * aqq);
-    c = 1.0;
-    s = 0.0;
-    t = 0.0;
-    npp = app;
-    nqq = aqq;
-    if (fabs(apq) <= thresh) return false;
-    const double zeta = (aqq - app) / (2.0 * apq);
-    t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hyp1(zeta));
-    c = 1.0 / hyp1(t);
+  // normalised off-diagonal |a_pq| / sqrt(a_pp a_qq) (NoConvergence payload)
+  static __device__ __forceinline__ double ratio(AT app, AT aqq, AT apq) { return fabs(apq) / sqrt(app * aqq); }
+  static __device__ __noinline__ double scaled_hypot(double x, double y, double big) {
+    int e;  // exact power-of-two rescaling keeps x^2 + y^2 finite and normal
+    frexp(big, &e);
+    const double xs = ldexp(x, -e), ys = ldexp(y, -e);
+    return ldexp(sqrt(fma(xs, xs, ys * ys)), e);
+  }
+  // Annihilating rotation (jacobi.cpp:524-546). With x = a_qq - a_pp,
+  // y = 2 a_pq, r = sqrt(x^2 + y^2):
+  //   t = sign(x) y / (|x| + r)   (= sign(zeta)/(|zeta| + hypot(1, zeta))),
+  //   c = sqrt((|x| + r) / (2 r)) (= 1/sqrt(1 + t^2)),   s = c t,
+  // t = +1 at x == 0 (the reference's sign(0) = +1): three dependent
+  // square-root/division steps instead of five. Diagonal: a_pp - t a_pq,
+  // a_qq + t a_pq (fused).
+  static __device__ __forceinline__ void rotate(AT app, AT aqq, AT apq, AT& c, AT& s, AT& npp, AT& nqq) {
+    const double x = aqq - app, y = 2.0 * apq, ax = fabs(x);
+    const double big = fmax(ax, fabs(y));
+    const double r = (big < 0x1p500 && big > 0x1p-500) ? sqrt(fma(x, x, y * y)) : scaled_hypot(x, y, big);
+    const double den = ax + r;
+    const double t = x == 0.0 ? 1.0 : (x > 0.0 ? y : -y) / den;
+    c = sqrt(den / (2.0 * r));
     s = c * t;
     npp = fma(-t, apq, app);
     nqq = fma(t, apq, aqq);
-    return true;
   }
 };
 
@@ -102,24 +113,36 @@ struct Arith<double2> {
   static __device__ __forceinline__ AT rot_hi(AT c, AT s, AT x, AT y) {
     return dd_add(dd_mul(s, x), dd_mul(c, y));
   }
-  static __device__ __forceinline__ bool rotation(AT app, AT aqq, AT apq, double tol, AT& c, AT& s,
-                                                  AT& t, AT& npp, AT& nqq, double& ratio) {
-    const dd thresh = dd_mul(dd_mul(dd_from(tol), dd_sqrt(app)), dd_sqrt(aqq));
-    ratio = fabs(apq.hi) / sqrt(app.hi * aqq.hi);
-    c = dd_from(1.0);
-    s = dd_from(0.0);
-    t = dd_from(0.0);
-    npp = app;
-    nqq = aqq;
-    if (dd_le(dd_abs(apq), thresh)) return false;
-    const dd zeta = dd_div(dd_sub(aqq, app), dd_scale2(apq));
-    t = dd_div(dd_from(zeta.hi >= 0.0 ? 1.0 : -1.0), dd_add(dd_abs(zeta), dd_hyp1(zeta)));
-    c = dd_div(dd_from(1.0), dd_hyp1(t));
+  // The stop test of the double-double solver is evaluated on the leading
+  // words (a relative 2^-53 wobble of a 2^-104-scale threshold is immaterial).
+  static __device__ __forceinline__ bool active(AT app, AT aqq, AT apq, double tol) {
+    const double pr = app.hi * aqq.hi;
+    const double thresh = (pr > 0x1p-1000 && pr < 0x1p1000) ? tol * sqrt(pr) : tol * sqrt(app.hi) * sqrt(aqq.hi);
+    return !(fabs(apq.hi) <= thresh);
+  }
+  static __device__ __forceinline__ double ratio(AT app, AT aqq, AT apq) {
+    return fabs(apq.hi) / sqrt(app.hi * aqq.hi);
+  }
+  static __device__ __noinline__ dd scaled_hypot(dd x, dd y, double big) {
+    int e;
+    frexp(big, &e);
+    const dd xs = dd_make(ldexp(x.hi, -e), ldexp(x.lo, -e));
+    const dd ys = dd_make(ldexp(y.hi, -e), ldexp(y.lo, -e));
+    const dd rs = dd_sqrt(dd_add(dd_mul(xs, xs), dd_mul(ys, ys)));
+    return dd_make(ldexp(rs.hi, e), ldexp(rs.lo, e));
+  }
+  static __device__ __forceinline__ void rotate(AT app, AT aqq, AT apq, AT& c, AT& s, AT& npp, AT& nqq) {
+    const dd x = dd_sub(aqq, app), y = dd_scale2(apq), ax = dd_abs(x);
+    const double big = fmax(ax.hi, fabs(y.hi));
+    const dd r = (big < 0x1p250 && big > 0x1p-250) ? dd_sqrt(dd_add(dd_mul(x, x), dd_mul(y, y)))
+                                                    : scaled_hypot(x, y, big);
+    const dd den = dd_add(ax, r);
+    const dd t = x.hi == 0.0 ? dd_from(1.0) : dd_div(x.hi > 0.0 ? y : dd_neg(y), den);
+    c = dd_sqrt(dd_div(den, dd_scale2(r)));
     s = dd_mul(c, t);
     const dd tapq = dd_mul(t, apq);
     npp = dd_sub(app, tapq);
     nqq = dd_add(aqq, tapq);
-    return true;
   }
 };
 
@@ -127,17 +150,23 @@ struct Arith<double2> {
 constexpr int kJacobiThreads = 256;
 
 template <typename ST>
-struct RotSmem {
-  typename Arith<ST>::AT* c;
-  typename Arith<ST>::AT* s;
-  typename Arith<ST>::AT* npp;
-  typename Arith<ST>::AT* nqq;
-  int* act;
-};
-
-template <typename ST>
 __host__ __device__ constexpr size_t rot_smem_bytes(int np) {
+  // c, s, new a_pp, new a_qq (AT each) + packed pair/active word
   return (size_t)np * (4 * sizeof(typename Arith<ST>::AT) + sizeof(int));
+}
+
+// Reduction helpers over one warp (all 32 lanes participate).
+__device__ __forceinline__ int warp_sum(int v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
 template <typename ST, bool kSmem>
@@ -148,27 +177,29 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   using AT = typename A_::AT;
   extern __shared__ __align__(16) unsigned char jsm[];
   const int N = n + (n & 1), np = N / 2, R = N - 1;
-  const int tid = threadIdx.x, bs = blockDim.x;
+  const int tid = threadIdx.x, bs = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const long long nblk = (long long)np * (np + 1) / 2;
+  const int lda = kSmem ? n + 1 : n;  // odd smem pitch: row and column walks hit distinct banks
+  const int nw_rot = min(bs, (np + 31) / 32 * 32) / 32;  // warps that own rotation slots
+  const unsigned FULL = 0xffffffffu;
 
-  // shared memory carve-up
-  RotSmem<ST> rs;
+  // shared memory: [A (smem variant)] [c][s][npp][nqq] [pair word] [block table (smem variant)]
   unsigned char* p = jsm;
   ST* a = a_glob;
   if (kSmem) {
     a = reinterpret_cast<ST*>(p);
-    p += (size_t)n * n * sizeof(ST);
+    p += (size_t)n * (n + 1) * sizeof(ST);
   }
-  rs.c = reinterpret_cast<AT*>(p);
-  p += np * sizeof(AT);
-  rs.s = reinterpret_cast<AT*>(p);
-  p += np * sizeof(AT);
-  rs.npp = reinterpret_cast<AT*>(p);
-  p += np * sizeof(AT);
-  rs.nqq = reinterpret_cast<AT*>(p);
-  p += np * sizeof(AT);
-  rs.act = reinterpret_cast<int*>(p);
-  __shared__ int s_cnt, s_bad;
-  __shared__ unsigned long long s_worst;
+  AT* rc = reinterpret_cast<AT*>(p);
+  AT* rsn = rc + np;
+  AT* rnpp = rsn + np;
+  AT* rnqq = rnpp + np;
+  int* pw = reinterpret_cast<int*>(rnqq + np);  // p | q << 15 | active << 30
+  int* blk = pw + np;                            // aa | bb << 16 (smem variant)
+  __shared__ int s_flag;
+  __shared__ int w_cnt[32], w_bad[32];
+  __shared__ double w_worst[32];
+  __shared__ unsigned s_sweep_flag;
 
   auto LD = [&](const ST* q) -> AT { return kSmem ? A_::lds(q) : A_::ldg(q); };
   auto gsync = [&]() {
@@ -177,48 +208,37 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
     else
       cg::this_grid().sync();
   };
+  auto AE = [&](int row, int col) -> ST* { return a + (long long)col * lda + row; };
 
   if (kSmem) {
-    for (long long e = tid; e < (long long)n * n; e += bs) a[e] = a_glob[e];
-    __syncthreads();
+    for (long long e = tid; e < (long long)n * n; e += bs) a[(e / n) * lda + e % n] = a_glob[e];
+    for (long long idx = tid; idx < nblk; idx += bs) {
+      int bb = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+      while ((long long)bb * (bb + 1) / 2 > idx) --bb;
+      while ((long long)(bb + 1) * (bb + 2) / 2 <= idx) ++bb;
+      blk[idx] = (int)(idx - (long long)bb * (bb + 1) / 2) | (bb << 16);
+    }
   }
+  if (tid == 0) s_flag = 0x7fffffff;
+  __syncthreads();
 
   // initial positive-definiteness check (jacobi.cpp:505-506): every CTA
   // evaluates it identically, so all exit together.
-  if (tid == 0) s_bad = 0x7fffffff;
-  __syncthreads();
   for (int k = tid; k < n; k += bs)
-    if (!A_::gt0(LD(a + (long long)k * n + k))) atomicMin(&s_bad, k);
+    if (!A_::gt0(LD(AE(k, k)))) atomicMin(&s_flag, k);
   __syncthreads();
-  if (s_bad != 0x7fffffff) {
+  if (s_flag != 0x7fffffff) {
     if (blockIdx.x == 0 && tid == 0) {
       status->status = kNotPositiveDefinite;
-      status->index = s_bad + 1;
-      status->value = A_::hi(LD(a + (long long)s_bad * n + s_bad));
+      status->index = s_flag + 1;
+      status->value = A_::hi(LD(AE(s_flag, s_flag)));
       status->sweeps = 0;
       status->rotations = 0;
     }
     return;
   }
 
-  // round-0 diagonal blocks for the multi-CTA path
-  if (!kSmem) {
-    const int gt = blockIdx.x * bs + tid, gs = gridDim.x * bs;
-    for (int k = gt; k < np; k += gs) {
-      int pp, qq;
-      rr_pair(n, 0, k, pp, qq);
-      if (qq < n) {
-        ST* d = diagbuf + 3 * k;
-        d[0] = a[(long long)pp * n + pp];
-        d[1] = a[(long long)qq * n + qq];
-        d[2] = a[(long long)qq * n + pp];
-      }
-    }
-    gsync();
-  }
-
   const int gtid = blockIdx.x * bs + tid, gstride = gridDim.x * bs;
-  const long long nblk = (long long)np * (np + 1) / 2;
   long long rotations = 0;
   double worst = 0.0;
   int sweeps = 0;
@@ -226,82 +246,228 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   long long g = 0;  // global round counter
 
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    // ---- sweep pre-check: if no pair passes the stop test now, this sweep
+    // would rotate nothing (A cannot change), i.e. it is the converged
+    // detection sweep of jacobi.cpp:561-565 — decided in one parallel pass.
+    {
+      if (kSmem) {
+        if (tid == 0) s_sweep_flag = 0;
+        __syncthreads();
+      }
+      unsigned found = 0;
+      const long long npairs = (long long)n * (n - 1) / 2;
+      for (long long e = kSmem ? tid : gtid; e < npairs && !found; e += kSmem ? bs : gstride) {
+        int j = (int)((sqrtf(8.0f * (float)e + 1.0f) + 1.0f) * 0.5f);
+        while ((long long)j * (j - 1) / 2 > e) --j;
+        while ((long long)(j + 1) * j / 2 <= e) ++j;
+        const int i = (int)(e - (long long)j * (j - 1) / 2);
+        found = A_::active(LD(AE(i, i)), LD(AE(j, j)), LD(AE(i, j)), tol) ? 1u : 0u;
+      }
+      if (kSmem) {
+        if (__any_sync(FULL, found) && lane == 0) s_sweep_flag = 1;
+        __syncthreads();
+        found = s_sweep_flag;
+      } else {
+        // grid-wide OR through the sweep parity word of the diag buffer tail
+        unsigned* flags = reinterpret_cast<unsigned*>(diagbuf + 6 * np);
+        if (__any_sync(FULL, found) && lane == 0) atomicOr(&flags[sweep & 1], 1u);
+        gsync();
+        found = *(volatile unsigned*)&flags[sweep & 1];
+        if (blockIdx.x == 0 && tid == 0) flags[(sweep + 1) & 1] = 0;  // reset for the next sweep
+      }
+      if (!found) {
+        ++sweeps;
+        converged = true;
+        break;
+      }
+    }
+    // round-0 diagonal blocks for the multi-CTA path
+    if (!kSmem && sweep == 0) {
+      ST* d0 = diagbuf + (g & 1) * 3 * np;
+      for (int k = gtid; k < np; k += gstride) {
+        int pp, qq;
+        rr_pair(n, 0, k, pp, qq);
+        if (qq < n) {
+          d0[3 * k] = a[(long long)pp * n + pp];
+          d0[3 * k + 1] = a[(long long)qq * n + qq];
+          d0[3 * k + 2] = a[(long long)qq * n + pp];
+        }
+      }
+      gsync();
+    }
     long long rot_sweep = 0;
     worst = 0.0;
+    const bool want_ratio = sweep + 1 == max_sweeps;
     for (int r = 0; r < R; ++r, ++g) {
-      const int rnext = (r + 1) % R;
-      const ST* dcur = diagbuf + (g & 1) * 3 * np;
-      ST* dnext = diagbuf + ((g + 1) & 1) * 3 * np;
-      // ---- phase 1: all rotations of the round (redundant per CTA)
-      if (tid == 0) {
-        s_cnt = 0;
-        s_bad = 0x7fffffff;
-        s_worst = 0ull;
-      }
-      __syncthreads();
-      for (int k = tid; k < np; k += bs) {
-        int pp, qq;
-        rr_pair(n, r, k, pp, qq);
-        AT c = A_::one(), s = A_::zero(), t = A_::zero(), npp = A_::zero(), nqq = A_::zero();
-        int act = 0;
-        if (qq < n) {
-          AT app, aqq, apq;
-          if (kSmem) {
-            app = LD(a + (long long)pp * n + pp);
-            aqq = LD(a + (long long)qq * n + qq);
-            apq = LD(a + (long long)qq * n + pp);
-          } else {
-            app = A_::ldg(dcur + 3 * k);
-            aqq = A_::ldg(dcur + 3 * k + 1);
-            apq = A_::ldg(dcur + 3 * k + 2);
+      const int par = (int)(g & 1);
+      const int rnext = (r + 1 == R) ? 0 : r + 1;
+      const ST* dcur = diagbuf + par * 3 * np;
+      ST* dnext = diagbuf + (par ^ 1) * 3 * np;
+      // ---- phase 1: all rotations of the round, redundantly in every CTA.
+      // Per-warp partial reductions land in w_* slots, combined after the
+      // barrier (slots are rewritten only after the phase-2 barrier).
+      if (warp < nw_rot) {
+        int act_sum = 0, bad = 0x7fffffff;
+        double wmax = 0.0;
+        for (int k0 = 0; k0 < np; k0 += bs) {  // uniform trip count within the warp
+          const int k = k0 + tid;
+          int pp = 0, qq = n;
+          if (k < np) rr_pair(n, r, k, pp, qq);
+          AT app = A_::one(), aqq = A_::one(), apq = A_::zero();
+          if (qq < n) {
+            if (kSmem) {
+              app = LD(AE(pp, pp));
+              aqq = LD(AE(qq, qq));
+              apq = LD(AE(pp, qq));
+            } else {
+              app = A_::ldg(dcur + 3 * k);
+              aqq = A_::ldg(dcur + 3 * k + 1);
+              apq = A_::ldg(dcur + 3 * k + 2);
+            }
           }
-          double ratio = 0.0;
-          act = A_::rotation(app, aqq, apq, tol, c, s, t, npp, nqq, ratio) ? 1 : 0;
-          atomicMax(&s_worst, (unsigned long long)__double_as_longlong(ratio));
-          if (act) {
-            atomicAdd(&s_cnt, 1);
-            if (!A_::gt0(npp)) atomicMin(&s_bad, pp);
-            if (!A_::gt0(nqq)) atomicMin(&s_bad, qq);
+          const bool act = qq < n && A_::active(app, aqq, apq, tol);
+          if (want_ratio && qq < n) wmax = fmax(wmax, A_::ratio(app, aqq, apq));
+          AT c = A_::one(), s = A_::zero(), npp = app, nqq = aqq;
+          if (__any_sync(FULL, act)) {
+            AT c2, s2, np2, nq2;
+            // inactive lanes rotate a harmless dummy block and discard it
+            A_::rotate(act ? app : A_::one(), act ? aqq : A_::one(), act ? apq : A_::one(), c2, s2, np2, nq2);
+            if (act) {
+              c = c2;
+              s = s2;
+              npp = np2;
+              nqq = nq2;
+              if (!A_::gt0(npp)) bad = min(bad, pp);
+              if (!A_::gt0(nqq)) bad = min(bad, qq);
+            }
+          }
+          act_sum += act ? 1 : 0;
+          if (k < np) {
+            rc[k] = c;
+            rsn[k] = s;
+            rnpp[k] = npp;
+            rnqq[k] = nqq;
+            pw[k] = pp | (qq << 15) | ((act ? 1 : 0) << 30);
           }
         }
-        rs.c[k] = c;
-        rs.s[k] = s;
-        rs.npp[k] = npp;
-        rs.nqq[k] = nqq;
-        rs.act[k] = act;
-        (void)t;
+        act_sum = warp_sum(act_sum);
+        bad = warp_min(bad);
+        if (want_ratio) wmax = warp_max(wmax);
+        if (lane == 0) {
+          w_cnt[warp] = act_sum;
+          w_bad[warp] = bad;
+          w_worst[warp] = wmax;
+        }
       }
       __syncthreads();
-      {
-        const double w = __longlong_as_double((long long)s_worst);
-        if (worst < w) worst = w;
+      int cnt = 0, badx = 0x7fffffff;
+      for (int w = 0; w < nw_rot; ++w) {
+        cnt += w_cnt[w];
+        badx = min(badx, w_bad[w]);
+        worst = fmax(worst, w_worst[w]);
       }
-      if (s_bad != 0x7fffffff) {  // NotPositiveDefiniteError(pivot, value), jacobi.cpp:547-548
+      if (badx != 0x7fffffff) {  // NotPositiveDefiniteError(pivot, value), jacobi.cpp:547-548
         if (blockIdx.x == 0 && tid == 0) {
-          const int x = s_bad;
+          const int x = badx;
           const int k = rr_slot(n, r, x);
-          int pp, qq;
-          rr_pair(n, r, k, pp, qq);
+          const int pp = pw[k] & 0x7fff;
           status->status = kNotPositiveDefinite;
           status->index = x + 1;
-          status->value = A_::hi(x == pp ? rs.npp[k] : rs.nqq[k]);
+          status->value = A_::hi(x == pp ? rnpp[k] : rnqq[k]);
           status->sweeps = sweeps;
           status->rotations = rotations;
         }
         return;
       }
-      rot_sweep += s_cnt;
-      rotations += s_cnt;
+      rot_sweep += cnt;
+      rotations += cnt;
       if (blockIdx.x == 0) {
         for (int k = tid; k < np; k += bs) {
           ST* lg = rot_log + 2 * ((long long)g * np + k);
-          A_::st(lg, rs.c[k]);
-          A_::st(lg + 1, rs.s[k]);
+          A_::st(lg, rc[k]);
+          A_::st(lg + 1, rsn[k]);
         }
       }
-      // ---- phase 2: 2x2 blocks between pairs a <= b
+      // ---- phase 2: 2x2 blocks between pairs aa <= bb; each element has
+      // exactly one owner. Off-diagonal blocks: column rotation of bb, then
+      // row rotation of aa, written to both triangles (exact symmetry).
+      if (kSmem) {
+        if (cnt != 0) {
+          for (long long idx = tid; idx < nblk; idx += bs) {
+            const int w = blk[idx];
+            const int aa = w & 0xffff, bb = w >> 16;
+            const int wa = pw[aa], wb = pw[bb];
+            const bool acta = (wa >> 30) & 1, actb = (wb >> 30) & 1;
+            if (!acta && !actb) continue;
+            const int p0 = wa & 0x7fff, q0 = (wa >> 15) & 0x7fff;
+            if (aa == bb) {  // diagonal block (jacobi.cpp:541-546)
+              A_::st(AE(p0, p0), rnpp[aa]);
+              A_::st(AE(q0, q0), rnqq[aa]);
+              A_::st(AE(p0, q0), A_::zero());
+              A_::st(AE(q0, p0), A_::zero());
+              continue;
+            }
+            const int k0 = wb & 0x7fff, l0 = (wb >> 15) & 0x7fff;
+            if (q0 < n && l0 < n) {
+              AT x00 = LD(AE(p0, k0)), x01 = LD(AE(p0, l0)), x10 = LD(AE(q0, k0)), x11 = LD(AE(q0, l0));
+              if (actb) {
+                const AT cb = rc[bb], sb = rsn[bb];
+                const AT y00 = A_::rot_lo(cb, sb, x00, x01), y01 = A_::rot_hi(cb, sb, x00, x01);
+                const AT y10 = A_::rot_lo(cb, sb, x10, x11), y11 = A_::rot_hi(cb, sb, x10, x11);
+                x00 = y00;
+                x01 = y01;
+                x10 = y10;
+                x11 = y11;
+              }
+              if (acta) {
+                const AT ca = rc[aa], sa = rsn[aa];
+                const AT y00 = A_::rot_lo(ca, sa, x00, x10), y10 = A_::rot_hi(ca, sa, x00, x10);
+                const AT y01 = A_::rot_lo(ca, sa, x01, x11), y11 = A_::rot_hi(ca, sa, x01, x11);
+                x00 = y00;
+                x10 = y10;
+                x01 = y01;
+                x11 = y11;
+              }
+              A_::st(AE(p0, k0), x00);
+              A_::st(AE(k0, p0), x00);
+              A_::st(AE(p0, l0), x01);
+              A_::st(AE(l0, p0), x01);
+              A_::st(AE(q0, k0), x10);
+              A_::st(AE(k0, q0), x10);
+              A_::st(AE(q0, l0), x11);
+              A_::st(AE(l0, q0), x11);
+            } else {  // one of the pairs holds the bye of an odd n
+              const int rows[2] = {p0, q0}, cols[2] = {k0, l0};
+              const int nr = q0 < n ? 2 : 1, nc = l0 < n ? 2 : 1;
+              AT x[2][2];
+              for (int u = 0; u < 2; ++u)
+                for (int v = 0; v < 2; ++v) x[u][v] = (u < nr && v < nc) ? LD(AE(rows[u], cols[v])) : A_::zero();
+              if (actb)
+                for (int u = 0; u < 2; ++u) {
+                  const AT x0 = x[u][0], x1 = x[u][1];
+                  x[u][0] = A_::rot_lo(rc[bb], rsn[bb], x0, x1);
+                  x[u][1] = A_::rot_hi(rc[bb], rsn[bb], x0, x1);
+                }
+              if (acta)
+                for (int v = 0; v < 2; ++v) {
+                  const AT y0 = x[0][v], y1 = x[1][v];
+                  x[0][v] = A_::rot_lo(rc[aa], rsn[aa], y0, y1);
+                  x[1][v] = A_::rot_hi(rc[aa], rsn[aa], y0, y1);
+                }
+              for (int u = 0; u < nr; ++u)
+                for (int v = 0; v < nc; ++v) {
+                  A_::st(AE(rows[u], cols[v]), x[u][v]);
+                  A_::st(AE(cols[v], rows[u]), x[u][v]);
+                }
+            }
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      // multi-CTA variant: every block is visited so that the entries the
+      // next round's rotations read are published to the diag buffer
       auto emit = [&](int x, int y, AT v) {
-        if (kSmem) return;
         const int s2 = rr_slot(n, rnext, x);
         int pp, qq;
         rr_pair(n, rnext, s2, pp, qq);
@@ -311,51 +477,50 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           A_::st(dnext + 3 * s2 + 2, v);
         }
       };
-      for (long long idx = kSmem ? tid : gtid; idx < nblk; idx += kSmem ? bs : gstride) {
-        int bb = (int)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+      for (long long idx = gtid; idx < nblk; idx += gstride) {
+        int bb = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
         while ((long long)bb * (bb + 1) / 2 > idx) --bb;
         while ((long long)(bb + 1) * (bb + 2) / 2 <= idx) ++bb;
         const int aa = (int)(idx - (long long)bb * (bb + 1) / 2);
-        int p0, q0;
-        rr_pair(n, r, aa, p0, q0);
+        const int wa = pw[aa];
+        const int p0 = wa & 0x7fff, q0 = (wa >> 15) & 0x7fff;
+        const bool acta = (wa >> 30) & 1;
         if (aa == bb) {
-          // diagonal block of pair aa (jacobi.cpp:541-546)
           if (q0 >= n) {
-            emit(p0, p0, LD(a + (long long)p0 * n + p0));
+            emit(p0, p0, LD(AE(p0, p0)));
             continue;
           }
           AT vpp, vqq, vpq;
-          if (rs.act[aa]) {
-            vpp = rs.npp[aa];
-            vqq = rs.nqq[aa];
+          if (acta) {
+            vpp = rnpp[aa];
+            vqq = rnqq[aa];
             vpq = A_::zero();
-            A_::st(a + (long long)p0 * n + p0, vpp);
-            A_::st(a + (long long)q0 * n + q0, vqq);
-            A_::st(a + (long long)q0 * n + p0, vpq);
-            A_::st(a + (long long)p0 * n + q0, vpq);
+            A_::st(AE(p0, p0), vpp);
+            A_::st(AE(q0, q0), vqq);
+            A_::st(AE(p0, q0), vpq);
+            A_::st(AE(q0, p0), vpq);
           } else {
-            vpp = LD(a + (long long)p0 * n + p0);
-            vqq = LD(a + (long long)q0 * n + q0);
-            vpq = LD(a + (long long)q0 * n + p0);
+            vpp = LD(AE(p0, p0));
+            vqq = LD(AE(q0, q0));
+            vpq = LD(AE(p0, q0));
           }
           emit(p0, p0, vpp);
           emit(q0, q0, vqq);
           emit(p0, q0, vpq);
           continue;
         }
-        int k0, l0;
-        rr_pair(n, r, bb, k0, l0);
+        const int wb = pw[bb];
+        const int k0 = wb & 0x7fff, l0 = (wb >> 15) & 0x7fff;
+        const bool actb = (wb >> 30) & 1;
         const int rows[2] = {p0, q0}, cols[2] = {k0, l0};
         const int nr = q0 < n ? 2 : 1, nc = l0 < n ? 2 : 1;
-        const bool acta = rs.act[aa] != 0, actb = rs.act[bb] != 0;
         AT x[2][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int w = 0; w < 2; ++w)
-            x[u][w] = (u < nr && w < nc) ? LD(a + (long long)cols[w] * n + rows[u]) : A_::zero();
+          for (int v = 0; v < 2; ++v) x[u][v] = (u < nr && v < nc) ? LD(AE(rows[u], cols[v])) : A_::zero();
         if (actb) {
-          const AT cb = rs.c[bb], sb = rs.s[bb];
+          const AT cb = rc[bb], sb = rsn[bb];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const AT x0 = x[u][0], x1 = x[u][1];
@@ -364,24 +529,24 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           }
         }
         if (acta) {
-          const AT ca = rs.c[aa], sa = rs.s[aa];
+          const AT ca = rc[aa], sa = rsn[aa];
 #pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            const AT y0 = x[0][w], y1 = x[1][w];
-            x[0][w] = A_::rot_lo(ca, sa, y0, y1);
-            x[1][w] = A_::rot_hi(ca, sa, y0, y1);
+          for (int v = 0; v < 2; ++v) {
+            const AT y0 = x[0][v], y1 = x[1][v];
+            x[0][v] = A_::rot_lo(ca, sa, y0, y1);
+            x[1][v] = A_::rot_hi(ca, sa, y0, y1);
           }
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            if (u < nr && w < nc) {
+          for (int v = 0; v < 2; ++v) {
+            if (u < nr && v < nc) {
               if (acta || actb) {
-                A_::st(a + (long long)cols[w] * n + rows[u], x[u][w]);
-                A_::st(a + (long long)rows[u] * n + cols[w], x[u][w]);
+                A_::st(AE(rows[u], cols[v]), x[u][v]);
+                A_::st(AE(cols[v], rows[u]), x[u][v]);
               }
-              emit(rows[u], cols[w], x[u][w]);
+              emit(rows[u], cols[v], x[u][v]);
             }
           }
       }
@@ -395,7 +560,8 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   }
 
   if (kSmem) {
-    for (long long e = tid; e < (long long)n * n; e += bs) a_glob[e] = a[e];
+    __syncthreads();
+    for (long long e = tid; e < (long long)n * n; e += bs) a_glob[e] = a[(e / n) * lda + e % n];
   }
   if (blockIdx.x == 0 && tid == 0) {
     status->status = converged ? kOk : kNoConvergence;
@@ -403,13 +569,14 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
     status->value = converged ? 0.0 : worst;
     status->sweeps = sweeps;
     status->rotations = rotations;
+    status->rounds = g;
   }
 }
 
 // ---------------------------------------------------------------------------
 // V replay: V = I, then every logged round's rotations applied to V's
-// columns (p, q); each CTA owns a few rows of V in shared memory and streams
-// the log in batches of rounds.
+// columns (p, q). Each CTA owns `rows` rows of V in shared memory (rows of V
+// never mix) and streams the log in batches of rounds.
 template <typename ST>
 __global__ void __launch_bounds__(kJacobiThreads)
 jacobi_replay(const ST* __restrict__ rot_log, int n, int rows_per_cta, int batch,
@@ -421,24 +588,25 @@ jacobi_replay(const ST* __restrict__ rot_log, int n, int rows_per_cta, int batch
   const int row0 = blockIdx.x * rows_per_cta;
   const int nrows = min(rows_per_cta, n - row0);
   if (nrows <= 0) return;
-  ST* vr = reinterpret_cast<ST*>(rsm);                          // [rows][n]
-  ST* rot = vr + (size_t)rows_per_cta * n;                      // [batch][np][2]
+  ST* vr = reinterpret_cast<ST*>(rsm);      // [rows][n]
+  ST* rot = vr + (size_t)rows_per_cta * n;  // [batch][np][2]
   const int tid = threadIdx.x, bs = blockDim.x;
   for (int e = tid; e < nrows * n; e += bs) {
-    const int rr = e / n, cc = e % n;
+    const int rr = e / n, cc = e - rr * n;
     A_::st(vr + e, (row0 + rr == cc) ? A_::one() : A_::zero());
   }
   const int st = status->status;
-  const long long total = (st == kOk || st == kNoConvergence) ? (long long)status->sweeps * R : 0;
+  const long long total = (st == kOk || st == kNoConvergence) ? status->rounds : 0;
   __syncthreads();
+  const int items = nrows * np;
   for (long long g0 = 0; g0 < total; g0 += batch) {
     const int nb = (int)min((long long)batch, total - g0);
     for (int e = tid; e < nb * np * 2; e += bs) rot[e] = rot_log[g0 * np * 2 + e];
     __syncthreads();
+    int r = (int)(g0 % R);
     for (int b = 0; b < nb; ++b) {
-      const int r = (int)((g0 + b) % R);
-      for (int w = tid; w < nrows * np; w += bs) {
-        const int rr = w / np, k = w % np;
+      for (int w = tid; w < items; w += bs) {
+        const int rr = w / np, k = w - rr * np;
         const AT c = A_::lds(rot + 2 * ((size_t)b * np + k));
         const AT s = A_::lds(rot + 2 * ((size_t)b * np + k) + 1);
         if (A_::is_identity(c, s)) continue;
@@ -450,10 +618,11 @@ jacobi_replay(const ST* __restrict__ rot_log, int n, int rows_per_cta, int batch
         A_::st(row + qq, A_::rot_hi(c, s, t1, t2));
       }
       __syncthreads();
+      if (++r == R) r = 0;
     }
   }
   for (int e = tid; e < nrows * n; e += bs) {
-    const int rr = e / n, cc = e % n;
+    const int rr = e / n, cc = e - rr * n;
     v_out[(size_t)cc * n + row0 + rr] = vr[e];
   }
 }
@@ -575,6 +744,7 @@ __global__ void finish_columns(const ST* __restrict__ v, int n, const DevStatus*
   const int imax = s_idx[0];
   const bool flip = A_::hi(A_::ldg(vc + imax)) < 0.0;
   const WT sj = (WT)sigma[jj];
+  const int ldw = av_ldw(n);
   if (v_full) {  // sorted, sign-fixed V in the higher precision (stage API)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       AT x = A_::ldg(vc + i);
@@ -590,7 +760,7 @@ __global__ void finish_columns(const ST* __restrict__ v, int n, const DevStatus*
     const WT vw = (WT)(flip ? -x : x);
     v_work[(long long)jj * n + i] = vw;
     // scale_columns(invert): true division; W stored row-major (W^T) for K7
-    w_work[(long long)i * n + jj] = vw / sj;
+    w_work[(long long)i * ldw + jj] = vw / sj;
   }
 }
 
@@ -604,13 +774,15 @@ template <typename ST>
 static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const JacobiWorkspace& ws,
                                    int sm_count, cudaStream_t st) {
   const int N = n + (n & 1), np = N / 2;
-  const size_t smem_a = (size_t)n * n * sizeof(ST);
+  const size_t smem_a = (size_t)n * (n + 1) * sizeof(ST) + (size_t)np * (np + 1) / 2 * sizeof(int);
   const size_t smem_rot = rot_smem_bytes<ST>(np);
   const size_t smem_limit = 200 * 1024;
   ST* a = (ST*)ws.a;
   ST* d = (ST*)ws.diagbuf;
   ST* lg = (ST*)ws.log;
   DevStatus* status = ws.status;
+  // zero the two sweep flag words that follow the double-buffered diag blocks
+  cudaMemsetAsync(reinterpret_cast<unsigned char*>(ws.diagbuf) + (size_t)6 * np * sizeof(ST), 0, 16, st);
   if (smem_a + smem_rot <= smem_limit) {
     auto k = jacobi_kernel<ST, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_a + smem_rot));
@@ -643,7 +815,9 @@ cudaError_t launch_jacobi(bool dd_mode, int n, double tol, int max_sweeps, const
 template <typename ST>
 static cudaError_t launch_replay_t(int n, const JacobiWorkspace& ws, cudaStream_t st) {
   const int N = n + (n & 1), np = N / 2;
-  int rows = (n + 147) / 148;
+  // enough rows per CTA that one round is ~256 independent rotations
+  int rows = (256 + np - 1) / np;
+  if (rows > n) rows = n;
   if (rows < 1) rows = 1;
   const size_t row_bytes = (size_t)rows * n * sizeof(ST);
   const size_t budget = 160 * 1024;

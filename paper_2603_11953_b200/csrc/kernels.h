@@ -17,12 +17,11 @@ cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* ti
 cudaError_t launch_gram_dd(const double* a, long long lda, int n, const int2* tiles, int ntp,
                            const longlong2* splits, int nsplit, double2* partials,
                            cudaStream_t st);
-cudaError_t launch_gram_combine_f64(const double* partials, int ntp, int n,
-                                    const int* block_split_begin, int nblocks, double* m_out,
-                                    double* block_out, cudaStream_t st);
-cudaError_t launch_gram_combine_dd(const double2* partials, int ntp, int n,
-                                   const int* block_split_begin, int nblocks, double2* m_out,
-                                   double2* block_out, cudaStream_t st);
+// sums: nblocks * ntp * 64 * 64 elements of workspace
+cudaError_t launch_gram_combine_f64(const double* partials, int ntp, int n, const int* block_split_begin,
+                                    int nblocks, double* sums, double* m_out, cudaStream_t st);
+cudaError_t launch_gram_combine_dd(const double2* partials, int ntp, int n, const int* block_split_begin,
+                                   int nblocks, double2* sums, double2* m_out, cudaStream_t st);
 cudaError_t launch_mirror_upper(double* m, int n, cudaStream_t st);
 cudaError_t launch_block_tree(const void* blocks, int nblocks, int n, void* m_out, bool dd,
                               cudaStream_t st);
@@ -50,6 +49,7 @@ cudaError_t launch_finish(bool dd, int n, const JacobiWorkspace& ws, int* perm, 
                           int working_f64, cudaStream_t st, void* v_full = nullptr);
 
 // compute_u.cu ----------------------------------------------------------------
+
 cudaError_t launch_av_f32(const float* a, long long lda, long long m, int n, const float* w,
                           float* u, long long ldu, const DevStatus* status, cudaStream_t st);
 cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w,
