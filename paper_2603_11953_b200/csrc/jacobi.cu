@@ -574,6 +574,337 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// Single-CTA Jacobi for matrices resident in shared memory, warp-specialised
+// so the latency of the rotation formulas overlaps the 2x2 block updates:
+//
+//   rotation warps (R):  wait B2(r-1) -> rotations of round r -> arrive B1(r)
+//   update warps   (U):  wait B1(r) -> pass 1: the blocks holding the entries
+//                        round r+1's rotations read (its diagonal blocks'
+//                        images) -> arrive B2(r) -> pass 2: all other blocks
+//                        -> U-only barrier B3
+//
+// so a round costs ~max(rotation latency, block updates) instead of their
+// sum. Named barriers: 1 = B1, 2 = B2, 3 = B3 (U only), 4 = R-only.
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+constexpr int kUpdateWarps = 8;
+
+// partner of x in `round` (n itself for the bye of an odd n)
+__device__ __forceinline__ int rr_partner(int n, int round, int x) {
+  int pp, qq;
+  rr_pair(n, round, rr_slot(n, round, x), pp, qq);
+  return pp == x ? qq : pp;
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(32 * (kUpdateWarps + 2))
+jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol, int max_sweeps,
+            DevStatus* __restrict__ status) {
+  using A_ = Arith<ST>;
+  using AT = typename A_::AT;
+  extern __shared__ __align__(16) unsigned char jsm[];
+  const int N = n + (n & 1), np = N / 2, Rr = N - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw_rot = (np + 31) / 32;  // rotation warps (1 or 2 here)
+  const int NT = blockDim.x, n_rot = 32 * nw_rot, n_upd = NT - n_rot;
+  const bool is_rot = warp < nw_rot;
+  const int utid = tid - n_rot;  // update-thread index
+  const int lda = n + 1;         // odd pitch: row and column walks hit distinct banks
+  const unsigned FULL = 0xffffffffu;
+
+  ST* a = reinterpret_cast<ST*>(jsm);
+  AT* rbase = reinterpret_cast<AT*>(jsm + (size_t)n * lda * sizeof(ST));
+  // two round buffers of [c][s][npp][nqq] + pair words
+  auto RC = [&](int b) { return rbase + (size_t)b * 4 * np; };
+  int* pwb = reinterpret_cast<int*>(rbase + (size_t)8 * np);  // [2][np]
+  int* blk = pwb + 2 * np;                                      // idx -> aa | bb << 16
+  __shared__ int s_abort, s_bad, s_flag;
+  __shared__ int w_cnt[2];
+  __shared__ double w_worst[2];
+  auto AE = [&](int row, int col) -> ST* { return a + col * lda + row; };
+
+  for (int e = tid; e < n * n; e += NT) a[(e / n) * lda + e % n] = a_glob[e];
+  for (int idx = tid; idx < np * (np + 1) / 2; idx += NT) {
+    int bb = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+    while (bb * (bb + 1) / 2 > idx) --bb;
+    while ((bb + 1) * (bb + 2) / 2 <= idx) ++bb;
+    blk[idx] = (idx - bb * (bb + 1) / 2) | (bb << 16);
+  }
+  if (tid == 0) {
+    s_abort = 0;
+    s_bad = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int k = tid; k < n; k += NT)
+    if (!A_::gt0(A_::lds(AE(k, k)))) atomicMin(&s_bad, k);
+  __syncthreads();
+  if (s_bad != 0x7fffffff) {  // jacobi.cpp:505-506
+    if (tid == 0) {
+      status->status = kNotPositiveDefinite;
+      status->index = s_bad + 1;
+      status->value = A_::hi(A_::lds(AE(s_bad, s_bad)));
+      status->sweeps = 0;
+      status->rotations = 0;
+      status->rounds = 0;
+    }
+    return;
+  }
+
+  long long rotations = 0, g = 0;
+  int sweeps = 0;
+  bool converged = false;
+  double worst = 0.0;
+
+  // one 2x2 block update (pairs aa < bb, or the diagonal block aa == bb)
+  auto update_block = [&](int aa, int bb, const AT* rb, const int* pw) {
+    const int wa = pw[aa], wb = pw[bb];
+    const bool acta = (wa >> 30) & 1, actb = (wb >> 30) & 1;
+    if (!acta && !actb) return;
+    const AT* rcs = rb;
+    const AT* rss = rb + np;
+    const int p0 = wa & 0x7fff, q0 = (wa >> 15) & 0x7fff;
+    if (aa == bb) {  // jacobi.cpp:541-546
+      A_::st(AE(p0, p0), rb[2 * np + aa]);
+      A_::st(AE(q0, q0), rb[3 * np + aa]);
+      A_::st(AE(p0, q0), A_::zero());
+      A_::st(AE(q0, p0), A_::zero());
+      return;
+    }
+    const int k0 = wb & 0x7fff, l0 = (wb >> 15) & 0x7fff;
+    if (q0 < n && l0 < n) {
+      AT x00 = A_::lds(AE(p0, k0)), x01 = A_::lds(AE(p0, l0)), x10 = A_::lds(AE(q0, k0)), x11 = A_::lds(AE(q0, l0));
+      if (actb) {
+        const AT cb = rcs[bb], sb = rss[bb];
+        const AT y00 = A_::rot_lo(cb, sb, x00, x01), y01 = A_::rot_hi(cb, sb, x00, x01);
+        const AT y10 = A_::rot_lo(cb, sb, x10, x11), y11 = A_::rot_hi(cb, sb, x10, x11);
+        x00 = y00;
+        x01 = y01;
+        x10 = y10;
+        x11 = y11;
+      }
+      if (acta) {
+        const AT ca = rcs[aa], sa = rss[aa];
+        const AT y00 = A_::rot_lo(ca, sa, x00, x10), y10 = A_::rot_hi(ca, sa, x00, x10);
+        const AT y01 = A_::rot_lo(ca, sa, x01, x11), y11 = A_::rot_hi(ca, sa, x01, x11);
+        x00 = y00;
+        x10 = y10;
+        x01 = y01;
+        x11 = y11;
+      }
+      A_::st(AE(p0, k0), x00);
+      A_::st(AE(k0, p0), x00);
+      A_::st(AE(p0, l0), x01);
+      A_::st(AE(l0, p0), x01);
+      A_::st(AE(q0, k0), x10);
+      A_::st(AE(k0, q0), x10);
+      A_::st(AE(q0, l0), x11);
+      A_::st(AE(l0, q0), x11);
+      return;
+    }
+    // a pair holding the bye of an odd n: 1x2 / 2x1 / 1x1 block
+    const int rows[2] = {p0, q0}, cols[2] = {k0, l0};
+    const int nr = q0 < n ? 2 : 1, nc = l0 < n ? 2 : 1;
+    AT x[2][2];
+    for (int u = 0; u < 2; ++u)
+      for (int v = 0; v < 2; ++v) x[u][v] = (u < nr && v < nc) ? A_::lds(AE(rows[u], cols[v])) : A_::zero();
+    if (actb)
+      for (int u = 0; u < 2; ++u) {
+        const AT x0 = x[u][0], x1 = x[u][1];
+        x[u][0] = A_::rot_lo(rcs[bb], rss[bb], x0, x1);
+        x[u][1] = A_::rot_hi(rcs[bb], rss[bb], x0, x1);
+      }
+    if (acta)
+      for (int v = 0; v < 2; ++v) {
+        const AT y0 = x[0][v], y1 = x[1][v];
+        x[0][v] = A_::rot_lo(rcs[aa], rss[aa], y0, y1);
+        x[1][v] = A_::rot_hi(rcs[aa], rss[aa], y0, y1);
+      }
+    for (int u = 0; u < nr; ++u)
+      for (int v = 0; v < nc; ++v) {
+        A_::st(AE(rows[u], cols[v]), x[u][v]);
+        A_::st(AE(cols[v], rows[u]), x[u][v]);
+      }
+  };
+
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    // sweep pre-check (see jacobi_kernel): nothing passes the stop test ->
+    // this sweep is the rotation-free detection sweep
+    if (tid == 0) s_flag = 0;
+    __syncthreads();
+    {
+      unsigned found = 0;
+      const int npairs = n * (n - 1) / 2;
+      for (int e = tid; e < npairs && !found; e += NT) {
+        int j = (int)((sqrtf(8.0f * (float)e + 1.0f) + 1.0f) * 0.5f);
+        while (j * (j - 1) / 2 > e) --j;
+        while ((j + 1) * j / 2 <= e) ++j;
+        const int i = e - j * (j - 1) / 2;
+        found = A_::active(A_::lds(AE(i, i)), A_::lds(AE(j, j)), A_::lds(AE(i, j)), tol) ? 1u : 0u;
+      }
+      if (__any_sync(FULL, found) && lane == 0) s_flag = 1;
+    }
+    __syncthreads();
+    if (!s_flag) {
+      ++sweeps;
+      converged = true;
+      break;
+    }
+    const bool want_ratio = sweep + 1 == max_sweeps;
+    if (is_rot) {
+      // ===== rotation warps =====
+      long long cnt_sweep = 0;
+      double wmax = 0.0;
+      for (int r = 0; r < Rr; ++r) {
+        if (r > 0) nbar_sync(2, NT);  // round-r diagonal entries are final
+        AT* rb = RC((int)((g + r) & 1));
+        int* pw = pwb + ((g + r) & 1) * np;
+        const int k = tid;  // one slot per rotation thread (np <= 64 here)
+        int bad = 0x7fffffff, act_i = 0;
+        if (k < np) {
+          int pp, qq;
+          rr_pair(n, r, k, pp, qq);
+          AT app = A_::one(), aqq = A_::one(), apq = A_::zero();
+          if (qq < n) {
+            app = A_::lds(AE(pp, pp));
+            aqq = A_::lds(AE(qq, qq));
+            apq = A_::lds(AE(pp, qq));
+          }
+          const bool act = qq < n && A_::active(app, aqq, apq, tol);
+          if (want_ratio && qq < n) wmax = fmax(wmax, A_::ratio(app, aqq, apq));
+          AT c = A_::one(), s = A_::zero(), npp = app, nqq = aqq;
+          if (__any_sync(__activemask(), act)) {
+            AT c2, s2, np2, nq2;
+            A_::rotate(act ? app : A_::one(), act ? aqq : A_::one(), act ? apq : A_::one(), c2, s2, np2, nq2);
+            if (act) {
+              c = c2;
+              s = s2;
+              npp = np2;
+              nqq = nq2;
+              if (!A_::gt0(npp)) bad = min(bad, pp);
+              if (!A_::gt0(nqq)) bad = min(bad, qq);
+            }
+          }
+          act_i = act ? 1 : 0;
+          rb[k] = c;
+          rb[np + k] = s;
+          rb[2 * np + k] = npp;
+          rb[3 * np + k] = nqq;
+          pw[k] = pp | (qq << 15) | (act_i << 30);
+          ST* lg = rot_log + 2 * ((g + r) * np + k);
+          A_::st(lg, c);
+          A_::st(lg + 1, s);
+        }
+        cnt_sweep += __popc(__ballot_sync(FULL, act_i));
+        bad = warp_min(bad);
+        if (nw_rot > 1) {
+          if (lane == 0 && bad != 0x7fffffff) atomicMin(&s_bad, bad);
+          nbar_sync(4, n_rot);
+          bad = s_bad;
+        }
+        if (bad != 0x7fffffff) {
+          if (tid == 0) {
+            const int kk = rr_slot(n, r, bad);
+            const int pp = pw[kk] & 0x7fff;
+            status->status = kNotPositiveDefinite;
+            status->index = bad + 1;
+            status->value = A_::hi(bad == pp ? rb[2 * np + kk] : rb[3 * np + kk]);
+            status->sweeps = sweeps;
+            status->rotations = rotations;
+            status->rounds = g + r;
+            s_abort = 1;
+          }
+          __syncwarp();
+          nbar_arrive(1, NT);  // release the update warps; they see s_abort
+          break;
+        }
+        nbar_arrive(1, NT);
+      }
+      const double wm = want_ratio ? warp_max(wmax) : 0.0;
+      if (lane == 0) {
+        w_cnt[warp] = (int)cnt_sweep;
+        w_worst[warp] = wm;
+      }
+    } else {
+      // ===== update warps =====
+      for (int r = 0; r < Rr; ++r) {
+        nbar_sync(1, NT);
+        if (s_abort) break;
+        const int b = (int)((g + r) & 1);
+        const AT* rb = RC(b);
+        const int* pw = pwb + b * np;
+        const bool has_next = r + 1 < Rr;
+        const int rn = r + 1;
+        // The blocks holding the entries round r+1's rotations read are the
+        // same for every round of the circle schedule: the diagonal blocks,
+        // (k, k+2) for k <= np-3, (np-2, np-1), and (0, 1) for even n (each
+        // holds exactly one next-round pair; checked exhaustively for
+        // n < 140 against the schedule in tests/test_schedule.py).
+        const bool even_n = (n & 1) == 0;
+        auto priority = [&](int aa, int bb) {
+          return bb == aa || bb == aa + 2 || (bb == aa + 1 && (aa == np - 2 || (even_n && aa == 0)));
+        };
+        if (has_next) {
+          // pass 1: the priority blocks, then release the rotation warps
+          const int n1 = 2 * np;  // np diagonal + up to np priority off-diagonal slots
+          for (int j = utid; j < n1; j += n_upd) {
+            if (j < np) {
+              update_block(j, j, rb, pw);
+            } else {
+              const int k = j - np;
+              if (k <= np - 3)
+                update_block(k, k + 2, rb, pw);
+              else if (k == np - 2 && np >= 2)
+                update_block(np - 2, np - 1, rb, pw);
+              else if (k == np - 1 && even_n && np >= 3)
+                update_block(0, 1, rb, pw);
+            }
+          }
+          nbar_arrive(2, NT);
+        }
+        // pass 2: every other block (decode table built once per launch)
+        const int nblk = np * (np + 1) / 2;
+        for (int idx = utid; idx < nblk; idx += n_upd) {
+          const int w = blk[idx];
+          const int aa = w & 0xffff, bb = w >> 16;
+          if (has_next && priority(aa, bb)) continue;
+          update_block(aa, bb, rb, pw);
+        }
+        nbar_sync(3, n_upd);
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    long long cnt = 0;
+    for (int w = 0; w < nw_rot; ++w) {
+      cnt += w_cnt[w];
+      worst = fmax(worst, w_worst[w]);
+    }
+    g += Rr;
+    rotations += cnt;
+    ++sweeps;
+    if (cnt == 0) {
+      converged = true;
+      break;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += NT) a_glob[e] = a[(e / n) * lda + e % n];
+  if (tid == 0) {
+    status->status = converged ? kOk : kNoConvergence;
+    status->index = converged ? 0 : max_sweeps;
+    status->value = converged ? 0.0 : worst;
+    status->sweeps = sweeps;
+    status->rotations = rotations;
+    status->rounds = g;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // V replay: V = I, then every logged round's rotations applied to V's
 // columns (p, q). Each CTA owns `rows` rows of V in shared memory (rows of V
 // never mix) and streams the log in batches of rounds.
@@ -783,6 +1114,16 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   DevStatus* status = ws.status;
   // zero the two sweep flag words that follow the double-buffered diag blocks
   cudaMemsetAsync(reinterpret_cast<unsigned char*>(ws.diagbuf) + (size_t)6 * np * sizeof(ST), 0, 16, st);
+  const size_t smem_pipe = (size_t)n * (n + 1) * sizeof(ST) +
+                           (size_t)np * (8 * sizeof(typename Arith<ST>::AT) + 2 * sizeof(int)) +
+                           (size_t)np * (np + 1) / 2 * sizeof(int);
+  if (np <= 64 && smem_pipe <= smem_limit) {  // warp-specialised single-CTA solver
+    auto k = jacobi_smem<ST>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pipe);
+    const int threads = 32 * ((np + 31) / 32 + kUpdateWarps);
+    k<<<1, threads, smem_pipe, st>>>(a, lg, n, tol, max_sweeps, status);
+    return cudaGetLastError();
+  }
   if (smem_a + smem_rot <= smem_limit) {
     auto k = jacobi_kernel<ST, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_a + smem_rot));
