@@ -74,7 +74,7 @@ namespace detail {
 // Page-locked when possible (cudaMallocHost), plain heap otherwise. Zeroed.
 struct HostBuffer {
   HostBuffer() = default;
-  explicit HostBuffer(std::size_t bytes);
+  explicit HostBuffer(std::size_t bytes, bool zero = true);
   HostBuffer(const HostBuffer& o);
   HostBuffer& operator=(const HostBuffer& o);
   HostBuffer(HostBuffer&& o) noexcept;
@@ -96,6 +96,8 @@ class DenseMatrix {
   DenseMatrix() = default;
   DenseMatrix(index_t rows, index_t cols, Precision prec);
   static DenseMatrix identity(index_t n, Precision prec);
+  // additive: storage left uninitialised (for outputs that are overwritten)
+  static DenseMatrix uninitialized(index_t rows, index_t cols, Precision prec);
 
   index_t rows() const { return rows_; }
   index_t cols() const { return cols_; }

@@ -199,23 +199,44 @@ class ThinSvdResult:
     jacobi_rotations: int = 0
 
 
+class _ResultOwner:
+    """Keeps an mpsvd_svd_result alive while numpy views of its U / V exist."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        if self.handle:
+            lib.mpsvd_svd_destroy(self.handle)
+            self.handle = None
+
+
+def _view(mat_handle, owner) -> np.ndarray:
+    m, n = lib.mpsvd_matrix_rows(mat_handle), lib.mpsvd_matrix_cols(mat_handle)
+    f32 = lib.mpsvd_matrix_precision(mat_handle) == Precision.WORKING
+    dt, ct = (np.float32, C.c_float) if f32 else (np.float64, C.c_double)
+    if m * n == 0:
+        return np.zeros((m, n), dt, order="F")
+    buf = (ct * (m * n)).from_address(lib.mpsvd_matrix_data(mat_handle))
+    buf._owner = owner  # the array's base keeps the result alive
+    return np.ndarray((m, n), dtype=dt, buffer=buf, order="F")
+
+
 def _result(r) -> ThinSvdResult:
-    try:
-        u = Matrix._borrow(lib.mpsvd_svd_u(r)).numpy().copy(order="F")
-        v = Matrix._borrow(lib.mpsvd_svd_v(r)).numpy().copy(order="F")
-        cnt = C.c_int64()
-        sp = lib.mpsvd_svd_sigma(r, C.byref(cnt))
-        sigma = np.ctypeslib.as_array(sp, shape=(cnt.value,)).copy() if cnt.value else np.zeros(0)
-        t = (C.c_double * 5)()
-        lib.mpsvd_svd_times(r, t)
-        sw = C.c_int()
-        rot = C.c_int64()
-        lib.mpsvd_svd_jacobi_stats(r, C.byref(sw), C.byref(rot))
-        return ThinSvdResult(u, sigma, v, PhaseTimes(*list(t)), lib.mpsvd_svd_sync_events(r),
-                             lib.mpsvd_svd_gram_blocks(r), bool(lib.mpsvd_svd_is_qr_baseline(r)), sw.value,
-                             rot.value)
-    finally:
-        lib.mpsvd_svd_destroy(r)
+    """Zero-copy: U and V are views of the library's (page-locked) result buffers."""
+    owner = _ResultOwner(r)
+    u = _view(lib.mpsvd_svd_u(r), owner)
+    v = _view(lib.mpsvd_svd_v(r), owner)
+    cnt = C.c_int64()
+    sp = lib.mpsvd_svd_sigma(r, C.byref(cnt))
+    sigma = np.ctypeslib.as_array(sp, shape=(cnt.value,)).copy() if cnt.value else np.zeros(0)
+    t = (C.c_double * 5)()
+    lib.mpsvd_svd_times(r, t)
+    sw = C.c_int()
+    rot = C.c_int64()
+    lib.mpsvd_svd_jacobi_stats(r, C.byref(sw), C.byref(rot))
+    return ThinSvdResult(u, sigma, v, PhaseTimes(*list(t)), lib.mpsvd_svd_sync_events(r),
+                         lib.mpsvd_svd_gram_blocks(r), bool(lib.mpsvd_svd_is_qr_baseline(r)), sw.value, rot.value)
 
 
 def mp_thin_svd(a, choice: EigensolverChoice = EigensolverChoice.TWOSIDED_JACOBI, threads: int = 1) -> ThinSvdResult:

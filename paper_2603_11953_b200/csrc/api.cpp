@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -55,18 +56,57 @@ TinySingularValueError::TinySingularValueError(index_t i, double v)
 namespace detail {
 static constexpr std::size_t kPinThreshold = 1u << 20;
 
-HostBuffer::HostBuffer(std::size_t bytes) : bytes_(bytes) {
+// Page-locking is expensive (the driver pins every page), so freed pinned
+// blocks are kept in a small size-keyed pool and handed to the next buffer
+// of the same size: repeated calls on the same shapes pay it once.
+namespace {
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<std::size_t, void*> free_blocks;
+  std::size_t cached = 0;
+  static constexpr std::size_t kMaxCached = std::size_t(48) << 30;
+  void* take(std::size_t bytes) {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = free_blocks.find(bytes);
+    if (it == free_blocks.end()) return nullptr;
+    void* p = it->second;
+    free_blocks.erase(it);
+    cached -= bytes;
+    return p;
+  }
+  void give(void* p, std::size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (cached + bytes <= kMaxCached) {
+        free_blocks.emplace(bytes, p);
+        cached += bytes;
+        return;
+      }
+    }
+    cudaFreeHost(p);
+  }
+};
+PinnedPool& pool() {
+  static PinnedPool* p = new PinnedPool;  // leaked on purpose: outlives static teardown
+  return *p;
+}
+}  // namespace
+
+HostBuffer::HostBuffer(std::size_t bytes, bool zero) : bytes_(bytes) {
   if (bytes == 0) return;
   if (bytes >= kPinThreshold && engine::device_available()) {
-    if (cudaMallocHost(&ptr_, bytes) == cudaSuccess) {
+    ptr_ = pool().take(bytes);
+    if (!ptr_ && cudaMallocHost(&ptr_, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      ptr_ = nullptr;
+    }
+    if (ptr_) {
       pinned_ = true;
-      std::memset(ptr_, 0, bytes);
+      if (zero) std::memset(ptr_, 0, bytes);
       return;
     }
-    cudaGetLastError();
-    ptr_ = nullptr;
   }
-  ptr_ = std::calloc(bytes, 1);
+  ptr_ = zero ? std::calloc(bytes, 1) : std::malloc(bytes);
   if (!ptr_) throw std::bad_alloc();
 }
 HostBuffer::HostBuffer(const HostBuffer& o) : HostBuffer(o.bytes_) {
@@ -100,7 +140,7 @@ HostBuffer::~HostBuffer() { release(); }
 void HostBuffer::release() {
   if (!ptr_) return;
   if (pinned_)
-    cudaFreeHost(ptr_);
+    pool().give(ptr_, bytes_);
   else
     std::free(ptr_);
   ptr_ = nullptr;
@@ -112,6 +152,17 @@ DenseMatrix::DenseMatrix(index_t rows, index_t cols, Precision prec)
   if (rows < 0 || cols < 0) throw InvalidArgument("negative matrix dimension");
   const std::size_t elt = prec == Precision::Working ? sizeof(float) : sizeof(double);
   buf_ = detail::HostBuffer(static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols) * elt);
+}
+
+DenseMatrix DenseMatrix::uninitialized(index_t rows, index_t cols, Precision prec) {
+  if (rows < 0 || cols < 0) throw InvalidArgument("negative matrix dimension");
+  DenseMatrix a;
+  a.rows_ = rows;
+  a.cols_ = cols;
+  a.prec_ = prec;
+  const std::size_t elt = prec == Precision::Working ? sizeof(float) : sizeof(double);
+  a.buf_ = detail::HostBuffer(static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols) * elt, false);
+  return a;
 }
 
 DenseMatrix DenseMatrix::identity(index_t n, Precision prec) {
@@ -213,8 +264,8 @@ ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f
   p.execute(b.d_a, m, b.d_u, m, b.d_sigma, b.d_v, st);
   const Precision wp = f64 ? Precision::Higher : Precision::Working;
   ThinSvdResult out;
-  out.factors.u = DenseMatrix(m, n, wp);
-  out.factors.v = DenseMatrix(n, n, wp);
+  out.factors.u = DenseMatrix::uninitialized(m, n, wp);  // fully overwritten by the D2H below
+  out.factors.v = DenseMatrix::uninitialized(n, n, wp);
   out.factors.sigma.assign(n, 0.0);
   out.factors.precision = wp;
   engine::check(cudaMemcpyAsync(out.factors.u.raw(), b.d_u, m * n * elt, cudaMemcpyDeviceToHost, st), "D2H U");

@@ -280,9 +280,13 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
 }
 
 void Plan::eigen(cudaStream_t st) {
-  check(dev::launch_jacobi(dd, (int)n, effective_tol(), max_sweeps, jws, sm_count, st), "jacobi");
-  check(dev::launch_jacobi_replay(dd, (int)n, jws, st), "jacobi_replay");
-  launches += 2;
+  bool fused = false;
+  check(dev::launch_jacobi(dd, (int)n, effective_tol(), max_sweeps, jws, sm_count, st, &fused), "jacobi");
+  launches += 1;
+  if (!fused) {
+    check(dev::launch_jacobi_replay(dd, (int)n, jws, st), "jacobi_replay");
+    launches += 1;
+  }
 }
 
 void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,

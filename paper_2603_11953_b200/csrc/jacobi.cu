@@ -26,6 +26,9 @@
 // embarrassingly parallel replay over its rows (rows of V never mix).
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -592,7 +595,12 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
-constexpr int kUpdateWarps = 8;
+constexpr int kUpdateWarps = 12;
+constexpr int kRotWarps = 4;
+
+// Optional per-round timestamps of the first sweep (MPSVD_JACOBI_TRACE=1).
+__device__ unsigned long long* g_jtrace = nullptr;
+__device__ int g_jexp = 0;  // experiment switches (tracing only): 1 fake rotations, 2 skip pass 2
 
 // partner of x in `round` (n itself for the bye of an odd n)
 __device__ __forceinline__ int rr_partner(int n, int round, int x) {
@@ -601,20 +609,111 @@ __device__ __forceinline__ int rr_partner(int n, int round, int x) {
   return pp == x ? qq : pp;
 }
 
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+constexpr unsigned long long kProgressDone = 1ull << 63;
+
+// Fused V replay CTA: owns `rows` rows of V (shared memory), applies every
+// round the solver CTA has published (progress word, release/acquire), and
+// writes its rows once the solver reports completion. The rows of V never
+// mix, so the replay overlaps the solve instead of following it.
 template <typename ST>
-__global__ void __launch_bounds__(32 * (kUpdateWarps + 2))
+__device__ void replay_consumer(const ST* __restrict__ rot_log, int n, DevStatus* status, ST* __restrict__ v_out,
+                                int rows, ST* vr) {
+  using A_ = Arith<ST>;
+  using AT = typename A_::AT;
+  const int N = n + (n & 1), np = N / 2, R = N - 1;
+  const int row0 = (blockIdx.x - 1) * rows;
+  const int nrows = min(rows, n - row0);
+  if (nrows <= 0) return;
+  const int tid = threadIdx.x, bs = blockDim.x;
+  __shared__ unsigned long long s_prog;
+  for (int e = tid; e < nrows * n; e += bs) {
+    const int rr = e / n, cc = e - rr * n;
+    A_::st(vr + e, (row0 + rr == cc) ? A_::one() : A_::zero());
+  }
+  long long g = 0;
+  int r = 0;
+  const int items = nrows * np;
+  while (true) {
+    if (tid == 0) {
+      unsigned long long p;
+      while (true) {
+        p = ld_acquire_u64(&status->progress);
+        if ((long long)(p & ~kProgressDone) > g || (p & kProgressDone)) break;
+        __nanosleep(64);
+      }
+      s_prog = p;
+    }
+    __syncthreads();
+    const unsigned long long p = s_prog;
+    const long long avail = (long long)(p & ~kProgressDone);
+    for (; g < avail; ++g) {
+      const ST* lg = rot_log + 2 * g * np;
+      for (int w = tid; w < items; w += bs) {
+        const int rr = w / np, k = w - rr * np;
+        const AT c = A_::ldg(lg + 2 * k), s = A_::ldg(lg + 2 * k + 1);
+        if (A_::is_identity(c, s)) continue;
+        int pp, qq;
+        rr_pair(n, r, k, pp, qq);
+        ST* row = vr + (size_t)rr * n;
+        const AT t1 = A_::lds(row + pp), t2 = A_::lds(row + qq);
+        A_::st(row + pp, A_::rot_lo(c, s, t1, t2));
+        A_::st(row + qq, A_::rot_hi(c, s, t1, t2));
+      }
+      __syncthreads();
+      if (++r == R) r = 0;
+    }
+    if (p & kProgressDone) break;
+    __syncthreads();  // s_prog is rewritten only after every thread read it
+  }
+  for (int e = tid; e < nrows * n; e += bs) {
+    const int rr = e / n, cc = e - rr * n;
+    v_out[(size_t)cc * n + row0 + rr] = vr[e];
+  }
+}
+
+template <typename ST>
+__global__ void __launch_bounds__(1024)
 jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol, int max_sweeps,
-            DevStatus* __restrict__ status) {
+            DevStatus* __restrict__ status, ST* __restrict__ v_out, int cons_rows) {
   using A_ = Arith<ST>;
   using AT = typename A_::AT;
   extern __shared__ __align__(16) unsigned char jsm[];
+  if (blockIdx.x > 0) {  // fused V replay (cooperative launch: all CTAs co-resident)
+    replay_consumer<ST>(rot_log, n, status, v_out, cons_rows, reinterpret_cast<ST*>(jsm));
+    return;
+  }
   const int N = n + (n & 1), np = N / 2, Rr = N - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw_rot = (np + 31) / 32;  // rotation warps (1 or 2 here)
+  const bool fused = v_out != nullptr;
+  unsigned long long* const progress = &status->progress;
+  // 16 warps. Warps 0, 4, 8, 12 (scheduler partition 0, warp % 4 == 0) are
+  // the rotation warps: the latency-critical rotation chain gets a scheduler
+  // and an fp64 pipe of its own; the 12 update warps fill partitions 1-3.
+  const int nw_rot = (int)(blockDim.x / 128);  // one rotation warp per 4 warps
   const int NT = blockDim.x, n_rot = 32 * nw_rot, n_upd = NT - n_rot;
-  const bool is_rot = warp < nw_rot;
-  const int utid = tid - n_rot;  // update-thread index
-  const int lda = n + 1;         // odd pitch: row and column walks hit distinct banks
+  const bool is_rot = (warp & 3) == 0;
+  const int wr = warp >> 2, rtid = wr * 32 + lane;  // rotation-warp / rotation-thread index
+  unsigned long long* const jt = g_jtrace;  // read once: a global load per use would be timed too
+  const int jexp = g_jexp;
+  const int utid = (warp - (warp >> 2) - 1) * 32 + lane;  // update-thread index
+  const int nw_act = (np + 31) / 32;                      // rotation warps with slots (1 or 2)
+  const int NB12 = 32 * nw_act + n_upd;                   // participants of B2
+  // B1 also releases the publisher warp (the last rotation warp, idle in the
+  // solve) that announces each finished round to the fused replay CTAs
+  const bool is_pub = fused && is_rot && wr == nw_rot - 1;
+  const int NB1 = NB12 + (fused ? 32 : 0);
+  // pitch n+2 (even n): the arithmetic progressions of the round-robin
+  // schedule ((r+k, r-k+2), (r+k, r+k), ...) then step by an odd number of
+  // 8-byte words, i.e. hit distinct banks (n+1 makes (r-k, r+k+2) step by n).
+  const int lda = (n | 1) + 1;
   const unsigned FULL = 0xffffffffu;
 
   ST* a = reinterpret_cast<ST*>(jsm);
@@ -624,8 +723,8 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
   int* pwb = reinterpret_cast<int*>(rbase + (size_t)8 * np);  // [2][np]
   int* blk = pwb + 2 * np;                                      // idx -> aa | bb << 16
   __shared__ int s_abort, s_bad, s_flag;
-  __shared__ int w_cnt[2];
-  __shared__ double w_worst[2];
+  __shared__ int w_cnt[8];
+  __shared__ double w_worst[8];
   auto AE = [&](int row, int col) -> ST* { return a + col * lda + row; };
 
   for (int e = tid; e < n * n; e += NT) a[(e / n) * lda + e % n] = a_glob[e];
@@ -634,6 +733,16 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     while (bb * (bb + 1) / 2 > idx) --bb;
     while ((bb + 1) * (bb + 2) / 2 <= idx) ++bb;
     blk[idx] = (idx - bb * (bb + 1) / 2) | (bb << 16);
+  }
+  // priority blocks (diagonal, (k, k+2), (np-2, np-1), (0, 1) for even n)
+  int* pri = blk + np * (np + 1) / 2;
+  int npri = 0;
+  {
+    const bool ev = (n & 1) == 0;
+    for (int k = 0; k < np; ++k) pri[npri++] = k | (k << 16);
+    for (int k = 0; k + 2 < np; ++k) pri[npri++] = k | ((k + 2) << 16);
+    if (np >= 2) pri[npri++] = (np - 2) | ((np - 1) << 16);
+    if (ev && np >= 3) pri[npri++] = 0 | (1 << 16);
   }
   if (tid == 0) {
     s_abort = 0;
@@ -651,6 +760,10 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
       status->sweeps = 0;
       status->rotations = 0;
       status->rounds = 0;
+      if (fused) {
+        __threadfence();
+        st_release_u64(progress, kProgressDone);
+      }
     }
     return;
   }
@@ -759,11 +872,12 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
       // ===== rotation warps =====
       long long cnt_sweep = 0;
       double wmax = 0.0;
-      for (int r = 0; r < Rr; ++r) {
-        if (r > 0) nbar_sync(2, NT);  // round-r diagonal entries are final
+      for (int r = 0; r < (wr < nw_act ? Rr : 0); ++r) {  // idle rotation warps skip the sweep
+        if (r > 0) nbar_sync(2, NB12);  // round-r diagonal entries are final
+        if (jt && sweep == 0 && r < 64 && rtid == 0) jt[r * 16 + 0] = clock64();
         AT* rb = RC((int)((g + r) & 1));
         int* pw = pwb + ((g + r) & 1) * np;
-        const int k = tid;  // one slot per rotation thread (np <= 64 here)
+        const int k = rtid;  // one slot per rotation thread (np <= 64 here)
         int bad = 0x7fffffff, act_i = 0;
         if (k < np) {
           int pp, qq;
@@ -774,11 +888,15 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
             aqq = A_::lds(AE(qq, qq));
             apq = A_::lds(AE(pp, qq));
           }
-          const bool act = qq < n && A_::active(app, aqq, apq, tol);
+          if (jt && sweep == 0 && r < 64 && rtid == 0 && A_::hi(app) != -1.0) jt[r * 16 + 6] = clock64();
+          const bool act = qq < n && ((jexp & 1) ? true : A_::active(app, aqq, apq, tol));
           if (want_ratio && qq < n) wmax = fmax(wmax, A_::ratio(app, aqq, apq));
           AT c = A_::one(), s = A_::zero(), npp = app, nqq = aqq;
           if (__any_sync(__activemask(), act)) {
             AT c2, s2, np2, nq2;
+            if (jexp & 1) {
+              c2 = A_::one(); s2 = A_::zero(); np2 = app; nq2 = aqq;
+            } else
             A_::rotate(act ? app : A_::one(), act ? aqq : A_::one(), act ? apq : A_::one(), c2, s2, np2, nq2);
             if (act) {
               c = c2;
@@ -789,6 +907,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
               if (!A_::gt0(nqq)) bad = min(bad, qq);
             }
           }
+          if (jt && sweep == 0 && r < 64 && rtid == 0 && A_::hi(c) != -7.0) jt[r * 16 + 7] = clock64();
           act_i = act ? 1 : 0;
           rb[k] = c;
           rb[np + k] = s;
@@ -801,13 +920,13 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
         }
         cnt_sweep += __popc(__ballot_sync(FULL, act_i));
         bad = warp_min(bad);
-        if (nw_rot > 1) {
+        if (nw_act > 1) {
           if (lane == 0 && bad != 0x7fffffff) atomicMin(&s_bad, bad);
-          nbar_sync(4, n_rot);
+          nbar_sync(4, 32 * nw_act);
           bad = s_bad;
         }
         if (bad != 0x7fffffff) {
-          if (tid == 0) {
+          if (rtid == 0) {
             const int kk = rr_slot(n, r, bad);
             const int pp = pw[kk] & 0x7fff;
             status->status = kNotPositiveDefinite;
@@ -819,20 +938,33 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
             s_abort = 1;
           }
           __syncwarp();
-          nbar_arrive(1, NT);  // release the update warps; they see s_abort
+          nbar_arrive(1, NB1);  // release the update warps; they see s_abort
           break;
         }
-        nbar_arrive(1, NT);
+        if (jt && sweep == 0 && r < 64 && rtid == 0) jt[r * 16 + 1] = clock64();
+        nbar_arrive(1, NB1);
+      }
+      if (is_pub) {  // publisher: round g+r's log entries are complete after B1
+        for (int r = 0; r < Rr; ++r) {
+          nbar_sync(1, NB1);
+          if (s_abort) break;
+          if (lane == 0) {
+            __threadfence();
+            st_release_u64(progress, (unsigned long long)(g + r + 1));
+          }
+        }
       }
       const double wm = want_ratio ? warp_max(wmax) : 0.0;
       if (lane == 0) {
-        w_cnt[warp] = (int)cnt_sweep;
-        w_worst[warp] = wm;
+        w_cnt[wr] = (int)cnt_sweep;
+        w_worst[wr] = wm;
       }
     } else {
       // ===== update warps =====
       for (int r = 0; r < Rr; ++r) {
-        nbar_sync(1, NT);
+        nbar_sync(1, NB1);
+        const bool trace = jt && sweep == 0 && r < 64 && utid == 0;
+        if (trace && blk[0] != -1) jt[r * 16 + 2] = clock64();  // after B1 really completed
         if (s_abort) break;
         const int b = (int)((g + r) & 1);
         const AT* rb = RC(b);
@@ -848,37 +980,40 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
         auto priority = [&](int aa, int bb) {
           return bb == aa || bb == aa + 2 || (bb == aa + 1 && (aa == np - 2 || (even_n && aa == 0)));
         };
-        if (has_next) {
-          // pass 1: the priority blocks, then release the rotation warps
-          const int n1 = 2 * np;  // np diagonal + up to np priority off-diagonal slots
-          for (int j = utid; j < n1; j += n_upd) {
-            if (j < np) {
-              update_block(j, j, rb, pw);
-            } else {
-              const int k = j - np;
-              if (k <= np - 3)
-                update_block(k, k + 2, rb, pw);
-              else if (k == np - 2 && np >= 2)
-                update_block(np - 2, np - 1, rb, pw);
-              else if (k == np - 1 && even_n && np >= 3)
-                update_block(0, 1, rb, pw);
-            }
-          }
-          nbar_arrive(2, NT);
-        }
-        // pass 2: every other block (decode table built once per launch)
+        // Two phases through ONE code path (a single inlined copy of the block
+        // update keeps the hot loop small in the instruction caches):
+        // phase 0 = the priority blocks, then release the rotation warps;
+        // phase 1 = every other block (decode table built once per launch).
         const int nblk = np * (np + 1) / 2;
-        for (int idx = utid; idx < nblk; idx += n_upd) {
-          const int w = blk[idx];
-          const int aa = w & 0xffff, bb = w >> 16;
-          if (has_next && priority(aa, bb)) continue;
-          update_block(aa, bb, rb, pw);
+        for (int ph = has_next ? 0 : 1; ph < 2; ++ph) {
+          const int cnt_ph = ph == 0 ? npri : ((jexp & 2) ? 0 : nblk);
+          const int* list = ph == 0 ? pri : blk;
+          for (int j = utid; j < cnt_ph; j += n_upd) {
+            const int w = list[j];
+            const int aa = w & 0xffff, bb = w >> 16;
+            if (ph == 1 && has_next && priority(aa, bb)) continue;
+            update_block(aa, bb, rb, pw);
+          }
+          if (ph == 0) {
+            if (trace) jt[r * 16 + 3] = clock64();
+            nbar_arrive(2, NB12);
+            nbar_sync(5, n_upd);  // pass-2 traffic waits for the critical blocks
+            if (trace && blk[1] != -1) jt[r * 16 + 8] = clock64();  // pass 1 of all U warps done
+          }
         }
+        if (trace) jt[r * 16 + 4] = clock64();
         nbar_sync(3, n_upd);
+        if (trace) jt[r * 16 + 5] = clock64();
       }
     }
     __syncthreads();
-    if (s_abort) return;
+    if (s_abort) {
+      if (fused && tid == 0) {
+        __threadfence();
+        st_release_u64(progress, kProgressDone);
+      }
+      return;
+    }
     long long cnt = 0;
     for (int w = 0; w < nw_rot; ++w) {
       cnt += w_cnt[w];
@@ -901,6 +1036,10 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     status->sweeps = sweeps;
     status->rotations = rotations;
     status->rounds = g;
+    if (fused) {
+      __threadfence();
+      st_release_u64(progress, kProgressDone | (unsigned long long)g);
+    }
   }
 }
 
@@ -1011,6 +1150,71 @@ __global__ void finish_sort(const ST* __restrict__ a, int n, DevStatus* __restri
   }
 }
 
+// V replay for fp64 and n <= 128: one warp per row of V, the row held in
+// registers (lane l owns columns l, l+32, ...); a rotation's partner value
+// comes from another lane by shuffle, so rounds need no block barrier.
+template <int NC>
+__global__ void __launch_bounds__(128)
+jacobi_replay_rows(const double2* __restrict__ rot_log, int n, const DevStatus* __restrict__ status,
+                   double* __restrict__ v_out) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n) return;  // warp-uniform
+  const int N = n + (n & 1), np = N / 2, R = N - 1;
+  const unsigned FULL = 0xffffffffu;
+  double v[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) v[j] = (lane + 32 * j == row) ? 1.0 : 0.0;
+  const int st = status->status;
+  const long long total = (st == kOk || st == kNoConvergence) ? status->rounds : 0;
+  int r = 0;
+#pragma unroll 2
+  for (long long g = 0; g < total; ++g) {
+    const double2* lg = rot_log + g * np;
+    int part[NC], slot[NC];
+    bool isp[NC];
+    double2 cs[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int col = lane + 32 * j;
+      part[j] = n;
+      isp[j] = true;
+      cs[j] = make_double2(1.0, 0.0);
+      if (col < n) {
+        slot[j] = rr_slot(n, r, col);
+        int pp, qq;
+        rr_pair(n, r, slot[j], pp, qq);
+        isp[j] = pp == col;
+        part[j] = isp[j] ? qq : pp;
+        cs[j] = __ldg(lg + slot[j]);
+      }
+    }
+    double vy[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) vy[j] = 0.0;
+#pragma unroll
+    for (int src = 0; src < NC; ++src) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const double t = __shfl_sync(FULL, v[src], part[j] & 31);
+        if ((part[j] >> 5) == src) vy[j] = t;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const double c = cs[j].x, s = cs[j].y;
+      if (part[j] < n && !(s == 0.0 && c == 1.0))
+        v[j] = isp[j] ? fma(c, v[j], -(s * vy[j])) : fma(s, vy[j], c * v[j]);
+    }
+    if (++r == R) r = 0;
+  }
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int col = lane + 32 * j;
+    if (col < n) v_out[(long long)col * n + row] = v[j];
+  }
+}
+
 template <typename ST, typename WT>
 __global__ void finish_columns(const ST* __restrict__ v, int n, const DevStatus* __restrict__ status,
                                const int* __restrict__ perm, const double* __restrict__ sigma,
@@ -1103,7 +1307,8 @@ size_t jacobi_log_elems(int n, int max_sweeps) {
 
 template <typename ST>
 static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const JacobiWorkspace& ws,
-                                   int sm_count, cudaStream_t st) {
+                                   int sm_count, cudaStream_t st, bool* fused_replay) {
+  if (fused_replay) *fused_replay = false;
   const int N = n + (n & 1), np = N / 2;
   const size_t smem_a = (size_t)n * (n + 1) * sizeof(ST) + (size_t)np * (np + 1) / 2 * sizeof(int);
   const size_t smem_rot = rot_smem_bytes<ST>(np);
@@ -1114,14 +1319,61 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   DevStatus* status = ws.status;
   // zero the two sweep flag words that follow the double-buffered diag blocks
   cudaMemsetAsync(reinterpret_cast<unsigned char*>(ws.diagbuf) + (size_t)6 * np * sizeof(ST), 0, 16, st);
-  const size_t smem_pipe = (size_t)n * (n + 1) * sizeof(ST) +
+  const size_t smem_pipe = (size_t)n * ((n | 1) + 1) * sizeof(ST) +
                            (size_t)np * (8 * sizeof(typename Arith<ST>::AT) + 2 * sizeof(int)) +
-                           (size_t)np * (np + 1) / 2 * sizeof(int);
+                           ((size_t)np * (np + 1) / 2 + 2 * np) * sizeof(int);
   if (np <= 64 && smem_pipe <= smem_limit) {  // warp-specialised single-CTA solver
     auto k = jacobi_smem<ST>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pipe);
-    const int threads = 32 * ((np + 31) / 32 + kUpdateWarps);
-    k<<<1, threads, smem_pipe, st>>>(a, lg, n, tol, max_sweeps, status);
+    static const int warps_env = getenv("MPSVD_JACOBI_WARPS") ? atoi(getenv("MPSVD_JACOBI_WARPS")) : 16;
+    const int threads = 32 * warps_env;
+    static const bool trace = getenv("MPSVD_JACOBI_TRACE") != nullptr;
+    unsigned long long* tbuf = nullptr;
+    if (trace) {
+      cudaMalloc(&tbuf, 64 * 16 * sizeof(unsigned long long));
+      cudaMemset(tbuf, 0, 64 * 16 * sizeof(unsigned long long));
+      cudaMemcpyToSymbol(g_jtrace, &tbuf, sizeof(tbuf));
+      const int ex = getenv("MPSVD_JACOBI_EXP") ? atoi(getenv("MPSVD_JACOBI_EXP")) : 0;
+      cudaMemcpyToSymbol(g_jexp, &ex, sizeof(ex));
+    }
+    // CTA 0 solves; CTAs 1.. replay V concurrently (cooperative launch, so
+    // every CTA is resident and the consumers' progress polling is safe)
+    const int rows = 8, ncons = (n + rows - 1) / rows;
+    ST* vout = (ST*)ws.v;
+    int nn = n, ms = max_sweeps, rw = rows;
+    double tl = tol;
+    void* args[] = {&a, &lg, &nn, &tl, &ms, &status, &vout, &rw};
+    const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k, dim3(1 + ncons), dim3(threads), args,
+                                                       smem_pipe, st);
+    if (le != cudaSuccess) return le;
+    if (fused_replay) *fused_replay = true;
+    if (trace) {
+      unsigned long long h[64 * 16];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);
+      unsigned long long* nul = nullptr;
+      cudaMemcpyToSymbol(g_jtrace, &nul, sizeof(nul));
+      cudaFree(tbuf);
+      // per round (cycles, SM clock): R = rotation warp, U = update warps
+      double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+      int cnt = 0;
+      for (int r = 1; r + 1 < 63 && h[(r + 1) * 16 + 0]; ++r, ++cnt) {
+        const unsigned long long* t = h + r * 16;
+        acc[0] += (double)(t[16 + 2] - t[2]);  // period (U B1 to next U B1)
+        acc[1] += (double)(t[6] - t[0]);        // R: B2 wait + loads
+        acc[2] += (double)(t[7] - t[6]);        // R: rotation math
+        acc[3] += (double)(t[1] - t[7]);        // R: stores + reductions
+        acc[4] += (double)(t[3] - t[2]);        // U: pass 1 (first U thread)
+        acc[5] += (double)(t[8] - t[3]);        // U: wait for all pass-1 warps
+        acc[6] += (double)(t[4] - t[8]);        // U: pass 2 (first U thread)
+      }
+      if (cnt)
+        fprintf(stderr,
+                "[jacobi trace n=%d] period %.0f | R: B2 wait+loads %.0f, math %.0f, tail %.0f | U: pass1 %.0f, "
+                "pass1 all %.0f, pass2 %.0f (cycles/round, %d rounds)\n",
+                n, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt, acc[6] / cnt,
+                cnt);
+    }
     return cudaGetLastError();
   }
   if (smem_a + smem_rot <= smem_limit) {
@@ -1148,9 +1400,9 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
 }
 
 cudaError_t launch_jacobi(bool dd_mode, int n, double tol, int max_sweeps, const JacobiWorkspace& ws,
-                          int sm_count, cudaStream_t st) {
-  return dd_mode ? launch_jacobi_t<double2>(n, tol, max_sweeps, ws, sm_count, st)
-                 : launch_jacobi_t<double>(n, tol, max_sweeps, ws, sm_count, st);
+                          int sm_count, cudaStream_t st, bool* fused_replay) {
+  return dd_mode ? launch_jacobi_t<double2>(n, tol, max_sweeps, ws, sm_count, st, fused_replay)
+                 : launch_jacobi_t<double>(n, tol, max_sweeps, ws, sm_count, st, fused_replay);
 }
 
 template <typename ST>
@@ -1175,6 +1427,18 @@ static cudaError_t launch_replay_t(int n, const JacobiWorkspace& ws, cudaStream_
 }
 
 cudaError_t launch_jacobi_replay(bool dd_mode, int n, const JacobiWorkspace& ws, cudaStream_t st) {
+  if (!dd_mode && n <= 128) {
+    const int grid = (n + 3) / 4;
+    const double2* lg = (const double2*)ws.log;
+    double* v = (double*)ws.v;
+    if (n <= 32)
+      jacobi_replay_rows<1><<<grid, 128, 0, st>>>(lg, n, ws.status, v);
+    else if (n <= 64)
+      jacobi_replay_rows<2><<<grid, 128, 0, st>>>(lg, n, ws.status, v);
+    else
+      jacobi_replay_rows<4><<<grid, 128, 0, st>>>(lg, n, ws.status, v);
+    return cudaGetLastError();
+  }
   return dd_mode ? launch_replay_t<double2>(n, ws, st) : launch_replay_t<double>(n, ws, st);
 }
 

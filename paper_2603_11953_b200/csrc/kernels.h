@@ -38,8 +38,10 @@ struct JacobiWorkspace {
   DevStatus* status;
 };
 size_t jacobi_log_elems(int n, int max_sweeps);
+// *fused_replay is set when the launch also rebuilt V (single-CTA solver with
+// co-resident replay CTAs); launch_jacobi_replay is then unnecessary.
 cudaError_t launch_jacobi(bool dd, int n, double tol, int max_sweeps, const JacobiWorkspace& ws,
-                          int sm_count, cudaStream_t st);
+                          int sm_count, cudaStream_t st, bool* fused_replay = nullptr);
 cudaError_t launch_jacobi_replay(bool dd, int n, const JacobiWorkspace& ws, cudaStream_t st);
 
 // finish: sort, sign, sigma, V in working precision, W = V / sigma.

@@ -214,3 +214,36 @@ def test_thin_svd_f64_dd_small(port):
     assert max_rel(r.sigma, o.sigma) <= g_sigma
     assert orth_err(r.v) <= g_orth
     assert orth_err(r.u) <= g_orth
+
+
+# ---------------------------------------------------------------------------
+# Device-resident plan API (bench path) and the NCCL exchange with one rank
+@pytest.mark.parametrize("working", ["f32", "f64"])
+def test_plan_api_matches_host_api_and_single_rank_nccl(working):
+    torch = pytest.importorskip("torch")
+    m, n = 8192, 40
+    if working == "f32":
+        a = inputs.graded(m, n, 4.0, seed=3)
+        prec = M.Precision.WORKING
+        host = M.mp_thin_svd(a)
+    else:
+        a = inputs.graded(m, n, 10.0, seed=3, dtype=np.float64)
+        prec = M.Precision.HIGHER
+        host = M.mp_thin_svd_f64(a)
+    dev = torch.device("cuda", 0)
+    a_t = torch.from_numpy(np.ascontiguousarray(a.T)).to(dev)  # (n, m) row-major = column-major m x n
+    outs = []
+    comm = M.Comm(M.Comm.unique_id(), 1, 0)
+    for c in (None, comm):
+        plan = M.Plan(m, n, prec, c)
+        u = torch.empty_like(a_t)
+        s = torch.empty(n, dtype=torch.float64, device=dev)
+        v = torch.empty((n, n), dtype=a_t.dtype, device=dev)
+        plan.execute(a_t.data_ptr(), m, u.data_ptr(), m, s.data_ptr(), v.data_ptr(), 0)
+        info = plan.wait()
+        assert info.status == 0 and info.kernel_launches >= 7
+        outs.append((u.T.cpu().numpy(), s.cpu().numpy(), v.T.cpu().numpy()))
+    for u, s, v in outs:
+        assert np.array_equal(s, host.sigma)
+        assert np.array_equal(v, host.v)
+        assert np.array_equal(u, host.u)

@@ -5,7 +5,7 @@ import csv
 import sys
 
 
-def main(path, pattern="mpsvd"):
+def main(path, pattern=""):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]

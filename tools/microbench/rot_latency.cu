@@ -1,0 +1,78 @@
+// Latency of one fp64 Jacobi rotation (the formula of csrc/jacobi.cu) for one
+// warp, dependent chain, vs the pieces (sqrt, div) on their own.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __noinline__ double scaled_hypot(double x, double y, double big) {
+  int e;
+  frexp(big, &e);
+  const double xs = ldexp(x, -e), ys = ldexp(y, -e);
+  return ldexp(sqrt(fma(xs, xs, ys * ys)), e);
+}
+
+__global__ void rot_chain(double* out, int iters, double tol) {
+  double app = 2.0 + threadIdx.x * 1e-3, aqq = 1.0, apq = 0.25;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const double pr = app * aqq;
+    const double thresh = (pr > 0x1p-1000 && pr < 0x1p1000) ? tol * sqrt(pr) : tol * sqrt(app) * sqrt(aqq);
+    const bool act = !(fabs(apq) <= thresh);
+    const double x = aqq - app, y = 2.0 * apq, ax = fabs(x);
+    const double big = fmax(ax, fabs(y));
+    const double r = (big < 0x1p500 && big > 0x1p-500) ? sqrt(fma(x, x, y * y)) : scaled_hypot(x, y, big);
+    const double den = ax + r;
+    const double t = x == 0.0 ? 1.0 : (x > 0.0 ? y : -y) / den;
+    const double c = sqrt(den / (2.0 * r));
+    const double s = c * t;
+    // feed back so iterations are dependent
+    app = 2.0 + s * 1e-9 + (act ? 0.0 : 1e-300);
+    apq = 0.25 + c * 1e-9;
+  }
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / iters; out[1] = app + apq; }
+}
+
+__global__ void sqrt_chain(double* out, int iters) {
+  double v = 2.0 + threadIdx.x;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) v = sqrt(v) + 1.0;
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / iters; out[1] = v; }
+}
+
+__global__ void div_chain(double* out, int iters) {
+  double v = 2.0 + threadIdx.x;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) v = 3.0 / v + 1.0;
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / iters; out[1] = v; }
+}
+
+__global__ void dfma_chain(double* out, int iters) {
+  double v = 2.0 + threadIdx.x;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) v = fma(v, 0.999, 1e-3);
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / iters; out[1] = v; }
+}
+
+int main() {
+  double* d;
+  cudaMalloc(&d, 16);
+  double h[2];
+  const int it = 2000;
+  rot_chain<<<1, 32>>>(d, it, 64 * 0x1p-53);
+  rot_chain<<<1, 32>>>(d, it, 64 * 0x1p-53);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("rotation chain: %.1f cycles/rotation\n", h[0]);
+  sqrt_chain<<<1, 32>>>(d, it);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("sqrt+add chain: %.1f cycles\n", h[0]);
+  div_chain<<<1, 32>>>(d, it);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("div+add chain: %.1f cycles\n", h[0]);
+  dfma_chain<<<1, 32>>>(d, it);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("dfma chain: %.1f cycles\n", h[0]);
+  return 0;
+}
