@@ -191,7 +191,13 @@ def run_ours(args, cfg):
         dist.broadcast_object_list(uid, src=0)
         comm = M.Comm(uid[0], world, rank)
 
-    a_t = inputs.device_make(cfg, seed=1 + rank, m=m_local, device=dev)  # (n, m) = column-major m x n
+    def allreduce_cpu(t):
+        c = t.cpu()
+        dist.all_reduce(c)
+        return c.to(t.device)
+
+    a_t = inputs.device_make(cfg, seed=1, m=m_local, device=dev, rank=rank,
+                             allreduce=allreduce_cpu if world > 1 else None)  # (n, m) = column-major m x n
     u_t = torch.empty_like(a_t)
     sig_t = torch.empty(n, dtype=torch.float64, device=dev)
     v_t = torch.empty((n, n), dtype=a_t.dtype, device=dev)
@@ -251,7 +257,10 @@ def run_ours(args, cfg):
     e2e = None
     if world == 1:
         host = M.Matrix(m_local, n, working)
-        host.numpy()[...] = a_t.T.cpu().numpy()
+        host.numpy()[...] = a_t.cpu().numpy().T
+        # free the device-resident arm before the API allocates its own buffers
+        del plan, a_t, u_t, v_t, sig_t
+        torch.cuda.empty_cache()
         call = M.mp_thin_svd if cfg.working == "f32" else M.mp_thin_svd_f64
         r = call(host)  # warm: plan, device buffers, pinned result buffers
         del r

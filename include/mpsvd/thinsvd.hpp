@@ -24,6 +24,17 @@ struct JacobiConfig {
   int max_sweeps = 30;  // NoConvergenceError beyond this
 };
 
+// Default for the double-double path (ADDITIVE). Two-sided Jacobi needs more
+// sweeps to reach tol = n * 2^-104 on ill-conditioned, non-graded Grams (the
+// BASELINE C5 matrices: ~30 sweeps at n = 128, ~37 at n = 256), so the
+// cap is 100 instead of the fp64 path's 30.
+constexpr int kDdMaxSweeps = 100;
+inline JacobiConfig dd_jacobi_config() {
+  JacobiConfig c;
+  c.max_sweeps = kDdMaxSweeps;
+  return c;
+}
+
 struct SvdFactors {
   DenseMatrix u;
   std::vector<double> sigma;  // descending, exact in `precision`
@@ -71,7 +82,8 @@ struct ThinSvdResult {
 ThinSvdResult mp_thin_svd(const DenseMatrix& a, EigensolverChoice choice,
                           const JacobiConfig& cfg = {}, int threads = 1);
 
-ThinSvdResult mp_thin_svd_f64(const DenseMatrix& a, const JacobiConfig& cfg = {}, int threads = 1);
+ThinSvdResult mp_thin_svd_f64(const DenseMatrix& a, const JacobiConfig& cfg = dd_jacobi_config(),
+                              int threads = 1);
 
 EigFactors twosided_jacobi_eig(const DenseMatrix& m, const JacobiConfig& cfg = {},
                                JacobiStats* stats = nullptr);

@@ -997,7 +997,8 @@ int port_thin_svd_f64dd(const double* a, int64_t m, int64_t n, int threads, int 
   double* lh = (double*)malloc(sizeof(double) * (size_t)n);
   double* ll = (double*)malloc(sizeof(double) * (size_t)n);
   double* vl = (double*)malloc(sizeof(double) * (size_t)(n * n));
-  int st = port_twosided_jacobi_dd(ghi, glo, n, 0.0, 30, sem, lh, ll, v, vl, NULL, err);
+  /* sweep cap of the double-double path: kDdMaxSweeps (include/mpsvd/thinsvd.hpp) */
+  int st = port_twosided_jacobi_dd(ghi, glo, n, 0.0, 100, sem, lh, ll, v, vl, NULL, err);
   free(ghi);
   free(glo);
   free(vl);

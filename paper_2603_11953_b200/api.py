@@ -251,6 +251,10 @@ def mp_thin_svd(a, choice: EigensolverChoice = EigensolverChoice.TWOSIDED_JACOBI
     return _result(r)
 
 
+# thinsvd.hpp kDdMaxSweeps: sweep cap of the double-double path
+DD_MAX_SWEEPS = 100
+
+
 def mp_thin_svd_f64(a, threads: int = 1) -> ThinSvdResult:
     """ADDITIVE: fp64 A, Gram + Jacobi in double-double, U in fp64."""
     mat = a if isinstance(a, Matrix) else Matrix.from_numpy(np.asarray(a, dtype=np.float64))
@@ -283,12 +287,14 @@ def gram(a: np.ndarray):
     return hi if prec == Precision.WORKING else (hi, lo)
 
 
-def twosided_jacobi_eig(m_hi, m_lo=None, dd: bool = False, tol: float = 0.0, max_sweeps: int = 30):
+def twosided_jacobi_eig(m_hi, m_lo=None, dd: bool = False, tol: float = 0.0, max_sweeps: int | None = None):
     """Device two-sided Jacobi (jacobi.hpp:45-46); returns (lambda, V, sweeps, rotations).
 
     With ``dd`` the matrix is double-double (``m_lo`` its low words) and
     lambda / V come back as (hi, lo) pairs.
     """
+    if max_sweeps is None:
+        max_sweeps = DD_MAX_SWEEPS if dd else 30
     m_hi = np.asfortranarray(m_hi, dtype=np.float64)
     n = m_hi.shape[0]
     lo_in = np.asfortranarray(m_lo, dtype=np.float64) if m_lo is not None else None

@@ -607,7 +607,7 @@ mpsvd_status mpsvd_thin_svd(const mpsvd_matrix* a, mpsvd_eigensolver eig, int th
 mpsvd_status mpsvd_thin_svd_f64(const mpsvd_matrix* a, int threads, mpsvd_svd_result** out) {
   return guarded([&] {
     require(a != nullptr && out != nullptr, "null argument");
-    *out = wrap(mpsvd::mp_thin_svd_f64(a->m, {}, threads));
+    *out = wrap(mpsvd::mp_thin_svd_f64(a->m, mpsvd::dd_jacobi_config(), threads));
   });
 }
 

@@ -177,6 +177,7 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   check(cudaGetDevice(&device), "cudaGetDevice");
   check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
   gram_occupancy = dd ? 1 : 2;
+  max_sweeps = dd ? 100 : 30;  // thinsvd.hpp kDdMaxSweeps / jacobi.hpp:31
   build_schedule(*this);
   const size_t nn = (size_t)n * n;
   const size_t esz = dd ? 2 : 1;  // doubles per element of the higher precision
@@ -202,7 +203,7 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   }
   jws.a = d_m;
   jws.diagbuf = dalloc<double>((size_t)2 * np * 3 * esz + 2, owned);  // + sweep flags
-  jws.log = dalloc<double>(dev::jacobi_log_elems((int)n, max_sweeps_cap) * esz, owned);
+  jws.log = nullptr;  // sized on first set_jacobi / execute for the requested sweep cap
   jws.v = dalloc<double>(nn * esz, owned);
   jws.status = dalloc<DevStatus>(1, owned);
   d_perm = dalloc<int>(n, owned);
@@ -222,14 +223,31 @@ Plan::~Plan() {
     if (e) cudaEventDestroy(e);
   if (own_stream) cudaStreamDestroy(own_stream);
   if (h_status) cudaFreeHost(h_status);
-  for (void* p : owned) cudaFree(p);
+  for (void* p : owned)
+    if (p) cudaFree(p);
 }
 
 void Plan::set_jacobi(double t, int sweeps) {
   if (sweeps < 1) throw std::invalid_argument("max_sweeps must be >= 1");
-  if (sweeps > max_sweeps_cap) throw std::invalid_argument("max_sweeps above the plan's log capacity (30)");
+  if (sweeps > 1000) throw std::invalid_argument("max_sweeps must be <= 1000");
   tol = t;
   max_sweeps = sweeps;
+  ensure_log();
+}
+
+// The rotation log holds every sweep's (c, s) pairs for the V replay, so its
+// size follows the sweep cap: reallocated (never shrunk) when a larger cap is
+// requested.
+void Plan::ensure_log() {
+  if (max_sweeps <= log_sweeps) return;
+  if (jws.log) {
+    check(cudaDeviceSynchronize(), "sync before log resize");
+    for (auto& p : owned)
+      if (p == jws.log) p = nullptr;
+    check(cudaFree(jws.log), "free log");
+  }
+  jws.log = dalloc<double>(dev::jacobi_log_elems((int)n, max_sweeps) * (dd ? 2 : 1), owned);
+  log_sweeps = max_sweeps;
 }
 
 double Plan::effective_tol() const {
@@ -280,6 +298,7 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
 }
 
 void Plan::eigen(cudaStream_t st) {
+  ensure_log();
   bool fused = false;
   check(dev::launch_jacobi(dd, (int)n, effective_tol(), max_sweeps, jws, sm_count, st, &fused), "jacobi");
   launches += 1;

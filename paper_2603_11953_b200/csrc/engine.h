@@ -27,6 +27,7 @@ class Plan {
   Plan& operator=(const Plan&) = delete;
 
   void set_jacobi(double tol, int max_sweeps);
+  void ensure_log();
   // Enqueue the whole pipeline on `st` (nullptr: the plan's stream).
   void execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                cudaStream_t st);
@@ -46,7 +47,7 @@ class Plan {
   int device = 0, sm_count = 148, gram_occupancy = 3;
   double tol = 0.0;
   int max_sweeps = 30;
-  static constexpr int max_sweeps_cap = 30;
+  int log_sweeps = 0;  // sweeps the rotation log (jws.log) can hold; grown by set_jacobi
 
   std::vector<int2> tiles;
   std::vector<longlong2> splits;

@@ -84,14 +84,21 @@ def make(cfg: Config, seed: int = 1, m: int | None = None):
     return a
 
 
-def device_make(cfg: Config, seed: int = 1, m: int | None = None, device="cuda"):
+def device_make(cfg: Config, seed: int = 1, m: int | None = None, device="cuda", rank: int = 0,
+                allreduce=None):
     """The same distribution generated on the GPU (torch), column-major as a
-    (n, m) row-major tensor whose transpose is the m x n matrix."""
+    (n, m) row-major tensor whose transpose is the m x n matrix.
+
+    For a row-sharded run each rank passes its ``rank`` (its rows come from
+    their own stream) and, for the prescribed-sigma kind, an ``allreduce``
+    callable summing an n x n fp64 tensor over ranks, so that U0 is
+    orthonormal over the global rows and V0 is shared.
+    """
     import torch
 
     m = cfg.m if m is None else m
     g = torch.Generator(device=device)
-    g.manual_seed(seed)
+    g.manual_seed(seed * 1000003 + rank)
     dt = torch.float32 if cfg.working == "f32" else torch.float64
     n = cfg.n
     if cfg.kind == "gaussian":
@@ -104,15 +111,24 @@ def device_make(cfg: Config, seed: int = 1, m: int | None = None, device="cuda")
             col /= torch.linalg.vector_norm(col)
             out[j] = (col * d[j]).to(dt)
         return out
-    # prescribed: CholQR2 in fp64 on the GPU for U0
-    x = torch.randn((m, n), generator=g, device=device, dtype=torch.float64)
+    # prescribed: A^T = V0 diag(sigma) U0^T with U0 from CholQR2 (fp64, on the
+    # GPU), kept as U0^T (n x m) throughout so no m x n transpose is needed.
+    xt = torch.randn((n, m), generator=g, device=device, dtype=torch.float64)
     for _ in range(2):
-        r = torch.linalg.cholesky(x.T @ x, upper=True)
-        x = torch.linalg.solve_triangular(r, x, upper=True, left=False)
-    gv = torch.randn((n, n), generator=g, device=device, dtype=torch.float64)
+        gram = xt @ xt.T
+        if allreduce is not None:
+            gram = allreduce(gram)
+        r = torch.linalg.cholesky(gram, upper=True)
+        xt = torch.linalg.solve_triangular(r.T, xt, upper=False, left=True)  # (X R^-1)^T
+        del gram, r
+    gv_gen = torch.Generator(device=device)
+    gv_gen.manual_seed(seed)  # V0 is shared by all ranks
+    gv = torch.randn((n, n), generator=gv_gen, device=device, dtype=torch.float64)
     qv, rv = torch.linalg.qr(gv)
     qv = qv * torch.sign(torch.diagonal(rv))[None, :]
     sigma = 10.0 ** (-cfg.decades * torch.arange(n, device=device, dtype=torch.float64) / max(n - 1, 1))
-    a = (x * sigma[None, :]) @ qv.T
-    del x
-    return a.T.contiguous()
+    xt.mul_(sigma[:, None])
+    at = qv @ xt
+    del xt
+    torch.cuda.empty_cache()
+    return at

@@ -131,6 +131,37 @@ def test_jacobi_dd_bitwise_vs_restatement(port, n):
     assert np.array_equal(vh, pvh) and np.array_equal(vl, pvl)
 
 
+# K5 on the C5 distribution (prescribed sigma over 10 decades, Haar V0): the
+# non-graded, ill-conditioned Gram needs more than the fp64 path's 30 sweeps
+# (kDdMaxSweeps = 100), still bit-identical to the restatement.
+@pytest.mark.parametrize("n", [64, 128])
+def test_jacobi_dd_prescribed_sigma_bitwise(port, n):
+    a, sigma = inputs.prescribed(2 * n, n, 10.0, seed=500 + n)
+    hi, lo = port.dd_gram(a, threads=8)
+    (lh, ll), (vh, vl), sw, rot = M.twosided_jacobi_eig(hi, lo, dd=True)
+    (plh, pll), (pvh, pvl), psw, prot = port.twosided_jacobi_dd(hi, lo, max_sweeps=100, sem=SEM_DEVICE)
+    assert (sw, rot) == (psw, prot)
+    if n == 128:
+        assert sw > 30
+    assert np.array_equal(lh, plh) and np.array_equal(ll, pll)
+    assert np.array_equal(vh, pvh) and np.array_equal(vl, pvl)
+    # sigma against the prescribed values: A formed in fp64 perturbs sigma_i
+    # by ~ u * ||A|| / sigma_i relative
+    s = np.sqrt(lh)
+    assert np.all(np.abs(s - sigma) <= 64 * U64 * n * sigma[0] + 1e-12 * sigma)
+
+
+def test_thin_svd_f64_prescribed_sigma_c5_shape(port):
+    n = 96
+    a, sigma = inputs.prescribed(4096, n, 10.0, seed=7)
+    r = M.mp_thin_svd_f64(a)
+    o = port.thin_svd_f64dd(a, threads=8, sem=SEM_DEVICE)
+    assert r.jacobi_sweeps > 0
+    assert max_rel(r.sigma, o.sigma) <= 10 * n * UDD * 1e10 + 4 * U64
+    assert orth_err(r.v) <= 10 * n * U64
+    assert orth_err(r.u) <= 10 * n * U64 * 1e2  # U columns of sigma ~1e-10 carry u*kappa(B)-level error
+
+
 # ---------------------------------------------------------------------------
 # Full pipeline through mpsvd_thin_svd
 def test_thin_svd_stacked_diagonal_exact():

@@ -126,6 +126,23 @@ def test_dd_jacobi_vs_reference_bisection(ref, port, sem):
     assert np.max(np.abs(lh - oracle) / oracle) <= 64 * U64
 
 
+@pytest.mark.parametrize("sem", [pyoracle.SEM_REFERENCE, pyoracle.SEM_DEVICE])
+def test_dd_jacobi_prescribed_sigma_needs_more_than_30_sweeps(port, sem):
+    # C5-shaped Gram (sigma over 10 decades, Haar V0), n = 128: both
+    # orderings need ~30 sweeps; the dd path's cap is 100 (kDdMaxSweeps)
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+    from paper_2603_11953_b200 import inputs
+    n = 128
+    a, sigma = inputs.prescribed(2 * n, n, 10.0, seed=500 + n)
+    hi, lo = port.dd_gram(a, threads=8)
+    with pytest.raises(pyoracle.OracleError):
+        port.twosided_jacobi_dd(hi, lo, max_sweeps=25, sem=sem)
+    (lh, _), _, sw, _ = port.twosided_jacobi_dd(hi, lo, max_sweeps=100, sem=sem)
+    assert 25 < sw <= 40
+    assert np.all(np.abs(np.sqrt(lh) - sigma) <= 64 * U64 * n + 1e-12 * sigma)
+
+
 def test_dd_thin_svd_vs_reference_dd_oracle(ref, port):
     # f64 working: sigma from dd Gram + dd Jacobi vs the reference dd oracle
     a = graded(64, 8, 10.0, seed=4, dtype=np.float64)
