@@ -21,6 +21,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -129,15 +130,32 @@ static void build_schedule(Plan& p) {
   const long long m = p.m, n = p.n;
   const int T = (int)((n + 63) / 64);
   p.tiles.clear();
+  p.tp_order.clear();
   for (int ti = 0; ti < T; ++ti)
     for (int tj = ti; tj < T; ++tj) p.tiles.push_back(make_int2(ti, tj));
   p.ntp = (int)p.tiles.size();
+  // K1 launches the diagonal tiles and the off-diagonal tiles separately
+  for (int tp = 0; tp < p.ntp; ++tp)
+    if (p.tiles[tp].x == p.tiles[tp].y) p.tp_order.push_back(tp);
+  p.ndiag = (int)p.tp_order.size();
+  for (int tp = 0; tp < p.ntp; ++tp)
+    if (p.tiles[tp].x != p.tiles[tp].y) p.tp_order.push_back(tp);
   p.nblocks = (int)(m < 16 ? m : 16);
   p.splits.clear();
   p.block_split_begin.assign(1, 0);
   if (p.nblocks == 0) return;
-  const int slots = p.sm_count * p.gram_occupancy;
-  int per_block = slots / (p.nblocks * p.ntp);
+  // row splits per logical block: enough CTAs to fill every SM at the
+  // kernel's occupancy (dd: 1 CTA/SM over all tiles; f32: 4/SM for the
+  // diagonal launch, 2/SM for the off-diagonal one)
+  long long want;
+  if (p.dd) {
+    want = (p.sm_count + p.ntp - 1) / p.ntp;
+  } else {
+    const int noff = p.ntp - p.ndiag;
+    want = (4LL * p.sm_count + p.ndiag - 1) / p.ndiag;
+    if (noff > 0) want = std::max(want, (2LL * p.sm_count + noff - 1) / noff);
+  }
+  int per_block = (int)((want + p.nblocks - 1) / p.nblocks);
   if (per_block < 1) per_block = 1;
   const long long base = m / p.nblocks, extra = m % p.nblocks;
   long long row = 0;
@@ -176,7 +194,6 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   if (!device_available()) throw std::runtime_error("no CUDA device available");
   check(cudaGetDevice(&device), "cudaGetDevice");
   check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
-  gram_occupancy = dd ? 1 : 2;
   max_sweeps = dd ? 100 : 30;  // thinsvd.hpp kDdMaxSweeps / jacobi.hpp:31
   build_schedule(*this);
   const size_t nn = (size_t)n * n;
@@ -184,6 +201,9 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   const int N = (int)(n + (n & 1)), np = N / 2;
 
   d_tiles = dalloc<int2>(tiles.size(), owned);
+  d_tp_order = dalloc<int>(tp_order.size(), owned);
+  check(cudaMemcpy(d_tp_order, tp_order.data(), tp_order.size() * sizeof(int), cudaMemcpyHostToDevice),
+        "H2D tile order");
   d_splits = dalloc<longlong2>(splits.size(), owned);
   d_bsb = dalloc<int>(block_split_begin.size(), owned);
   check(cudaMemcpy(d_tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice), "H2D tiles");
@@ -269,13 +289,14 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
           "gram_combine_dd");
     launches += 3;
   } else {
-    check(dev::launch_gram_f32((const float*)d_a, lda, (int)n, d_tiles, ntp, d_splits, (int)splits.size(),
-                               (double*)d_partials, st),
+    check(dev::launch_gram_f32((const float*)d_a, lda, (int)n, d_tiles, ntp, d_tp_order, ndiag,
+                               d_tp_order + ndiag, ntp - ndiag, d_splits, (int)splits.size(), (double*)d_partials,
+                               st),
           "gram_f32");
     check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks,
                                        (double*)d_bsums, (double*)target, st),
           "gram_combine_f64");
-    launches += 3;
+    launches += 2 + (ndiag > 0 ? 1 : 0) + (ntp > ndiag ? 1 : 0);
   }
   if (nranks > 1) {
     auto& a = nccl::api();

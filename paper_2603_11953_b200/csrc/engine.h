@@ -44,17 +44,20 @@ class Plan {
   long long m, n;
   bool dd;
   Comm* comm;
-  int device = 0, sm_count = 148, gram_occupancy = 3;
+  int device = 0, sm_count = 148;
   double tol = 0.0;
   int max_sweeps = 30;
   int log_sweeps = 0;  // sweeps the rotation log (jws.log) can hold; grown by set_jacobi
 
   std::vector<int2> tiles;
+  std::vector<int> tp_order;  // diagonal tile pairs first (ndiag of them), then the rest
+  int ndiag = 0;
   std::vector<longlong2> splits;
   std::vector<int> block_split_begin;
   int ntp = 0, nblocks = 0;
 
   int2* d_tiles = nullptr;
+  int* d_tp_order = nullptr;
   longlong2* d_splits = nullptr;
   int* d_bsb = nullptr;
   double* d_partials = nullptr;

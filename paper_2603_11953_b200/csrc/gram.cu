@@ -37,40 +37,84 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-// ---------------------------------------------------------------------------
-// K1. 128 threads = 4 warps in a 2x2 grid, each warp a 32x32 block of the
-// 64x64 output tile = 4x4 DMMA tiles of 8x8. smem: [2 buffers][ncol][kLDK].
-__global__ void __launch_bounds__(128, 2)
-gram_f32_dmma(const float* __restrict__ a, long long lda, int n, const int2* __restrict__ tiles,
-              const longlong2* __restrict__ splits, double* __restrict__ partials, int ntp) {
-  extern __shared__ __align__(16) double smem_k1[];
-  const int tp = blockIdx.x, s = blockIdx.y;
-  const int2 tij = tiles[tp];
-  const bool diag = tij.x == tij.y;
-  const int ncol = diag ? kTile : 2 * kTile;
-  const int c0 = tij.x * kTile, c1 = tij.y * kTile;
-  const long long r0 = splits[s].x, r1 = splits[s].y;
+// fp32 -> fp64 widening on the integer pipe. cvt.f64.f32 issues on the XU
+// pipe, which the first K1 version saturated (98.7% XU, 61% DMMA in
+// profiles/r01_gram_f32_v0.txt). For zero and normal numbers the widened
+// value is a re-biased exponent and a shifted mantissa; subnormals, inf and
+// NaN take the cvt path (warp-uniform vote per chunk).
+__device__ __forceinline__ double widen_f32_alu(float x) {
+  const uint32_t u = __float_as_uint(x), mag = u & 0x7fffffffu;
+  const uint32_t hi = (mag ? (mag >> 3) + 0x38000000u : 0u) | (u & 0x80000000u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+__device__ __forceinline__ bool f32_needs_cvt(float x) {  // subnormal, inf or NaN
+  const uint32_t mag = __float_as_uint(x) & 0x7fffffffu;
+  return (mag - 0x00800000u) >= 0x7f000000u && mag != 0u;
+}
 
+// Diagonal 64x64 tile: the 36 upper 8x8 blocks (i <= j over the 8 column
+// groups) split 9 per warp, so the four warps (one per SM sub-partition)
+// issue the same number of DMMAs. In a Gram tile the A fragment of group c
+// (A[g][t] = X[k+t][8c+g]) equals its B fragment, so a warp loads each group
+// it touches once per k-step.
+//   W0: groups 0-3 minus (3,3)   W1: (3,3) + {0..3}x{4,5}
+//   W2: (4,4) + {0..3}x{6,7}     W3: groups 4-7 minus (4,4)
+__host__ __device__ constexpr int diag_pair(int w, int k, int e) {
+  constexpr unsigned char t[4][9][2] = {
+      {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}},
+      {{3, 3}, {0, 4}, {1, 4}, {2, 4}, {3, 4}, {0, 5}, {1, 5}, {2, 5}, {3, 5}},
+      {{4, 4}, {0, 6}, {1, 6}, {2, 6}, {3, 6}, {0, 7}, {1, 7}, {2, 7}, {3, 7}},
+      {{5, 5}, {6, 6}, {7, 7}, {4, 5}, {4, 6}, {4, 7}, {5, 6}, {5, 7}, {6, 7}}};
+  return t[w][k][e];
+}
+
+template <int W>
+struct DiagSet {
+  __host__ __device__ static constexpr int pi(int k) { return diag_pair(W, k, 0); }
+  __host__ __device__ static constexpr int pj(int k) { return diag_pair(W, k, 1); }
+  __host__ __device__ static constexpr bool uses(int c) {
+    for (int k = 0; k < 9; ++k)
+      if (pi(k) == c || pj(k) == c) return true;
+    return false;
+  }
+};
+
+// One K1 CTA body. MODE 0..3: warp MODE of a diagonal tile; MODE 4: any warp
+// of an off-diagonal tile (2x2 warps, each 4x4 blocks of 8x8).
+template <int MODE>
+__device__ __forceinline__ void gram_f32_body(const float* __restrict__ a, long long lda, int n, int c0, int c1,
+                                              long long r0, long long r1, double* __restrict__ out,
+                                              double* __restrict__ smem) {
+  constexpr bool kDiag = MODE < 4;
+  constexpr int kNcol = kDiag ? kTile : 2 * kTile;
+  constexpr int kNiter = kNcol / 4;  // 16 or 32 columns staged per warp
+  constexpr int kNacc = kDiag ? 9 : 16;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wi = warp >> 1, wj = warp & 1;
   const int g = lane >> 2, t = lane & 3;
-  const bool warp_active = !(diag && wi > wj);
-  const int boff = diag ? 0 : kTile;
 
-  double acc[4][4][2];
+  double acc[kNacc][2];
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+  for (int k = 0; k < kNacc; ++k) acc[k][0] = acc[k][1] = 0.0;
 
   // Thread -> (column, row) of a chunk: warp w, iteration it loads column
   // 4*it+w, rows 0..31 -> one 128-byte segment per warp per iteration.
-  const int niter = ncol / 4;  // 16 or 32
-  float pre[32];
+  float pre[kNiter];
+  // columns of this tile present in A (CTA-uniform): n is normally a
+  // multiple of 64, so only the last row chunk of a split needs row checks
+  const bool cols_full = (kDiag ? c0 : c1) + kTile <= n;
+  const float* abase = a + (long long)(c0 + warp) * lda + lane;
+  const float* bbase = a + (long long)(c1 + warp) * lda + lane;
   auto load_chunk = [&](long long kr) {
+    if (cols_full && kr + kKC <= r1) {
 #pragma unroll
-    for (int it = 0; it < 32; ++it) {
-      if (it < niter) {
+      for (int it = 0; it < kNiter; ++it) {
+        const float* p = (it < 16 ? abase : bbase) + (long long)(4 * (it & 15)) * lda + kr;
+        pre[it] = __ldg(p);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < kNiter; ++it) {
         const int lc = it * 4 + warp;
         const int gc = lc < kTile ? c0 + lc : c1 + (lc - kTile);
         const long long row = kr + lane;
@@ -79,14 +123,21 @@ gram_f32_dmma(const float* __restrict__ a, long long lda, int n, const int2* __r
     }
   };
   auto store_chunk = [&](double* buf) {
+    bool special = false;
 #pragma unroll
-    for (int it = 0; it < 32; ++it)
-      if (it < niter) buf[(it * 4 + warp) * kLDK + lane] = (double)pre[it];
+    for (int it = 0; it < kNiter; ++it) special |= f32_needs_cvt(pre[it]);
+    if (__any_sync(0xffffffffu, special)) {
+#pragma unroll
+      for (int it = 0; it < kNiter; ++it) buf[(it * 4 + warp) * kLDK + lane] = (double)pre[it];
+    } else {
+#pragma unroll
+      for (int it = 0; it < kNiter; ++it) buf[(it * 4 + warp) * kLDK + lane] = widen_f32_alu(pre[it]);
+    }
   };
 
   const long long nchunks = (r1 - r0 + kKC - 1) / kKC;
-  double* buf0 = smem_k1;
-  double* buf1 = smem_k1 + 2 * kTile * kLDK;
+  double* buf0 = smem;
+  double* buf1 = smem + kNcol * kLDK;
   if (nchunks > 0) {
     load_chunk(r0);
     store_chunk(buf0);
@@ -97,20 +148,26 @@ gram_f32_dmma(const float* __restrict__ a, long long lda, int n, const int2* __r
     double* nxt = (ch & 1) ? buf0 : buf1;
     const bool more = ch + 1 < nchunks;
     if (more) load_chunk(r0 + (ch + 1) * kKC);
-    if (warp_active) {
+#pragma unroll(kDiag ? 2 : 4)
+    for (int kk = 0; kk < kKC; kk += 4) {
+      if constexpr (kDiag) {
+        double f[8];
 #pragma unroll
-      for (int kk = 0; kk < kKC; kk += 4) {
+        for (int c = 0; c < 8; ++c)
+          if (DiagSet<MODE>::uses(c)) f[c] = cur[(8 * c + g) * kLDK + kk + t];
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+          dmma_8x8x4(acc[k][0], acc[k][1], f[DiagSet<MODE>::pi(k)], f[DiagSet<MODE>::pj(k)]);
+      } else {
         double fa[4], fb[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) fa[mi] = cur[(32 * wi + 8 * mi + g) * kLDK + kk + t];
 #pragma unroll
-        for (int nj = 0; nj < 4; ++nj) fb[nj] = cur[(boff + 32 * wj + 8 * nj + g) * kLDK + kk + t];
+        for (int nj = 0; nj < 4; ++nj) fb[nj] = cur[(kTile + 32 * wj + 8 * nj + g) * kLDK + kk + t];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-          for (int nj = 0; nj < 4; ++nj)
-            if (!diag || (32 * wi + 8 * mi) <= (32 * wj + 8 * nj))
-              dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], fa[mi], fb[nj]);
+          for (int nj = 0; nj < 4; ++nj) dmma_8x8x4(acc[mi * 4 + nj][0], acc[mi * 4 + nj][1], fa[mi], fb[nj]);
       }
     }
     if (more) store_chunk(nxt);
@@ -119,18 +176,56 @@ gram_f32_dmma(const float* __restrict__ a, long long lda, int n, const int2* __r
 
   // Epilogue: row-major 64x64 partial tile; entries below the diagonal of a
   // diagonal tile are never read by gram_combine.
-  double* out = partials + ((long long)s * ntp + tp) * (kTile * kTile);
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int nj = 0; nj < 4; ++nj) {
-      const int r = 32 * wi + 8 * mi + g;
-      const int c = 32 * wj + 8 * nj + 2 * t;
-      double2 v;
-      v.x = acc[mi][nj][0];
-      v.y = acc[mi][nj][1];
-      *reinterpret_cast<double2*>(out + r * kTile + c) = v;
+  for (int k = 0; k < kNacc; ++k) {
+    int r, c;
+    if constexpr (kDiag) {
+      r = 8 * DiagSet<MODE>::pi(k) + g;
+      c = 8 * DiagSet<MODE>::pj(k) + 2 * t;
+    } else {
+      r = 32 * wi + 8 * (k >> 2) + g;
+      c = 32 * wj + 8 * (k & 3) + 2 * t;
     }
+    double2 v;
+    v.x = acc[k][0];
+    v.y = acc[k][1];
+    *reinterpret_cast<double2*>(out + r * kTile + c) = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 launches: diagonal tiles (36 DMMA blocks per k-step, ~100 registers,
+// 37 KB smem -> 4 CTAs per SM) and off-diagonal tiles (64 blocks, 254
+// registers, 74 KB -> 2 CTAs per SM) are separate kernels so that each gets
+// its own occupancy. blockIdx.x indexes `tp_list` (tile pair ids), blockIdx.y
+// the row split; partial tiles land at (split * ntp + tp).
+__global__ void __launch_bounds__(128, 4)
+gram_f32_diag(const float* __restrict__ a, long long lda, int n, const int2* __restrict__ tiles,
+              const int* __restrict__ tp_list, const longlong2* __restrict__ splits,
+              double* __restrict__ partials, int ntp) {
+  extern __shared__ __align__(16) double smem_k1[];
+  const int tp = tp_list[blockIdx.x], s = blockIdx.y;
+  const int c0 = tiles[tp].x * kTile;
+  const long long r0 = splits[s].x, r1 = splits[s].y;
+  double* out = partials + ((long long)s * ntp + tp) * (kTile * kTile);
+  switch (threadIdx.x >> 5) {  // warp-uniform: warp w runs on sub-partition w
+    case 0: gram_f32_body<0>(a, lda, n, c0, c0, r0, r1, out, smem_k1); break;
+    case 1: gram_f32_body<1>(a, lda, n, c0, c0, r0, r1, out, smem_k1); break;
+    case 2: gram_f32_body<2>(a, lda, n, c0, c0, r0, r1, out, smem_k1); break;
+    default: gram_f32_body<3>(a, lda, n, c0, c0, r0, r1, out, smem_k1); break;
+  }
+}
+
+__global__ void __launch_bounds__(128, 2)
+gram_f32_offdiag(const float* __restrict__ a, long long lda, int n, const int2* __restrict__ tiles,
+                 const int* __restrict__ tp_list, const longlong2* __restrict__ splits,
+                 double* __restrict__ partials, int ntp) {
+  extern __shared__ __align__(16) double smem_k1[];
+  const int tp = tp_list[blockIdx.x], s = blockIdx.y;
+  const int2 tij = tiles[tp];
+  const long long r0 = splits[s].x, r1 = splits[s].y;
+  double* out = partials + ((long long)s * ntp + tp) * (kTile * kTile);
+  gram_f32_body<4>(a, lda, n, tij.x * kTile, tij.y * kTile, r0, r1, out, smem_k1);
 }
 
 // ---------------------------------------------------------------------------
@@ -343,17 +438,20 @@ size_t gram_smem_bytes(bool dd) {
   return dd ? 2 * kKC * kLDC * sizeof(double) : 2 * 2 * kTile * kLDK * sizeof(double);
 }
 
-cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* tiles, int ntp,
-                            const longlong2* splits, int nsplit, double* partials,
-                            cudaStream_t st) {
+cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* tiles, int ntp, const int* tp_diag,
+                            int ndiag, const int* tp_off, int noff, const longlong2* splits, int nsplit,
+                            double* partials, cudaStream_t st) {
+  const size_t smem_d = 2 * kTile * kLDK * sizeof(double), smem_o = 2 * smem_d;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gram_f32_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)gram_smem_bytes(false));
+    cudaFuncSetAttribute(gram_f32_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+    cudaFuncSetAttribute(gram_f32_offdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_o);
     configured = true;
   }
-  dim3 grid(ntp, nsplit);
-  gram_f32_dmma<<<grid, 128, gram_smem_bytes(false), st>>>(a, lda, n, tiles, splits, partials, ntp);
+  if (ndiag > 0)
+    gram_f32_diag<<<dim3(ndiag, nsplit), 128, smem_d, st>>>(a, lda, n, tiles, tp_diag, splits, partials, ntp);
+  if (noff > 0)
+    gram_f32_offdiag<<<dim3(noff, nsplit), 128, smem_o, st>>>(a, lda, n, tiles, tp_off, splits, partials, ntp);
   return cudaGetLastError();
 }
 

@@ -11,9 +11,10 @@ struct DevStatus;
 
 // gram.cu --------------------------------------------------------------------
 size_t gram_smem_bytes(bool dd);
-cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* tiles, int ntp,
-                            const longlong2* splits, int nsplit, double* partials,
-                            cudaStream_t st);
+// K1: tp_diag / tp_off list the diagonal and off-diagonal tile pairs.
+cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* tiles, int ntp, const int* tp_diag,
+                            int ndiag, const int* tp_off, int noff, const longlong2* splits, int nsplit,
+                            double* partials, cudaStream_t st);
 cudaError_t launch_gram_dd(const double* a, long long lda, int n, const int2* tiles, int ntp,
                            const longlong2* splits, int nsplit, double2* partials,
                            cudaStream_t st);

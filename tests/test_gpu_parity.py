@@ -157,9 +157,14 @@ def test_thin_svd_f64_prescribed_sigma_c5_shape(port):
     r = M.mp_thin_svd_f64(a)
     o = port.thin_svd_f64dd(a, threads=8, sem=SEM_DEVICE)
     assert r.jacobi_sweeps > 0
-    assert max_rel(r.sigma, o.sigma) <= 10 * n * UDD * 1e10 + 4 * U64
+    # sigma^2 = lambda(M) with kappa(M) = kappa(B)^2 = 1e20: the device and
+    # the restatement sum the dd Gram in different orders (2^-104-level
+    # differences), amplified by kappa(M) in the smallest sigma
+    assert max_rel(r.sigma, o.sigma) <= 10 * n * UDD * 1e20 + 4 * U64
     assert orth_err(r.v) <= 10 * n * U64
-    assert orth_err(r.u) <= 10 * n * U64 * 1e2  # U columns of sigma ~1e-10 carry u*kappa(B)-level error
+    # U = A V Sigma^-1 loses orthogonality ~ u * kappa(B) (1e-6 here) by
+    # construction; the restatement shows the same loss
+    assert orth_err(r.u) <= 2 * orth_err(o.u) + 10 * n * U64
 
 
 # ---------------------------------------------------------------------------
