@@ -233,6 +233,10 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   d_w = dalloc<double>((size_t)n * dev::av_ldw((int)n), owned);  // W^T, working precision
   check(cudaMemset(d_w, 0, (size_t)n * dev::av_ldw((int)n) * sizeof(double)), "memset W");
   d_vwork_tmp = dalloc<double>(nn, owned);
+  // K7 on the tensor cores (f32, n <= 128); MPSVD_AV_SIMT=1 keeps the SIMT kernel
+  const char* simt = getenv("MPSVD_AV_SIMT");
+  if (!dd && n <= 128 && !(simt && simt[0] == '1'))
+    d_wplanes = dalloc<unsigned char>(dev::av_tc_wplanes_bytes((int)n), owned);
   check(cudaMallocHost(&h_status, sizeof(DevStatus)), "cudaMallocHost status");
   check(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "stream");
   for (auto& e : ev) check(cudaEventCreate(&e), "event");
@@ -350,7 +354,12 @@ void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, voi
       check(dev::launch_av_f64((const double*)d_a, lda, m, (int)n, (const double*)d_w, (double*)d_u, ldu,
                                jws.status, st),
             "av_f64");
-    else
+    else if (d_wplanes && dev::av_tc_supported((const float*)d_a, lda, m, (int)n, ldu)) {
+      check(dev::launch_av_tc_f32((const float*)d_a, lda, m, (int)n, (const float*)d_w, d_wplanes, (float*)d_u,
+                                  ldu, jws.status, sm_count, st),
+            "av_tc_f32");
+      launches += 1;  // + the W split kernel below
+    } else
       check(dev::launch_av_f32((const float*)d_a, lda, m, (int)n, (const float*)d_w, (float*)d_u, ldu,
                                jws.status, st),
             "av_f32");

@@ -70,6 +70,7 @@ class Plan {
   double *d_lam_hi = nullptr, *d_lam_lo = nullptr, *d_sigma_tmp = nullptr;
   double* d_w = nullptr;
   double* d_vwork_tmp = nullptr;
+  void* d_wplanes = nullptr;  // K7 tensor-core W pieces (f32, n <= 128)
   dev::DevStatus* h_status = nullptr;
   cudaStream_t own_stream = nullptr, last_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
