@@ -48,6 +48,66 @@ def flops(m: int, n: int):
     return float(m) * n * (n + 1), 2.0 * m * n * n
 
 
+# fp64 FMA-pipe rate (DFMA, profiles/r01_microbench.txt): the double-double
+# kernels are bound by fp64 instruction issue, one operation per lane-cycle
+DFMA_TFLOPS = 34.2
+
+
+def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
+    """Roofline of every pipeline phase of one SVD on one GPU.
+
+    gram  f32: m n (n+1) flops on the DMMA pipe (K1; the phase also holds
+               the two small combine kernels)
+    gram  f64: m n (n+1)/2 multiply-adds x 9 fp64 operations (Dot2:
+               two_prod 2, two_sum 6, error add 1) on the fp64 pipe (K2)
+    eigen    : two-sided Jacobi, latency bound; 18 n flops per rotation
+               (2 rows + 2 columns of M, 2 columns of V) against fp64 peak
+    compute_u: f32: read A + write U (2 m n 4 bytes) against HBM (K7 on the
+               tensor cores, which are far from their bf16 bound);
+               f64: 2 m n^2 flops on the fp64 pipe (SIMT DFMA kernel)
+    """
+    out = {}
+    if cfg.working == "f32":
+        a = m_local * n * (n + 1) / (med["gram"] * 1e-3) / 1e12
+        out["gram"] = {"kernel": "gram_f32_diag/offdiag (DMMA)", "bound": "tensor", "achieved": a,
+                       "peak": fp64_peak, "unit": "TFLOP/s", "frac": a / fp64_peak,
+                       "peak_source": "live DMMA m8n8k4 probe (MEASURED_PEAKS.json has no fp64 figure)",
+                       "algorithmic": "m*n*(n+1) flops per SVD"}
+        b = 2.0 * m_local * n * 4 / (med["compute_u"] * 1e-3) / 1e9
+        out["compute_u"] = {"kernel": "av_tc_f32 (tcgen05 bf16x3)", "bound": "hbm", "achieved": b, "peak": hbm,
+                            "unit": "GB/s", "frac": b / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                            "algorithmic": "2*m*n*4 bytes (read A, write U) per SVD"}
+    else:
+        ops = m_local * n * (n + 1) / 2 * 9
+        peak = DFMA_TFLOPS / 2
+        a = ops / (med["gram"] * 1e-3) / 1e12
+        out["gram"] = {"kernel": "gram_f64_dd (Dot2)", "bound": "fp64", "achieved": a, "peak": peak,
+                       "unit": "Tops/s", "frac": a / peak,
+                       "peak_source": "DFMA issue rate (profiles/r01_microbench.txt 34.2 TFLOP/s / 2)",
+                       "algorithmic": "9 fp64 ops per multiply-add, m*n*(n+1)/2 multiply-adds"}
+        f = 2.0 * m_local * n * n / (med["compute_u"] * 1e-3) / 1e12
+        out["compute_u"] = {"kernel": "av_kernel<double> (DFMA)", "bound": "fp64", "achieved": f,
+                            "peak": DFMA_TFLOPS, "unit": "TFLOP/s", "frac": f / DFMA_TFLOPS,
+                            "peak_source": "DFMA (profiles/r01_microbench.txt)",
+                            "algorithmic": "2*m*n^2 flops per SVD"}
+    jf = 18.0 * n * info.rotations / (med["eigen"] * 1e-3) / 1e12
+    out["eigen"] = {"kernel": "jacobi_smem / jacobi_kernel", "bound": "latency", "achieved": jf,
+                    "peak": DFMA_TFLOPS, "unit": "TFLOP/s", "frac": jf / DFMA_TFLOPS,
+                    "algorithmic": "18*n flops per rotation; one CTA, ~n/2 rotations per barrier round"}
+    return out
+
+
+def traffic_for(kernel: str, config: str):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full
+    capture (profiles/r01_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(config, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
@@ -286,24 +346,13 @@ def run_ours(args, cfg):
     pk = peaks()
     fp64_peak = M.fp64_peak_tflops(local)
     hbm = pk.get("hbm_gbs", 6650.0)
-    # dominant kernel share and roofline
-    shares = {k: v for k, v in med.items()}
-    dom = max(shares, key=shares.get)
-    if dom == "gram":
-        achieved = fg / world / (med["gram"] * 1e-3) / 1e12 if world == 1 else fg / world / (med["gram"] * 1e-3) / 1e12
-        roof = {"kernel": "gram_f32_dmma" if cfg.working == "f32" else "gram_f64_dd", "bound": "tensor",
-                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "traffic": None, "peak_source": "live DMMA m8n8k4 probe (MEASURED_PEAKS.json has no fp64 figure)",
-                "algorithmic": "m*n*(n+1) flops per launch (upper-triangle SYRK)"}
-    elif dom == "compute_u":
-        byts = 2.0 * m_local * n * esz
-        achieved = byts / (med["compute_u"] * 1e-3) / 1e9
-        roof = {"kernel": "av_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "algorithmic": "read A + write U = 2*m*n*s bytes per launch"}
-    else:
-        roof = {"kernel": "jacobi_kernel", "bound": "latency", "achieved": med["eigen"], "peak": None,
-                "unit": "ms", "frac": None, "traffic": None}
+    # per-phase rooflines: algorithmic work per launch over
+    # the phase's CUDA-event time on the plan's stream; the dominant phase is
+    # the headline `roofline`
+    phases = phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info)
+    dom = max(med, key=med.get)
+    roof = dict(phases[dom])
+    roof["traffic"] = traffic_for(roof["kernel"], cfg.name)
     # north_star roofline for the whole Gram+AV pair
     t_hbm = 2.0 * m_global / world * n * esz / (hbm * 1e9)
     t_cmp = (fg + fa) / world / (fp64_peak * 1e12) if cfg.working == "f32" else (fg * 5 + fa) / world / (fp64_peak * 1e12)
@@ -321,6 +370,7 @@ def run_ours(args, cfg):
                    "parallelism": f"rows{world}"},
         "phase_ms": med,
         "roofline": roof,
+        "roofline_phases": phases,
         "svd_roofline": {"definition": "max(2*m*n*s/HBM, F_gram/P_gram + F_AV/P_fp64) (north_star)",
                          "t_roof_ms": t_roof * 1e3, "gram_plus_av_ms": gram_av_ms,
                          "frac": (t_roof * 1e3) / gram_av_ms if gram_av_ms > 0 else None,

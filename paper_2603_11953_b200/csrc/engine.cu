@@ -144,19 +144,34 @@ static void build_schedule(Plan& p) {
   p.splits.clear();
   p.block_split_begin.assign(1, 0);
   if (p.nblocks == 0) return;
-  // row splits per logical block: enough CTAs to fill every SM at the
-  // kernel's occupancy (dd: 1 CTA/SM over all tiles; f32: 4/SM for the
-  // diagonal launch, 2/SM for the off-diagonal one)
-  long long want;
-  if (p.dd) {
-    want = (p.sm_count + p.ntp - 1) / p.ntp;
-  } else {
-    const int noff = p.ntp - p.ndiag;
-    want = (4LL * p.sm_count + p.ndiag - 1) / p.ndiag;
-    if (noff > 0) want = std::max(want, (2LL * p.sm_count + noff - 1) / noff);
+  // Row splits per logical block. Every launch runs a whole number of
+  // waves as far as possible: a 2nd wave holding a few CTAs doubles a
+  // launch's time (C3: 160 CTAs on 148 SMs). Pick per_block (splits per
+  // block) minimising  rows_per_split x sum_launch(waves x cost_per_row),
+  // with kernels at 1 CTA/SM (dd), 4/SM (f32 diagonal tiles: 36 DMMA blocks
+  // per k-step) and 2/SM (f32 off-diagonal tiles: 64 blocks).
+  const long long max_pb = std::max(1LL, (m / p.nblocks + 31) / 32);
+  int per_block = 1;
+  double best = 1e300;
+  const long long tile_bytes = 64LL * 64 * 8 * (p.dd ? 2 : 1);
+  for (int pb = 1; pb <= 64 && pb <= max_pb; ++pb) {
+    const long long S = (long long)pb * p.nblocks;
+    if (pb > 1 && S * p.ntp * tile_bytes > (512LL << 20)) break;  // partial-tile workspace cap
+    double cost;
+    if (p.dd) {
+      const long long waves = (p.ntp * S + p.sm_count - 1) / p.sm_count;
+      cost = (double)waves / (double)S;
+    } else {
+      const int noff = p.ntp - p.ndiag;
+      const long long wd = (p.ndiag * S + 4LL * p.sm_count - 1) / (4LL * p.sm_count);
+      const long long wo = noff ? (noff * S + 2LL * p.sm_count - 1) / (2LL * p.sm_count) : 0;
+      cost = (9.0 * (double)wd + 32.0 * (double)wo) / (double)S;
+    }
+    if (cost < best * 0.999) {  // prefer fewer splits on ties (smaller combine)
+      best = cost;
+      per_block = pb;
+    }
   }
-  int per_block = (int)((want + p.nblocks - 1) / p.nblocks);
-  if (per_block < 1) per_block = 1;
   const long long base = m / p.nblocks, extra = m % p.nblocks;
   long long row = 0;
   for (int b = 0; b < p.nblocks; ++b) {
