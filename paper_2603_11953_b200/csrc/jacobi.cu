@@ -726,6 +726,10 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
   __shared__ int w_cnt[8];
   __shared__ double w_worst[8];
   auto AE = [&](int row, int col) -> ST* { return a + col * lda + row; };
+  // Store-once symmetric storage: entry (i, j) lives at its upper-triangle
+  // position (min, max); the 2x2 block updates read and write one copy
+  // (4 loads + 4 stores instead of 4 + 8 shared-memory accesses).
+  auto CE = [&](int i, int j) -> ST* { return i <= j ? a + j * lda + i : a + i * lda + j; };
 
   for (int e = tid; e < n * n; e += NT) a[(e / n) * lda + e % n] = a_glob[e];
   for (int idx = tid; idx < np * (np + 1) / 2; idx += NT) {
@@ -784,13 +788,16 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     if (aa == bb) {  // jacobi.cpp:541-546
       A_::st(AE(p0, p0), rb[2 * np + aa]);
       A_::st(AE(q0, q0), rb[3 * np + aa]);
-      A_::st(AE(p0, q0), A_::zero());
-      A_::st(AE(q0, p0), A_::zero());
+      A_::st(AE(p0, q0), A_::zero());  // p0 < q0: the canonical copy
       return;
     }
     const int k0 = wb & 0x7fff, l0 = (wb >> 15) & 0x7fff;
     if (q0 < n && l0 < n) {
-      AT x00 = A_::lds(AE(p0, k0)), x01 = A_::lds(AE(p0, l0)), x10 = A_::lds(AE(q0, k0)), x11 = A_::lds(AE(q0, l0));
+      ST* const e00 = CE(p0, k0);
+      ST* const e01 = CE(p0, l0);
+      ST* const e10 = CE(q0, k0);
+      ST* const e11 = CE(q0, l0);
+      AT x00 = A_::lds(e00), x01 = A_::lds(e01), x10 = A_::lds(e10), x11 = A_::lds(e11);
       if (actb) {
         const AT cb = rcs[bb], sb = rss[bb];
         const AT y00 = A_::rot_lo(cb, sb, x00, x01), y01 = A_::rot_hi(cb, sb, x00, x01);
@@ -809,14 +816,10 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
         x01 = y01;
         x11 = y11;
       }
-      A_::st(AE(p0, k0), x00);
-      A_::st(AE(k0, p0), x00);
-      A_::st(AE(p0, l0), x01);
-      A_::st(AE(l0, p0), x01);
-      A_::st(AE(q0, k0), x10);
-      A_::st(AE(k0, q0), x10);
-      A_::st(AE(q0, l0), x11);
-      A_::st(AE(l0, q0), x11);
+      A_::st(e00, x00);
+      A_::st(e01, x01);
+      A_::st(e10, x10);
+      A_::st(e11, x11);
       return;
     }
     // a pair holding the bye of an odd n: 1x2 / 2x1 / 1x1 block
@@ -824,7 +827,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     const int nr = q0 < n ? 2 : 1, nc = l0 < n ? 2 : 1;
     AT x[2][2];
     for (int u = 0; u < 2; ++u)
-      for (int v = 0; v < 2; ++v) x[u][v] = (u < nr && v < nc) ? A_::lds(AE(rows[u], cols[v])) : A_::zero();
+      for (int v = 0; v < 2; ++v) x[u][v] = (u < nr && v < nc) ? A_::lds(CE(rows[u], cols[v])) : A_::zero();
     if (actb)
       for (int u = 0; u < 2; ++u) {
         const AT x0 = x[u][0], x1 = x[u][1];
@@ -839,8 +842,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
       }
     for (int u = 0; u < nr; ++u)
       for (int v = 0; v < nc; ++v) {
-        A_::st(AE(rows[u], cols[v]), x[u][v]);
-        A_::st(AE(cols[v], rows[u]), x[u][v]);
+        A_::st(CE(rows[u], cols[v]), x[u][v]);
       }
   };
 
@@ -892,12 +894,16 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
           const bool act = qq < n && ((jexp & 1) ? true : A_::active(app, aqq, apq, tol));
           if (want_ratio && qq < n) wmax = fmax(wmax, A_::ratio(app, aqq, apq));
           AT c = A_::one(), s = A_::zero(), npp = app, nqq = aqq;
-          if (__any_sync(__activemask(), act)) {
+          {
+            // The rotation is evaluated for every slot, independently of the
+            // stop test (off the critical path: stop-test sqrt and rotation
+            // chain run concurrently), and kept only for active pairs: the
+            // active pairs' values are the same operations on the same inputs.
             AT c2, s2, np2, nq2;
             if (jexp & 1) {
               c2 = A_::one(); s2 = A_::zero(); np2 = app; nq2 = aqq;
             } else
-            A_::rotate(act ? app : A_::one(), act ? aqq : A_::one(), act ? apq : A_::one(), c2, s2, np2, nq2);
+            A_::rotate(app, aqq, apq, c2, s2, np2, nq2);
             if (act) {
               c = c2;
               s = s2;
@@ -1028,7 +1034,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     }
   }
   __syncthreads();
-  for (int e = tid; e < n * n; e += NT) a_glob[e] = a[(e / n) * lda + e % n];
+  for (int e = tid; e < n * n; e += NT) a_glob[e] = *CE(e % n, e / n);
   if (tid == 0) {
     status->status = converged ? kOk : kNoConvergence;
     status->index = converged ? 0 : max_sweeps;
