@@ -29,6 +29,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -1414,12 +1416,23 @@ cudaError_t launch_jacobi(bool dd_mode, int n, double tol, int max_sweeps, const
 template <typename ST>
 static cudaError_t launch_replay_t(int n, const JacobiWorkspace& ws, cudaStream_t st) {
   const int N = n + (n & 1), np = N / 2;
-  // enough rows per CTA that one round is ~256 independent rotations
+  // Every CTA streams the whole rotation log, so the log traffic is
+  // (CTAs x log bytes): use about one CTA per SM (n = 1024 dd: 7 rows of V
+  // per CTA instead of 1 cut the replay from 846 ms to a few tens), and at
+  // least ~256 independent rotations per round per CTA.
+  static int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
   int rows = (256 + np - 1) / np;
+  rows = std::max(rows, (n + sms - 1) / sms);
   if (rows > n) rows = n;
   if (rows < 1) rows = 1;
+  const size_t budget = 200 * 1024;
+  while (rows > 1 && (size_t)rows * n * sizeof(ST) + (size_t)np * 2 * sizeof(ST) > budget) --rows;
   const size_t row_bytes = (size_t)rows * n * sizeof(ST);
-  const size_t budget = 160 * 1024;
   size_t per_round = (size_t)np * 2 * sizeof(ST);
   int batch = row_bytes < budget ? (int)((budget - row_bytes) / per_round) : 1;
   if (batch < 1) batch = 1;
