@@ -64,7 +64,7 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
                (2 rows + 2 columns of M, 2 columns of V) against fp64 peak
     compute_u: f32: read A + write U (2 m n 4 bytes) against HBM (K7 on the
                tensor cores, which are far from their bf16 bound);
-               f64: 2 m n^2 flops on the fp64 pipe (SIMT DFMA kernel)
+               f64: 2 m n^2 flops on the DMMA pipe (av_dmma_f64)
     """
     out = {}
     if cfg.working == "f32":
@@ -86,9 +86,9 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
                        "peak_source": "DFMA issue rate (profiles/r01_microbench.txt 34.2 TFLOP/s / 2)",
                        "algorithmic": "9 fp64 ops per multiply-add, m*n*(n+1)/2 multiply-adds"}
         f = 2.0 * m_local * n * n / (med["compute_u"] * 1e-3) / 1e12
-        out["compute_u"] = {"kernel": "av_kernel<double> (DFMA)", "bound": "fp64", "achieved": f,
-                            "peak": DFMA_TFLOPS, "unit": "TFLOP/s", "frac": f / DFMA_TFLOPS,
-                            "peak_source": "DFMA (profiles/r01_microbench.txt)",
+        out["compute_u"] = {"kernel": "av_dmma_f64 (DMMA)", "bound": "tensor", "achieved": f,
+                            "peak": fp64_peak, "unit": "TFLOP/s", "frac": f / fp64_peak,
+                            "peak_source": "live DMMA m8n8k4 probe",
                             "algorithmic": "2*m*n^2 flops per SVD"}
     jf = 18.0 * n * info.rotations / (med["eigen"] * 1e-3) / 1e12
     out["eigen"] = {"kernel": "jacobi_smem / jacobi_kernel", "bound": "latency", "achieved": jf,

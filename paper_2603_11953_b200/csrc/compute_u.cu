@@ -182,5 +182,131 @@ cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, co
   return launch_av_t<double, 64, 8, 4, 32>(a, lda, m, n, w, ldw, u, ldu, status, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// K7 (fp64) on the DMMA pipe: U = A * W, A m x n column-major, W row-major
+// (wt[l * ldw + j] = W(l, j)). CTA tile 128 rows x 64 columns, K chunks of 16
+// double-buffered with cp.async; 8 warps as 4 (rows) x 2 (columns), each a
+// 32 x 32 block = 4 x 4 mma.sync.m8n8k4.f64 tiles. Shared tiles are k-major
+// with a 4-word pad so that the fragment loads (k = t, rows 8i + g) hit 32
+// distinct banks. fp64 products and sums on the tensor pipe: U differs from an
+// fp64 fma chain by summation order only.
+namespace av64 {
+constexpr int BM = 128, BN = 64, BK = 16;
+constexpr int LDA_S = BM + 4, LDW_S = BN + 4;
+constexpr int kStage = BK * (LDA_S + LDW_S);  // doubles per stage
+}  // namespace av64
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 2)
+av_dmma_f64(const double* __restrict__ a, long long lda, long long m, int n, const double* __restrict__ wt, int ldw,
+            double* __restrict__ u, long long ldu, const DevStatus* __restrict__ status) {
+  using namespace av64;
+  if (status && status->status != kOk) return;
+  extern __shared__ __align__(16) double av64s[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wi = warp >> 1, wj = warp & 1, g = lane >> 2, t = lane & 3;
+  const long long r0 = (long long)blockIdx.x * BM;
+  const int c0 = blockIdx.y * BN;
+  const bool vec_a = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
+  const bool vec_w = (ldw % 2 == 0) && ((reinterpret_cast<uintptr_t>(wt) & 15) == 0);
+
+  auto stage = [&](int ch, int buf) {
+    double* as = av64s + buf * kStage;
+    double* ws = as + BK * LDA_S;
+    const int k0 = ch * BK;
+    // A: BK columns x BM rows, 16-byte pieces (2 rows)
+    for (int e = tid; e < BK * BM / 2; e += 256) {
+      const int kk = e / (BM / 2), ip = e - kk * (BM / 2);
+      const long long row = r0 + 2 * ip;
+      const int l = k0 + kk;
+      double* dst = as + kk * LDA_S + 2 * ip;
+      if (vec_a && l < n && row + 1 < m) {
+        cp_async16(dst, a + (long long)l * lda + row, 16);
+      } else {
+        dst[0] = (l < n && row < m) ? a[(long long)l * lda + row] : 0.0;
+        dst[1] = (l < n && row + 1 < m) ? a[(long long)l * lda + row + 1] : 0.0;
+      }
+    }
+    // W: BK rows x BN columns
+    for (int e = tid; e < BK * BN / 2; e += 256) {
+      const int kk = e / (BN / 2), jp = e - kk * (BN / 2);
+      const int l = k0 + kk, col = c0 + 2 * jp;
+      double* dst = ws + kk * LDW_S + 2 * jp;
+      if (vec_w && l < n && col + 1 < n) {
+        cp_async16(dst, wt + (long long)l * ldw + col, 16);
+      } else {
+        dst[0] = (l < n && col < n) ? wt[(long long)l * ldw + col] : 0.0;
+        dst[1] = (l < n && col + 1 < n) ? wt[(long long)l * ldw + col + 1] : 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nch = (n + BK - 1) / BK;
+  stage(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      stage(ch + 1, (ch + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = av64s + (ch & 1) * kStage;
+    const double* ws = as + BK * LDA_S;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = as[(kk + t) * LDA_S + 32 * wi + 8 * i + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = ws[(kk + t) * LDW_S + 32 * wj + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long row = r0 + 32 * wi + 8 * i + g;
+    if (row >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = c0 + 32 * wj + 8 * j + 2 * t;
+      if (col < n) u[(long long)col * ldu + row] = acc[i][j][0];
+      if (col + 1 < n) u[(long long)(col + 1) * ldu + row] = acc[i][j][1];
+    }
+  }
+}
+
+cudaError_t launch_av_dmma_f64(const double* a, long long lda, long long m, int n, const double* w, double* u,
+                               long long ldu, const DevStatus* status, cudaStream_t st) {
+  using namespace av64;
+  if (m <= 0) return cudaSuccess;
+  const size_t smem = 2 * (size_t)kStage * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(av_dmma_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  dim3 grid((unsigned)((m + BM - 1) / BM), (unsigned)((n + BN - 1) / BN));
+  av_dmma_f64<<<grid, 256, smem, st>>>(a, lda, m, n, w, av_ldw(n), u, ldu, status);
+  return cudaGetLastError();
+}
+
 }  // namespace dev
 }  // namespace mpsvd

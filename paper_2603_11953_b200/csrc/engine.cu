@@ -366,9 +366,9 @@ void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, voi
   check(cudaEventRecord(ev[2], st), "event");
   if (d_u && m > 0) {
     if (dd)
-      check(dev::launch_av_f64((const double*)d_a, lda, m, (int)n, (const double*)d_w, (double*)d_u, ldu,
-                               jws.status, st),
-            "av_f64");
+      check(dev::launch_av_dmma_f64((const double*)d_a, lda, m, (int)n, (const double*)d_w, (double*)d_u, ldu,
+                                    jws.status, st),
+            "av_dmma_f64");
     else if (d_wplanes && dev::av_tc_supported((const float*)d_a, lda, m, (int)n, ldu)) {
       check(dev::launch_av_tc_f32((const float*)d_a, lda, m, (int)n, (const float*)d_w, d_wplanes, (float*)d_u,
                                   ldu, jws.status, sm_count, st),

@@ -61,6 +61,9 @@ bool av_tc_supported(const float* a, long long lda, long long m, int n, long lon
 size_t av_tc_wplanes_bytes(int n);
 cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, const float* w, void* wplanes,
                              float* u, long long ldu, const DevStatus* status, int sm_count, cudaStream_t st);
+// K7 fp64 on the DMMA pipe (compute_u.cu)
+cudaError_t launch_av_dmma_f64(const double* a, long long lda, long long m, int n, const double* w, double* u,
+                               long long ldu, const DevStatus* status, cudaStream_t st);
 cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w,
                           double* u, long long ldu, const DevStatus* status, cudaStream_t st);
 

@@ -243,13 +243,24 @@ def test_thin_svd_device_semantics_bitwise(port):
     assert_av_bound(a, w, port.av_f32(a, w))
 
 
-def assert_av_bound(a, w, u, c=2.0):
-    """|U - A W| <= c * n * u32 * (|A| |W|) elementwise, A W in fp64."""
+def assert_av_bound(a, w, u, c=2.0, unit=U32):
+    """|U - A W| <= c * n * unit * (|A| |W|) elementwise, A W in fp64
+    (for fp64 operands the reference product carries its own ~n u64 error,
+    inside the same bound)."""
     a64, w64 = a.astype(np.float64), w.astype(np.float64)
     exact = a64 @ w64
-    bound = c * a.shape[1] * U32 * (np.abs(a64) @ np.abs(w64)) + 1e-45
+    bound = c * a.shape[1] * unit * (np.abs(a64) @ np.abs(w64)) + 1e-300
     err = np.abs(u.astype(np.float64) - exact)
     assert np.all(err <= bound), float(np.max(err / bound))
+
+
+# K7 fp64 on the DMMA pipe: ragged tiles, odd m (unaligned columns), n = 1
+@pytest.mark.parametrize("m,n", [(3, 1), (129, 7), (1001, 64), (4096, 100), (2050, 130)])
+def test_compute_u_f64_dmma_bound(m, n):
+    a = inputs.graded(m, n, 4.0, seed=m + 3 * n, dtype=np.float64)
+    r = M.mp_thin_svd_f64(a)
+    w = r.v / r.sigma[None, :]
+    assert_av_bound(a, w, r.u, c=4.0, unit=U64)
 
 
 # K7 on tcgen05: ragged tiles (m % 128 != 0), n not a multiple of 16, n = 1
