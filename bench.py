@@ -53,13 +53,26 @@ def flops(m: int, n: int):
 DFMA_TFLOPS = 34.2
 
 
+def config_dict(cfg, world: int):
+    """The workload both arms report (the reference arm times a row sample of
+    it, named in its cpu_baseline.sample)."""
+    m_global = cfg.m * world if cfg.name == "c2" else cfg.m
+    m_local = cfg.m if cfg.name == "c2" else -(-cfg.m // world)
+    esz = 4 if cfg.working == "f32" else 8
+    return {"workload": cfg.name, "m": m_global, "n": cfg.n, "working": cfg.working,
+            "gram": "fp64" if cfg.working == "f32" else "double-double",
+            "l2": f"inputs larger than L2 (A = {m_local * cfg.n * esz / 2**20:.0f} MiB per GPU > 126 MB)",
+            "parallelism": f"rows{world}"}
+
+
 def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
     """Roofline of every pipeline phase of one SVD on one GPU.
 
     gram  f32: m n (n+1) flops on the DMMA pipe (K1; the phase also holds
                the two small combine kernels)
-    gram  f64: m n (n+1)/2 multiply-adds x 9 fp64 operations (Dot2:
-               two_prod 2, two_sum 6, error add 1) on the fp64 pipe (K2)
+    gram  f64: m n (n+1)/2 multiply-adds x 10 fp64 operations (Dot2:
+               two_prod 2, two_sum 6, error accumulation 2; c_dd = 10 as
+               SURVEY.md §8(d) defines it) on the fp64 pipe (K2)
     eigen    : two-sided Jacobi, latency bound; 18 n flops per rotation
                (2 rows + 2 columns of M, 2 columns of V) against fp64 peak
     compute_u: f32: read A + write U (2 m n 4 bytes) against HBM (K7 on the
@@ -78,13 +91,13 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
                             "unit": "GB/s", "frac": b / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                             "algorithmic": "2*m*n*4 bytes (read A, write U) per SVD"}
     else:
-        ops = m_local * n * (n + 1) / 2 * 9
+        ops = m_local * n * (n + 1) / 2 * 10
         peak = DFMA_TFLOPS / 2
         a = ops / (med["gram"] * 1e-3) / 1e12
         out["gram"] = {"kernel": "gram_f64_dd (Dot2)", "bound": "fp64", "achieved": a, "peak": peak,
                        "unit": "Tops/s", "frac": a / peak,
                        "peak_source": "DFMA issue rate (profiles/r01_microbench.txt 34.2 TFLOP/s / 2)",
-                       "algorithmic": "9 fp64 ops per multiply-add, m*n*(n+1)/2 multiply-adds"}
+                       "algorithmic": "c_dd = 10 fp64 ops per multiply-add, m*n*(n+1)/2 multiply-adds"}
         f = 2.0 * m_local * n * n / (med["compute_u"] * 1e-3) / 1e12
         out["compute_u"] = {"kernel": "av_dmma_f64 (DMMA)", "bound": "tensor", "achieved": f,
                             "peak": fp64_peak, "unit": "TFLOP/s", "frac": f / fp64_peak,
@@ -206,7 +219,7 @@ def run_reference(args, cfg):
         "scaling": "weak" if cfg.name == "c2" else "strong", "vs_baseline": None,
         "dtype": "f64" if cfg.working == "f32" else "f64x2",
         "data": "synthetic (seeded, BASELINE.json distribution)",
-        "config": {"workload": cfg.name, "m": m_s, "n": n, "working": cfg.working},
+        "config": dict(config_dict(cfg, args.gpus), sample_rows=m_s),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -339,6 +352,38 @@ def run_ours(args, cfg):
                "ms_per_step": t_e2e * 1e3,
                "phase_s": {"gram": times.gram, "eigen": times.eigen, "compute_u": times.compute_u,
                            "overlap": times.overlap, "total": times.total}}
+    else:
+        # N > 1: the multi-GPU public API (Plan + Comm, C ABI mpsvd_plan_*)
+        # with page-locked host buffers per rank: H2D of the rank's rows of A,
+        # the pipeline (one NCCL exchange inside), D2H of U, sigma and V;
+        # wall time per step, max over ranks
+        h_a = torch.empty(a_t.shape, dtype=a_t.dtype, pin_memory=True)
+        h_a.copy_(a_t)
+        h_u = torch.empty(a_t.shape, dtype=a_t.dtype, pin_memory=True)
+        h_s = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        h_v = torch.empty((n, n), dtype=a_t.dtype, pin_memory=True)
+        reps = 5
+        t_e2e = 0.0
+        for i in range(reps + 1):
+            dist.barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):
+                a_t.copy_(h_a, non_blocking=True)
+                step()
+                h_u.copy_(u_t, non_blocking=True)
+                h_s.copy_(sig_t, non_blocking=True)
+                h_v.copy_(v_t, non_blocking=True)
+            stream.synchronize()
+            if i > 0:  # first repetition is a warm-up
+                t_e2e += time.perf_counter() - t0
+        t_e2e /= reps
+        tt = torch.tensor([t_e2e], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+        e2e = {"value": (fg + fa) / t_e2e / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": m_local * n * esz,
+               "d2h_bytes_per_step": m_local * n * esz + n * n * esz + n * 8,
+               "ms_per_step": t_e2e * 1e3, "path": "mpsvd_plan_* with an NCCL communicator, per-rank bytes"}
 
     if rank != 0:
         return None
@@ -364,10 +409,7 @@ def run_ours(args, cfg):
         "scaling": "weak" if cfg.name == "c2" else "strong", "vs_baseline": None,
         "dtype": "f64" if cfg.working == "f32" else "f64x2",
         "data": "synthetic (seeded torch generator, BASELINE.json distribution)",
-        "config": {"workload": cfg.name, "m": m_global, "n": n, "working": cfg.working,
-                   "gram": "fp64 (DMMA)" if cfg.working == "f32" else "double-double (Dot2)",
-                   "l2": f"inputs larger than L2 (A = {m_local * n * esz / 2**20:.0f} MiB per GPU > 126 MB)",
-                   "parallelism": f"rows{world}"},
+        "config": config_dict(cfg, world),
         "phase_ms": med,
         "roofline": roof,
         "roofline_phases": phases,

@@ -208,6 +208,38 @@ def test_thin_svd_config_c1(port, seed):
     assert rowwise_backward(a, r.u, r.sigma, r.v) <= 100.0 * np.sqrt(cfg.n) * U32
 
 
+# Shape sweep over every kernel-selection boundary: n in {1, ..} around the
+# 64-column tile, the shared-memory Jacobi limit (n <= 128 fp64 / np <= 64),
+# the tensor-core K7 limit (n <= 128) and beyond (multi-CTA Jacobi, SIMT U);
+# m ragged with respect to the 128-row tiles and the 16 logical blocks.
+@pytest.mark.parametrize("m,n", [(1, 1), (17, 16), (200, 63), (515, 65), (1000, 127), (1024, 128), (1300, 129),
+                                 (3001, 200), (4096, 256), (2048, 300)])
+def test_thin_svd_shape_sweep_f32(port, m, n):
+    a = inputs.graded(m, n, 3.0, seed=m * 7 + n)
+    r = M.mp_thin_svd(a)
+    o = port.thin_svd(a, threads=8)
+    kb = kappa_b(a)
+    g_sigma, g_orth = north_star_gates(n, U32, kb)
+    assert max_rel(r.sigma, o.sigma) <= g_sigma
+    assert orth_err(r.v) <= g_orth
+    if m >= n:
+        assert orth_err(r.u) <= max(g_orth, 4 * orth_err(o.u))
+    w = r.v.astype(np.float32) / r.sigma.astype(np.float32)[None, :]
+    assert_av_bound(a, w, r.u)
+
+
+@pytest.mark.parametrize("m,n", [(5, 3), (640, 64), (900, 129), (2000, 200)])
+def test_thin_svd_shape_sweep_f64(port, m, n):
+    a = inputs.graded(m, n, 8.0, seed=m + n, dtype=np.float64)
+    r = M.mp_thin_svd_f64(a)
+    o = port.thin_svd_f64dd(a, threads=8, sem=SEM_DEVICE)
+    kb = kappa_b(a)
+    g_sigma, g_orth = north_star_gates(n, U64, kb)
+    assert max_rel(r.sigma, o.sigma) <= g_sigma
+    assert orth_err(r.v) <= g_orth
+    assert orth_err(r.u) <= max(g_orth, 4 * orth_err(o.u))
+
+
 def test_thin_svd_tiny_sigma():
     # proj/tests/test_thinsvd.cpp:244-264; test_capi.cpp:220-225
     a = stacked_diag(2, [1.0, 1e-39])
