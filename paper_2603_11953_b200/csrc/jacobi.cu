@@ -682,7 +682,7 @@ __device__ void replay_consumer(const ST* __restrict__ rot_log, int n, DevStatus
 }
 
 template <typename ST>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(512, 1)
 jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol, int max_sweeps,
             DevStatus* __restrict__ status, ST* __restrict__ v_out, int cons_rows) {
   using A_ = Arith<ST>;
@@ -755,6 +755,32 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     s_bad = 0x7fffffff;
   }
   __syncthreads();
+  // the update warps walk only the non-priority blocks: compact the block
+  // table in place (warp 0, ballot ranks; writes never pass the read index)
+  __shared__ int s_nnon;
+  if (warp == 0) {
+    const bool ev = (n & 1) == 0;
+    const int nb = np * (np + 1) / 2;
+    int cnt = 0;
+    for (int base = 0; base < nb; base += 32) {
+      const int idx = base + lane;
+      int w = 0;
+      bool keep = false;
+      if (idx < nb) {
+        w = blk[idx];
+        const int aa = w & 0xffff, bb = w >> 16;
+        keep = !(bb == aa || bb == aa + 2 || (bb == aa + 1 && (aa == np - 2 || (ev && aa == 0))));
+      }
+      const unsigned m = __ballot_sync(FULL, keep);
+      __syncwarp();
+      if (keep) blk[cnt + __popc(m & ((1u << lane) - 1))] = w;
+      cnt += __popc(m);
+      __syncwarp();
+    }
+    if (lane == 0) s_nnon = cnt;
+  }
+  __syncthreads();
+  const int nnon = s_nnon;
   for (int k = tid; k < n; k += NT)
     if (!A_::gt0(A_::lds(AE(k, k)))) atomicMin(&s_bad, k);
   __syncthreads();
@@ -872,85 +898,109 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
       break;
     }
     const bool want_ratio = sweep + 1 == max_sweeps;
+    const bool even_n = (n & 1) == 0;
+    // priority blocks: the blocks of a round that hold every entry the next
+    // round's rotations read (the same slot pairs in every round of the
+    // circle schedule; tests/test_schedule.py checks this exhaustively)
+    auto priority = [&](int aa, int bb) {
+      return bb == aa || bb == aa + 2 || (bb == aa + 1 && (aa == np - 2 || (even_n && aa == 0)));
+    };
     if (is_rot) {
-      // ===== rotation warps =====
+      // ===== rotation warps: rot(r) -> [U finished round r-1] -> release U
+      // for round r -> the priority blocks of round r (which feed rot(r+1)),
+      // shared by every rotation warp but the publisher, so the rotation
+      // chain never waits for the bulk update. (Carrying each slot's next
+      // inputs in registers, with each slot thread updating "its" priority
+      // block, was slower: the per-thread block chain sits on the critical
+      // path, 2.37 k vs 2.16 k cycles per round at n = 64.)
       long long cnt_sweep = 0;
       double wmax = 0.0;
-      for (int r = 0; r < (wr < nw_act ? Rr : 0); ++r) {  // idle rotation warps skip the sweep
-        if (r > 0) nbar_sync(2, NB12);  // round-r diagonal entries are final
-        if (jt && sweep == 0 && r < 64 && rtid == 0) jt[r * 16 + 0] = clock64();
-        AT* rb = RC((int)((g + r) & 1));
-        int* pw = pwb + ((g + r) & 1) * np;
-        const int k = rtid;  // one slot per rotation thread (np <= 64 here)
-        int bad = 0x7fffffff, act_i = 0;
-        if (k < np) {
-          int pp, qq;
-          rr_pair(n, r, k, pp, qq);
-          AT app = A_::one(), aqq = A_::one(), apq = A_::zero();
-          if (qq < n) {
-            app = A_::lds(AE(pp, pp));
-            aqq = A_::lds(AE(qq, qq));
-            apq = A_::lds(AE(pp, qq));
-          }
-          if (jt && sweep == 0 && r < 64 && rtid == 0 && A_::hi(app) != -1.0) jt[r * 16 + 6] = clock64();
-          const bool act = qq < n && ((jexp & 1) ? true : A_::active(app, aqq, apq, tol));
-          if (want_ratio && qq < n) wmax = fmax(wmax, A_::ratio(app, aqq, apq));
-          AT c = A_::one(), s = A_::zero(), npp = app, nqq = aqq;
-          {
-            // The rotation is evaluated for every slot, independently of the
-            // stop test (off the critical path: stop-test sqrt and rotation
-            // chain run concurrently), and kept only for active pairs: the
-            // active pairs' values are the same operations on the same inputs.
-            AT c2, s2, np2, nq2;
-            if (jexp & 1) {
-              c2 = A_::one(); s2 = A_::zero(); np2 = app; nq2 = aqq;
-            } else
-            A_::rotate(app, aqq, apq, c2, s2, np2, nq2);
-            if (act) {
-              c = c2;
-              s = s2;
-              npp = np2;
-              nqq = nq2;
-              if (!A_::gt0(npp)) bad = min(bad, pp);
-              if (!A_::gt0(nqq)) bad = min(bad, qq);
+      bool aborted = false;
+      const int n_prio_w = nw_rot - (fused ? 1 : 0);
+      const int NPR = 32 * n_prio_w;
+      if (wr < n_prio_w) {
+        const bool rot_warp = wr < nw_act;
+        for (int r = 0; r < Rr; ++r) {
+          const bool trace = jt && sweep == 0 && r < 64 && rtid == 0;
+          if (trace) jt[r * 16 + 0] = clock64();
+          AT* rb = RC((int)((g + r) & 1));
+          int* pw = pwb + ((g + r) & 1) * np;
+          if (rot_warp) {
+            const int k = rtid;  // one slot per rotation thread (np <= 64 here)
+            int bad = 0x7fffffff, act_i = 0;
+            if (k < np) {
+              int pp, qq;
+              rr_pair(n, r, k, pp, qq);
+              AT app = A_::one(), aqq = A_::one(), apq = A_::zero();
+              if (qq < n) {
+                app = A_::lds(AE(pp, pp));
+                aqq = A_::lds(AE(qq, qq));
+                apq = A_::lds(AE(pp, qq));
+              }
+              const bool act = qq < n && A_::active(app, aqq, apq, tol);
+              if (want_ratio && qq < n) wmax = fmax(wmax, A_::ratio(app, aqq, apq));
+              AT c = A_::one(), s = A_::zero(), npp = app, nqq = aqq;
+              {
+                // evaluated for every slot, concurrently with the stop test,
+                // and kept only for active pairs (same operations, same inputs)
+                AT c2, s2, np2, nq2;
+                A_::rotate(app, aqq, apq, c2, s2, np2, nq2);
+                if (act) {
+                  c = c2;
+                  s = s2;
+                  npp = np2;
+                  nqq = nq2;
+                  if (!A_::gt0(npp)) bad = min(bad, pp);
+                  if (!A_::gt0(nqq)) bad = min(bad, qq);
+                }
+              }
+              act_i = act ? 1 : 0;
+              rb[k] = c;
+              rb[np + k] = s;
+              rb[2 * np + k] = npp;
+              rb[3 * np + k] = nqq;
+              pw[k] = pp | (qq << 15) | (act_i << 30);
+              ST* lg = rot_log + 2 * ((g + r) * np + k);
+              A_::st(lg, c);
+              A_::st(lg + 1, s);
             }
+            cnt_sweep += __popc(__ballot_sync(FULL, act_i));
+            if (__any_sync(FULL, bad != 0x7fffffff)) bad = warp_min(bad);
+            if (nw_act > 1) {
+              if (lane == 0 && bad != 0x7fffffff) atomicMin(&s_bad, bad);
+              nbar_sync(4, 32 * nw_act);
+              bad = s_bad;
+            }
+            if (trace) jt[r * 16 + 1] = clock64();
+            if (r > 0) nbar_sync(3, NB12);  // the update warps finished round r-1
+            if (trace) jt[r * 16 + 2] = clock64();
+            if (bad != 0x7fffffff && rtid == 0) {
+              const int kk = rr_slot(n, r, bad);
+              const int pp = pw[kk] & 0x7fff;
+              status->status = kNotPositiveDefinite;
+              status->index = bad + 1;
+              status->value = A_::hi(bad == pp ? rb[2 * np + kk] : rb[3 * np + kk]);
+              status->sweeps = sweeps;
+              status->rotations = rotations;
+              status->rounds = g + r;
+              s_abort = 1;
+            }
+            if (bad != 0x7fffffff) __syncwarp();
+            nbar_arrive(1, NB1);  // round r's rotations are published (or the abort)
           }
-          if (jt && sweep == 0 && r < 64 && rtid == 0 && A_::hi(c) != -7.0) jt[r * 16 + 7] = clock64();
-          act_i = act ? 1 : 0;
-          rb[k] = c;
-          rb[np + k] = s;
-          rb[2 * np + k] = npp;
-          rb[3 * np + k] = nqq;
-          pw[k] = pp | (qq << 15) | (act_i << 30);
-          ST* lg = rot_log + 2 * ((g + r) * np + k);
-          A_::st(lg, c);
-          A_::st(lg + 1, s);
-        }
-        cnt_sweep += __popc(__ballot_sync(FULL, act_i));
-        bad = warp_min(bad);
-        if (nw_act > 1) {
-          if (lane == 0 && bad != 0x7fffffff) atomicMin(&s_bad, bad);
-          nbar_sync(4, 32 * nw_act);
-          bad = s_bad;
-        }
-        if (bad != 0x7fffffff) {
-          if (rtid == 0) {
-            const int kk = rr_slot(n, r, bad);
-            const int pp = pw[kk] & 0x7fff;
-            status->status = kNotPositiveDefinite;
-            status->index = bad + 1;
-            status->value = A_::hi(bad == pp ? rb[2 * np + kk] : rb[3 * np + kk]);
-            status->sweeps = sweeps;
-            status->rotations = rotations;
-            status->rounds = g + r;
-            s_abort = 1;
+          nbar_sync(5, NPR);  // rb / pw (and s_abort) visible to every priority thread
+          if (s_abort) {
+            aborted = true;
+            break;
           }
-          __syncwarp();
-          nbar_arrive(1, NB1);  // release the update warps; they see s_abort
-          break;
+          for (int j = rtid; j < npri; j += NPR) {
+            const int w = pri[j];
+            update_block(w & 0xffff, w >> 16, rb, pw);
+          }
+          nbar_sync(5, NPR);  // rot(r+1) reads the priority blocks
+          if (trace) jt[r * 16 + 3] = clock64();
         }
-        if (jt && sweep == 0 && r < 64 && rtid == 0) jt[r * 16 + 1] = clock64();
-        nbar_arrive(1, NB1);
+        if (rot_warp && !aborted) nbar_sync(3, NB12);  // the update warps finished the last round
       }
       if (is_pub) {  // publisher: round g+r's log entries are complete after B1
         for (int r = 0; r < Rr; ++r) {
@@ -968,50 +1018,22 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
         w_worst[wr] = wm;
       }
     } else {
-      // ===== update warps =====
+      // ===== update warps: every non-priority block of round r, once round
+      // r's rotations are published (B1); done -> B3
       for (int r = 0; r < Rr; ++r) {
         nbar_sync(1, NB1);
         const bool trace = jt && sweep == 0 && r < 64 && utid == 0;
-        if (trace && blk[0] != -1) jt[r * 16 + 2] = clock64();  // after B1 really completed
+        if (trace) jt[r * 16 + 4] = clock64();
         if (s_abort) break;
         const int b = (int)((g + r) & 1);
         const AT* rb = RC(b);
         const int* pw = pwb + b * np;
-        const bool has_next = r + 1 < Rr;
-        const int rn = r + 1;
-        // The blocks holding the entries round r+1's rotations read are the
-        // same for every round of the circle schedule: the diagonal blocks,
-        // (k, k+2) for k <= np-3, (np-2, np-1), and (0, 1) for even n (each
-        // holds exactly one next-round pair; checked exhaustively for
-        // n < 140 against the schedule in tests/test_schedule.py).
-        const bool even_n = (n & 1) == 0;
-        auto priority = [&](int aa, int bb) {
-          return bb == aa || bb == aa + 2 || (bb == aa + 1 && (aa == np - 2 || (even_n && aa == 0)));
-        };
-        // Two phases through ONE code path (a single inlined copy of the block
-        // update keeps the hot loop small in the instruction caches):
-        // phase 0 = the priority blocks, then release the rotation warps;
-        // phase 1 = every other block (decode table built once per launch).
-        const int nblk = np * (np + 1) / 2;
-        for (int ph = has_next ? 0 : 1; ph < 2; ++ph) {
-          const int cnt_ph = ph == 0 ? npri : ((jexp & 2) ? 0 : nblk);
-          const int* list = ph == 0 ? pri : blk;
-          for (int j = utid; j < cnt_ph; j += n_upd) {
-            const int w = list[j];
-            const int aa = w & 0xffff, bb = w >> 16;
-            if (ph == 1 && has_next && priority(aa, bb)) continue;
-            update_block(aa, bb, rb, pw);
-          }
-          if (ph == 0) {
-            if (trace) jt[r * 16 + 3] = clock64();
-            nbar_arrive(2, NB12);
-            nbar_sync(5, n_upd);  // pass-2 traffic waits for the critical blocks
-            if (trace && blk[1] != -1) jt[r * 16 + 8] = clock64();  // pass 1 of all U warps done
-          }
+        for (int j = utid; j < nnon; j += n_upd) {
+          const int w = blk[j];
+          update_block(w & 0xffff, w >> 16, rb, pw);
         }
-        if (trace) jt[r * 16 + 4] = clock64();
-        nbar_sync(3, n_upd);
         if (trace) jt[r * 16 + 5] = clock64();
+        nbar_arrive(3, NB12);
       }
     }
     __syncthreads();
@@ -1333,7 +1355,12 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   if (np <= 64 && smem_pipe <= smem_limit) {  // warp-specialised single-CTA solver
     auto k = jacobi_smem<ST>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pipe);
-    static const int warps_env = getenv("MPSVD_JACOBI_WARPS") ? atoi(getenv("MPSVD_JACOBI_WARPS")) : 16;
+    // 16 warps (__launch_bounds__(512): 128 registers, no spills); fewer via
+    // MPSVD_JACOBI_WARPS (a multiple of 4, for experiments)
+    static const int warps_env = [] {
+      const int w = getenv("MPSVD_JACOBI_WARPS") ? atoi(getenv("MPSVD_JACOBI_WARPS")) : 16;
+      return (w >= 8 && w <= 16 && w % 4 == 0) ? w : 16;
+    }();
     const int threads = 32 * warps_env;
     static const bool trace = getenv("MPSVD_JACOBI_TRACE") != nullptr;
     unsigned long long* tbuf = nullptr;
@@ -1363,24 +1390,21 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
       cudaMemcpyToSymbol(g_jtrace, &nul, sizeof(nul));
       cudaFree(tbuf);
       // per round (cycles, SM clock): R = rotation warp, U = update warps
-      double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+      double acc[5] = {0, 0, 0, 0, 0};
       int cnt = 0;
       for (int r = 1; r + 1 < 63 && h[(r + 1) * 16 + 0]; ++r, ++cnt) {
         const unsigned long long* t = h + r * 16;
-        acc[0] += (double)(t[16 + 2] - t[2]);  // period (U B1 to next U B1)
-        acc[1] += (double)(t[6] - t[0]);        // R: B2 wait + loads
-        acc[2] += (double)(t[7] - t[6]);        // R: rotation math
-        acc[3] += (double)(t[1] - t[7]);        // R: stores + reductions
-        acc[4] += (double)(t[3] - t[2]);        // U: pass 1 (first U thread)
-        acc[5] += (double)(t[8] - t[3]);        // U: wait for all pass-1 warps
-        acc[6] += (double)(t[4] - t[8]);        // U: pass 2 (first U thread)
+        acc[0] += (double)(t[16 + 0] - t[0]);  // period (R round start to next)
+        acc[1] += (double)(t[1] - t[0]);        // R: rotations
+        acc[2] += (double)(t[2] - t[1]);        // R: wait for U's previous round
+        acc[3] += (double)(t[3] - t[2]);        // R: priority blocks
+        acc[4] += (double)(t[5] - t[4]);        // U: bulk update
       }
       if (cnt)
         fprintf(stderr,
-                "[jacobi trace n=%d] period %.0f | R: B2 wait+loads %.0f, math %.0f, tail %.0f | U: pass1 %.0f, "
-                "pass1 all %.0f, pass2 %.0f (cycles/round, %d rounds)\n",
-                n, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt, acc[6] / cnt,
-                cnt);
+                "[jacobi trace n=%d] period %.0f | R: rotations %.0f, wait U %.0f, priority blocks %.0f | "
+                "U: bulk %.0f (cycles/round, %d rounds)\n",
+                n, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, cnt);
     }
     return cudaGetLastError();
   }
