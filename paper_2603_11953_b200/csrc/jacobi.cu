@@ -174,6 +174,9 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Optional per-round timestamps of the first sweep (MPSVD_JACOBI_TRACE=1).
+__device__ unsigned long long* g_jtrace = nullptr;
+
 template <typename ST, bool kSmem>
 __global__ void __launch_bounds__(kJacobiThreads)
 jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict__ rot_log, int n,
@@ -304,6 +307,8 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
     worst = 0.0;
     const bool want_ratio = sweep + 1 == max_sweeps;
     for (int r = 0; r < R; ++r, ++g) {
+      const bool trace = !kSmem && g_jtrace && sweep == 0 && r < 64 && blockIdx.x == 0 && tid == 0;
+      if (trace) g_jtrace[r * 16 + 0] = clock64();
       const int par = (int)(g & 1);
       const int rnext = (r + 1 == R) ? 0 : r + 1;
       const ST* dcur = diagbuf + par * 3 * np;
@@ -365,6 +370,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         }
       }
       __syncthreads();
+      if (trace) g_jtrace[r * 16 + 1] = clock64();
       int cnt = 0, badx = 0x7fffffff;
       for (int w = 0; w < nw_rot; ++w) {
         cnt += w_cnt[w];
@@ -555,7 +561,9 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
             }
           }
       }
+      if (trace) g_jtrace[r * 16 + 2] = clock64();
       gsync();
+      if (trace) g_jtrace[r * 16 + 3] = clock64();
     }
     ++sweeps;
     if (rot_sweep == 0) {
@@ -600,8 +608,6 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 constexpr int kUpdateWarps = 12;
 constexpr int kRotWarps = 4;
 
-// Optional per-round timestamps of the first sweep (MPSVD_JACOBI_TRACE=1).
-__device__ unsigned long long* g_jtrace = nullptr;
 __device__ int g_jexp = 0;  // experiment switches (tracing only): 1 fake rotations, 2 skip pass 2
 
 // partner of x in `round` (n itself for the bye of an odd n)
@@ -1427,8 +1433,38 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   int nn = n, ms = max_sweeps;
   double tl = tol;
   void* args[] = {&a, &d, &lg, &nn, &tl, &ms, &status};
-  return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(kJacobiThreads), args,
-                                     smem_rot, st);
+  static const bool trace = getenv("MPSVD_JACOBI_TRACE") != nullptr;
+  unsigned long long* tbuf = nullptr;
+  if (trace) {
+    cudaMalloc(&tbuf, 64 * 16 * sizeof(unsigned long long));
+    cudaMemset(tbuf, 0, 64 * 16 * sizeof(unsigned long long));
+    cudaMemcpyToSymbol(g_jtrace, &tbuf, sizeof(tbuf));
+  }
+  const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(kJacobiThreads), args,
+                                                     smem_rot, st);
+  if (trace) {
+    unsigned long long h[64 * 16];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);
+    unsigned long long* nul = nullptr;
+    cudaMemcpyToSymbol(g_jtrace, &nul, sizeof(nul));
+    cudaFree(tbuf);
+    double acc[4] = {0, 0, 0, 0};
+    int cnt = 0;
+    for (int r = 1; r + 1 < 63 && h[(r + 1) * 16 + 0]; ++r, ++cnt) {
+      const unsigned long long* t = h + r * 16;
+      acc[0] += (double)(t[16] - t[0]);
+      acc[1] += (double)(t[1] - t[0]);
+      acc[2] += (double)(t[2] - t[1]);
+      acc[3] += (double)(t[3] - t[2]);
+    }
+    if (cnt)
+      fprintf(stderr,
+              "[jacobi multi-CTA trace n=%d grid=%lld] period %.0f | rotations %.0f, block updates %.0f, grid sync %.0f "
+              "(cycles/round, %d rounds)\n",
+              n, grid, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, cnt);
+  }
+  return le;
 }
 
 cudaError_t launch_jacobi(bool dd_mode, int n, double tol, int max_sweeps, const JacobiWorkspace& ws,
