@@ -26,7 +26,7 @@ __global__ void rate(int iters, unsigned long long* cyc) {
   unsigned char* b = sm + 3 * 4096;      // 3 planes x 16 x N bf16
   for (int i = threadIdx.x; i < (3 * 4096 + 3 * 32 * N) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3f803f80u;
   if (threadIdx.x < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(256));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (threadIdx.x == 0) {
@@ -69,7 +69,7 @@ __global__ void rate(int iters, unsigned long long* cyc) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
-  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(256));
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
 }
 
 template <int N, int MAJOR>
@@ -102,6 +102,7 @@ int run(const char* name) {
 int main() {
   run<64, 1>("MN-major no-swizzle");
   run<128, 1>("MN-major no-swizzle");
+  run<256, 1>("MN-major no-swizzle");
   run<64, 0>("K-major no-swizzle");
   run<128, 0>("K-major no-swizzle");
   return 0;
