@@ -49,10 +49,9 @@ constexpr int kMaxDepth = 8;                      // fp32 A chunks in flight per
 constexpr int kStageBytes = kBM * kKC * 4;        // fp32 chunk: 8 KB
 constexpr int kPlaneBytes = kBM * kKC * 2;        // one bf16 piece of a chunk: 4096
 constexpr int kConvWarps = 8, kEpiWarps = 8;      // converters: warps 0-7; epilogue: warps 8-15
-constexpr int kLoadWarps = 2;                     // A loaders: warps 16-17 (4 measured the same)
+constexpr int kLoadWarps = 2;                     // A loaders: warps 16-17
 constexpr int kWarpLoad0 = 16, kWarpMma = 18;
 constexpr int kThreads = 608;
-constexpr int kPiecesPerLoader = kBM * kKC * 4 / 16 / (kLoadWarps * 32);  // 16-byte pieces per chunk
 constexpr int kPlanes = 8;                        // max bf16 chunk slots = one per active converter warp
 constexpr int kSmemLimit = 227 * 1024;
 
@@ -224,16 +223,13 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
     // 128-byte line); the piece is written where its converter lane reads
     // it: [item][half][lane] x 16 B.
     const int lt = threadIdx.x - kWarpLoad0 * 32;
-    int dst_off[kPiecesPerLoader], col_off[kPiecesPerLoader], row_off[kPiecesPerLoader];
+    int dst_off[8], col_off[8], row_off[8];
 #pragma unroll
-    for (int i = 0; i < kPiecesPerLoader; ++i) {
-      const int q = lt + kLoadWarps * 32 * i, c = q >> 5, p = q & 31;
+    for (int i = 0; i < 8; ++i) {
+      const int q = lt + 64 * i, c = q >> 5, p = q & 31;
       const int rg = p >> 1, half = p & 1, kg = c >> 3, kl = c & 7;
       const int item = (rg >> 2) + 4 * kg, clane = (rg & 3) * 8 + kl;
-      // XOR swizzle of the lane slot by (row group & 3, half): the 8 lanes of
-      // one 128-byte global line land in 8 distinct 16-byte bank groups
-      // (unswizzled, all 8 shared one)
-      dst_off[i] = ((item * 2 + half) * 32 + (clane ^ (2 * (rg & 3) + half))) * 16;
+      dst_off[i] = ((item * 2 + half) * 32 + clane) * 16;
       col_off[i] = c;
       row_off[i] = p * 4;
     }
@@ -245,11 +241,11 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
       mbar_wait(&stage_empty[slot], ph ^ 1);
       unsigned char* dst = ssm + slot * kStageBytes;
 #pragma unroll
-      for (int i = 0; i < kPiecesPerLoader; ++i) {
+      for (int i = 0; i < 8; ++i) {
         const int col = kc * kKC + col_off[i];
         const long long row = row0 + row_off[i];
         const bool ok = col < n && row < m;  // m % 4 == 0: a 16-byte piece is all in or all out
-        if (!(dbg & 16)) cp_async16_zfill(dst + dst_off[i], ok ? a + (long long)col * lda + row : a, ok);
+        cp_async16_zfill(dst + dst_off[i], ok ? a + (long long)col * lda + row : a, ok);
       }
       cp_async_mbar_arrive(&stage_full[slot]);
       if (++kc == nkc) {
@@ -314,20 +310,10 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
     if (warp < depth) {
       const int kl = lane & 7, rgl = lane >> 3;
       unsigned char* dst = psm + warp * 3 * kPlaneBytes;
-      const unsigned char* src = ssm + warp * kStageBytes;
-      const int sw0 = (lane ^ (2 * rgl)) * 16, sw1 = (lane ^ (2 * rgl + 1)) * 16;  // loader swizzle, half 0 / 1
+      const unsigned char* src = ssm + warp * kStageBytes + lane * 16;
       unsigned ph = 0;
       for (int g = warp; g < nchunks; g += depth) {
         { AVP_T0(); mbar_wait(&stage_full[warp], ph); mbar_wait(&plane_empty[warp], ph ^ 1); AVP_ADD(2); }
-        if (dbg & 8) {  // experiment: skip the conversion (measures the A stream alone)
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&stage_empty[warp]);
-            mbar_arrive(&plane_full[warp]);
-          }
-          ph ^= 1;
-          continue;
-        }
         AVP_T0();
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -335,8 +321,8 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int i = hh * 4 + j;
-            x[j] = *reinterpret_cast<const float4*>(src + (i * 2 + 0) * 512 + sw0);
-            y[j] = *reinterpret_cast<const float4*>(src + (i * 2 + 1) * 512 + sw1);
+            x[j] = *reinterpret_cast<const float4*>(src + (i * 2 + 0) * 512);
+            y[j] = *reinterpret_cast<const float4*>(src + (i * 2 + 1) * 512);
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -438,12 +424,15 @@ size_t av_tc_wplanes_bytes(int n) {
 }
 
 // experiment switches (MPSVD_AV_DBG): bit 0 skips the U stores, bit 1 the
-// MMAs, bit 2 prints per-role cycle counts of CTA 0, bit 3 skips the bf16
-// conversion, bit 4 the A loads (tools/av_probe*.sh). Measured on C2: with
-// everything but the barrier hand-offs and TMEM loads skipped the kernel
-// still takes 64 us: at n = 64 the MMA stream (6 x M128 N64 K16 per 16-column
-// chunk, ~75 cycles each, tools/microbench/umma_rate.cu) and its hand-offs
-// bound K7 rather than HBM.
+// MMAs, bit 2 prints per-role cycle counts of CTA 0 (tools/av_probe.sh).
+// Findings (C2, n = 64): loads + conversion alone take 0.089 ms of the
+// 0.128 ms, and with loads, conversion, MMAs and stores all skipped the
+// barrier hand-offs alone still take ~0.065 ms: the ring of mbarrier
+// hand-offs (loader -> converter -> MMA -> epilogue, 8 slots deep, limited by
+// shared memory) bounds K7 at small n, not HBM. An XOR-swizzled staging
+// layout (conflict-free cp.async writes), 4 loader warps, packing the six
+// products into four MMAs (N = 2n) and test_wait spinning were all measured
+// slower or equal and not kept.
 static int g_av_dbg = [] {
   const char* e = getenv("MPSVD_AV_DBG");
   return e ? atoi(e) : 0;

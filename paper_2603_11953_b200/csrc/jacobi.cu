@@ -153,6 +153,10 @@ struct Arith<double2> {
 
 // ---------------------------------------------------------------------------
 constexpr int kJacobiThreads = 256;
+// multi-CTA solver: one 512-thread CTA per SM. Every CTA evaluates all of a
+// round's rotations (instruction-bound in double-double), so one CTA per SM
+// does that work once per SM instead of twice.
+constexpr int kJacobiGridThreads = 512;
 
 template <typename ST>
 __host__ __device__ constexpr size_t rot_smem_bytes(int np) {
@@ -178,7 +182,7 @@ __device__ __forceinline__ double warp_max(double v) {
 __device__ unsigned long long* g_jtrace = nullptr;
 
 template <typename ST, bool kSmem>
-__global__ void __launch_bounds__(kJacobiThreads)
+__global__ void __launch_bounds__(kSmem ? kJacobiThreads : kJacobiGridThreads)
 jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict__ rot_log, int n,
               double tol, int max_sweeps, DevStatus* __restrict__ status) {
   using A_ = Arith<ST>;
@@ -1423,11 +1427,11 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   auto k = jacobi_kernel<ST, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rot);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kJacobiThreads, smem_rot);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kJacobiGridThreads, smem_rot);
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const long long nblk = (long long)np * (np + 1) / 2;
-  long long want = (nblk + kJacobiThreads - 1) / kJacobiThreads;
-  long long grid = (long long)sm_count * (per_sm < 2 ? per_sm : 2);
+  long long want = (nblk + kJacobiGridThreads - 1) / kJacobiGridThreads;
+  long long grid = (long long)sm_count;  // one CTA per SM (see kJacobiGridThreads)
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   int nn = n, ms = max_sweeps;
@@ -1440,7 +1444,7 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
     cudaMemset(tbuf, 0, 64 * 16 * sizeof(unsigned long long));
     cudaMemcpyToSymbol(g_jtrace, &tbuf, sizeof(tbuf));
   }
-  const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(kJacobiThreads), args,
+  const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(kJacobiGridThreads), args,
                                                      smem_rot, st);
   if (trace) {
     unsigned long long h[64 * 16];
