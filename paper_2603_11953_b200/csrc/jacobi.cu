@@ -160,8 +160,9 @@ constexpr int kJacobiGridThreads = 512;
 
 template <typename ST>
 __host__ __device__ constexpr size_t rot_smem_bytes(int np) {
-  // c, s, new a_pp, new a_qq (AT each) + packed pair/active word
-  return (size_t)np * (4 * sizeof(typename Arith<ST>::AT) + sizeof(int));
+  // c, s, new a_pp, new a_qq (AT each) + packed pair/active word + (multi-CTA)
+  // next-round slot and partner of every player (2 x N ints, N = 2 np)
+  return (size_t)np * (4 * sizeof(typename Arith<ST>::AT) + sizeof(int)) + (size_t)4 * np * sizeof(int);
 }
 
 // Reduction helpers over one warp (all 32 lanes participate).
@@ -208,6 +209,8 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   AT* rnqq = rnpp + np;
   int* pw = reinterpret_cast<int*>(rnqq + np);  // p | q << 15 | active << 30
   int* blk = pw + np;                            // aa | bb << 16 (smem variant)
+  int* nsl = pw + np;                            // multi-CTA: next-round slot | (player is q) << 16
+  int* npart = nsl + 2 * np;                     // multi-CTA: next-round partner (n for the bye)
   __shared__ int s_flag;
   __shared__ int w_cnt[32], w_bad[32];
   __shared__ double w_worst[32];
@@ -373,6 +376,15 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           w_worst[warp] = wmax;
         }
       }
+      if (!kSmem) {  // round rnext's slot and partner of every player, for emit()
+        for (int x = tid; x < n; x += bs) {
+          const int s2 = rr_slot(n, rnext, x);
+          int pp, qq;
+          rr_pair(n, rnext, s2, pp, qq);
+          nsl[x] = s2 | ((pp == x ? 0 : 1) << 16);
+          npart[x] = pp == x ? qq : pp;
+        }
+      }
       __syncthreads();
       if (trace) g_jtrace[r * 16 + 1] = clock64();
       int cnt = 0, badx = 0x7fffffff;
@@ -481,15 +493,18 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         continue;
       }
       // multi-CTA variant: every block is visited so that the entries the
-      // next round's rotations read are published to the diag buffer
+      // next round's rotations read are published to the diag buffer.
+      // Store-once symmetric storage: entry (i, j) lives at its upper-triangle
+      // position (min, max) (4 stores per 2x2 block instead of 8; the sweep
+      // pre-check, the round-0 buffer and the final diagonal read only the
+      // upper triangle).
+      auto CEg = [&](int i, int j) -> ST* { return i <= j ? AE(i, j) : AE(j, i); };
       auto emit = [&](int x, int y, AT v) {
-        const int s2 = rr_slot(n, rnext, x);
-        int pp, qq;
-        rr_pair(n, rnext, s2, pp, qq);
+        const int w = nsl[x];
         if (x == y) {
-          A_::st(dnext + 3 * s2 + (pp == x ? 0 : 1), v);
-        } else if ((pp == x && qq == y) || (pp == y && qq == x)) {
-          A_::st(dnext + 3 * s2 + 2, v);
+          A_::st(dnext + 3 * (w & 0xffff) + (w >> 16), v);
+        } else if (npart[x] == y) {
+          A_::st(dnext + 3 * (w & 0xffff) + 2, v);
         }
       };
       for (long long idx = gtid; idx < nblk; idx += gstride) {
@@ -512,8 +527,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
             vpq = A_::zero();
             A_::st(AE(p0, p0), vpp);
             A_::st(AE(q0, q0), vqq);
-            A_::st(AE(p0, q0), vpq);
-            A_::st(AE(q0, p0), vpq);
+            A_::st(AE(p0, q0), vpq);  // p0 < q0: the canonical copy
           } else {
             vpp = LD(AE(p0, p0));
             vqq = LD(AE(q0, q0));
@@ -529,11 +543,15 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         const bool actb = (wb >> 30) & 1;
         const int rows[2] = {p0, q0}, cols[2] = {k0, l0};
         const int nr = q0 < n ? 2 : 1, nc = l0 < n ? 2 : 1;
+        ST* e[2][2];
         AT x[2][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int v = 0; v < 2; ++v) x[u][v] = (u < nr && v < nc) ? LD(AE(rows[u], cols[v])) : A_::zero();
+          for (int v = 0; v < 2; ++v) {
+            e[u][v] = CEg(rows[u], cols[v]);
+            x[u][v] = (u < nr && v < nc) ? LD(e[u][v]) : A_::zero();
+          }
         if (actb) {
           const AT cb = rc[bb], sb = rsn[bb];
 #pragma unroll
@@ -557,10 +575,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
             if (u < nr && v < nc) {
-              if (acta || actb) {
-                A_::st(AE(rows[u], cols[v]), x[u][v]);
-                A_::st(AE(cols[v], rows[u]), x[u][v]);
-              }
+              if (acta || actb) A_::st(e[u][v], x[u][v]);
               emit(rows[u], cols[v], x[u][v]);
             }
           }
