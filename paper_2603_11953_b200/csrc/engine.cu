@@ -258,6 +258,7 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
 }
 
 Plan::~Plan() {
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -269,6 +270,10 @@ Plan::~Plan() {
 void Plan::set_jacobi(double t, int sweeps) {
   if (sweeps < 1) throw std::invalid_argument("max_sweeps must be >= 1");
   if (sweeps > 1000) throw std::invalid_argument("max_sweeps must be <= 1000");
+  if (t != tol || sweeps != max_sweeps) {  // the captured graph holds the old kernel arguments
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+  }
   tol = t;
   max_sweeps = sweeps;
   ensure_log();
@@ -279,6 +284,10 @@ void Plan::set_jacobi(double t, int sweeps) {
 // requested.
 void Plan::ensure_log() {
   if (max_sweeps <= log_sweeps) return;
+  if (graph_exec) {  // the captured graph holds the old log pointer
+    cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+  }
   if (jws.log) {
     check(cudaDeviceSynchronize(), "sync before log resize");
     for (auto& p : owned)
@@ -348,22 +357,78 @@ void Plan::eigen(cudaStream_t st) {
   }
 }
 
+// The pipeline is captured once per set of device pointers into a CUDA graph
+// and replayed (saves the per-kernel launch gaps; ~9 launches per SVD).
+// MPSVD_NO_GRAPH=1 launches the kernels directly; so does any capture error.
 void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                    cudaStream_t st) {
   if (!st) st = own_stream;
   last_stream = st;
+  ensure_log();
+  static const bool no_graph = getenv("MPSVD_NO_GRAPH") != nullptr || getenv("MPSVD_JACOBI_TRACE") != nullptr ||
+                               getenv("MPSVD_AV_DBG") != nullptr;
+  if (no_graph || graph_failed) {
+    enqueue(d_a, lda, d_u, ldu, d_sigma, d_v, st);
+    return;
+  }
+  const GraphKey key{d_a, lda, d_u, ldu, d_sigma, d_v};
+  if (!graph_exec || !(key == graph_key)) {
+    if (graph_exec) {
+      cudaGraphExecDestroy(graph_exec);
+      graph_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(own_stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      try {
+        enqueue(d_a, lda, d_u, ldu, d_sigma, d_v, own_stream);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(own_stream, &g) == cudaSuccess) && ok && g;
+    }
+    if (ok) ok = cudaGraphInstantiate(&graph_exec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      cudaGetLastError();  // clear a capture error; run uncaptured from now on
+      graph_exec = nullptr;
+      graph_failed = true;
+      enqueue(d_a, lda, d_u, ldu, d_sigma, d_v, st);
+      return;
+    }
+    graph_key = key;
+    graph_launches = launches;
+  }
+  check(cudaGraphLaunch(graph_exec, st), "graph launch");
+  launches = graph_launches;
+  events_recorded = true;
+}
+
+// Phase events: plain records, or external event nodes while the pipeline
+// is being captured into a graph (so they still time the replayed graph).
+static void record_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  check(cudaStreamIsCapturing(st, &cs), "capture status");
+  if (cs == cudaStreamCaptureStatusActive)
+    check(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event");
+  else
+    check(cudaEventRecord(e, st), "event");
+}
+
+void Plan::enqueue(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
+                   cudaStream_t st) {
   launches = 0;
   check(cudaMemsetAsync(jws.status, 0, sizeof(DevStatus), st), "status reset");
-  check(cudaEventRecord(ev[0], st), "event");
+  record_event(ev[0], st);
   gram(d_a, lda, st);
-  check(cudaEventRecord(ev[1], st), "event");
+  record_event(ev[1], st);
   eigen(st);
   double* sig = d_sigma ? (double*)d_sigma : d_sigma_tmp;
   void* vw = d_v ? d_v : d_vwork_tmp;
   check(dev::launch_finish(dd, (int)n, jws, d_perm, d_lam_hi, d_lam_lo, sig, vw, d_w, dd ? 1 : 0, st),
         "finish");
   launches += 2;
-  check(cudaEventRecord(ev[2], st), "event");
+  record_event(ev[2], st);
   if (d_u && m > 0) {
     if (dd)
       check(dev::launch_av_dmma_f64((const double*)d_a, lda, m, (int)n, (const double*)d_w, (double*)d_u, ldu,
@@ -380,7 +445,7 @@ void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, voi
             "av_f32");
     launches += 1;
   }
-  check(cudaEventRecord(ev[3], st), "event");
+  record_event(ev[3], st);
   events_recorded = true;
   check(cudaMemcpyAsync(h_status, jws.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status D2H");
 }

@@ -31,6 +31,9 @@ class Plan {
   // Enqueue the whole pipeline on `st` (nullptr: the plan's stream).
   void execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                cudaStream_t st);
+  // the kernel sequence of execute (captured into graph_exec)
+  void enqueue(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
+               cudaStream_t st);
   mpsvd_exec_info wait();
   // status word handling around hand-assembled stage sequences
   void reset_status(cudaStream_t st);
@@ -76,6 +79,21 @@ class Plan {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int launches = 0;
   bool events_recorded = false;
+  struct GraphKey {
+    const void* a;
+    long long lda;
+    void* u;
+    long long ldu;
+    void* sigma;
+    void* v;
+    bool operator==(const GraphKey& o) const {
+      return a == o.a && lda == o.lda && u == o.u && ldu == o.ldu && sigma == o.sigma && v == o.v;
+    }
+  };
+  cudaGraphExec_t graph_exec = nullptr;
+  GraphKey graph_key{};
+  int graph_launches = 0;
+  bool graph_failed = false;
   std::vector<void*> owned;
 };
 
