@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <memory>
@@ -201,7 +202,9 @@ struct Bundle {
   void* d_u = nullptr;
   double* d_sigma = nullptr;
   void* d_v = nullptr;
+  double* h_sigma = nullptr;  // page-locked
   ~Bundle() {
+    if (h_sigma) cudaFreeHost(h_sigma);
     cudaFree(d_a);
     cudaFree(d_u);
     cudaFree(d_sigma);
@@ -224,6 +227,7 @@ Bundle& bundle_for(long long m, long long n, bool f64) {
   engine::check(cudaMalloc(&b->d_u, std::max<std::size_t>(1, m * n * elt)), "cudaMalloc U");
   engine::check(cudaMalloc((void**)&b->d_sigma, n * sizeof(double)), "cudaMalloc sigma");
   engine::check(cudaMalloc(&b->d_v, n * n * elt), "cudaMalloc V");
+  engine::check(cudaMallocHost((void**)&b->h_sigma, n * sizeof(double)), "cudaMallocHost sigma");
   auto& ref = *b;
   cache.emplace(key, std::move(b));
   return ref;
@@ -259,20 +263,20 @@ ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f
   engine::Plan& p = *b.plan;
   p.set_jacobi(cfg.tol, cfg.max_sweeps);
   const std::size_t elt = f64 ? 8 : 4;
+  (void)elt;
   cudaStream_t st = p.own_stream;
-  engine::check(cudaMemcpyAsync(b.d_a, a.raw(), m * n * elt, cudaMemcpyHostToDevice, st), "H2D A");
-  p.execute(b.d_a, m, b.d_u, m, b.d_sigma, b.d_v, st);
   const Precision wp = f64 ? Precision::Higher : Precision::Working;
   ThinSvdResult out;
-  out.factors.u = DenseMatrix::uninitialized(m, n, wp);  // fully overwritten by the D2H below
+  out.factors.u = DenseMatrix::uninitialized(m, n, wp);  // fully overwritten by the D2H copies
   out.factors.v = DenseMatrix::uninitialized(n, n, wp);
   out.factors.sigma.assign(n, 0.0);
   out.factors.precision = wp;
-  engine::check(cudaMemcpyAsync(out.factors.u.raw(), b.d_u, m * n * elt, cudaMemcpyDeviceToHost, st), "D2H U");
-  engine::check(cudaMemcpyAsync(out.factors.v.raw(), b.d_v, n * n * elt, cudaMemcpyDeviceToHost, st), "D2H V");
-  engine::check(cudaMemcpyAsync(out.factors.sigma.data(), b.d_sigma, n * sizeof(double), cudaMemcpyDeviceToHost, st),
-                "D2H sigma");
+  // H2D of A and D2H of U in row chunks overlapped with the Gram and U
+  // kernels (engine.cu, Plan::execute_host); sigma is downloaded through a
+  // page-locked staging slot of the plan
+  p.execute_host(a.raw(), b.d_a, out.factors.u.raw(), b.d_u, b.h_sigma, b.d_sigma, out.factors.v.raw(), b.d_v, st);
   const mpsvd_exec_info info = p.wait();
+  std::copy(b.h_sigma, b.h_sigma + n, out.factors.sigma.begin());
   raise_device_status(info, cfg.max_sweeps);
   out.eigensolver = EigensolverChoice::TwoSidedJacobi;
   out.gram_sync_events = 1;  // one global combine of the partial Grams

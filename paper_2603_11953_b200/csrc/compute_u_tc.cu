@@ -439,13 +439,15 @@ static int g_av_dbg = [] {
 }();
 
 cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, const float* w, void* wplanes,
-                             float* u, long long ldu, const DevStatus* status, int sm_count, cudaStream_t st) {
+                             float* u, long long ldu, const DevStatus* status, int sm_count, cudaStream_t st,
+                             bool prep) {
   using namespace tc;
   const int np = (n + 15) / 16 * 16;
   const int ldw = av_ldw(n);
   const int prep_threads = 256;
-  av_tc_prep_w<<<(np * np + prep_threads - 1) / prep_threads, prep_threads, 0, st>>>(
-      w, ldw, n, np, reinterpret_cast<__nv_bfloat16*>(wplanes), status);
+  if (prep)
+    av_tc_prep_w<<<(np * np + prep_threads - 1) / prep_threads, prep_threads, 0, st>>>(
+        w, ldw, n, np, reinterpret_cast<__nv_bfloat16*>(wplanes), status);
   const size_t wbytes = ((size_t)3 * np * np * 2 + 1023) & ~(size_t)1023;
   // one staging slot + one plane slot per active converter warp
   int depth = kConvWarps;

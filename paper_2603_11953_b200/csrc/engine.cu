@@ -259,6 +259,12 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
 
 Plan::~Plan() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  for (auto& e : cev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : uev)
+    if (e) cudaEventDestroy(e);
+  if (cdone) cudaEventDestroy(cdone);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -448,6 +454,118 @@ void Plan::enqueue(const void* d_a, long long lda, void* d_u, long long ldu, voi
   record_event(ev[3], st);
   events_recorded = true;
   check(cudaMemcpyAsync(h_status, jws.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status D2H");
+}
+
+// Host-buffer pipeline (the C ABI / C++ API path on one GPU). The upload of
+// A is cut at the 16 logical row blocks and each block's Gram kernels start
+// as soon as its rows have landed (same kernels, splits and partial slots as
+// execute(), so the result is bit-identical to it); U is formed in row
+// chunks, each downloaded while the next one is computed. The PCIe copies,
+// not the kernels, dominate this path (C2: ~10 ms of copies vs 0.57 ms of
+// kernels); this hides the Gram and U kernels behind them.
+void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double* h_sigma, double* d_sigma, void* h_v,
+                        void* d_v, cudaStream_t st) {
+  if (comm) throw std::invalid_argument("execute_host: single-GPU plans only");
+  ensure_log();
+  if (!copy_stream) {
+    check(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (auto& e : cev) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : uev) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&cdone, cudaEventDisableTiming), "event");
+  }
+  cudaStream_t cs = copy_stream;
+  last_stream = st;
+  launches = 0;
+  const size_t elt = dd ? 8 : 4;
+  const size_t pitch = (size_t)m * elt;
+  const size_t esz = dd ? 2 : 1;
+  check(cudaMemsetAsync(jws.status, 0, sizeof(DevStatus), st), "status reset");
+  // the copy stream must not overtake work already queued on st
+  check(cudaEventRecord(cdone, st), "event");
+  check(cudaStreamWaitEvent(cs, cdone, 0), "wait");
+  record_event(ev[0], st);
+  {
+    const long long base = m / nblocks, extra = m % nblocks;
+    long long row = 0;
+    for (int b = 0; b < nblocks; ++b) {
+      const long long len = base + (b < extra ? 1 : 0);
+      check(cudaMemcpy2DAsync((char*)d_a + row * elt, pitch, (const char*)h_a + row * elt, pitch, len * elt, n,
+                              cudaMemcpyHostToDevice, cs),
+            "H2D A block");
+      check(cudaEventRecord(cev[b], cs), "event");
+      check(cudaStreamWaitEvent(st, cev[b], 0), "wait");
+      const int sb = block_split_begin[b], cnt = block_split_begin[b + 1] - sb;
+      if (dd) {
+        check(dev::launch_gram_dd((const double*)d_a, m, (int)n, d_tiles, ntp, d_splits + sb, cnt,
+                                  (double2*)d_partials + (size_t)sb * ntp * 64 * 64, st),
+              "gram_dd");
+        launches += 1;
+      } else {
+        check(dev::launch_gram_f32((const float*)d_a, m, (int)n, d_tiles, ntp, d_tp_order, ndiag, d_tp_order + ndiag,
+                                   ntp - ndiag, d_splits + sb, cnt, d_partials + (size_t)sb * ntp * 64 * 64, st),
+              "gram_f32");
+        launches += (ndiag > 0 ? 1 : 0) + (ntp > ndiag ? 1 : 0);
+      }
+      row += len;
+    }
+  }
+  if (dd)
+    check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, d_bsb, nblocks, (double2*)d_bsums,
+                                      (double2*)d_m, st),
+          "gram_combine_dd");
+  else
+    check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks, (double*)d_bsums,
+                                       (double*)d_m, st),
+          "gram_combine_f64");
+  launches += 2;
+  (void)esz;
+  record_event(ev[1], st);
+  eigen(st);
+  check(dev::launch_finish(dd, (int)n, jws, d_perm, d_lam_hi, d_lam_lo, d_sigma, d_v, d_w, dd ? 1 : 0, st),
+        "finish");
+  launches += 2;
+  record_event(ev[2], st);
+  // sigma and V travel while U is formed
+  check(cudaEventRecord(cdone, st), "event");
+  check(cudaStreamWaitEvent(cs, cdone, 0), "wait");
+  check(cudaMemcpyAsync(h_sigma, d_sigma, n * sizeof(double), cudaMemcpyDeviceToHost, cs), "D2H sigma");
+  check(cudaMemcpyAsync(h_v, d_v, (size_t)n * n * elt, cudaMemcpyDeviceToHost, cs), "D2H V");
+  const bool tc = !dd && d_wplanes && dev::av_tc_supported((const float*)d_a, m, m, (int)n, m);
+  constexpr int kChunks = 16;
+  long long r0 = 0;
+  bool first = true;  // the first launched chunk splits W into its pieces
+  for (int k = 0; k < kChunks && r0 < m; ++k) {
+    long long r1 = (k + 1 == kChunks) ? m : ((long long)(k + 1) * m / kChunks) / 128 * 128;
+    if (r1 <= r0) continue;
+    const long long rows = r1 - r0;
+    if (dd)
+      check(dev::launch_av_dmma_f64((const double*)d_a + r0, m, rows, (int)n, (const double*)d_w, (double*)d_u + r0, m,
+                                    jws.status, st),
+            "av_dmma_f64");
+    else if (tc) {
+      check(dev::launch_av_tc_f32((const float*)d_a + r0, m, rows, (int)n, (const float*)d_w, d_wplanes,
+                                  (float*)d_u + r0, m, jws.status, sm_count, st, first),
+            "av_tc_f32");
+      if (first) launches += 1;
+      first = false;
+    } else
+      check(dev::launch_av_f32((const float*)d_a + r0, m, rows, (int)n, (const float*)d_w, (float*)d_u + r0, m,
+                               jws.status, st),
+            "av_f32");
+    launches += 1;
+    check(cudaEventRecord(uev[k], st), "event");
+    check(cudaStreamWaitEvent(cs, uev[k], 0), "wait");
+    check(cudaMemcpy2DAsync((char*)h_u + r0 * elt, pitch, (const char*)d_u + r0 * elt, pitch, rows * elt, n,
+                            cudaMemcpyDeviceToHost, cs),
+          "D2H U chunk");
+    r0 = r1;
+  }
+  record_event(ev[3], st);
+  events_recorded = true;
+  check(cudaMemcpyAsync(h_status, jws.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status D2H");
+  // join: wait() synchronises st, which now also covers the copy stream
+  check(cudaEventRecord(cdone, cs), "event");
+  check(cudaStreamWaitEvent(st, cdone, 0), "wait");
 }
 
 void Plan::reset_status(cudaStream_t st) {

@@ -31,6 +31,9 @@ class Plan {
   // Enqueue the whole pipeline on `st` (nullptr: the plan's stream).
   void execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                cudaStream_t st);
+  // host buffers (page-locked) in and out, copies overlapped with the kernels
+  void execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double* h_sigma, double* d_sigma, void* h_v,
+                    void* d_v, cudaStream_t st);
   // the kernel sequence of execute (captured into graph_exec)
   void enqueue(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                cudaStream_t st);
@@ -90,6 +93,8 @@ class Plan {
       return a == o.a && lda == o.lda && u == o.u && ldu == o.ldu && sigma == o.sigma && v == o.v;
     }
   };
+  cudaStream_t copy_stream = nullptr;  // execute_host's copy engine stream
+  cudaEvent_t cev[16] = {}, uev[16] = {}, cdone = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   GraphKey graph_key{};
   int graph_launches = 0;

@@ -60,7 +60,8 @@ cudaError_t launch_av_f32(const float* a, long long lda, long long m, int n, con
 bool av_tc_supported(const float* a, long long lda, long long m, int n, long long ldu);
 size_t av_tc_wplanes_bytes(int n);
 cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, const float* w, void* wplanes,
-                             float* u, long long ldu, const DevStatus* status, int sm_count, cudaStream_t st);
+                             float* u, long long ldu, const DevStatus* status, int sm_count, cudaStream_t st,
+                             bool prep = true);  // prep: split W into its bf16 pieces first
 // K7 fp64 on the DMMA pipe (compute_u.cu)
 cudaError_t launch_av_dmma_f64(const double* a, long long lda, long long m, int n, const double* w, double* u,
                                long long ldu, const DevStatus* status, cudaStream_t st);
