@@ -295,6 +295,11 @@ def run_ours(args, cfg):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
+    # timed region: barrier + synchronize on both sides, device events on the
+    # plan's stream, max over ranks below
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     phase = {"gram": [], "eigen": [], "compute_u": []}
@@ -303,6 +308,8 @@ def run_ours(args, cfg):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     total_ms = e0.elapsed_time(e1)
     # per-phase device times (CUDA events inside the library, same stream),
     # from separately synchronised steps so each phase is isolated
