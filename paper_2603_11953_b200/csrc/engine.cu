@@ -373,7 +373,9 @@ void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, voi
   ensure_log();
   static const bool no_graph = getenv("MPSVD_NO_GRAPH") != nullptr || getenv("MPSVD_JACOBI_TRACE") != nullptr ||
                                getenv("MPSVD_AV_DBG") != nullptr;
-  if (no_graph || graph_failed) {
+  // multi-GPU plans launch directly: a failed capture must never leave a
+  // half-recorded NCCL collective behind (and the graph saves only ~15 us)
+  if (no_graph || graph_failed || (comm && comm->nranks > 1)) {
     enqueue(d_a, lda, d_u, ldu, d_sigma, d_v, st);
     return;
   }
