@@ -409,6 +409,239 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols));
 }
 
+
+// ---------------------------------------------------------------------------
+// K7, TMEM variant: the bf16 pieces of A are written to tensor memory with
+// tcgen05.st (thread = row) and fed to the MMA as its A operand (K-major in
+// TMEM, two K-neighbours per 32-bit column, low half = even k; encoding
+// checked by tools/microbench/umma_tmem_a.cu). No shared-memory planes and
+// no generic->async proxy fence; the freed shared memory deepens the fp32
+// staging ring. Roles:
+//   warps 0-7   converters, two groups of four (one warp per TMEM lane
+//               quarter); group g converts chunks g, g + 2, ... into TMEM
+//               A slots {g, g + 2} (each slot has one owner group)
+//   warps 8-15  epilogue (as in av_tc_f32)
+//   warps 16-17 loaders: fp32 chunk [16 columns][128 rows] by cp.async
+//   warp 18     W pieces (bulk copy) + MMA issue
+namespace tm {
+constexpr int kASlots = 4;          // TMEM A slots (24 columns each: 3 pieces x 8)
+constexpr int kACols = 3 * 8;
+constexpr int kGroups = 2;
+}  // namespace tm
+
+__global__ void __launch_bounds__(tc::kThreads, 1)
+av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, int np,
+               const __nv_bfloat16* __restrict__ wplanes, float* __restrict__ u, long long ldu,
+               const DevStatus* __restrict__ status, int nstage, int acc_stride, int a_col0, int tcols) {
+  using namespace tc;
+  using namespace tm;
+  if (status && status->status != kOk) return;
+  extern __shared__ __align__(1024) unsigned char smem_tc[];
+  const int nkc = np / kKC;
+  const uint32_t wbytes = 3u * np * np * 2u;
+  unsigned char* wsm = smem_tc;
+  unsigned char* ssm = wsm + ((wbytes + 1023) & ~1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ssm + nstage * kStageBytes);
+  uint64_t* stage_full = bars;
+  uint64_t* stage_empty = stage_full + nstage;
+  uint64_t* a_full = stage_empty + nstage;
+  uint64_t* a_empty = a_full + kASlots;
+  uint64_t* acc_full = a_empty + kASlots;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* w_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long ntiles = (m + kBM - 1) / kBM;
+  const int my_tiles = (int)(ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  const int nchunks = my_tiles * nkc;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(&stage_full[i], kLoadWarps * 32);
+      mbar_init(&stage_empty[i], 4);  // the four warps of the converting group
+    }
+    for (int i = 0; i < kASlots; ++i) {
+      mbar_init(&a_full[i], 4);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kEpiWarps);
+    }
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= kWarpLoad0 && warp < kWarpLoad0 + kLoadWarps) {
+    // chunk = 16 columns x 128 rows fp32, column-major in the slot (512 B per
+    // column): loader thread lt fetches pieces q = lt + 64 i, each 16 bytes of
+    // one column, a warp a whole 512-byte column segment per instruction
+    const int lt = threadIdx.x - kWarpLoad0 * 32;
+    long long row0 = (long long)blockIdx.x * kBM;
+    const long long row_step = (long long)gridDim.x * kBM;
+    int kc = 0, slot = 0;
+    unsigned ph = 0;
+    for (int g = 0; g < nchunks; ++g) {
+      mbar_wait(&stage_empty[slot], ph ^ 1);
+      unsigned char* dst = ssm + slot * kStageBytes;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int q = lt + 64 * i, c = q >> 5, p = q & 31;
+        const int col = kc * kKC + c;
+        const long long row = row0 + p * 4;
+        const bool ok = col < n && row < m;  // m % 4 == 0: a 16-byte piece is all in or all out
+        cp_async16_zfill(dst + q * 16, ok ? a + (long long)col * lda + row : a, ok);
+      }
+      cp_async_mbar_arrive(&stage_full[slot]);
+      if (++kc == nkc) {
+        kc = 0;
+        row0 += row_step;
+      }
+      if (++slot == nstage) {
+        slot = 0;
+        ph ^= 1;
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp == kWarpMma) {
+    if (lane == 0) {
+      // D f32, A bf16 K-major (TMEM), B bf16 MN-major (smem), N = np, M = 128
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(np >> 3) << 17) |
+                             ((uint32_t)(kBM >> 4) << 24);
+      const uint32_t w_lbo = (uint32_t)(np / 8) * 128;
+      const uint32_t wbase = saddr(wsm);
+      const uint32_t wplane = (uint32_t)np * np * 2u;
+      const int pa[6] = {2, 1, 0, 1, 0, 0}, pw[6] = {0, 1, 2, 0, 1, 0};
+      mbar_expect_tx(w_full, wbytes);
+      bulk_g2s(wsm, wplanes, wbytes, w_full);
+      mbar_wait(w_full, 0);
+      int ab = 0;
+      unsigned aph = 0;
+      int g = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(&acc_empty[ab], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(ab * acc_stride);
+        for (int kc = 0; kc < nkc; ++kc, ++g) {
+          const int sl = g % kASlots;
+          mbar_wait(&a_full[sl], (unsigned)((g / kASlots) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t at = tmem + (uint32_t)(a_col0 + sl * kACols);
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            const uint64_t bd = umma_desc(wbase + (uint32_t)pw[q] * wplane + (uint32_t)kc * 2u * w_lbo, w_lbo, 128);
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                "r"(at + (uint32_t)(pa[q] * 8)), "l"(bd), "r"(idesc), "r"((kc > 0 || q > 0) ? 1u : 0u));
+          }
+          umma_commit(&a_empty[sl]);
+        }
+        umma_commit(&acc_full[ab]);
+        if (++ab == 2) {
+          ab = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // converter group grp = warp / 4; quarter q = warp % 4 owns TMEM lanes
+    // 32q .. 32q + 31 (rows of the tile)
+    const int grp = warp >> 2, q = warp & 3;
+    const int row = q * 32 + lane;
+    int slot = grp % nstage;
+    unsigned sph = (unsigned)((grp / nstage) & 1);
+    for (int g = grp; g < nchunks; g += kGroups) {
+      const int sl = g % kASlots;
+      mbar_wait(&stage_full[slot], sph);
+      const float* src = reinterpret_cast<const float*>(ssm + slot * kStageBytes);
+      float v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = src[c * kBM + row];  // consecutive lanes: consecutive rows
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&stage_empty[slot]);
+      slot += kGroups;
+      if (slot >= nstage) {
+        slot -= nstage;
+        sph ^= 1;
+      }
+      uint32_t hp[8], mp[8], lp[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) split3(v[2 * c], v[2 * c + 1], hp[c], mp[c], lp[c]);
+      mbar_wait(&a_empty[sl], (unsigned)(((g / kASlots) & 1) ^ 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_col0 + sl * kACols);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta), "r"(hp[0]),
+                   "r"(hp[1]), "r"(hp[2]), "r"(hp[3]), "r"(hp[4]), "r"(hp[5]), "r"(hp[6]), "r"(hp[7]));
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta + 8u),
+                   "r"(mp[0]), "r"(mp[1]), "r"(mp[2]), "r"(mp[3]), "r"(mp[4]), "r"(mp[5]), "r"(mp[6]), "r"(mp[7]));
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta + 16u),
+                   "r"(lp[0]), "r"(lp[1]), "r"(lp[2]), "r"(lp[3]), "r"(lp[4]), "r"(lp[5]), "r"(lp[6]), "r"(lp[7]));
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[sl]);
+    }
+  } else if (warp < kConvWarps + kEpiWarps) {
+    const int q = warp & 3, e = (warp - kConvWarps) >> 2;
+    int ab = 0;
+    unsigned aph = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&acc_full[ab], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const long long row = tile * kBM + q * 32 + lane;
+      const bool row_ok = row < m;
+      float* base = u + row;
+      for (int c0 = 16 * e; c0 < np; c0 += 32) {
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * acc_stride + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+            "[%16];\n"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (row_ok) {
+          float* p = base + (long long)c0 * ldu;
+          if (c0 + 16 <= n) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              *p = __uint_as_float(r[j]);
+              p += ldu;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < n) p[(long long)j * ldu] = __uint_as_float(r[j]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      if (++ab == 2) {
+        ab = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == kWarpMma)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols));
+}
+
 // ---------------------------------------------------------------------------
 bool av_tc_supported(const float* a, long long lda, long long m, int n, long long ldu) {
   (void)ldu;
@@ -449,6 +682,25 @@ cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, 
     av_tc_prep_w<<<(np * np + prep_threads - 1) / prep_threads, prep_threads, 0, st>>>(
         w, ldw, n, np, reinterpret_cast<__nv_bfloat16*>(wplanes), status);
   const size_t wbytes = ((size_t)3 * np * np * 2 + 1023) & ~(size_t)1023;
+  static const bool planes = getenv("MPSVD_AV_PLANES") != nullptr;  // the shared-memory-plane variant
+  if (!planes && !(g_av_dbg & 7)) {
+    // TMEM variant: accumulators [0, 2 acc_stride), A slots after them
+    const int acc_stride = np <= 32 ? 32 : np <= 64 ? 64 : 128;
+    const int a_col0 = 2 * acc_stride;
+    const int need = a_col0 + tm::kASlots * tm::kACols;
+    const int tcols = need <= 128 ? 128 : need <= 256 ? 256 : 512;
+    int nstage = (int)((kSmemLimit - wbytes - 1024) / kStageBytes);
+    if (nstage > 16) nstage = 16;
+    if (nstage < tm::kGroups) return cudaErrorInvalidConfiguration;
+    const size_t smem = wbytes + (size_t)nstage * kStageBytes + 1024;
+    cudaError_t e = cudaFuncSetAttribute(av_tc_tmem_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long ntiles = (m + kBM - 1) / kBM;
+    const int grid = (int)(ntiles < sm_count ? ntiles : sm_count);
+    av_tc_tmem_f32<<<grid, kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const __nv_bfloat16*>(wplanes),
+                                                 u, ldu, status, nstage, acc_stride, a_col0, tcols);
+    return cudaGetLastError();
+  }
   // one staging slot + one plane slot per active converter warp
   int depth = kConvWarps;
   auto smem_for = [&](int d) { return wbytes + (size_t)d * (3 * kPlaneBytes + kStageBytes) + 512; };
