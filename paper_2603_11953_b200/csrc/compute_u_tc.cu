@@ -39,6 +39,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef TM_LOAD_WARPS
+#define TM_LOAD_WARPS 2  // loader warps of the TMEM variant (4 measured 5% slower)
+#endif
+
 namespace mpsvd {
 namespace dev {
 namespace tc {
@@ -424,12 +428,15 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
 //   warps 16-17 loaders: fp32 chunk [16 columns][128 rows] by cp.async
 //   warp 18     W pieces (bulk copy) + MMA issue
 namespace tm {
-constexpr int kASlots = 4;          // TMEM A slots (24 columns each: 3 pieces x 8)
+constexpr int kASlots = 4;          // TMEM A slots (24 columns each: 3 pieces x 8); 8 measured the same
 constexpr int kACols = 3 * 8;
 constexpr int kGroups = 2;
+constexpr int kLoad0 = 16, kLoadWarps = TM_LOAD_WARPS, kMma = kLoad0 + kLoadWarps;
+constexpr int kThreads = 32 * (kMma + 1);
+constexpr int kPieces = 512 / (32 * kLoadWarps);  // 16-byte pieces per loader thread per chunk
 }  // namespace tm
 
-__global__ void __launch_bounds__(tc::kThreads, 1)
+__global__ void __launch_bounds__(tm::kThreads, 1)
 av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, int np,
                const __nv_bfloat16* __restrict__ wplanes, float* __restrict__ u, long long ldu,
                const DevStatus* __restrict__ status, int nstage, int acc_stride, int a_col0, int tcols) {
@@ -457,7 +464,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nstage; ++i) {
-      mbar_init(&stage_full[i], kLoadWarps * 32);
+      mbar_init(&stage_full[i], tm::kLoadWarps * 32);
       mbar_init(&stage_empty[i], 4);  // the four warps of the converting group
     }
     for (int i = 0; i < kASlots; ++i) {
@@ -471,7 +478,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == kWarpMma) {
+  if (warp == tm::kMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
                  "r"(tcols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -481,11 +488,11 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= kWarpLoad0 && warp < kWarpLoad0 + kLoadWarps) {
+  if (warp >= tm::kLoad0 && warp < tm::kLoad0 + tm::kLoadWarps) {
     // chunk = 16 columns x 128 rows fp32, column-major in the slot (512 B per
     // column): loader thread lt fetches pieces q = lt + 64 i, each 16 bytes of
     // one column, a warp a whole 512-byte column segment per instruction
-    const int lt = threadIdx.x - kWarpLoad0 * 32;
+    const int lt = threadIdx.x - tm::kLoad0 * 32;
     long long row0 = (long long)blockIdx.x * kBM;
     const long long row_step = (long long)gridDim.x * kBM;
     int kc = 0, slot = 0;
@@ -494,8 +501,8 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
       mbar_wait(&stage_empty[slot], ph ^ 1);
       unsigned char* dst = ssm + slot * kStageBytes;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int q = lt + 64 * i, c = q >> 5, p = q & 31;
+      for (int i = 0; i < tm::kPieces; ++i) {
+        const int q = lt + 32 * tm::kLoadWarps * i, c = q >> 5, p = q & 31;
         const int col = kc * kKC + c;
         const long long row = row0 + p * 4;
         const bool ok = col < n && row < m;  // m % 4 == 0: a 16-byte piece is all in or all out
@@ -512,7 +519,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
       }
     }
     cp_async_wait<0>();
-  } else if (warp == kWarpMma) {
+  } else if (warp == tm::kMma) {
     if (lane == 0) {
       // D f32, A bf16 K-major (TMEM), B bf16 MN-major (smem), N = np, M = 128
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(np >> 3) << 17) |
@@ -638,7 +645,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == kWarpMma)
+  if (warp == tm::kMma)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols));
 }
 
@@ -656,7 +663,8 @@ size_t av_tc_wplanes_bytes(int n) {
   return 3ull * np * np * 2ull;
 }
 
-// experiment switches (MPSVD_AV_DBG): bit 0 skips the U stores, bit 1 the
+// experiment switches of the shared-memory-plane variant (MPSVD_AV_PLANES=1,
+// or any MPSVD_AV_DBG bit selects it) — MPSVD_AV_DBG: bit 0 skips the U stores, bit 1 the
 // MMAs, bit 2 prints per-role cycle counts of CTA 0 (tools/av_probe.sh).
 // Findings (C2, n = 64): loads + conversion alone take 0.089 ms of the
 // 0.128 ms, and with loads, conversion, MMAs and stores all skipped the
@@ -697,7 +705,7 @@ cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, 
     if (e != cudaSuccess) return e;
     const long long ntiles = (m + kBM - 1) / kBM;
     const int grid = (int)(ntiles < sm_count ? ntiles : sm_count);
-    av_tc_tmem_f32<<<grid, kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const __nv_bfloat16*>(wplanes),
+    av_tc_tmem_f32<<<grid, tm::kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const __nv_bfloat16*>(wplanes),
                                                  u, ldu, status, nstage, acc_stride, a_col0, tcols);
     return cudaGetLastError();
   }
