@@ -329,6 +329,18 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
+    # full-size validation of the factorisation just timed, on the device
+    # (SURVEY.md §8(f)-2): max row-wise backward error, max over ranks
+    bw = M.backward_error_device(a_t.T, u_t.T, sig_t, v_t.T, stream)
+    validation = {"rowwise_backward_error": bw.max_rel, "skipped_rows": bw.skipped_rows,
+                  "unit_roundoff": 2.0 ** -24 if cfg.working == "f32" else 2.0 ** -53,
+                  "definition": "max_i ||(U diag(s) V^T - A)(i,:)|| / ||A(i,:)||, binary64 (metrics.cpp:40-70)"}
+    if world > 1:
+        t = torch.tensor([bw.max_rel, float(bw.skipped_rows)], dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        validation["rowwise_backward_error"], validation["skipped_rows"] = float(t[0]), int(t[1])
+
     fg, fa = flops(m_global, n)
     value = (fg + fa) / (ms * 1e-3) / 1e12
     med = {k: statistics.median(v) for k, v in phase.items()}
@@ -428,6 +440,7 @@ def run_ours(args, cfg):
         "clocks": clk,
         "e2e": e2e,
         "sweeps": info.sweeps,
+        "validation": validation,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)

@@ -67,6 +67,22 @@ int mpsvd_matrix_bitwise_equal(const mpsvd_matrix* a, const mpsvd_matrix* b); /*
 void* mpsvd_matrix_data(mpsvd_matrix* a);
 /* ||A^T A - I||_F in binary64 (mpsvd.h:85), A^T A formed on the GPU. */
 mpsvd_status mpsvd_orth_error(const mpsvd_matrix* a, double* out);
+/* max_i |computed_i - reference_i| / reference_i (mpsvd.h:147-148,
+ * metrics.cpp:26-38); MPSVD_ERR_INVALID_ARGUMENT on a non-positive reference. */
+mpsvd_status mpsvd_max_rel_sv_error(const double* computed, const double* reference, int64_t count,
+                                    double* out);
+/* max_i ||(U diag(sigma) V^T - A)(i,:)|| / ||A(i,:)|| in binary64, zero rows
+ * skipped and counted (mpsvd.h:150-153, metrics.cpp:40-70); on the GPU. */
+mpsvd_status mpsvd_rowwise_backward_error(const mpsvd_matrix* a, const mpsvd_matrix* u,
+                                          const double* sigma, int64_t count, const mpsvd_matrix* v,
+                                          double* max_rel, int64_t* skipped_rows);
+/* ADDITIVE: the same on device-resident factors (column-major, leading
+ * dimensions lda/ldu >= m, ldv >= n; prec selects float/double storage of
+ * A, U, V; d_sigma: n doubles). Synchronous on `stream` (NULL: legacy). */
+mpsvd_status mpsvd_backward_error_device(mpsvd_precision prec, const void* d_a, int64_t lda, const void* d_u,
+                                         int64_t ldu, const double* d_sigma, const void* d_v, int64_t ldv,
+                                         int64_t m, int64_t n, void* stream, double* max_rel,
+                                         int64_t* skipped_rows);
 
 /* ---- thin SVD -------------------------------------------------------------- */
 /* proj/include/mpsvd.h:116-117: f32 A (m >= n >= 1), Gram + Jacobi in fp64,

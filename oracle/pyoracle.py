@@ -164,6 +164,31 @@ class Ref:
             self._check(self.lib.refx_orth_error_f64(_d(q), _i64(m), _i64(n), C.byref(out)))
         return out.value
 
+    def rowwise_backward_error(self, a, u, sigma, v):
+        """(max_rel, skipped_rows) of proj/src/metrics.cpp:40-70; f32 or f64 factors."""
+        a = np.asfortranarray(a)
+        m, n = a.shape
+        mr = C.c_double(0)
+        sk = _i64(0)
+        s = np.ascontiguousarray(sigma, dtype=np.float64)
+        if a.dtype == np.float32:
+            st = self.lib.refx_rowwise_backward_error_f32(_f(a), _f(_fcol(u, np.float32)), _d(s),
+                                                          _f(_fcol(v, np.float32)), _i64(m), _i64(n),
+                                                          C.byref(mr), C.byref(sk))
+        else:
+            st = self.lib.refx_rowwise_backward_error_f64(_d(_fcol(a, np.float64)), _d(_fcol(u, np.float64)), _d(s),
+                                                          _d(_fcol(v, np.float64)), _i64(m), _i64(n),
+                                                          C.byref(mr), C.byref(sk))
+        self._check(st)
+        return mr.value, sk.value
+
+    def max_rel_sv_error(self, computed, reference):
+        c = np.ascontiguousarray(computed, dtype=np.float64)
+        r = np.ascontiguousarray(reference, dtype=np.float64)
+        out = C.c_double(0)
+        self._check(self.lib.refx_max_rel_sv_error(_d(c), _d(r), _i64(r.size), C.byref(out)))
+        return out.value
+
     def build_problem(self, m, n, kappa_d, kappa_b, matrix_id, seed):
         a = np.zeros((m, n), np.float32, order="F")
         s = np.zeros(n)

@@ -195,6 +195,35 @@ int refx_orth_error_f64(const double* q, int64_t m, int64_t n, double* out) {
   return run([&] { *out = orth_error(from_f64(q, m, n)); });
 }
 
+// rowwise_backward_error / max_rel_sv_error (proj/src/metrics.cpp:26-70):
+// A, U, V in Working (f32) storage, the thin-SVD factors' layout.
+int refx_rowwise_backward_error_f32(const float* a, const float* u, const double* sigma, const float* v,
+                                    int64_t m, int64_t n, double* max_rel, int64_t* skipped) {
+  return run([&] {
+    const auto rep = rowwise_backward_error(from_f32(a, m, n), from_f32(u, m, n),
+                                            std::vector<double>(sigma, sigma + n), from_f32(v, n, n));
+    *max_rel = rep.max_rel;
+    *skipped = rep.skipped_rows;
+  });
+}
+
+int refx_rowwise_backward_error_f64(const double* a, const double* u, const double* sigma, const double* v,
+                                    int64_t m, int64_t n, double* max_rel, int64_t* skipped) {
+  return run([&] {
+    const auto rep = rowwise_backward_error(from_f64(a, m, n), from_f64(u, m, n),
+                                            std::vector<double>(sigma, sigma + n), from_f64(v, n, n));
+    *max_rel = rep.max_rel;
+    *skipped = rep.skipped_rows;
+  });
+}
+
+int refx_max_rel_sv_error(const double* computed, const double* reference, int64_t count, double* out) {
+  return run([&] {
+    *out = max_rel_sv_error(std::vector<double>(computed, computed + count),
+                            std::vector<double>(reference, reference + count));
+  });
+}
+
 // build_problem (proj/src/matgen.cpp:266-289): the acceptance-grid generator.
 int refx_build_problem(int64_t m, int64_t n, double kappa_d, double kappa_b,
                        int matrix_id, uint64_t seed, float* a, double* sigma_ref,

@@ -5,6 +5,7 @@ C-ABI library ``libmpsvd_b200.so`` (include/mpsvd.h) runs the Gram (DMMA /
 double-double SYRK), the two-sided Jacobi, and U = A V Sigma^-1 on the GPU.
 """
 from .api import (  # noqa: F401
+    BackwardErrorReport,
     CastOverflowError,
     Comm,
     EigensolverChoice,
@@ -21,12 +22,15 @@ from .api import (  # noqa: F401
     TinySingularValueError,
     ZeroColumnError,
     ZeroDivisorError,
+    backward_error_device,
     device_available,
     fp64_peak_tflops,
     gram,
+    max_rel_sv_error,
     mp_thin_svd,
     mp_thin_svd_f64,
     orth_error,
+    rowwise_backward_error,
     twosided_jacobi_eig,
 )
 from ._lib import LIB_PATH  # noqa: F401

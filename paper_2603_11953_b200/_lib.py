@@ -45,6 +45,10 @@ SIGNATURES = [
     ("mpsvd_matrix_bitwise_equal", C.c_int, [vp, vp]),
     ("mpsvd_matrix_data", vp, [vp]),
     ("mpsvd_orth_error", C.c_int, [vp, dp]),
+    ("mpsvd_max_rel_sv_error", C.c_int, [dp, dp, i64, dp]),
+    ("mpsvd_rowwise_backward_error", C.c_int, [vp, vp, dp, i64, vp, dp, C.POINTER(i64)]),
+    ("mpsvd_backward_error_device", C.c_int, [C.c_int, vp, i64, vp, i64, vp, vp, i64, i64, i64, vp, dp,
+                                              C.POINTER(i64)]),
     ("mpsvd_thin_svd", C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
     ("mpsvd_thin_svd_f64", C.c_int, [vp, C.c_int, C.POINTER(vp)]),
     ("mpsvd_svd_destroy", None, [vp]),

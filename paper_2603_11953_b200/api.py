@@ -270,6 +270,64 @@ def orth_error(q) -> float:
     return out.value
 
 
+@dataclass
+class BackwardErrorReport:
+    """proj/include/mpsvd/metrics.hpp:44-47"""
+    max_rel: float = 0.0
+    skipped_rows: int = 0
+
+
+def _dptr(x: np.ndarray):
+    return x.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def max_rel_sv_error(computed, reference) -> float:
+    """max_i |computed_i - reference_i| / reference_i (proj/src/metrics.cpp:26-38);
+    InvalidArgument on a length mismatch or a non-positive reference entry."""
+    c = np.ascontiguousarray(computed, dtype=np.float64)
+    r = np.ascontiguousarray(reference, dtype=np.float64)
+    if c.size != r.size:
+        raise InvalidArgument("singular value arrays differ in length")
+    out = C.c_double()
+    _check(lib.mpsvd_max_rel_sv_error(_dptr(c), _dptr(r), int(r.size), C.byref(out)))
+    return out.value
+
+
+def rowwise_backward_error(a, u, sigma, v) -> BackwardErrorReport:
+    """max_i ||(U diag(sigma) V^T - A)(i,:)|| / ||A(i,:)|| in binary64 on the GPU,
+    zero rows of A skipped and counted (proj/src/metrics.cpp:40-70)."""
+    mats = [x if isinstance(x, Matrix) else Matrix.from_numpy(np.asarray(x)) for x in (a, u, v)]
+    s = np.ascontiguousarray(sigma, dtype=np.float64)
+    out, skipped = C.c_double(), C.c_int64()
+    _check(lib.mpsvd_rowwise_backward_error(mats[0].handle, mats[1].handle, _dptr(s), int(s.size), mats[2].handle,
+                                            C.byref(out), C.byref(skipped)))
+    return BackwardErrorReport(out.value, skipped.value)
+
+
+def backward_error_device(a, u, sigma, v, stream=None) -> BackwardErrorReport:
+    """The same on device-resident column-major torch tensors (a, u: m x n,
+    v: n x n, all float32 or all float64; sigma: n float64). Row-sharded
+    factors give per-rank maxima; the caller takes the max over ranks."""
+    import torch
+
+    f64 = a.dtype == torch.float64
+    for t in (a, u, v):
+        if t.dtype != a.dtype or not t.is_cuda:
+            raise InvalidArgument("backward_error_device: a, u, v must be CUDA tensors of one dtype")
+        if t.stride(0) != 1:
+            raise InvalidArgument("backward_error_device: tensors must be column-major")
+    if sigma.dtype != torch.float64 or not sigma.is_cuda:
+        raise InvalidArgument("backward_error_device: sigma must be a float64 CUDA tensor")
+    m, n = a.shape
+    ld = lambda t: max(int(t.stride(1)), int(t.shape[0]), 1)
+    st = stream if stream is not None else torch.cuda.current_stream(a.device)
+    out, skipped = C.c_double(), C.c_int64()
+    _check(lib.mpsvd_backward_error_device(int(Precision.HIGHER if f64 else Precision.WORKING), a.data_ptr(), ld(a),
+                                           u.data_ptr(), ld(u), sigma.data_ptr(), v.data_ptr(), ld(v), m, n,
+                                           st.cuda_stream, C.byref(out), C.byref(skipped)))
+    return BackwardErrorReport(out.value, skipped.value)
+
+
 # ---------------------------------------------------------------------------
 # stage entry points (parity tests)
 

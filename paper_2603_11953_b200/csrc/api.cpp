@@ -22,6 +22,7 @@
 
 #include "engine.h"
 #include "mpsvd.h"
+#include "mpsvd/metrics.hpp"
 #include "mpsvd/thinsvd.hpp"
 #include "mpsvd/types.hpp"
 
@@ -433,6 +434,97 @@ double orth_error(const DenseMatrix& q) {
   return std::sqrt(sum);
 }
 
+double max_rel_sv_error(const std::vector<double>& computed, const std::vector<double>& reference) {
+  if (computed.size() != reference.size()) throw InvalidArgument("singular value arrays differ in length");
+  double worst = 0.0;
+  for (std::size_t i = 0; i < reference.size(); ++i) {
+    if (!(reference[i] > 0.0))
+      throw InvalidArgument("reference singular value " + std::to_string(i + 1) + " is not positive");
+    worst = std::max(worst, std::abs(computed[i] - reference[i]) / reference[i]);
+  }
+  return worst;
+}
+
+// device-resident backward error (bench validation, the host entry below)
+BackwardErrorReport backward_error_device(bool f64, const void* d_a, long long lda, const void* d_u, long long ldu,
+                                          const double* d_sigma, const void* d_v, long long ldv, long long m,
+                                          long long n, cudaStream_t st) {
+  BackwardErrorReport rep;
+  if (m == 0 || n == 0) return rep;
+  double* partial = nullptr;
+  unsigned long long* out = nullptr;
+  engine::check(cudaMalloc((void**)&partial, dev::backward_partial_elems(m, (int)n) * sizeof(double)),
+                "cudaMalloc backward partials");
+  engine::check(cudaMalloc((void**)&out, 2 * sizeof(unsigned long long)), "cudaMalloc backward out");
+  unsigned long long h[2] = {0, 0};
+  cudaError_t e = dev::launch_backward_error(f64, d_a, lda, d_u, ldu, d_sigma, d_v, ldv, m, (int)n, partial, out, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(partial);
+  cudaFree(out);
+  engine::check(e, "backward error");
+  double worst;
+  std::memcpy(&worst, &h[0], sizeof(worst));
+  rep.max_rel = worst;
+  rep.skipped_rows = (index_t)h[1];
+  return rep;
+}
+
+BackwardErrorReport rowwise_backward_error(const DenseMatrix& a, const DenseMatrix& u,
+                                           const std::vector<double>& sigma, const DenseMatrix& v) {
+  const index_t m = a.rows(), n = a.cols();
+  if (u.rows() != m || u.cols() != n || (index_t)sigma.size() != n || v.rows() != n || v.cols() != n)
+    throw InvalidArgument("factor shapes do not match A");
+  if (m == 0 || n == 0) return {};
+  require_device();
+  // one storage type for the kernel: all Working -> float; otherwise every
+  // Working operand is widened (exactly) to binary64 first
+  const bool f64 = a.precision() == Precision::Higher || u.precision() == Precision::Higher ||
+                   v.precision() == Precision::Higher;
+  std::vector<double> wide[3];
+  auto host_ptr = [&](const DenseMatrix& x, int slot) -> const void* {
+    if (!f64 || x.precision() == Precision::Higher) return x.raw();
+    const float* f = x.fptr();
+    wide[slot].resize((std::size_t)x.size());
+    for (std::size_t k = 0; k < wide[slot].size(); ++k) wide[slot][k] = f[k];
+    return wide[slot].data();
+  };
+  const void* ha = host_ptr(a, 0);
+  const void* hu = host_ptr(u, 1);
+  const void* hv = host_ptr(v, 2);
+  const std::size_t elt = f64 ? 8 : 4;
+  cudaStream_t st = nullptr;
+  engine::check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  void *da = nullptr, *du = nullptr, *dv = nullptr;
+  double* ds = nullptr;
+  cudaError_t e = cudaMalloc(&da, (std::size_t)m * n * elt);
+  if (e == cudaSuccess) e = cudaMalloc(&du, (std::size_t)m * n * elt);
+  if (e == cudaSuccess) e = cudaMalloc(&dv, (std::size_t)n * n * elt);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&ds, (std::size_t)n * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(da, ha, (std::size_t)m * n * elt, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(du, hu, (std::size_t)m * n * elt, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dv, hv, (std::size_t)n * n * elt, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ds, sigma.data(), (std::size_t)n * 8, cudaMemcpyHostToDevice, st);
+  BackwardErrorReport rep;
+  std::string err;
+  if (e != cudaSuccess) {
+    err = cudaGetErrorString(e);
+  } else {
+    try {
+      rep = backward_error_device(f64, da, m, du, m, ds, dv, n, m, n, st);
+    } catch (const std::exception& ex) {
+      err = ex.what();
+    }
+  }
+  cudaFree(da);
+  cudaFree(du);
+  cudaFree(dv);
+  cudaFree(ds);
+  cudaStreamDestroy(st);
+  if (!err.empty()) throw std::runtime_error("rowwise_backward_error: " + err);
+  return rep;
+}
+
 // entry points for the C ABI below
 void raise_device_status_public(const mpsvd_exec_info& info, int max_sweeps) {
   raise_device_status(info, max_sweeps);
@@ -593,6 +685,42 @@ mpsvd_status mpsvd_orth_error(const mpsvd_matrix* a, double* out) {
   return guarded([&] {
     require(a != nullptr && out != nullptr, "null argument");
     *out = mpsvd::orth_error(a->m);
+  });
+}
+
+mpsvd_status mpsvd_max_rel_sv_error(const double* computed, const double* reference, int64_t count, double* out) {
+  return guarded([&] {
+    require(computed != nullptr && reference != nullptr && out != nullptr, "null argument");
+    require(count >= 0, "negative count");
+    *out = mpsvd::max_rel_sv_error(std::vector<double>(computed, computed + count),
+                                   std::vector<double>(reference, reference + count));
+  });
+}
+
+mpsvd_status mpsvd_rowwise_backward_error(const mpsvd_matrix* a, const mpsvd_matrix* u, const double* sigma,
+                                          int64_t count, const mpsvd_matrix* v, double* max_rel,
+                                          int64_t* skipped_rows) {
+  return guarded([&] {
+    require(a != nullptr && u != nullptr && v != nullptr && max_rel != nullptr, "null argument");
+    require(count >= 0 && (sigma != nullptr || count == 0), "bad sigma");
+    const auto rep = mpsvd::rowwise_backward_error(a->m, u->m, std::vector<double>(sigma, sigma + count), v->m);
+    *max_rel = rep.max_rel;
+    if (skipped_rows) *skipped_rows = rep.skipped_rows;
+  });
+}
+
+mpsvd_status mpsvd_backward_error_device(mpsvd_precision prec, const void* d_a, int64_t lda, const void* d_u,
+                                         int64_t ldu, const double* d_sigma, const void* d_v, int64_t ldv,
+                                         int64_t m, int64_t n, void* stream, double* max_rel, int64_t* skipped_rows) {
+  return guarded([&] {
+    require(max_rel != nullptr, "null argument");
+    require(m >= 0 && n >= 0 && lda >= m && ldu >= m && ldv >= n, "bad shape / leading dimension");
+    require(m == 0 || n == 0 || (d_a && d_u && d_sigma && d_v), "null device pointer");
+    mpsvd::require_device();
+    const auto rep = mpsvd::backward_error_device(prec == MPSVD_PRECISION_HIGHER, d_a, lda, d_u, ldu, d_sigma, d_v,
+                                                  ldv, m, n, (cudaStream_t)stream);
+    *max_rel = rep.max_rel;
+    if (skipped_rows) *skipped_rows = rep.skipped_rows;
   });
 }
 

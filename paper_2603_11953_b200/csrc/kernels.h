@@ -68,6 +68,16 @@ cudaError_t launch_av_dmma_f64(const double* a, long long lda, long long m, int 
 cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w,
                           double* u, long long ldu, const DevStatus* status, cudaStream_t st);
 
+// metrics.cu ------------------------------------------------------------------
+// Row-wise backward error max_i ||(U diag(sigma) V^T - A)(i,:)|| / ||A(i,:)||
+// (proj/src/metrics.cpp:40-70) in binary64; f64 selects double storage of
+// A, U, V (else float). `partial` holds backward_partial_elems(m, n) doubles;
+// out[0] = bit pattern of the maximum, out[1] = zero rows skipped.
+size_t backward_partial_elems(long long m, int n);
+cudaError_t launch_backward_error(bool f64, const void* a, long long lda, const void* u, long long ldu,
+                                  const double* sigma, const void* v, long long ldv, long long m, int n,
+                                  double* partial, unsigned long long* out, cudaStream_t st);
+
 // microbench.cu ---------------------------------------------------------------
 double measure_fp64_peak_tflops(int device);
 
