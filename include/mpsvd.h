@@ -37,7 +37,7 @@ typedef enum mpsvd_status {
 /* proj/include/mpsvd.h:39-42 */
 typedef enum mpsvd_precision { MPSVD_PRECISION_WORKING = 0, MPSVD_PRECISION_HIGHER = 1 } mpsvd_precision;
 
-/* proj/include/mpsvd.h:44-48 (only TWOSIDED_JACOBI runs on the GPU path) */
+/* proj/include/mpsvd.h:44-48 (every branch runs on the GPU path) */
 typedef enum mpsvd_eigensolver {
   MPSVD_EIG_TWOSIDED_JACOBI = 0,
   MPSVD_EIG_GRAM_CHOL_SVD = 1,
@@ -134,6 +134,9 @@ mpsvd_status mpsvd_plan_create(int64_t m_local, int64_t n, mpsvd_precision worki
  * Asynchronous; completes on `stream`. */
 mpsvd_status mpsvd_plan_execute(mpsvd_plan* p, const void* d_a, int64_t lda, void* d_u, int64_t ldu,
                                 void* d_sigma, void* d_v, void* stream);
+/* Spectral branch of later executes (default MPSVD_EIG_TWOSIDED_JACOBI; the
+ * one-sided branches need a MPSVD_PRECISION_WORKING plan). */
+mpsvd_status mpsvd_plan_set_eigensolver(mpsvd_plan* p, mpsvd_eigensolver eig);
 /* Blocks until the last execute finished; reports the device status. */
 mpsvd_status mpsvd_plan_wait(mpsvd_plan* p, mpsvd_exec_info* info);
 /* Timed region helpers for the dominant kernels (CUDA events, ms). */
@@ -149,6 +152,13 @@ mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, in
 mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, int64_t n, double tol,
                                 int max_sweeps, double* lam_hi, double* lam_lo, double* v_hi,
                                 double* v_lo, int* sweeps, int64_t* rotations);
+
+/* Spectral phase of MPSVD_EIG_GRAM_CHOL_SVD / MPSVD_EIG_ONESIDED_JACOBI_GRAM on
+ * a binary64 Gram m_hi (n x n): Cholesky + binary32 one-sided Jacobi of R, or
+ * binary64 one-sided Jacobi of M (thinsvd.cpp:37-47,90-104); outputs the
+ * sorted working-precision sigma and sign-fixed binary32 V. */
+mpsvd_status mpsvd_stage_onesided(mpsvd_eigensolver eig, const double* m_hi, int64_t n, double tol,
+                                  int max_sweeps, double* sigma, float* v, int* sweeps, int64_t* rotations);
 
 /* ---- ADDITIVE: measured device peaks (roofline denominators) --------------- */
 double mpsvd_fp64_peak_tflops(int device);

@@ -9,8 +9,9 @@
 //   mp_thin_svd_f64   ADDITIVE: fp64 A; Gram + Jacobi in double-double; U fp64.
 //   twosided_jacobi_eig  drop-in for jacobi.hpp:45-46 (fp64 M), on the GPU.
 //
-// Only EigensolverChoice::TwoSidedJacobi runs on the GPU path; the other
-// choices throw InvalidArgument (no CPU fallback is shipped).
+// Every EigensolverChoice runs on the GPU: TwoSidedJacobi (K4/K5), and the
+// GramCholSvd / OneSidedJacobiOnGram branches of thinsvd.cpp:37-47,90-104
+// (Cholesky K8 + one-sided Jacobi K9, csrc/onesided.cu), binary32 A only.
 #pragma once
 
 #include <vector>

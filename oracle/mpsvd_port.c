@@ -21,7 +21,9 @@ enum {
   ST_INVALID = 1,
   ST_NPD = 2,
   ST_NOCONV = 3,
+  ST_ZERO_COLUMN = 4,
   ST_ZERO_DIVISOR = 5,
+  ST_CAST_OVERFLOW = 6,
   ST_TINY_SV = 7,
   ST_INTERNAL = 10
 };
@@ -442,6 +444,313 @@ int port_twosided_jacobi_f64(const double* mtx, int64_t n, double tol, int max_s
 }
 
 /* ======================================================================== */
+/* One-sided branches of mp_thin_svd (proj/src/thinsvd.cpp:37-47,90-104)     */
+/* ======================================================================== */
+
+/* cholesky_impl (proj/src/dense.cpp:39-58), upper factor, strict lower part
+ * zero. The device's right-looking K8 applies the same operations to every
+ * entry in the same order, so one restatement serves both semantics. */
+int port_cholesky_f64(const double* m, int64_t n, double* r, port_error* err) {
+  set_err(err, ST_OK, 0, 0.0);
+  memset(r, 0, sizeof(double) * (size_t)(n * n));
+  for (int64_t k = 0; k < n; ++k) {
+    double d = m[k * n + k];
+    for (int64_t i = 0; i < k; ++i) {
+      const double rik = r[k * n + i];
+      d -= rik * rik;
+    }
+    if (!(d > 0.0)) return set_err(err, ST_NPD, k + 1, d);
+    const double rkk = sqrt(d);
+    r[k * n + k] = rkk;
+    for (int64_t j = k + 1; j < n; ++j) {
+      double s = m[j * n + k];
+      for (int64_t i = 0; i < k; ++i) s -= r[k * n + i] * r[j * n + i];
+      r[j * n + k] = s / rkk;
+    }
+  }
+  return ST_OK;
+}
+
+/* One-sided Jacobi cores, generated for float and double.
+ *   reference: onesided_impl (proj/src/jacobi.cpp:49-118), cyclic by rows,
+ *              make_rotation with hypot (:34-40), scaled_norm_t (:12-28);
+ *   device:    K9 (csrc/onesided.cu): round-robin pairs, per-lane fma
+ *              partials + xor butterfly, the closed-form rotation, fma
+ *              column updates, two-pass max-scaled norms.
+ * x: m x n (rotated in place), v: n x n (set to I), sig: n column norms.
+ * Returns the status; *worst = the last sweep's worst ratio. */
+#define DEFINE_ONESIDED(T, SUF, SQRT, FABS, HYPOT, FMA, FMAX, FREXP, LDEXP, BIG, SMALL)                      \
+  static T scaled_norm_ref_##SUF(const T* x, int64_t len) {                                                   \
+    T scale = (T)0, ssq = (T)1;                                                                              \
+    for (int64_t k = 0; k < len; ++k) {                                                                       \
+      if (x[k] != (T)0) {                                                                                    \
+        const T ax = FABS(x[k]);                                                                              \
+        if (scale < ax) {                                                                                     \
+          const T r = scale / ax;                                                                             \
+          ssq = (T)1 + ssq * r * r;                                                                           \
+          scale = ax;                                                                                         \
+        } else {                                                                                              \
+          const T r = ax / scale;                                                                             \
+          ssq += r * r;                                                                                       \
+        }                                                                                                     \
+      }                                                                                                       \
+    }                                                                                                         \
+    return scale * SQRT(ssq);                                                                                 \
+  }                                                                                                           \
+  static T butterfly_sum_##SUF(T* l) {                                                                        \
+    for (int o = 16; o > 0; o >>= 1) {                                                                        \
+      T t[32];                                                                                                \
+      for (int i = 0; i < 32; ++i) t[i] = l[i] + l[i ^ o];                                                    \
+      memcpy(l, t, sizeof(t));                                                                                \
+    }                                                                                                         \
+    return l[0];                                                                                              \
+  }                                                                                                           \
+  static void rotate_cols_##SUF(T* xi, T* xj, int64_t len, T cs, T sn, int dev) {                             \
+    for (int64_t k = 0; k < len; ++k) {                                                                       \
+      const T t1 = xi[k], t2 = xj[k];                                                                         \
+      if (dev) {                                                                                              \
+        xi[k] = FMA(cs, t1, -(sn * t2));                                                                      \
+        xj[k] = FMA(sn, t1, cs * t2);                                                                         \
+      } else {                                                                                                \
+        xi[k] = cs * t1 - sn * t2;                                                                            \
+        xj[k] = sn * t1 + cs * t2;                                                                            \
+      }                                                                                                       \
+    }                                                                                                         \
+  }                                                                                                           \
+  /* one pair; returns 1 if rotated, -1/-2 for a zero column i/j */                                           \
+  static int pair_##SUF(T* x, T* v, int64_t m, int64_t n, int64_t i, int64_t j, T reltol, int dev,            \
+                        double* worst) {                                                                      \
+    T* xi = x + i * m;                                                                                        \
+    T* xj = x + j * m;                                                                                        \
+    T a = (T)0, b = (T)0, c = (T)0;                                                                           \
+    if (dev) {                                                                                                \
+      T la[32], lb[32], lc[32];                                                                               \
+      for (int l = 0; l < 32; ++l) {                                                                         \
+        la[l] = lb[l] = lc[l] = (T)0;                                                                         \
+        for (int64_t e = l; e < m; e += 32) {                                                                 \
+          la[l] = FMA(xi[e], xi[e], la[l]);                                                                   \
+          lb[l] = FMA(xj[e], xj[e], lb[l]);                                                                   \
+          lc[l] = FMA(xi[e], xj[e], lc[l]);                                                                   \
+        }                                                                                                     \
+      }                                                                                                       \
+      a = butterfly_sum_##SUF(la);                                                                            \
+      b = butterfly_sum_##SUF(lb);                                                                            \
+      c = butterfly_sum_##SUF(lc);                                                                            \
+    } else {                                                                                                  \
+      for (int64_t k = 0; k < m; ++k) {                                                                       \
+        a += xi[k] * xi[k];                                                                                   \
+        b += xj[k] * xj[k];                                                                                   \
+        c += xi[k] * xj[k];                                                                                   \
+      }                                                                                                       \
+    }                                                                                                         \
+    if (a == (T)0) return -1;                                                                                 \
+    if (b == (T)0) return -2;                                                                                 \
+    const T thresh = reltol * SQRT(a) * SQRT(b);                                                              \
+    const double ratio = (double)FABS(c) / (sqrt((double)a) * sqrt((double)b));                               \
+    if (ratio > *worst) *worst = ratio;                                                                       \
+    if (FABS(c) <= thresh) return 0;                                                                          \
+    T cs, sn;                                                                                                 \
+    if (dev) {                                                                                                \
+      const T dx = b - a, dy = (T)2 * c, ax = FABS(dx);                                                       \
+      const T big = FMAX(ax, FABS(dy));                                                                       \
+      T rr;                                                                                                   \
+      if (big < BIG && big > SMALL) {                                                                         \
+        rr = SQRT(FMA(dx, dx, dy * dy));                                                                      \
+      } else {                                                                                                \
+        int e2;                                                                                               \
+        FREXP(big, &e2);                                                                                      \
+        const T xs = LDEXP(dx, -e2), ys = LDEXP(dy, -e2);                                                     \
+        rr = LDEXP(SQRT(FMA(xs, xs, ys * ys)), e2);                                                           \
+      }                                                                                                       \
+      const T den = ax + rr;                                                                                  \
+      const T tt = dx == (T)0 ? (T)1 : (dx > (T)0 ? dy : -dy) / den;                                          \
+      cs = SQRT(den / ((T)2 * rr));                                                                           \
+      sn = cs * tt;                                                                                           \
+    } else {                                                                                                  \
+      const T zeta = (b - a) / ((T)2 * c);                                                                    \
+      const T t = (zeta >= (T)0 ? (T)1 : (T)-1) / (FABS(zeta) + HYPOT((T)1, zeta));                         \
+      cs = (T)1 / HYPOT((T)1, t);                                                                             \
+      sn = cs * t;                                                                                            \
+    }                                                                                                         \
+    rotate_cols_##SUF(xi, xj, m, cs, sn, dev);                                                                \
+    rotate_cols_##SUF(v + i * n, v + j * n, n, cs, sn, dev);                                                  \
+    return 1;                                                                                                 \
+  }                                                                                                           \
+  static int onesided_##SUF(T* x, T* v, int64_t m, int64_t n, double tol, int max_sweeps, int dev, T* sig,    \
+                            port_jacobi_stats* st, port_error* err) {                                         \
+    memset(v, 0, sizeof(T) * (size_t)(n * n));                                                               \
+    for (int64_t i = 0; i < n; ++i) v[i * n + i] = (T)1;                                                      \
+    const T reltol = (T)tol;                                                                                  \
+    double worst = 0.0;                                                                                       \
+    int converged = 0, sweep = 0;                                                                             \
+    int64_t rotations = 0;                                                                                    \
+    const int64_t N = n + (n & 1), np = N / 2;                                                                \
+    for (; sweep < max_sweeps; ++sweep) {                                                                     \
+      int rotated = 0;                                                                                        \
+      int64_t bad = -1;                                                                                       \
+      worst = 0.0;                                                                                            \
+      if (dev) {                                                                                              \
+        for (int64_t r = 0; r < N - 1; ++r)                                                                   \
+          for (int64_t k = 0; k < np; ++k) {                                                                  \
+            int64_t p, q;                                                                                     \
+            port_rr_pair(n, r, k, &p, &q);                                                                    \
+            if (q >= n) continue;                                                                             \
+            const int res = pair_##SUF(x, v, m, n, p, q, reltol, 1, &worst);                                  \
+            if (res < 0) {                                                                                    \
+              const int64_t col = res == -1 ? p : q;                                                          \
+              if (bad < 0 || col < bad) bad = col;                                                            \
+            } else if (res) {                                                                                 \
+              rotated = 1;                                                                                    \
+              ++rotations;                                                                                    \
+            }                                                                                                 \
+          }                                                                                                   \
+        if (bad >= 0) {                                                                                       \
+          if (st) st->sweeps = sweep + 1;                                                                     \
+          return set_err(err, ST_ZERO_COLUMN, bad + 1, 0.0);                                                  \
+        }                                                                                                     \
+      } else {                                                                                                \
+        for (int64_t i = 0; i < n - 1; ++i)                                                                   \
+          for (int64_t j = i + 1; j < n; ++j) {                                                               \
+            const int res = pair_##SUF(x, v, m, n, i, j, reltol, 0, &worst);                                  \
+            if (res < 0) return set_err(err, ST_ZERO_COLUMN, (res == -1 ? i : j) + 1, 0.0);                   \
+            if (res) {                                                                                        \
+              rotated = 1;                                                                                    \
+              ++rotations;                                                                                    \
+            }                                                                                                 \
+          }                                                                                                   \
+      }                                                                                                       \
+      if (!rotated) {                                                                                         \
+        converged = 1;                                                                                        \
+        ++sweep;                                                                                              \
+        break;                                                                                                \
+      }                                                                                                       \
+    }                                                                                                         \
+    if (st) {                                                                                                 \
+      st->sweeps = sweep;                                                                                     \
+      st->rotations = rotations;                                                                              \
+      st->pairs_per_sweep = n * (n - 1) / 2;                                                                  \
+    }                                                                                                         \
+    if (!converged) return set_err(err, ST_NOCONV, max_sweeps, worst);                                        \
+    for (int64_t j = 0; j < n; ++j) {                                                                         \
+      const T* xj = x + j * m;                                                                                \
+      T s;                                                                                                    \
+      if (dev) {                                                                                              \
+        T mx = (T)0;                                                                                          \
+        for (int64_t e = 0; e < m; ++e) mx = FMAX(mx, FABS(xj[e]));                                           \
+        T l[32];                                                                                              \
+        for (int ll = 0; ll < 32; ++ll) {                                                                     \
+          l[ll] = (T)0;                                                                                       \
+          if (mx > (T)0)                                                                                      \
+            for (int64_t e = ll; e < m; e += 32) {                                                            \
+              const T y = xj[e] / mx;                                                                         \
+              l[ll] = FMA(y, y, l[ll]);                                                                       \
+            }                                                                                                 \
+        }                                                                                                     \
+        s = mx * SQRT(butterfly_sum_##SUF(l));                                                                \
+      } else {                                                                                                \
+        s = scaled_norm_ref_##SUF(xj, m);                                                                     \
+      }                                                                                                       \
+      sig[j] = s;                                                                                             \
+    }                                                                                                         \
+    return ST_OK;                                                                                             \
+  }
+
+DEFINE_ONESIDED(double, f64, sqrt, fabs, hypot, fma, fmax, frexp, ldexp, 0x1p500, 0x1p-500)
+DEFINE_ONESIDED(float, f32, sqrtf, fabsf, hypotf, fmaf, fmaxf, frexpf, ldexpf, 0x1p60f, 0x1p-60f)
+
+/* The spectral phase of the two one-sided branches on the Gram mh (n x n,
+ * binary64): sigma (working-precision values) and V (binary32), sorted
+ * descending, sign of each V column fixed by its first largest entry
+ * (jacobi.cpp:143-167), tiny-sigma check (thinsvd.cpp:22-26).
+ *   choice 1 GramCholSvd: R = chol(mh), fl32(R) with the cast checks,
+ *            one-sided Jacobi in binary32, sigma = sigma(R);
+ *   choice 2 OneSidedJacobiOnGram: one-sided Jacobi of mh in binary64,
+ *            sigma = fl32(sqrt(sigma(M))). */
+int port_onesided_spectral(int choice, const double* mh, int64_t n, double tol, int max_sweeps, int sem,
+                           double* sigma, float* v, port_jacobi_stats* stats, port_error* err) {
+  set_err(err, ST_OK, 0, 0.0);
+  if (choice != 1 && choice != 2) return set_err(err, ST_INVALID, 0, 0.0);
+  const int dev = sem == PORT_SEM_DEVICE;
+  const size_t nn = (size_t)(n * n);
+  double* raw = (double*)malloc(sizeof(double) * (size_t)n);
+  double* vd = (double*)malloc(sizeof(double) * nn); /* V widened (exact) */
+  int st = ST_OK;
+  if (choice == 1) {
+    double* r = (double*)malloc(sizeof(double) * nn);
+    st = port_cholesky_f64(mh, n, r, err);
+    float* x = (float*)malloc(sizeof(float) * nn);
+    float* vf = (float*)malloc(sizeof(float) * nn);
+    float* sg = (float*)malloc(sizeof(float) * (size_t)n);
+    if (st == ST_OK)
+      for (int64_t j = 0; j < n && st == ST_OK; ++j) /* cast (dense.cpp:163-176) */
+        for (int64_t i = 0; i < n; ++i) {
+          const double val = r[j * n + i];
+          if (!isfinite(val)) {
+            st = set_err(err, ST_INVALID, i + 1, val);
+            break;
+          }
+          if (fabs(val) > (double)FLT_MAX) {
+            st = set_err(err, ST_CAST_OVERFLOW, i + 1, val);
+            break;
+          }
+          x[j * n + i] = (float)val;
+        }
+    if (st == ST_OK) {
+      const double t = tol > 0.0 ? tol : (double)n * 0x1p-24;
+      st = onesided_f32(x, vf, n, n, t, max_sweeps, dev, sg, stats, err);
+    }
+    if (st == ST_OK) {
+      for (int64_t j = 0; j < n; ++j) raw[j] = (double)sg[j];
+      for (size_t k = 0; k < nn; ++k) vd[k] = (double)vf[k];
+    }
+    free(r);
+    free(x);
+    free(vf);
+    free(sg);
+  } else {
+    double* x = (double*)malloc(sizeof(double) * nn);
+    memcpy(x, mh, sizeof(double) * nn);
+    const double t = tol > 0.0 ? tol : (double)n * 0x1p-53;
+    st = onesided_f64(x, vd, n, n, t, max_sweeps, dev, raw, stats, err);
+    free(x);
+  }
+  if (st == ST_OK) {
+    for (int64_t j = 0; j < n; ++j)
+      if (!(raw[j] > 0.0)) { /* jacobi.cpp:113-114 */
+        st = set_err(err, ST_ZERO_COLUMN, j + 1, 0.0);
+        break;
+      }
+  }
+  if (st == ST_OK) {
+    int64_t* perm = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    descending_perm_f64(raw, n, perm);
+    for (int64_t jj = 0; jj < n; ++jj) {
+      const int64_t src = perm[jj];
+      const double* vc = vd + src * n;
+      int64_t imax = 0;
+      double amax = -1.0;
+      for (int64_t i = 0; i < n; ++i)
+        if (fabs(vc[i]) > amax) {
+          amax = fabs(vc[i]);
+          imax = i;
+        }
+      const int flip = vc[imax] < 0.0;
+      for (int64_t i = 0; i < n; ++i) v[jj * n + i] = (float)(flip ? -vc[i] : vc[i]);
+      sigma[jj] = choice == 1 ? raw[src] : (double)(float)sqrt(raw[src]);
+    }
+    free(perm);
+    for (int64_t i = 0; i < n; ++i) /* check_sigma_normal */
+      if ((float)sigma[i] < FLT_MIN) {
+        st = set_err(err, ST_TINY_SV, i + 1, sigma[i]);
+        break;
+      }
+  }
+  free(raw);
+  free(vd);
+  return st;
+}
+
+/* ======================================================================== */
 /* fp32 thin SVD (proj/src/thinsvd.cpp:49-123)                              */
 /* ======================================================================== */
 
@@ -491,6 +800,11 @@ int port_av_f32(const float* a, int64_t m, int64_t n, const float* w, float* u, 
 int port_thin_svd_f32(const float* a, int64_t m, int64_t n, int threads, int sem,
                       float* u, double* sigma, float* v, double* times5,
                       port_error* err) {
+  return port_thin_svd_f32_choice(a, m, n, threads, sem, 0, u, sigma, v, times5, err);
+}
+
+int port_thin_svd_f32_choice(const float* a, int64_t m, int64_t n, int threads, int sem, int choice,
+                             float* u, double* sigma, float* v, double* times5, port_error* err) {
   const double t0 = now_s();
   set_err(err, ST_OK, 0, 0.0);
   if (m < n || n < 1) return set_err(err, ST_INVALID, 0, 0.0);
@@ -505,19 +819,25 @@ int port_thin_svd_f32(const float* a, int64_t m, int64_t n, int threads, int sem
     return set_err(err, st, 0, 0.0);
   }
   const double te = now_s();
-  double* lam = (double*)malloc(sizeof(double) * (size_t)n);
-  double* vh = (double*)malloc(sizeof(double) * (size_t)(n * n));
-  st = port_twosided_jacobi_f64(mh, n, 0.0, 30, sem, lam, vh, NULL, err);
-  free(mh);
-  if (st != ST_OK) {
+  if (choice != 0) {
+    st = port_onesided_spectral(choice, mh, n, 0.0, 30, sem, sigma, v, NULL, err);
+    free(mh);
+    if (st != ST_OK) return st;
+  } else {
+    double* lam = (double*)malloc(sizeof(double) * (size_t)n);
+    double* vh = (double*)malloc(sizeof(double) * (size_t)(n * n));
+    st = port_twosided_jacobi_f64(mh, n, 0.0, 30, sem, lam, vh, NULL, err);
+    free(mh);
+    if (st != ST_OK) {
+      free(lam);
+      free(vh);
+      return st;
+    }
+    for (int64_t i = 0; i < n; ++i) sigma[i] = (double)(float)sqrt(lam[i]);
+    for (int64_t k = 0; k < n * n; ++k) v[k] = (float)vh[k];
     free(lam);
     free(vh);
-    return st;
   }
-  for (int64_t i = 0; i < n; ++i) sigma[i] = (double)(float)sqrt(lam[i]);
-  for (int64_t k = 0; k < n * n; ++k) v[k] = (float)vh[k];
-  free(lam);
-  free(vh);
   for (int64_t i = 0; i < n; ++i) /* check_sigma_normal, thinsvd.cpp:22-26 */
     if ((float)sigma[i] < FLT_MIN) return set_err(err, ST_TINY_SV, i + 1, sigma[i]);
   const double t_eig = now_s() - te;

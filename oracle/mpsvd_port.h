@@ -67,6 +67,16 @@ int port_thin_svd_f32(const float* a, int64_t m, int64_t n, int threads, int sem
 
 int port_av_f32(const float* a, int64_t m, int64_t n, const float* w, float* u, int threads);
 
+/* ---- the one-sided branches (thinsvd.cpp:37-47,90-104) ------------------- */
+/* choice: 0 TwoSidedJacobi, 1 GramCholSvd, 2 OneSidedJacobiOnGram */
+int port_thin_svd_f32_choice(const float* a, int64_t m, int64_t n, int threads, int sem, int choice,
+                             float* u, double* sigma, float* v, double* times5, port_error* err);
+/* cholesky (dense.cpp:39-58): upper R, strict lower part zero */
+int port_cholesky_f64(const double* m, int64_t n, double* r, port_error* err);
+/* spectral phase of choice 1 / 2 on the Gram mh: sorted working sigma, V */
+int port_onesided_spectral(int choice, const double* mh, int64_t n, double tol, int max_sweeps, int sem,
+                           double* sigma, float* v, port_jacobi_stats* stats, port_error* err);
+
 /* ---- double-double ------------------------------------------------------- */
 void port_dd_add(double ah, double al, double bh, double bl, double* rh, double* rl);
 void port_dd_mul(double ah, double al, double bh, double bl, double* rh, double* rl);

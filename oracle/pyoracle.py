@@ -302,7 +302,7 @@ class Port:
         self._raise(st, err)
         return lam, v, stt.sweeps, stt.rotations
 
-    def thin_svd(self, a, threads=1, sem=SEM_REFERENCE) -> SvdOut:
+    def thin_svd(self, a, threads=1, sem=SEM_REFERENCE, choice=0) -> SvdOut:
         a = _fcol(a, np.float32)
         m, n = a.shape
         u = np.zeros((m, n), np.float32, order="F")
@@ -310,10 +310,32 @@ class Port:
         s = np.zeros(n)
         t = np.zeros(5)
         err = _PortErr()
-        st = self.lib.port_thin_svd_f32(_f(a), _i64(m), _i64(n), C.c_int(threads), C.c_int(sem),
-                                        _f(u), _d(s), _f(v), _d(t), C.byref(err))
+        st = self.lib.port_thin_svd_f32_choice(_f(a), _i64(m), _i64(n), C.c_int(threads), C.c_int(sem),
+                                               C.c_int(choice), _f(u), _d(s), _f(v), _d(t), C.byref(err))
         self._raise(st, err)
         return SvdOut(u, s, v, t, 1, min(16, m))
+
+    def cholesky(self, mtx):
+        mtx = _fcol(mtx, np.float64)
+        n = mtx.shape[0]
+        r = np.zeros((n, n), order="F")
+        err = _PortErr()
+        self._raise(self.lib.port_cholesky_f64(_d(mtx), _i64(n), _d(r), C.byref(err)), err)
+        return r
+
+    def onesided_spectral(self, choice, mtx, tol=0.0, max_sweeps=30, sem=SEM_DEVICE):
+        """(sigma, V float32, sweeps, rotations) of the GramCholSvd (1) or
+        OneSidedJacobiOnGram (2) spectral phase on the Gram mtx."""
+        mtx = _fcol(mtx, np.float64)
+        n = mtx.shape[0]
+        s = np.zeros(n)
+        v = np.zeros((n, n), np.float32, order="F")
+        stt = _PortStats()
+        err = _PortErr()
+        st = self.lib.port_onesided_spectral(C.c_int(choice), _d(mtx), _i64(n), C.c_double(tol), C.c_int(max_sweeps),
+                                             C.c_int(sem), _d(s), _f(v), C.byref(stt), C.byref(err))
+        self._raise(st, err)
+        return s, v, stt.sweeps, stt.rotations
 
     def av_f32(self, a, w, threads=8):
         a = _fcol(a, np.float32)

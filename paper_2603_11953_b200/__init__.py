@@ -29,6 +29,7 @@ from .api import (  # noqa: F401
     max_rel_sv_error,
     mp_thin_svd,
     mp_thin_svd_f64,
+    onesided_spectral,
     orth_error,
     rowwise_backward_error,
     twosided_jacobi_eig,

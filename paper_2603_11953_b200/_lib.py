@@ -70,6 +70,9 @@ SIGNATURES = [
     ("mpsvd_stage_gram", C.c_int, [C.c_int, vp, i64, i64, dp, dp]),
     ("mpsvd_stage_jacobi", C.c_int, [C.c_int, dp, dp, i64, C.c_double, C.c_int, dp, dp, dp, dp,
                                      C.POINTER(C.c_int), C.POINTER(i64)]),
+    ("mpsvd_stage_onesided", C.c_int, [C.c_int, dp, i64, C.c_double, C.c_int, dp, C.POINTER(C.c_float),
+                                       C.POINTER(C.c_int), C.POINTER(i64)]),
+    ("mpsvd_plan_set_eigensolver", C.c_int, [vp, C.c_int]),
     ("mpsvd_fp64_peak_tflops", C.c_double, [C.c_int]),
     ("mpsvd_device_available", C.c_int, []),
 ]

@@ -197,6 +197,7 @@ class ThinSvdResult:
     qr_baseline: bool = False
     jacobi_sweeps: int = 0
     jacobi_rotations: int = 0
+    eigensolver: int = 0  # EigensolverChoice of the call (thinsvd.hpp ThinSvdResult::eigensolver)
 
 
 class _ResultOwner:
@@ -248,7 +249,9 @@ def mp_thin_svd(a, choice: EigensolverChoice = EigensolverChoice.TWOSIDED_JACOBI
     mat = a if isinstance(a, Matrix) else Matrix.from_numpy(np.asarray(a))
     r = C.c_void_p()
     _check(lib.mpsvd_thin_svd(mat.handle, int(choice), int(threads), C.byref(r)))
-    return _result(r)
+    out = _result(r)
+    out.eigensolver = EigensolverChoice(int(choice))
+    return out
 
 
 # thinsvd.hpp kDdMaxSweeps: sweep cap of the double-double path
@@ -371,6 +374,21 @@ def twosided_jacobi_eig(m_hi, m_lo=None, dd: bool = False, tol: float = 0.0, max
     return lh, vh, sw.value, rot.value
 
 
+def onesided_spectral(choice, m_hi, tol: float = 0.0, max_sweeps: int = 30):
+    """Spectral phase of the GRAM_CHOL_SVD / ONESIDED_JACOBI_GRAM branches
+    (thinsvd.cpp:37-47,90-104) on the device for a binary64 Gram: returns
+    (sigma, V float32, sweeps, rotations), sorted and sign-fixed."""
+    m_hi = np.asfortranarray(m_hi, dtype=np.float64)
+    n = m_hi.shape[0]
+    sig = np.zeros(n)
+    v = np.zeros((n, n), np.float32, order="F")
+    sw = C.c_int()
+    rot = C.c_int64()
+    _check(lib.mpsvd_stage_onesided(int(choice), _dptr(m_hi), n, float(tol), int(max_sweeps), _dptr(sig),
+                                    v.ctypes.data_as(C.POINTER(C.c_float)), C.byref(sw), C.byref(rot)))
+    return sig, v, sw.value, rot.value
+
+
 # ---------------------------------------------------------------------------
 # device-resident plans (bench, multi-GPU)
 
@@ -407,6 +425,9 @@ class Plan:
 
     def execute(self, d_a: int, lda: int, d_u: int, ldu: int, d_sigma: int, d_v: int, stream: int = 0) -> None:
         _check(lib.mpsvd_plan_execute(self._h, d_a, lda, d_u, ldu, d_sigma, d_v, stream or None))
+
+    def set_eigensolver(self, choice: EigensolverChoice) -> None:
+        _check(lib.mpsvd_plan_set_eigensolver(self._h, int(choice)))
 
     def wait(self) -> ExecInfo:
         info = ExecInfo()

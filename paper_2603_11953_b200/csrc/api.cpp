@@ -248,6 +248,13 @@ void raise_device_status(const mpsvd_exec_info& info, int max_sweeps) {
       throw NoConvergenceError(max_sweeps, info.error_value);
     case 7:
       throw TinySingularValueError(info.error_index, info.error_value);
+    case 4:
+      throw ZeroColumnError(info.error_index);
+    case 6:  // the column travels in the sweeps field (no sweep has run)
+      throw CastOverflowError(info.error_index, info.sweeps, info.error_value);
+    case 1:
+      throw InvalidArgument("non-finite entry (" + std::to_string(info.error_index) + "," +
+                            std::to_string(info.sweeps) + ") in cast");
     default:
       throw std::runtime_error("device pipeline failed with status " + std::to_string(info.status));
   }
@@ -255,7 +262,8 @@ void raise_device_status(const mpsvd_exec_info& info, int max_sweeps) {
 
 using Clock = std::chrono::steady_clock;
 
-ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f64) {
+ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f64,
+                           EigensolverChoice choice = EigensolverChoice::TwoSidedJacobi) {
   const auto t0 = Clock::now();
   const long long m = a.rows(), n = a.cols();
   if (cfg.max_sweeps < 1) throw InvalidArgument("max_sweeps must be >= 1");
@@ -263,8 +271,7 @@ ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f
   Bundle& b = bundle_for(m, n, f64);
   engine::Plan& p = *b.plan;
   p.set_jacobi(cfg.tol, cfg.max_sweeps);
-  const std::size_t elt = f64 ? 8 : 4;
-  (void)elt;
+  p.set_eigensolver(choice == EigensolverChoice::TwoSidedJacobi ? 0 : choice == EigensolverChoice::GramCholSvd ? 1 : 2);
   cudaStream_t st = p.own_stream;
   const Precision wp = f64 ? Precision::Higher : Precision::Working;
   ThinSvdResult out;
@@ -279,7 +286,7 @@ ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f
   const mpsvd_exec_info info = p.wait();
   std::copy(b.h_sigma, b.h_sigma + n, out.factors.sigma.begin());
   raise_device_status(info, cfg.max_sweeps);
-  out.eigensolver = EigensolverChoice::TwoSidedJacobi;
+  out.eigensolver = choice;
   out.gram_sync_events = 1;  // one global combine of the partial Grams
   out.gram_blocks = p.nblocks;
   out.jacobi_sweeps = info.sweeps;
@@ -303,9 +310,7 @@ ThinSvdResult mp_thin_svd(const DenseMatrix& a, EigensolverChoice choice, const 
   if (a.precision() != Precision::Working) throw InvalidArgument("mp_thin_svd expects a Working-precision matrix");
   if (a.rows() < a.cols() || a.cols() < 1) throw InvalidArgument("mp_thin_svd: need m >= n >= 1");
   if (threads < 1) throw InvalidArgument("mp_thin_svd: thread count must be positive");
-  if (choice != EigensolverChoice::TwoSidedJacobi)
-    throw InvalidArgument("mp_thin_svd: only EigensolverChoice::TwoSidedJacobi runs on the GPU path");
-  return run_thin_svd(a, cfg, false);
+  return run_thin_svd(a, cfg, false, choice);
 }
 
 ThinSvdResult mp_thin_svd_f64(const DenseMatrix& a, const JacobiConfig& cfg, int threads) {
@@ -532,6 +537,32 @@ void raise_device_status_public(const mpsvd_exec_info& info, int max_sweeps) {
 void gpu_gram_public(bool f64, const void* a, long long m, long long n, double* m_hi, double* m_lo) {
   gpu_gram(f64, a, m, n, m_hi, m_lo);
 }
+// the spectral phase of the one-sided branches on an uploaded fp64 Gram:
+// sorted working-precision sigma and V (binary32), as port_onesided_spectral
+void gpu_onesided_public(int choice, const double* m_hi, long long n, double tol, int max_sweeps, double* sigma,
+                         float* v, int* sweeps, long long* rotations) {
+  require_device();
+  if (n < 1) throw InvalidArgument("onesided: empty matrix");
+  if (max_sweeps < 1) throw InvalidArgument("max_sweeps must be >= 1");
+  if (choice != 1 && choice != 2) throw InvalidArgument("choice must be GRAM_CHOL_SVD or ONESIDED_JACOBI_GRAM");
+  engine::Plan p(0, n, false, nullptr);
+  p.set_jacobi(tol, max_sweeps);
+  p.set_eigensolver(choice);
+  cudaStream_t st = p.own_stream;
+  const std::size_t nn = (std::size_t)n * n;
+  engine::check(cudaMemcpyAsync(p.d_m, m_hi, nn * 8, cudaMemcpyHostToDevice, st), "H2D M");
+  p.reset_status(st);
+  p.eigen(st);
+  p.finish(p.d_sigma_tmp, p.d_vwork_tmp, st);
+  p.fetch_status(st);
+  engine::check(cudaMemcpyAsync(sigma, p.d_sigma_tmp, n * 8, cudaMemcpyDeviceToHost, st), "D2H sigma");
+  engine::check(cudaMemcpyAsync(v, p.d_vwork_tmp, nn * 4, cudaMemcpyDeviceToHost, st), "D2H V");
+  const mpsvd_exec_info info = p.wait();
+  raise_device_status(info, max_sweeps);
+  if (sweeps) *sweeps = info.sweeps;
+  if (rotations) *rotations = info.rotations;
+}
+
 void gpu_jacobi_public(bool dd, const double* m_hi, const double* m_lo, long long n, double tol, int max_sweeps,
                        double* lam_hi, double* lam_lo, double* v_hi, double* v_lo, int* sweeps,
                        long long* rotations) {
@@ -835,6 +866,27 @@ mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, 
     long long rot = 0;
     mpsvd::gpu_jacobi_public(dd != 0, m_hi, m_lo, n, tol, max_sweeps, lam_hi, lam_lo, v_hi, v_lo, sweeps, &rot);
     if (rotations) *rotations = rot;
+  });
+}
+
+mpsvd_status mpsvd_stage_onesided(mpsvd_eigensolver eig, const double* m_hi, int64_t n, double tol, int max_sweeps,
+                                  double* sigma, float* v, int* sweeps, int64_t* rotations) {
+  return guarded([&] {
+    require(m_hi != nullptr && sigma != nullptr && v != nullptr, "null argument");
+    long long rot = 0;
+    mpsvd::gpu_onesided_public((int)eig, m_hi, n, tol, max_sweeps, sigma, v, sweeps, &rot);
+    if (rotations) *rotations = rot;
+  });
+}
+
+mpsvd_status mpsvd_plan_set_eigensolver(mpsvd_plan* p, mpsvd_eigensolver eig) {
+  return guarded([&] {
+    require(p != nullptr && p->p, "null plan");
+    require(eig == MPSVD_EIG_TWOSIDED_JACOBI || eig == MPSVD_EIG_GRAM_CHOL_SVD || eig == MPSVD_EIG_ONESIDED_JACOBI_GRAM,
+            "unknown eigensolver value");
+    if (eig != MPSVD_EIG_TWOSIDED_JACOBI && p->p->dd)
+      throw mpsvd::InvalidArgument("the one-sided branches take a binary32 working matrix");
+    p->p->set_eigensolver((int)eig);
   });
 }
 

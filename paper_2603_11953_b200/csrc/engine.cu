@@ -304,6 +304,25 @@ void Plan::ensure_log() {
   log_sweeps = max_sweeps;
 }
 
+void Plan::set_eigensolver(int choice) {
+  if (choice < 0 || choice > 2) throw std::invalid_argument("unknown eigensolver choice");
+  if (choice != 0 && dd) throw std::invalid_argument("the one-sided branches take a binary32 working matrix");
+  if (choice == eig_choice) return;
+  if (graph_exec) {  // the captured graph holds the other branch's kernels
+    cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+  }
+  eig_choice = choice;
+  if (choice != 0 && !d_osv) {
+    const size_t nn = (size_t)n * n;
+    d_r64 = dalloc<double>(nn, owned);
+    d_x32 = dalloc<float>(nn, owned);
+    d_osv = dalloc<double>(nn, owned);
+    d_sigraw = dalloc<double>(n, owned);
+    d_osaux = dalloc<unsigned long long>(dev::onesided_aux_words(1000), owned);
+  }
+}
+
 double Plan::effective_tol() const {
   if (tol > 0.0) return tol;
   return (double)n * (dd ? 0x1p-104 : 0x1p-53);  // jacobi.cpp:579-580; u_dd = 2^-104
@@ -353,6 +372,21 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
 }
 
 void Plan::eigen(cudaStream_t st) {
+  if (eig_choice == 1) {  // GramCholSvd: chol in binary64, one-sided Jacobi of fl32(R)
+    check(dev::launch_chol_upper(d_m, (int)n, d_r64, (float*)d_x32, jws.status, st), "chol_upper");
+    check(dev::launch_onesided(true, d_x32, d_osv, (int)n, (int)n, tol > 0.0 ? tol : (double)n * 0x1p-24, max_sweeps,
+                               jws.status, d_sigraw, (double*)jws.v, d_osaux, sm_count, st),
+          "onesided f32");
+    launches += 2;
+    return;
+  }
+  if (eig_choice == 2) {  // OneSidedJacobiOnGram: one-sided Jacobi of M in binary64 (M rotated in place)
+    check(dev::launch_onesided(false, d_m, d_osv, (int)n, (int)n, tol > 0.0 ? tol : (double)n * 0x1p-53, max_sweeps,
+                               jws.status, d_sigraw, (double*)jws.v, d_osaux, sm_count, st),
+          "onesided f64");
+    launches += 1;
+    return;
+  }
   ensure_log();
   bool fused = false;
   check(dev::launch_jacobi(dd, (int)n, effective_tol(), max_sweeps, jws, sm_count, st, &fused), "jacobi");
@@ -366,6 +400,18 @@ void Plan::eigen(cudaStream_t st) {
 // The pipeline is captured once per set of device pointers into a CUDA graph
 // and replayed (saves the per-kernel launch gaps; ~9 launches per SVD).
 // MPSVD_NO_GRAPH=1 launches the kernels directly; so does any capture error.
+void Plan::finish(double* sig, void* vw, cudaStream_t st) {
+  if (eig_choice == 0) {
+    check(dev::launch_finish(dd, (int)n, jws, d_perm, d_lam_hi, d_lam_lo, sig, vw, d_w, dd ? 1 : 0, st), "finish");
+  } else {
+    check(dev::launch_onesided_sort(d_sigraw, (int)n, eig_choice == 1 ? 0 : 1, jws.status, d_perm, sig, st),
+          "onesided sort");
+    check(dev::launch_finish_columns_f64((int)n, (const double*)jws.v, jws.status, d_perm, sig, vw, d_w, 0, st),
+          "finish columns");
+  }
+  launches += 2;
+}
+
 void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                    cudaStream_t st) {
   if (!st) st = own_stream;
@@ -433,9 +479,7 @@ void Plan::enqueue(const void* d_a, long long lda, void* d_u, long long ldu, voi
   eigen(st);
   double* sig = d_sigma ? (double*)d_sigma : d_sigma_tmp;
   void* vw = d_v ? d_v : d_vwork_tmp;
-  check(dev::launch_finish(dd, (int)n, jws, d_perm, d_lam_hi, d_lam_lo, sig, vw, d_w, dd ? 1 : 0, st),
-        "finish");
-  launches += 2;
+  finish(sig, vw, st);
   record_event(ev[2], st);
   if (d_u && m > 0) {
     if (dd)
@@ -523,9 +567,7 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
   (void)esz;
   record_event(ev[1], st);
   eigen(st);
-  check(dev::launch_finish(dd, (int)n, jws, d_perm, d_lam_hi, d_lam_lo, d_sigma, d_v, d_w, dd ? 1 : 0, st),
-        "finish");
-  launches += 2;
+  finish(d_sigma, d_v, st);
   record_event(ev[2], st);
   // sigma and V travel while U is formed
   check(cudaEventRecord(cdone, st), "event");

@@ -27,6 +27,9 @@ class Plan {
   Plan& operator=(const Plan&) = delete;
 
   void set_jacobi(double tol, int max_sweeps);
+  // spectral branch (thinsvd.cpp:79-105): 0 TwoSidedJacobi, 1 GramCholSvd,
+  // 2 OneSidedJacobiOnGram (the last two: binary32 working precision only)
+  void set_eigensolver(int choice);
   void ensure_log();
   // Enqueue the whole pipeline on `st` (nullptr: the plan's stream).
   void execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
@@ -45,6 +48,8 @@ class Plan {
   // stages (used by execute and by the stage-level entry points)
   void gram(const void* d_a, long long lda, cudaStream_t st);
   void eigen(cudaStream_t st);
+  // sort / sign / sigma / V in working precision / W = V Sigma^-1
+  void finish(double* sigma, void* v_work, cudaStream_t st);
   double effective_tol() const;
 
   long long m, n;
@@ -53,6 +58,7 @@ class Plan {
   int device = 0, sm_count = 148;
   double tol = 0.0;
   int max_sweeps = 30;
+  int eig_choice = 0;
   int log_sweeps = 0;  // sweeps the rotation log (jws.log) can hold; grown by set_jacobi
 
   std::vector<int2> tiles;
@@ -77,6 +83,12 @@ class Plan {
   double* d_w = nullptr;
   double* d_vwork_tmp = nullptr;
   void* d_wplanes = nullptr;  // K7 tensor-core W pieces (f32, n <= 128)
+  // one-sided branches (onesided.cu), allocated by set_eigensolver
+  double* d_r64 = nullptr;      // R = chol(M), binary64
+  void* d_x32 = nullptr;        // binary32 R, rotated in place
+  double* d_osv = nullptr;      // V scratch of the one-sided solver
+  double* d_sigraw = nullptr;   // column norms after convergence
+  unsigned long long* d_osaux = nullptr;  // per-sweep flags of the grid-wide solver
   dev::DevStatus* h_status = nullptr;
   cudaStream_t own_stream = nullptr, last_stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};

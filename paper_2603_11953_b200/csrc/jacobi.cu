@@ -1566,5 +1566,17 @@ cudaError_t launch_finish(bool dd_mode, int n, const JacobiWorkspace& ws, int* p
   return cudaGetLastError();
 }
 
+cudaError_t launch_finish_columns_f64(int n, const double* v, const DevStatus* status, const int* perm,
+                                      const double* sigma, void* v_work, void* w_work, int working_f64,
+                                      cudaStream_t st) {
+  if (working_f64)
+    finish_columns<double, double><<<n, 256, 0, st>>>(v, n, status, perm, sigma, (double*)v_work, (double*)w_work,
+                                                      (double*)nullptr);
+  else
+    finish_columns<double, float><<<n, 256, 0, st>>>(v, n, status, perm, sigma, (float*)v_work, (float*)w_work,
+                                                     (double*)nullptr);
+  return cudaGetLastError();
+}
+
 }  // namespace dev
 }  // namespace mpsvd

@@ -68,6 +68,24 @@ cudaError_t launch_av_dmma_f64(const double* a, long long lda, long long m, int 
 cudaError_t launch_av_f64(const double* a, long long lda, long long m, int n, const double* w,
                           double* u, long long ldu, const DevStatus* status, cudaStream_t st);
 
+// onesided.cu -----------------------------------------------------------------
+// K8: R = chol(M) (fp64, upper; r64 n*n doubles, also the workspace when M
+// does not fit in shared memory) and its binary32 image r32 (n*n floats).
+cudaError_t launch_chol_upper(const double* m, int n, double* r64, float* r32, DevStatus* status, cudaStream_t st);
+// K9: one-sided Jacobi on x (m x n, T = float when f32 else double, rotated
+// in place), v: n*n T scratch; sig_raw: n doubles; v_out: n*n doubles;
+// aux: onesided_aux_words(max_sweeps) words.
+size_t onesided_aux_words(int max_sweeps);
+cudaError_t launch_onesided(bool f32, void* x, void* v, int m, int n, double tol, int max_sweeps, DevStatus* status,
+                            double* sig_raw, double* v_out, unsigned long long* aux, int sm_count, cudaStream_t st);
+// mode 0: GramCholSvd (sigma = sig_raw), 1: OneSidedJacobiOnGram (fl32(sqrt))
+cudaError_t launch_onesided_sort(const double* sig_raw, int n, int mode, DevStatus* status, int* perm, double* sigma,
+                                 cudaStream_t st);
+// finish_columns on an fp64 V (sorted by perm, signed, cast; W = V / sigma)
+cudaError_t launch_finish_columns_f64(int n, const double* v, const DevStatus* status, const int* perm,
+                                      const double* sigma, void* v_work, void* w_work, int working_f64,
+                                      cudaStream_t st);
+
 // metrics.cu ------------------------------------------------------------------
 // Row-wise backward error max_i ||(U diag(sigma) V^T - A)(i,:)|| / ||A(i,:)||
 // (proj/src/metrics.cpp:40-70) in binary64; f64 selects double storage of

@@ -69,8 +69,6 @@ def test_validation_precedes_device_use():
         M.mp_thin_svd(np.zeros((2, 3), np.float32))
     with pytest.raises(M.InvalidArgument):
         M.mp_thin_svd(np.eye(2, dtype=np.float32), threads=0)
-    with pytest.raises(M.InvalidArgument):
-        M.mp_thin_svd(np.eye(2, dtype=np.float32), choice=M.EigensolverChoice.GRAM_CHOL_SVD)
     r = C.c_void_p()
     assert lib.mpsvd_thin_svd(M.Matrix(4, 2, M.Precision.WORKING).handle, 9, 1, C.byref(r)) == 1
 
