@@ -53,7 +53,11 @@ def flops(m: int, n: int):
 DFMA_TFLOPS = 34.2
 
 
-def config_dict(cfg, world: int):
+EIG = {"twosided": 0, "gramchol": 1, "onesided": 2}
+EIG_NAME = {0: "TwoSidedJacobi", 1: "GramCholSvd", 2: "OneSidedJacobiOnGram"}
+
+
+def config_dict(cfg, world: int, eig: int = 0):
     """The workload both arms report (the reference arm times a row sample of
     it, named in its cpu_baseline.sample)."""
     m_global = cfg.m * world if cfg.name == "c2" else cfg.m
@@ -62,7 +66,7 @@ def config_dict(cfg, world: int):
     return {"workload": cfg.name, "m": m_global, "n": cfg.n, "working": cfg.working,
             "gram": "fp64" if cfg.working == "f32" else "double-double",
             "l2": f"inputs larger than L2 (A = {m_local * cfg.n * esz / 2**20:.0f} MiB per GPU > 126 MB)",
-            "parallelism": f"rows{world}"}
+            "parallelism": f"rows{world}", "eigensolver": EIG_NAME[eig]}
 
 
 def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
@@ -186,15 +190,16 @@ def run_reference(args, cfg):
 
     cores = os.cpu_count() or 1
     n = cfg.n
+    eig = EIG[args.eig]
     if cfg.working == "f32":
         m_s = min(cfg.m, 1 << 18)
         a = inputs.make(cfg, seed=1, m=m_s)
         if pyoracle.ref_available():
             lib, kind = pyoracle.Ref(), "reference"
-            fn = lambda: lib.thin_svd(a, threads=cores)  # noqa: E731
+            fn = lambda: lib.thin_svd(a, threads=cores, choice=eig)  # noqa: E731
         else:
             lib, kind = pyoracle.Port(), "port"
-            fn = lambda: lib.thin_svd(a, threads=cores)  # noqa: E731
+            fn = lambda: lib.thin_svd(a, threads=cores, choice=eig)  # noqa: E731
     else:
         m_s = min(cfg.m, 1 << 13)
         a = inputs.make(cfg, seed=1, m=m_s)
@@ -211,7 +216,7 @@ def run_reference(args, cfg):
     fg, fa = flops(m_s, n)
     value = (fg + fa) / t / 1e12
     sample = (f"{cfg.name} distribution with m={m_s} rows (of {cfg.m}), n={n}; median of {args.steps} "
-              f"after {args.warmup} warm-up; mp_thin_svd TwoSidedJacobi"
+              f"after {args.warmup} warm-up; mp_thin_svd {EIG_NAME[eig]}"
               + ("" if kind == "reference" else " (restated double-double oracle, reference has no fp64 path)"))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
@@ -219,16 +224,16 @@ def run_reference(args, cfg):
         "scaling": "weak" if cfg.name == "c2" else "strong", "vs_baseline": None,
         "dtype": "f64" if cfg.working == "f32" else "f64x2",
         "data": "synthetic (seeded, BASELINE.json distribution)",
-        "config": dict(config_dict(cfg, args.gpus), sample_rows=m_s),
+        "config": dict(config_dict(cfg, args.gpus, eig), sample_rows=m_s),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return line
 
 
-def cpu_baseline(cfg):
+def cpu_baseline(cfg, eig="twosided"):
     """Reported baseline (not the target): same sample as the reference arm."""
-    ns = argparse.Namespace(steps=3, warmup=1, gpus=1)
+    ns = argparse.Namespace(steps=3, warmup=1, gpus=1, eig=eig)
     line = run_reference(ns, cfg)
     return line["cpu_baseline"] if line else None
 
@@ -275,6 +280,11 @@ def run_ours(args, cfg):
     sig_t = torch.empty(n, dtype=torch.float64, device=dev)
     v_t = torch.empty((n, n), dtype=a_t.dtype, device=dev)
     plan = M.Plan(m_local, n, working, comm)
+    eig = EIG[args.eig]
+    if eig:
+        if cfg.working != "f32":
+            raise SystemExit("--eig gramchol/onesided: binary32 configs only (the reference has no fp64 path)")
+        plan.set_eigensolver(eig)
     # a dedicated (non-legacy) stream: the plan enqueues every kernel on it and
     # the CUDA events below are recorded on the same stream
     stream = torch.cuda.Stream(dev)
@@ -353,7 +363,7 @@ def run_ours(args, cfg):
         # free the device-resident arm before the API allocates its own buffers
         del plan, a_t, u_t, v_t, sig_t
         torch.cuda.empty_cache()
-        call = M.mp_thin_svd if cfg.working == "f32" else M.mp_thin_svd_f64
+        call = (lambda h: M.mp_thin_svd(h, choice=eig)) if cfg.working == "f32" else M.mp_thin_svd_f64
         r = call(host)  # warm: plan, device buffers, pinned result buffers
         del r
         reps = 5
@@ -428,7 +438,7 @@ def run_ours(args, cfg):
         "scaling": "weak" if cfg.name == "c2" else "strong", "vs_baseline": None,
         "dtype": "f64" if cfg.working == "f32" else "f64x2",
         "data": "synthetic (seeded torch generator, BASELINE.json distribution)",
-        "config": config_dict(cfg, world),
+        "config": config_dict(cfg, world, eig),
         "phase_ms": med,
         "roofline": roof,
         "roofline_phases": phases,
@@ -443,7 +453,7 @@ def run_ours(args, cfg):
         "validation": validation,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg)
+        line["cpu_baseline"] = cpu_baseline(cfg, args.eig)
     return line
 
 
@@ -455,6 +465,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eig", default="twosided", choices=list(EIG),
+                    help="mp_thin_svd spectral branch (GramCholSvd / OneSidedJacobiOnGram: binary32 configs)")
     args = ap.parse_args()
     from paper_2603_11953_b200.inputs import CONFIGS
 

@@ -100,7 +100,7 @@ def test_gpu_spectral_bitwise_vs_device_restatement(port, choice, n):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("choice", [GRAM_CHOL, ONESIDED])
-@pytest.mark.parametrize("m,n,kd", [(4096, 32, 6.0), (1 << 16, 64, 4.0), (20000, 100, 3.0), (8192, 128, 2.0)])
+@pytest.mark.parametrize("m,n,kd", [(4096, 32, 6.0), (1 << 15, 64, 4.0), (2000, 100, 3.0), (1024, 128, 2.0)])
 def test_gpu_thin_svd_as_accurate_as_reference(ref, choice, m, n, kd):
     a = inputs.graded(m, n, kd, seed=7 + n)
     r = M.mp_thin_svd(a, choice=choice)
