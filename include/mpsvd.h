@@ -89,6 +89,10 @@ mpsvd_status mpsvd_backward_error_device(mpsvd_precision prec, const void* d_a, 
  * U in f32. `threads` must be >= 1 (it does not change any bit). */
 mpsvd_status mpsvd_thin_svd(const mpsvd_matrix* a, mpsvd_eigensolver eig, int threads,
                             mpsvd_svd_result** out);
+/* proj/include/mpsvd.h:136-139: mixed-precision Cholesky QR. Gram and
+ * Cholesky in binary64, R cast to binary32, row-wise forward substitution in
+ * binary32 (thinsvd.cpp:125-154); new Working matrices Q (m x n), R (n x n). */
+mpsvd_status mpsvd_cholesky_qr(const mpsvd_matrix* a, mpsvd_matrix** q_out, mpsvd_matrix** r_out);
 /* ADDITIVE: f64 A, Gram + Jacobi in double-double, U in f64. */
 mpsvd_status mpsvd_thin_svd_f64(const mpsvd_matrix* a, int threads, mpsvd_svd_result** out);
 
@@ -137,6 +141,11 @@ mpsvd_status mpsvd_plan_execute(mpsvd_plan* p, const void* d_a, int64_t lda, voi
 /* Spectral branch of later executes (default MPSVD_EIG_TWOSIDED_JACOBI; the
  * one-sided branches need a MPSVD_PRECISION_WORKING plan). */
 mpsvd_status mpsvd_plan_set_eigensolver(mpsvd_plan* p, mpsvd_eigensolver eig);
+/* Cholesky QR of device-resident A (binary32 plan): Q (ldq >= m_local), R
+ * (n x n binary32, may be NULL) on `stream`; complete with mpsvd_plan_wait.
+ * Multi-rank plans all-reduce the Gram; Q stays row-sharded. */
+mpsvd_status mpsvd_plan_cholesky_qr(mpsvd_plan* p, const void* d_a, int64_t lda, void* d_q, int64_t ldq,
+                                    float* d_r, void* stream);
 /* Blocks until the last execute finished; reports the device status. */
 mpsvd_status mpsvd_plan_wait(mpsvd_plan* p, mpsvd_exec_info* info);
 /* Timed region helpers for the dominant kernels (CUDA events, ms). */

@@ -86,6 +86,16 @@ ThinSvdResult mp_thin_svd(const DenseMatrix& a, EigensolverChoice choice,
 ThinSvdResult mp_thin_svd_f64(const DenseMatrix& a, const JacobiConfig& cfg = dd_jacobi_config(),
                               int threads = 1);
 
+// proj/include/mpsvd/thinsvd.hpp:67-75: Gram (K1) and Cholesky (K8) in
+// binary64, R cast to binary32 (with the cast's overflow checks), then every
+// row of Q from Q(i,:) R = A(i,:) by forward substitution in binary32 (K10,
+// the reference's operation order). NotPositiveDefiniteError(pivot, value).
+struct CholQrFactors {
+  DenseMatrix q;
+  DenseMatrix r;
+};
+CholQrFactors mp_cholesky_qr(const DenseMatrix& a);
+
 EigFactors twosided_jacobi_eig(const DenseMatrix& m, const JacobiConfig& cfg = {},
                                JacobiStats* stats = nullptr);
 

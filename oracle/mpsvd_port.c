@@ -750,6 +750,63 @@ int port_onesided_spectral(int choice, const double* mh, int64_t n, double tol, 
   return st;
 }
 
+/* Row-wise forward substitution Q(i,:) R = A(i,:) in binary32
+ * (thinsvd.cpp:136-152): per entry, subtract q_k r_kj for k ascending
+ * (product and difference rounded separately), then divide. Device K10
+ * performs the same sequence. */
+void port_cholqr_solve(const float* a, int64_t m, int64_t n, const float* r, float* q) {
+  for (int64_t j = 0; j < n; ++j) {
+    float* qj = q + j * m;
+    const float* aj = a + j * m;
+    for (int64_t i = 0; i < m; ++i) qj[i] = aj[i];
+    for (int64_t k = 0; k < j; ++k) {
+      const float rkj = r[j * n + k];
+      const float* qk = q + k * m;
+      for (int64_t i = 0; i < m; ++i) qj[i] -= qk[i] * rkj;
+    }
+    const float rjj = r[j * n + j];
+    for (int64_t i = 0; i < m; ++i) qj[i] /= rjj;
+  }
+}
+
+/* mp_cholesky_qr (thinsvd.cpp:125-154) with the reference's own Gram
+ * (gram_impl, dense.cpp:15-36: one accumulator per entry, ascending rows). */
+int port_cholesky_qr_f32(const float* a, int64_t m, int64_t n, float* q, float* r, port_error* err) {
+  set_err(err, ST_OK, 0, 0.0);
+  if (m < n || n < 1) return set_err(err, ST_INVALID, 0, 0.0);
+  const size_t nn = (size_t)(n * n);
+  double* g = (double*)calloc(nn, sizeof(double));
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i <= j; ++i) {
+      double acc = 0.0;
+      const float* ci = a + i * m;
+      const float* cj = a + j * m;
+      for (int64_t k = 0; k < m; ++k) acc += (double)ci[k] * (double)cj[k];
+      g[j * n + i] = acc;
+      g[i * n + j] = acc;
+    }
+  double* rh = (double*)malloc(sizeof(double) * nn);
+  int st = port_cholesky_f64(g, n, rh, err);
+  if (st == ST_OK)
+    for (int64_t j = 0; j < n && st == ST_OK; ++j)
+      for (int64_t i = 0; i < n; ++i) {
+        const double v = rh[j * n + i];
+        if (!isfinite(v)) {
+          st = set_err(err, ST_INVALID, i + 1, v);
+          break;
+        }
+        if (fabs(v) > (double)FLT_MAX) {
+          st = set_err(err, ST_CAST_OVERFLOW, i + 1, v);
+          break;
+        }
+        r[j * n + i] = (float)v;
+      }
+  if (st == ST_OK) port_cholqr_solve(a, m, n, r, q);
+  free(g);
+  free(rh);
+  return st;
+}
+
 /* ======================================================================== */
 /* fp32 thin SVD (proj/src/thinsvd.cpp:49-123)                              */
 /* ======================================================================== */

@@ -71,6 +71,10 @@ int port_av_f32(const float* a, int64_t m, int64_t n, const float* w, float* u, 
 /* choice: 0 TwoSidedJacobi, 1 GramCholSvd, 2 OneSidedJacobiOnGram */
 int port_thin_svd_f32_choice(const float* a, int64_t m, int64_t n, int threads, int sem, int choice,
                              float* u, double* sigma, float* v, double* times5, port_error* err);
+/* mixed-precision Cholesky QR (thinsvd.cpp:125-154), reference semantics;
+ * the row solve alone (shared by the device K10) */
+int port_cholesky_qr_f32(const float* a, int64_t m, int64_t n, float* q, float* r, port_error* err);
+void port_cholqr_solve(const float* a, int64_t m, int64_t n, const float* r, float* q);
 /* cholesky (dense.cpp:39-58): upper R, strict lower part zero */
 int port_cholesky_f64(const double* m, int64_t n, double* r, port_error* err);
 /* spectral phase of choice 1 / 2 on the Gram mh: sorted working sigma, V */

@@ -164,6 +164,14 @@ class Ref:
             self._check(self.lib.refx_orth_error_f64(_d(q), _i64(m), _i64(n), C.byref(out)))
         return out.value
 
+    def cholesky_qr(self, a):
+        a = _fcol(a, np.float32)
+        m, n = a.shape
+        q = np.zeros((m, n), np.float32, order="F")
+        r = np.zeros((n, n), np.float32, order="F")
+        self._check(self.lib.refx_cholesky_qr(_f(a), _i64(m), _i64(n), _f(q), _f(r)))
+        return q, r
+
     def rowwise_backward_error(self, a, u, sigma, v):
         """(max_rel, skipped_rows) of proj/src/metrics.cpp:40-70; f32 or f64 factors."""
         a = np.asfortranarray(a)
@@ -314,6 +322,23 @@ class Port:
                                                C.c_int(choice), _f(u), _d(s), _f(v), _d(t), C.byref(err))
         self._raise(st, err)
         return SvdOut(u, s, v, t, 1, min(16, m))
+
+    def cholesky_qr(self, a):
+        a = _fcol(a, np.float32)
+        m, n = a.shape
+        q = np.zeros((m, n), np.float32, order="F")
+        r = np.zeros((n, n), np.float32, order="F")
+        err = _PortErr()
+        self._raise(self.lib.port_cholesky_qr_f32(_f(a), _i64(m), _i64(n), _f(q), _f(r), C.byref(err)), err)
+        return q, r
+
+    def cholqr_solve(self, a, r):
+        a = _fcol(a, np.float32)
+        r = _fcol(r, np.float32)
+        m, n = a.shape
+        q = np.zeros((m, n), np.float32, order="F")
+        self.lib.port_cholqr_solve(_f(a), _i64(m), _i64(n), _f(r), _f(q))
+        return q
 
     def cholesky(self, mtx):
         mtx = _fcol(mtx, np.float64)

@@ -195,6 +195,15 @@ int refx_orth_error_f64(const double* q, int64_t m, int64_t n, double* out) {
   return run([&] { *out = orth_error(from_f64(q, m, n)); });
 }
 
+// mp_cholesky_qr (proj/src/thinsvd.cpp:125-154).
+int refx_cholesky_qr(const float* a, int64_t m, int64_t n, float* q, float* r) {
+  return run([&] {
+    const auto f = mp_cholesky_qr(from_f32(a, m, n));
+    std::memcpy(q, f.q.fptr(), sizeof(float) * static_cast<size_t>(m * n));
+    std::memcpy(r, f.r.fptr(), sizeof(float) * static_cast<size_t>(n * n));
+  });
+}
+
 // rowwise_backward_error / max_rel_sv_error (proj/src/metrics.cpp:26-70):
 // A, U, V in Working (f32) storage, the thin-SVD factors' layout.
 int refx_rowwise_backward_error_f32(const float* a, const float* u, const double* sigma, const float* v,

@@ -51,6 +51,8 @@ SIGNATURES = [
                                               C.POINTER(i64)]),
     ("mpsvd_thin_svd", C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
     ("mpsvd_thin_svd_f64", C.c_int, [vp, C.c_int, C.POINTER(vp)]),
+    ("mpsvd_cholesky_qr", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
+    ("mpsvd_plan_cholesky_qr", C.c_int, [vp, vp, i64, vp, i64, vp, vp]),
     ("mpsvd_svd_destroy", None, [vp]),
     ("mpsvd_svd_u", vp, [vp]),
     ("mpsvd_svd_v", vp, [vp]),

@@ -125,6 +125,14 @@ class Matrix:
         return self
 
     @classmethod
+    def _adopt(cls, handle):
+        """Take ownership of a matrix the library created (e.g. CholQR's Q, R)."""
+        self = cls.__new__(cls)
+        self._h = C.c_void_p(handle)
+        self._own = True
+        return self
+
+    @classmethod
     def from_numpy(cls, a: np.ndarray) -> "Matrix":
         a = np.asarray(a)
         prec = Precision.WORKING if a.dtype == np.float32 else Precision.HIGHER
@@ -264,6 +272,16 @@ def mp_thin_svd_f64(a, threads: int = 1) -> ThinSvdResult:
     r = C.c_void_p()
     _check(lib.mpsvd_thin_svd_f64(mat.handle, int(threads), C.byref(r)))
     return _result(r)
+
+
+def mp_cholesky_qr(a):
+    """mp_cholesky_qr (proj/include/mpsvd/thinsvd.hpp:67-75) via mpsvd_cholesky_qr:
+    returns (Q float32 m x n, R float32 n x n)."""
+    mat = a if isinstance(a, Matrix) else Matrix.from_numpy(np.asarray(a))
+    q, r = C.c_void_p(), C.c_void_p()
+    _check(lib.mpsvd_cholesky_qr(mat.handle, C.byref(q), C.byref(r)))
+    qm, rm = Matrix._adopt(q.value), Matrix._adopt(r.value)
+    return qm.numpy().copy(), rm.numpy().copy()
 
 
 def orth_error(q) -> float:
@@ -425,6 +443,10 @@ class Plan:
 
     def execute(self, d_a: int, lda: int, d_u: int, ldu: int, d_sigma: int, d_v: int, stream: int = 0) -> None:
         _check(lib.mpsvd_plan_execute(self._h, d_a, lda, d_u, ldu, d_sigma, d_v, stream or None))
+
+    def cholesky_qr(self, d_a: int, lda: int, d_q: int, ldq: int, d_r: int = 0, stream: int = 0) -> None:
+        """Device-resident mixed-precision Cholesky QR (binary32 plans); finish with wait()."""
+        _check(lib.mpsvd_plan_cholesky_qr(self._h, d_a, lda, d_q, ldq, d_r or None, stream or None))
 
     def set_eigensolver(self, choice: EigensolverChoice) -> None:
         _check(lib.mpsvd_plan_set_eigensolver(self._h, int(choice)))

@@ -313,6 +313,25 @@ ThinSvdResult mp_thin_svd(const DenseMatrix& a, EigensolverChoice choice, const 
   return run_thin_svd(a, cfg, false, choice);
 }
 
+CholQrFactors mp_cholesky_qr(const DenseMatrix& a) {
+  // validation of proj/src/thinsvd.cpp:126-129
+  if (a.precision() != Precision::Working) throw InvalidArgument("mp_cholesky_qr expects a Working-precision matrix");
+  const long long m = a.rows(), n = a.cols();
+  if (m < n || n < 1) throw InvalidArgument("mp_cholesky_qr: need m >= n >= 1");
+  require_device();
+  Bundle& b = bundle_for(m, n, false);
+  engine::Plan& p = *b.plan;
+  cudaStream_t st = p.own_stream;
+  CholQrFactors out{DenseMatrix::uninitialized(m, n, Precision::Working), DenseMatrix(n, n, Precision::Working)};
+  engine::check(cudaMemcpyAsync(b.d_a, a.raw(), (size_t)m * n * 4, cudaMemcpyHostToDevice, st), "H2D A");
+  p.cholqr(b.d_a, m, b.d_u, m, st);
+  engine::check(cudaMemcpyAsync(out.q.raw(), b.d_u, (size_t)m * n * 4, cudaMemcpyDeviceToHost, st), "D2H Q");
+  engine::check(cudaMemcpyAsync(out.r.raw(), p.d_x32, (size_t)n * n * 4, cudaMemcpyDeviceToHost, st), "D2H R");
+  const mpsvd_exec_info info = p.wait();
+  raise_device_status(info, 0);
+  return out;
+}
+
 ThinSvdResult mp_thin_svd_f64(const DenseMatrix& a, const JacobiConfig& cfg, int threads) {
   if (a.precision() != Precision::Higher) throw InvalidArgument("mp_thin_svd_f64 expects a Higher-precision matrix");
   if (a.rows() < a.cols() || a.cols() < 1) throw InvalidArgument("mp_thin_svd_f64: need m >= n >= 1");
@@ -764,6 +783,29 @@ mpsvd_status mpsvd_thin_svd(const mpsvd_matrix* a, mpsvd_eigensolver eig, int th
                   : eig == MPSVD_EIG_GRAM_CHOL_SVD ? mpsvd::EigensolverChoice::GramCholSvd
                                                    : mpsvd::EigensolverChoice::OneSidedJacobiOnGram;
     *out = wrap(mpsvd::mp_thin_svd(a->m, choice, {}, threads));
+  });
+}
+
+mpsvd_status mpsvd_cholesky_qr(const mpsvd_matrix* a, mpsvd_matrix** q_out, mpsvd_matrix** r_out) {
+  return guarded([&] {
+    require(a != nullptr && q_out != nullptr && r_out != nullptr, "null argument");
+    auto f = mpsvd::mp_cholesky_qr(a->m);
+    *q_out = new mpsvd_matrix{std::move(f.q)};
+    *r_out = new mpsvd_matrix{std::move(f.r)};
+  });
+}
+
+mpsvd_status mpsvd_plan_cholesky_qr(mpsvd_plan* p, const void* d_a, int64_t lda, void* d_q, int64_t ldq, float* d_r,
+                                    void* stream) {
+  return guarded([&] {
+    require(p != nullptr && p->p, "null plan");
+    require(!p->p->dd, "cholesky QR takes a MPSVD_PRECISION_WORKING plan");
+    require(lda >= p->p->m && ldq >= p->p->m, "leading dimension too small");
+    cudaStream_t st = stream ? (cudaStream_t)stream : p->p->own_stream;
+    p->p->cholqr(d_a, lda, d_q, ldq, st);
+    if (d_r)
+      mpsvd::engine::check(cudaMemcpyAsync(d_r, p->p->d_x32, (size_t)p->p->n * p->p->n * 4, cudaMemcpyDeviceToDevice, st),
+                           "R copy");
   });
 }
 

@@ -304,6 +304,17 @@ void Plan::ensure_log() {
   log_sweeps = max_sweeps;
 }
 
+// Phase events: plain records, or external event nodes while the pipeline
+// is being captured into a graph (so they still time the replayed graph).
+static void record_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  check(cudaStreamIsCapturing(st, &cs), "capture status");
+  if (cs == cudaStreamCaptureStatusActive)
+    check(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event");
+  else
+    check(cudaEventRecord(e, st), "event");
+}
+
 void Plan::set_eigensolver(int choice) {
   if (choice < 0 || choice > 2) throw std::invalid_argument("unknown eigensolver choice");
   if (choice != 0 && dd) throw std::invalid_argument("the one-sided branches take a binary32 working matrix");
@@ -313,14 +324,37 @@ void Plan::set_eigensolver(int choice) {
     graph_exec = nullptr;
   }
   eig_choice = choice;
-  if (choice != 0 && !d_osv) {
-    const size_t nn = (size_t)n * n;
-    d_r64 = dalloc<double>(nn, owned);
-    d_x32 = dalloc<float>(nn, owned);
-    d_osv = dalloc<double>(nn, owned);
-    d_sigraw = dalloc<double>(n, owned);
-    d_osaux = dalloc<unsigned long long>(dev::onesided_aux_words(1000), owned);
-  }
+  if (choice != 0) ensure_onesided_buffers();
+}
+
+void Plan::ensure_onesided_buffers() {
+  if (d_osv) return;
+  const size_t nn = (size_t)n * n;
+  d_r64 = dalloc<double>(nn, owned);
+  d_x32 = dalloc<float>(nn, owned);
+  d_osv = dalloc<double>(nn, owned);
+  d_sigraw = dalloc<double>(n, owned);
+  d_osaux = dalloc<unsigned long long>(dev::onesided_aux_words(1000), owned);
+}
+
+void Plan::cholqr(const void* d_a, long long lda, void* d_q, long long ldq, cudaStream_t st) {
+  if (dd) throw std::invalid_argument("cholesky QR takes a binary32 working matrix");
+  ensure_onesided_buffers();
+  last_stream = st;
+  launches = 0;
+  check(cudaMemsetAsync(jws.status, 0, sizeof(DevStatus), st), "status reset");
+  record_event(ev[0], st);
+  gram(d_a, lda, st);
+  record_event(ev[1], st);
+  check(dev::launch_chol_upper(d_m, (int)n, d_r64, (float*)d_x32, jws.status, st), "chol_upper");
+  record_event(ev[2], st);
+  check(dev::launch_cholqr_rows((const float*)d_a, lda, m, (int)n, (const float*)d_x32, (float*)d_q, ldq, jws.status,
+                                sm_count, st),
+        "cholqr_rows");
+  launches += 2;
+  record_event(ev[3], st);
+  events_recorded = true;
+  check(cudaMemcpyAsync(h_status, jws.status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status D2H");
 }
 
 double Plan::effective_tol() const {
@@ -458,16 +492,6 @@ void Plan::execute(const void* d_a, long long lda, void* d_u, long long ldu, voi
   events_recorded = true;
 }
 
-// Phase events: plain records, or external event nodes while the pipeline
-// is being captured into a graph (so they still time the replayed graph).
-static void record_event(cudaEvent_t e, cudaStream_t st) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  check(cudaStreamIsCapturing(st, &cs), "capture status");
-  if (cs == cudaStreamCaptureStatusActive)
-    check(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event");
-  else
-    check(cudaEventRecord(e, st), "event");
-}
 
 void Plan::enqueue(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
                    cudaStream_t st) {

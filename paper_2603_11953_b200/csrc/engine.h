@@ -30,6 +30,7 @@ class Plan {
   // spectral branch (thinsvd.cpp:79-105): 0 TwoSidedJacobi, 1 GramCholSvd,
   // 2 OneSidedJacobiOnGram (the last two: binary32 working precision only)
   void set_eigensolver(int choice);
+  void ensure_onesided_buffers();
   void ensure_log();
   // Enqueue the whole pipeline on `st` (nullptr: the plan's stream).
   void execute(const void* d_a, long long lda, void* d_u, long long ldu, void* d_sigma, void* d_v,
@@ -48,6 +49,9 @@ class Plan {
   // stages (used by execute and by the stage-level entry points)
   void gram(const void* d_a, long long lda, cudaStream_t st);
   void eigen(cudaStream_t st);
+  // mixed-precision Cholesky QR (thinsvd.cpp:125-154): Gram (K1), chol (K8),
+  // row solves (K10). Q: m x n binary32 (ldq), R: the plan's d_x32 (n x n)
+  void cholqr(const void* d_a, long long lda, void* d_q, long long ldq, cudaStream_t st);
   // sort / sign / sigma / V in working precision / W = V Sigma^-1
   void finish(double* sigma, void* v_work, cudaStream_t st);
   double effective_tol() const;

@@ -86,6 +86,12 @@ cudaError_t launch_finish_columns_f64(int n, const double* v, const DevStatus* s
                                       const double* sigma, void* v_work, void* w_work, int working_f64,
                                       cudaStream_t st);
 
+// cholqr.cu -------------------------------------------------------------------
+// K10: Q(i,:) R = A(i,:) by forward substitution per row in binary32 (R: the
+// n x n binary32 upper factor, column-major).
+cudaError_t launch_cholqr_rows(const float* a, long long lda, long long m, int n, const float* r, float* q,
+                               long long ldq, const DevStatus* status, int sm_count, cudaStream_t st);
+
 // metrics.cu ------------------------------------------------------------------
 // Row-wise backward error max_i ||(U diag(sigma) V^T - A)(i,:)|| / ||A(i,:)||
 // (proj/src/metrics.cpp:40-70) in binary64; f64 selects double storage of
