@@ -564,7 +564,8 @@ int port_cholesky_f64(const double* m, int64_t n, double* r, port_error* err) {
       }                                                                                                       \
       const T den = ax + rr;                                                                                  \
       const T tt = dx == (T)0 ? (T)1 : (dx > (T)0 ? dy : -dy) / den;                                          \
-      cs = SQRT(den / ((T)2 * rr));                                                                           \
+      cs = sizeof(T) == 4 ? (T)1 / (T)sqrt((double)tt * (double)tt + 1.0) /* K9 OsTraits<float>::cosine */    \
+                          : SQRT(den / ((T)2 * rr));                                                          \
       sn = cs * tt;                                                                                           \
     } else {                                                                                                  \
       const T zeta = (b - a) / ((T)2 * c);                                                                    \

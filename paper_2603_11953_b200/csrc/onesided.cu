@@ -58,6 +58,7 @@ struct OsTraits<double> {
     return e;
   }
   static __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
+  static __device__ __forceinline__ double cosine(double den, double rr, double) { return sqrt(den / (2.0 * rr)); }
 };
 template <>
 struct OsTraits<float> {
@@ -73,6 +74,13 @@ struct OsTraits<float> {
     return e;
   }
   static __device__ __forceinline__ float ldg(const float* p) { return __ldcg(p); }
+  // cs = 1 / hypot(1, t) as the reference computes it in binary32
+  // (jacobi.cpp:37): glibc's hypotf evaluates sqrt(t*t + 1) in binary64 and
+  // rounds once; t*t is exact there. The closed form sqrt((|x| + r) / 2r)
+  // in binary32 left V 4-5x less orthogonal than the reference's.
+  static __device__ __forceinline__ float cosine(float, float, float t) {
+    return 1.0f / (float)sqrt(__dadd_rn(__dmul_rn((double)t, (double)t), 1.0));
+  }
 };
 
 template <typename T>
@@ -221,6 +229,7 @@ onesided_jacobi(T* __restrict__ xg, T* __restrict__ vg, int m, int n, double tol
         if (TR::ab(c) <= thresh) continue;
         // rotation (jacobi.cpp:34-40): x = b - a, y = 2c, r = hypot(x, y),
         // t = sign(x) y / (|x| + r) (t = 1 at x == 0), cs = sqrt((|x| + r) / 2r)
+        // (binary64) or 1 / fl32(sqrt(t^2 + 1)) (binary32, see OsTraits)
         const T dx = b - a, dy = T(2) * c, ax = TR::ab(dx);
         const T big = TR::mx(ax, TR::ab(dy));
         T rr;
@@ -233,7 +242,7 @@ onesided_jacobi(T* __restrict__ xg, T* __restrict__ vg, int m, int n, double tol
         }
         const T den = ax + rr;
         const T tt = dx == T(0) ? T(1) : (dx > T(0) ? dy : -dy) / den;
-        const T cs = TR::sq(den / (T(2) * rr));
+        const T cs = TR::cosine(den, rr, tt);
         const T sn = cs * tt;
         for (int e = lane; e < m; e += 32) {
           const T u = LD(xp + e), w = LD(xq + e);

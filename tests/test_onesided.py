@@ -60,6 +60,17 @@ def test_port_device_semantics_accuracy(ref, port, choice):
     assert orth_err(d.v) <= 10 * 48 * U32
 
 
+@pytest.mark.parametrize("m,n,kd", [(1024, 128, 2.0), (2000, 100, 3.0), (4096, 32, 6.0)])
+def test_port_device_semantics_v_orthogonality_like_reference(ref, port, m, n, kd):
+    # GramCholSvd runs the one-sided Jacobi in binary32: the rotation's cosine
+    # must be as accurate as the reference's 1 / hypotf(1, t) (jacobi.cpp:37);
+    # the binary32 closed form sqrt((|x| + r) / 2r) left V 4-5x less orthogonal
+    a = inputs.graded(m, n, kd, seed=7 + n)
+    r = ref.thin_svd(a, choice=GRAM_CHOL)
+    d = port.thin_svd(a, choice=GRAM_CHOL, sem=pyoracle.SEM_DEVICE)
+    assert orth_err(d.v) <= 2.0 * orth_err(r.v)
+
+
 def test_port_npd_matches_reference(ref, port):
     a = _dup_column(300, 6, 1)
     with pytest.raises(pyoracle.OracleError) as er:
