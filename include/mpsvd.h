@@ -156,6 +156,12 @@ void mpsvd_plan_destroy(mpsvd_plan* p);
  * double-double M (m_hi + m_lo). */
 mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, int64_t n, double* m_hi,
                               double* m_lo);
+/* The double-double Gram schedule of an m x n plan: *ozaki = 1 when the
+ * int8 tensor-core Gram (K2z) runs; split s covers 32-row chunks
+ * [scb[s], scb[s + 1]); logical block b holds splits [bsb[b], bsb[b + 1]).
+ * cap bounds both arrays. */
+mpsvd_status mpsvd_stage_gram_schedule(int64_t m, int64_t n, int cap, int* nsplit, int* nblocks, int* scb,
+                                       int* bsb, int* ozaki);
 /* Two-sided Jacobi on the GPU: dd = 0 fp64 (m_lo ignored), 1 double-double.
  * Outputs sorted/sign-fixed eigenpairs in the higher precision. */
 mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, int64_t n, double tol,

@@ -1058,6 +1058,146 @@ int port_dd_gram(const double* a, int64_t m, int64_t n, int threads, double* hi,
   return ST_OK;
 }
 
+/* K2z, the double-double Gram on the int8 tensor cores
+ * (paper_2603_11953_b200/csrc/gram_ozaki.cu), replayed bit for bit: the
+ * per-split column exponents, the 11 balanced 8-bit digits of
+ * trunc(x 2^(86 - E)), the exact integer digit-product sums per weight and
+ * exact-accumulation span, their conversion to double-double
+ * (V = acc_wlo 2^8 + acc_whi; (fl(V), V - fl(V)) scaled by
+ * 2^(E_i + E_j + 4 - 8 w_hi)), the running dd_add per partial slot
+ * (split * 6 + group), then the engine's combine: slots of a logical block
+ * summed in order from zero, blocks along the reference tree
+ * (parallel_gram.cpp:93-102). Semantics follow dd_gram (dd.cpp:75-88) up to
+ * the digit truncation. */
+#define OZ_L 11
+#define OZ_G 6
+#define OZ_BAD (1 << 20)
+static void oz_fixed88(double x, int e_col, uint32_t w[3]) {
+  uint64_t bits;
+  memcpy(&bits, &x, 8);
+  const int e = (int)((bits >> 52) & 0x7ff);
+  const uint64_t mant = (bits & 0xFFFFFFFFFFFFFull) | (e ? (1ull << 52) : 0ull);
+  const int s = (e ? e : 1) - 989 - e_col;
+  uint64_t lo = 0, hi = 0;
+  if (s >= 0) {
+    lo = mant << s;
+    hi = s ? (mant >> (64 - s)) : 0ull;
+  } else if (s > -64) {
+    lo = mant >> (-s);
+  }
+  const uint64_t olo = 0x8080808080808080ull, ohi = 0x808080ull;
+  uint64_t rlo, rhi;
+  if ((int64_t)bits >= 0) {
+    rlo = olo + lo;
+    rhi = ohi + hi + (rlo < lo ? 1ull : 0ull);
+  } else {
+    rlo = olo - lo;
+    rhi = ohi - hi - (olo < lo ? 1ull : 0ull);
+  }
+  w[0] = (uint32_t)rlo;
+  w[1] = (uint32_t)(rlo >> 32);
+  w[2] = (uint32_t)rhi;
+}
+
+int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const int* scb, int nblocks,
+                       const int* bsb, int span_cap, double* out_hi, double* out_lo) {
+  if (m < 1 || n < 1 || nsplit < 1 || nblocks < 1 || nblocks > 16) return ST_INVALID;
+  int* E = (int*)malloc(sizeof(int) * (size_t)(nsplit * n));
+  for (int s = 0; s < nsplit; ++s) {
+    const int64_t r0 = (int64_t)scb[s] * 32;
+    int64_t r1 = (int64_t)scb[s + 1] * 32;
+    if (r1 > m) r1 = m;
+    for (int64_t c = 0; c < n; ++c) {
+      double mx = 0.0;
+      int bad = 0;
+      for (int64_t r = r0; r < r1; ++r) {
+        const double v = fabs(a[c * m + r]);
+        if (!(v <= DBL_MAX)) bad = 1;
+        mx = fmax(mx, v);
+      }
+      int e = 0;
+      if (mx > 0.0) frexp(mx, &e);
+      E[s * n + c] = bad ? OZ_BAD : e;
+    }
+  }
+  int8_t* D = (int8_t*)malloc((size_t)(m * n * OZ_L));
+  int* rsplit = (int*)malloc(sizeof(int) * (size_t)m);
+  for (int s = 0; s < nsplit; ++s)
+    for (int64_t r = (int64_t)scb[s] * 32; r < (int64_t)scb[s + 1] * 32 && r < m; ++r) rsplit[r] = s;
+  for (int64_t r = 0; r < m; ++r)
+    for (int64_t c = 0; c < n; ++c) {
+      const int e = E[rsplit[r] * n + c];
+      uint32_t w[3];
+      oz_fixed88(e == OZ_BAD ? 0.0 : a[c * m + r], e, w);
+      for (int p = 1; p <= OZ_L; ++p) {
+        const int b = OZ_L - p;
+        D[(r * n + c) * OZ_L + p - 1] = (int8_t)(((w[b >> 2] >> (8 * (b & 3))) & 0xffu) ^ 0x80u);
+      }
+    }
+  const int64_t nslot = (int64_t)nsplit * OZ_G;
+  dd* part = (dd*)calloc((size_t)(nslot * n * n), sizeof(dd));
+  for (int s = 0; s < nsplit; ++s)
+    for (int g = 0; g < OZ_G; ++g) {
+      const int whi = 12 - 2 * g, wlo = g == 5 ? 0 : whi - 1;
+      const int maxpairs = whi - 1 < 11 ? whi - 1 : (23 - whi < 11 ? 23 - whi : 11);
+      int span = 1;
+      while (span * 2 * 32 * maxpairs <= (1 << 17)) span *= 2;
+      if (span > span_cap) span = span_cap;
+      const int64_t c0 = scb[s], c1 = scb[s + 1];
+      dd* P = part + ((int64_t)s * OZ_G + g) * n * n;
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = i; j < n; ++j) {
+          dd run = {0.0, 0.0};
+          const int ei = E[s * n + i], ej = E[s * n + j];
+          for (int64_t ch = c0; ch < c1; ch += span) {
+            const int64_t ce = ch + span < c1 ? ch + span : c1;
+            int64_t ahi = 0, alo = 0;
+            for (int64_t r = ch * 32; r < ce * 32 && r < m; ++r) {
+              const int8_t* di = D + (r * n + i) * OZ_L - 1; /* di[p], p = 1..11 */
+              const int8_t* dj = D + (r * n + j) * OZ_L - 1;
+              for (int p = 1; p <= OZ_L; ++p) {
+                const int qh = whi - p, ql = wlo - p;
+                if (qh >= 1 && qh <= OZ_L) ahi += (int64_t)di[p] * dj[qh];
+                if (wlo && ql >= 1 && ql <= OZ_L) alo += (int64_t)di[p] * dj[ql];
+              }
+            }
+            const int64_t v = alo * 256 + ahi;
+            const double h = (double)v;
+            const double l = (double)(v - (int64_t)h);
+            dd t;
+            if (ei == OZ_BAD || ej == OZ_BAD) {
+              t.hi = NAN;
+              t.lo = 0.0;
+            } else {
+              const int sc = ei + ej + 4 - 8 * whi;
+              t.hi = scalbn(h, sc);
+              t.lo = scalbn(l, sc);
+            }
+            run = ch == c0 ? t : dd_add(run, t);
+          }
+          P[i * n + j] = run;
+        }
+    }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i; j < n; ++j) {
+      dd slot[16];
+      for (int b = 0; b < nblocks; ++b) {
+        dd acc = {0.0, 0.0};
+        for (int64_t k = (int64_t)bsb[b] * OZ_G; k < (int64_t)bsb[b + 1] * OZ_G; ++k) acc = dd_add(acc, part[k * n * n + i * n + j]);
+        slot[b] = acc;
+      }
+      for (int width = 1; width < nblocks; width *= 2)
+        for (int b = 0; b + width < nblocks; b += 2 * width) slot[b] = dd_add(slot[b], slot[b + width]);
+      out_hi[j * n + i] = out_hi[i * n + j] = slot[0].hi;
+      out_lo[j * n + i] = out_lo[i * n + j] = slot[0].lo;
+    }
+  free(part);
+  free(D);
+  free(rsplit);
+  free(E);
+  return ST_OK;
+}
+
 static void finish_dd(const dd* A, const dd* V, int64_t n, double* lam_hi, double* lam_lo,
                       double* vhi, double* vlo) {
   /* sort keys: dd values compared lexicographically (hi, lo); stable. */

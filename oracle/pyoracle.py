@@ -389,6 +389,23 @@ class Port:
             raise OracleError(st)
         return hi, lo
 
+    def gram_dd_ozaki(self, a, scb, bsb, span_cap=1 << 20):
+        """K2z's double-double Gram (csrc/gram_ozaki.cu) on the split schedule
+        scb (chunks) / bsb (logical blocks), bit for bit."""
+        a = _fcol(a, np.float64)
+        m, n = a.shape
+        scb = np.ascontiguousarray(scb, dtype=np.int32)
+        bsb = np.ascontiguousarray(bsb, dtype=np.int32)
+        hi = np.zeros((n, n), order="F")
+        lo = np.zeros((n, n), order="F")
+        P = C.POINTER(C.c_int)
+        st = self.lib.port_gram_dd_ozaki(_d(a), _i64(m), _i64(n), C.c_int(len(scb) - 1), scb.ctypes.data_as(P),
+                                         C.c_int(len(bsb) - 1), bsb.ctypes.data_as(P), C.c_int(span_cap), _d(hi),
+                                         _d(lo))
+        if st:
+            raise OracleError(st)
+        return hi, lo
+
     def twosided_jacobi_dd(self, mhi, mlo=None, tol=0.0, max_sweeps=30, sem=SEM_REFERENCE):
         mhi = _fcol(mhi, np.float64)
         n = mhi.shape[0]

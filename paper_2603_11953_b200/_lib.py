@@ -70,6 +70,7 @@ SIGNATURES = [
     ("mpsvd_plan_wait", C.c_int, [vp, C.POINTER(ExecInfo)]),
     ("mpsvd_plan_destroy", None, [vp]),
     ("mpsvd_stage_gram", C.c_int, [C.c_int, vp, i64, i64, dp, dp]),
+    ("mpsvd_stage_gram_schedule", C.c_int, [i64, i64, C.c_int] + [C.POINTER(C.c_int)] * 5),
     ("mpsvd_stage_jacobi", C.c_int, [C.c_int, dp, dp, i64, C.c_double, C.c_int, dp, dp, dp, dp,
                                      C.POINTER(C.c_int), C.POINTER(i64)]),
     ("mpsvd_stage_onesided", C.c_int, [C.c_int, dp, i64, C.c_double, C.c_int, dp, C.POINTER(C.c_float),

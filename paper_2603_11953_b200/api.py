@@ -366,6 +366,20 @@ def gram(a: np.ndarray):
     return hi if prec == Precision.WORKING else (hi, lo)
 
 
+def gram_schedule(m: int, n: int):
+    """The double-double Gram schedule of an m x n plan (parity tests):
+    (ozaki, scb, bsb) - split s covers 32-row chunks [scb[s], scb[s+1]),
+    logical block b holds splits [bsb[b], bsb[b+1])."""
+    cap = m // 32 + 64
+    P = C.POINTER(C.c_int)
+    scb = np.zeros(cap, np.int32)
+    bsb = np.zeros(cap, np.int32)
+    ns, nb, oz = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib.mpsvd_stage_gram_schedule(m, n, cap, C.byref(ns), C.byref(nb), scb.ctypes.data_as(P),
+                                         bsb.ctypes.data_as(P), C.byref(oz)))
+    return bool(oz.value), scb[: ns.value + 1].copy(), bsb[: nb.value + 1].copy()
+
+
 def twosided_jacobi_eig(m_hi, m_lo=None, dd: bool = False, tol: float = 0.0, max_sweeps: int | None = None):
     """Device two-sided Jacobi (jacobi.hpp:45-46); returns (lambda, V, sweeps, rotations).
 

@@ -556,6 +556,18 @@ void raise_device_status_public(const mpsvd_exec_info& info, int max_sweeps) {
 void gpu_gram_public(bool f64, const void* a, long long m, long long n, double* m_hi, double* m_lo) {
   gpu_gram(f64, a, m, n, m_hi, m_lo);
 }
+// the double-double Gram schedule of a plan (parity tests replay K2z with it)
+void gpu_gram_schedule_public(long long m, long long n, int cap, int* nsplit, int* nblocks, int* scb, int* bsb,
+                              int* ozaki) {
+  require_device();
+  engine::Plan p(m, n, true, nullptr);
+  *ozaki = p.ozaki ? 1 : 0;
+  *nsplit = (int)p.splits.size();
+  *nblocks = p.nblocks;
+  if ((int)p.splits.size() + 1 > cap || p.nblocks + 1 > cap) throw InvalidArgument("schedule: capacity too small");
+  for (size_t i = 0; i < p.scb.size(); ++i) scb[i] = p.scb[i];
+  for (size_t i = 0; i < p.block_split_begin.size(); ++i) bsb[i] = p.block_split_begin[i];
+}
 // the spectral phase of the one-sided branches on an uploaded fp64 Gram:
 // sorted working-precision sigma and V (binary32), as port_onesided_spectral
 void gpu_onesided_public(int choice, const double* m_hi, long long n, double tol, int max_sweeps, double* sigma,
@@ -897,6 +909,14 @@ mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, in
   return guarded([&] {
     require(a != nullptr && m_hi != nullptr, "null argument");
     mpsvd::gpu_gram_public(prec == MPSVD_PRECISION_HIGHER, a, m, n, m_hi, m_lo);
+  });
+}
+
+mpsvd_status mpsvd_stage_gram_schedule(int64_t m, int64_t n, int cap, int* nsplit, int* nblocks, int* scb, int* bsb,
+                                       int* ozaki) {
+  return guarded([&] {
+    require(nsplit && nblocks && scb && bsb && ozaki, "null argument");
+    mpsvd::gpu_gram_schedule_public(m, n, cap, nsplit, nblocks, scb, bsb, ozaki);
   });
 }
 

@@ -152,9 +152,19 @@ static void build_schedule(Plan& p) {
   // per k-step) and 2/SM (f32 off-diagonal tiles: 64 blocks).
   const long long max_pb = std::max(1LL, (m / p.nblocks + 31) / 32);
   int per_block = 1;
+  if (p.ozaki) {
+    // K2z: tiles x 6 weight groups x splits CTAs of unequal length (21 ... 1
+    // products per chunk); at least 4 waves so the block scheduler evens them out
+    dev::ozaki_tiles((int)n, p.oz_tiles);
+    const long long per_split = (long long)p.oz_tiles.size() * dev::ozaki_groups();
+    const long long slot_bytes = (long long)p.ntp * 64 * 64 * 16 * dev::ozaki_groups();
+    while (per_block < 64 && per_block < max_pb && per_split * p.nblocks * per_block < 4LL * p.sm_count &&
+           (long long)p.nblocks * (per_block + 1) * slot_bytes <= (1536LL << 20))
+      ++per_block;
+  }
   double best = 1e300;
   const long long tile_bytes = 64LL * 64 * 8 * (p.dd ? 2 : 1);
-  for (int pb = 1; pb <= 64 && pb <= max_pb; ++pb) {
+  for (int pb = 1; pb <= 64 && pb <= max_pb && !p.ozaki; ++pb) {
     const long long S = (long long)pb * p.nblocks;
     if (pb > 1 && S * p.ntp * tile_bytes > (512LL << 20)) break;  // partial-tile workspace cap
     double cost;
@@ -192,6 +202,13 @@ static void build_schedule(Plan& p) {
     p.block_split_begin.push_back((int)p.splits.size());
     row += len;
   }
+  if (p.ozaki) {
+    // K2z splits are whole 32-row chunks: split starts rounded down
+    const long long nch = (m + 31) / 32;
+    p.scb.resize(p.splits.size() + 1);
+    for (size_t i = 0; i < p.splits.size(); ++i) p.scb[i] = (int)(p.splits[i].x / 32);
+    p.scb[p.splits.size()] = (int)nch;
+  }
 }
 
 template <typename T>
@@ -210,6 +227,23 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   check(cudaGetDevice(&device), "cudaGetDevice");
   check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
   max_sweeps = dd ? 100 : 30;  // thinsvd.hpp kDdMaxSweeps / jacobi.hpp:31
+  if (dd && m > 0) {
+    // K2z from 4096 local rows: its error (2^-80 of ||a_i|| ||a_j||, any m)
+    // is then inside K2's Dot2 bound 4 (m u)^2; MPSVD_DD_GRAM=dot2|ozaki forces one
+    const char* g = getenv("MPSVD_DD_GRAM");
+    const std::string gs = g ? g : "";
+    ozaki = gs == "ozaki" || (gs != "dot2" && m >= 4096);
+    if (ozaki) {  // the digit planes (11 bytes per entry); K2 when they do not fit
+      void* ptr = nullptr;
+      if (cudaMalloc(&ptr, dev::ozaki_digit_bytes(m, (int)n)) == cudaSuccess) {
+        d_digits = static_cast<unsigned char*>(ptr);
+        owned.push_back(ptr);
+      } else {
+        cudaGetLastError();
+        ozaki = false;
+      }
+    }
+  }
   build_schedule(*this);
   const size_t nn = (size_t)n * n;
   const size_t esz = dd ? 2 : 1;  // doubles per element of the higher precision
@@ -228,7 +262,20 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   check(cudaMemcpy(d_bsb, block_split_begin.data(), block_split_begin.size() * sizeof(int),
                    cudaMemcpyHostToDevice),
         "H2D bsb");
-  d_partials = dalloc<double>(splits.size() * tiles.size() * 64 * 64 * esz, owned);
+  const size_t slots = splits.size() * (ozaki ? dev::ozaki_groups() : 1);
+  d_partials = dalloc<double>(slots * tiles.size() * 64 * 64 * esz, owned);
+  if (ozaki) {
+    d_oz_tiles = dalloc<int2>(oz_tiles.size(), owned);
+    check(cudaMemcpy(d_oz_tiles, oz_tiles.data(), oz_tiles.size() * sizeof(int2), cudaMemcpyHostToDevice),
+          "H2D ozaki tiles");
+    d_scb = dalloc<int>(scb.size(), owned);
+    check(cudaMemcpy(d_scb, scb.data(), scb.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D scb");
+    std::vector<int> b6(block_split_begin.size());
+    for (size_t i = 0; i < b6.size(); ++i) b6[i] = block_split_begin[i] * dev::ozaki_groups();
+    d_bsb_oz = dalloc<int>(b6.size(), owned);
+    check(cudaMemcpy(d_bsb_oz, b6.data(), b6.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D bsb");
+    d_oz_e = dalloc<int>(splits.size() * (size_t)n, owned);
+  }
   d_bsums = dalloc<double>((size_t)(nblocks > 0 ? nblocks : 1) * tiles.size() * 64 * 64 * esz, owned);
   d_m = dalloc<double>(nn * esz, owned);
   const int nranks = comm ? comm->nranks : 1;
@@ -368,13 +415,11 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
   if (nblocks == 0) {
     check(cudaMemsetAsync(target, 0, (size_t)n * n * sizeof(double) * (dd ? 2 : 1), st), "memset M");
   } else if (dd) {
-    check(dev::launch_gram_dd((const double*)d_a, lda, (int)n, d_tiles, ntp, d_splits, (int)splits.size(),
-                              (double2*)d_partials, st),
-          "gram_dd");
-    check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, d_bsb, nblocks,
+    gram_dd_splits(d_a, lda, 0, (int)splits.size(), st);
+    check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, ozaki ? d_bsb_oz : d_bsb, nblocks,
                                       (double2*)d_bsums, (double2*)target, st),
           "gram_combine_dd");
-    launches += 3;
+    launches += 2;
   } else {
     check(dev::launch_gram_f32((const float*)d_a, lda, (int)n, d_tiles, ntp, d_tp_order, ndiag,
                                d_tp_order + ndiag, ntp - ndiag, d_splits, (int)splits.size(), (double*)d_partials,
@@ -402,6 +447,21 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
       check(dev::launch_block_tree(d_gather, comm->nranks, (int)n, d_m, true, st), "rank combine");
       launches += 1;
     }
+  }
+}
+
+void Plan::gram_dd_splits(const void* d_a, long long lda, int sb, int cnt, cudaStream_t st) {
+  if (ozaki) {
+    check(dev::launch_gram_ozaki((const double*)d_a, lda, m, (int)n, d_scb, scb.data(), (int)splits.size(), sb, cnt,
+                                 d_oz_tiles, (int)oz_tiles.size(), d_oz_e, d_digits, (double2*)d_partials, ntp,
+                                 sm_count, st),
+          "gram_ozaki");
+    launches += 3;
+  } else {
+    check(dev::launch_gram_dd((const double*)d_a, lda, (int)n, d_tiles, ntp, d_splits + sb, cnt,
+                              (double2*)d_partials + (size_t)sb * ntp * 64 * 64, st),
+          "gram_dd");
+    launches += 1;
   }
 }
 
@@ -566,10 +626,7 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
       check(cudaStreamWaitEvent(st, cev[b], 0), "wait");
       const int sb = block_split_begin[b], cnt = block_split_begin[b + 1] - sb;
       if (dd) {
-        check(dev::launch_gram_dd((const double*)d_a, m, (int)n, d_tiles, ntp, d_splits + sb, cnt,
-                                  (double2*)d_partials + (size_t)sb * ntp * 64 * 64, st),
-              "gram_dd");
-        launches += 1;
+        gram_dd_splits(d_a, m, sb, cnt, st);
       } else {
         check(dev::launch_gram_f32((const float*)d_a, m, (int)n, d_tiles, ntp, d_tp_order, ndiag, d_tp_order + ndiag,
                                    ntp - ndiag, d_splits + sb, cnt, d_partials + (size_t)sb * ntp * 64 * 64, st),
@@ -580,8 +637,8 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
     }
   }
   if (dd)
-    check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, d_bsb, nblocks, (double2*)d_bsums,
-                                      (double2*)d_m, st),
+    check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, ozaki ? d_bsb_oz : d_bsb, nblocks,
+                                      (double2*)d_bsums, (double2*)d_m, st),
           "gram_combine_dd");
   else
     check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks, (double*)d_bsums,

@@ -48,6 +48,8 @@ class Plan {
 
   // stages (used by execute and by the stage-level entry points)
   void gram(const void* d_a, long long lda, cudaStream_t st);
+  // double-double Gram kernels of splits [sb, sb + cnt) (K2z Ozaki or K2 Dot2)
+  void gram_dd_splits(const void* d_a, long long lda, int sb, int cnt, cudaStream_t st);
   void eigen(cudaStream_t st);
   // mixed-precision Cholesky QR (thinsvd.cpp:125-154): Gram (K1), chol (K8),
   // row solves (K10). Q: m x n binary32 (ldq), R: the plan's d_x32 (n x n)
@@ -71,6 +73,15 @@ class Plan {
   std::vector<longlong2> splits;
   std::vector<int> block_split_begin;
   int ntp = 0, nblocks = 0;
+  // K2z (double-double Gram on the int8 tensor cores); MPSVD_DD_GRAM=dot2 selects K2
+  bool ozaki = false;
+  std::vector<int2> oz_tiles;
+  std::vector<int> scb;  // split s = 32-row chunks [scb[s], scb[s + 1])
+  int2* d_oz_tiles = nullptr;
+  int* d_scb = nullptr;
+  int* d_bsb_oz = nullptr;  // block_split_begin x ozaki_groups()
+  int* d_oz_e = nullptr;    // column exponents per split
+  unsigned char* d_digits = nullptr;
 
   int2* d_tiles = nullptr;
   int* d_tp_order = nullptr;

@@ -1,0 +1,536 @@
+// K2z: the double-double Gram M = A^T A of a binary64 A on the int8 tensor
+// cores (Ozaki scheme), replacing K2's Dot2 loop on the fp64 pipe.
+//
+// Reference semantics: dd_gram (proj/tests/support/dd.cpp:75-88) - exact
+// products, double-double accumulation - on the row-block plan of
+// partitioned_gram (proj/src/parallel_gram.cpp:20-112). The result is not
+// bit-identical to Dot2; it carries a normwise error far below the Dot2
+// bound the tests hold K2 to (tests/test_ozaki.py).
+//
+// 1. ozaki_colexp: per row split s and column c, E[s][c] = the exponent with
+//    max |a_kc| < 2^E over the split's rows (frexp of the column maximum).
+// 2. ozaki_slice: every entry becomes the 88-bit fixed-point integer
+//    X = trunc(x * 2^(86 - E)) (|X| < 2^86), written as 11 signed 8-bit
+//    digits X = sum_p d_p 2^(8 (11 - p)), d_p in [-128, 127]: the bytes of
+//    X + 0x80...80 (11 bytes), each XOR 0x80 (balanced digits, carries
+//    resolved by the addition). Digit planes are stored as UMMA operand
+//    images: [32-row chunk][digit][128-column block] x 4 KB, K-major,
+//    no swizzle (8x16-byte core matrices; K neighbours 128 B apart, 8-row
+//    groups 256 B apart), so the Gram kernel moves them with plain bulk copies.
+// 3. gram_dd_ozaki: for a 128 x 256 output tile, sum_k x_ki x_kj =
+//    2^(E_i + E_j - 172) sum_{p,q} 2^(8 (22 - p - q)) sum_k d_p(x_ki) d_q(x_kj).
+//    The digit products with p + q = w <= 12 are kept (dropped terms are
+//    below 2^-82 of |x_ki x_kj| per row); every product is an exact int8 MMA
+//    (tcgen05.mma kind::i8, M = 128, N = 256, K = 32) into an int32 TMEM
+//    accumulator per weight w. TMEM holds two 128 x 256 accumulators, so the
+//    weights are dealt to six CTAs per tile: {12,11} {10,9} {8,7} {6,5}
+//    {4,3} {2}. Accumulators stay exact (|d_p d_q| <= 2^14, at most 11
+//    products per weight and chunk, spans of <= 2^17 / 11 rows) and are
+//    drained every span into the CTA's double-double partial tile:
+//    V = acc_wlo * 2^8 + acc_whi (exact in int64), (hi, lo) = (fl(V), V - fl(V)),
+//    scaled by 2^(E_i + E_j + 4 - 8 w_hi) and added with dd_add.
+//    Partials use K2's layout ([slot][64x64 tile pair][64x64] double2,
+//    slot = split * 6 + group), so the combine, the reference tree and the
+//    multi-GPU exchange are K2's.
+//
+// Measured on B200 (tools/microbench/umma_i8.cu): one kind::i8 MMA issues
+// every ~152 cycles for any N <= 256 (s8 x s8), so N = 256 runs at 83% of
+// the nominal 4.5 POPS and N = 128 at half of that.
+#include <cfloat>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mpsvd {
+namespace dev {
+namespace oz {
+
+constexpr int kL = 11;                 // digits per entry
+constexpr int kKC = 32;                // rows per chunk = UMMA K (int8)
+constexpr int kCB = 128;               // columns per digit block = UMMA M
+constexpr int kPlane = kCB * kKC;      // 4096 bytes
+constexpr int kGroups = 6;
+constexpr int kBad = 1 << 20;          // E sentinel: the column holds inf/NaN
+constexpr int kAS = 16, kBS = 16;      // A (4 KB) and B (8 KB) plane ring slots
+constexpr int kThreads = 192;          // warp 0 loader, warp 1 MMA, warps 2-5 drain
+constexpr int kMaxProd = 21;
+
+// weights {w_hi, w_lo} per group (w_lo = 0: a single weight)
+__host__ __device__ __forceinline__ void group_weights(int g, int& whi, int& wlo) {
+  whi = 12 - 2 * g;
+  wlo = g == 5 ? 0 : whi - 1;
+}
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(saddr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint64_t kdesc(uint32_t addr) {  // K-major, no swizzle, LBO 128, SBO 256
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(saddr(bar))
+               : "memory");
+}
+
+// X + 0x80..80 (11 bytes) as three words (bits 0-31, 32-63, 64-87) for
+// X = sign(x) trunc(|x| 2^(86 - E)); requires |x| < 2^E.
+__device__ __forceinline__ void fixed88(double x, int e_col, uint32_t& w0, uint32_t& w1, uint32_t& w2) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int e = (int)((bits >> 52) & 0x7ff);
+  const unsigned long long mant = (bits & 0xFFFFFFFFFFFFFull) | (e ? (1ull << 52) : 0ull);
+  const int s = (e ? e : 1) - 989 - e_col;  // |x| = mant 2^(e - 1075); X = mant 2^s, s <= 33
+  unsigned long long lo = 0, hi = 0;
+  if (s >= 0) {
+    lo = mant << s;
+    hi = s ? (mant >> (64 - s)) : 0ull;
+  } else if (s > -64) {
+    lo = mant >> (-s);
+  }
+  const unsigned long long olo = 0x8080808080808080ull, ohi = 0x808080ull;
+  unsigned long long rlo, rhi;
+  if ((long long)bits >= 0) {
+    rlo = olo + lo;
+    rhi = ohi + hi + (rlo < lo ? 1ull : 0ull);
+  } else {
+    rlo = olo - lo;
+    rhi = ohi - hi - (olo < lo ? 1ull : 0ull);
+  }
+  w0 = (uint32_t)rlo;
+  w1 = (uint32_t)(rlo >> 32);
+  w2 = (uint32_t)rhi;
+}
+
+}  // namespace oz
+
+// ---------------------------------------------------------------------------
+// 1. column exponents per split: one warp per (split, column)
+__global__ void __launch_bounds__(256)
+ozaki_colexp(const double* __restrict__ a, long long lda, long long m, int n, const int* __restrict__ scb, int s0,
+             int* __restrict__ e_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + warp, s = s0 + blockIdx.y;
+  if (c >= n) return;
+  const long long r0 = (long long)scb[s] * oz::kKC;
+  long long r1 = (long long)scb[s + 1] * oz::kKC;
+  if (r1 > m) r1 = m;
+  const double* col = a + (long long)c * lda;
+  double mx = 0.0;
+  bool bad = false;
+  for (long long r = r0 + lane; r < r1; r += 128) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (r + 32 * u < r1) ? fabs(__ldg(col + r + 32 * u)) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bad |= !(v[u] <= DBL_MAX);
+      mx = fmax(mx, v[u]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, (int)bad, o) != 0;
+  }
+  if (lane == 0) {
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): mx < 2^e
+    e_out[(long long)s * n + c] = bad ? oz::kBad : e;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2. digit planes: one (chunk, 128-column block) unit per iteration, 256
+// threads = 128 columns x 2 row halves; A staged through shared memory with
+// coalesced column reads.
+__global__ void __launch_bounds__(256)
+ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, const int* __restrict__ e_cols,
+            const int* __restrict__ scb, int nsplit, long long ch0, long long ch1, int ncb2,
+            unsigned char* __restrict__ digits) {
+  __shared__ double st[oz::kCB * 33];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int col = tid & 127, half = tid >> 7;
+  const long long units = (ch1 - ch0) * ncb2;
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const long long ch = ch0 + u / ncb2;
+    const int cb = (int)(u % ncb2);
+    const long long r0 = ch * oz::kKC;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const int c = warp + 8 * i, gc = cb * oz::kCB + c;
+      const long long r = r0 + lane;
+      st[c * 33 + lane] = (gc < n && r < m) ? __ldg(a + (long long)gc * lda + r) : 0.0;
+    }
+    // split of this chunk: last s with scb[s] <= ch
+    int lo = 0, hi = nsplit - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (scb[mid] <= ch) lo = mid;
+      else hi = mid - 1;
+    }
+    const int gc = cb * oz::kCB + col;
+    const int e_col = gc < n ? e_cols[(long long)lo * n + gc] : 0;
+    __syncthreads();
+    uint32_t w[16][3];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double x = st[col * 33 + 16 * half + r];
+      if (e_col == oz::kBad) x = 0.0;
+      oz::fixed88(x, e_col, w[r][0], w[r][1], w[r][2]);
+    }
+    unsigned char* base = digits + ((ch * oz::kL) * ncb2 + cb) * (long long)oz::kPlane + (col >> 3) * 256 +
+                          half * 128 + (col & 7) * 16;
+#pragma unroll
+    for (int p = 1; p <= oz::kL; ++p) {
+      const int b = oz::kL - p, wd = b >> 2, bb = b & 3;  // byte b of X' = digit p
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t t01 = __byte_perm(w[4 * j][wd], w[4 * j + 1][wd], bb | ((4 + bb) << 4));
+        const uint32_t t23 = __byte_perm(w[4 * j + 2][wd], w[4 * j + 3][wd], bb | ((4 + bb) << 4));
+        o[j] = __byte_perm(t01, t23, 0x5410) ^ 0x80808080u;
+      }
+      *reinterpret_cast<uint4*>(base + (long long)(p - 1) * ncb2 * oz::kPlane) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. the Gram tiles. grid = (tiles x 6 groups, splits). Per CTA:
+//   warp 0 (one thread): streams digit planes in the order the MMAs use
+//     them into two rings: A planes (block I, 4 KB) and B planes (block J,
+//     two adjacent 128-column blocks, 8 KB);
+//   warp 1 (one thread): TMEM allocation, the product list, MMA issue; every
+//     plane is released (tcgen05.commit -> its empty barrier) right after
+//     its last product, so the next chunk streams in behind the current one;
+//   warps 2-5: drain (thread = tile row, tcgen05.ld 32x32b) into the
+//     double-double partial tile.
+struct OzProduct {
+  signed char p, q, acc, flags;  // flags: 1 A first use, 2 A last use, 4 B first, 8 B last
+};
+
+__global__ void __launch_bounds__(oz::kThreads, 1)
+gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
+              const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
+              double2* __restrict__ partials, int span_cap) {
+  using namespace oz;
+  extern __shared__ __align__(1024) unsigned char smem_oz[];
+  unsigned char* aring = smem_oz;
+  unsigned char* bring = aring + kAS * kPlane;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kBS * 2 * kPlane);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kAS;
+  uint64_t* b_full = a_empty + kAS;
+  uint64_t* b_empty = b_full + kBS;
+  uint64_t* acc_full = b_empty + kBS;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  int* ej = reinterpret_cast<int*>(tmem_slot + 4);              // 256 column exponents of block J
+  OzProduct* prods = reinterpret_cast<OzProduct*>(ej + 256);   // kMaxProd
+  int* nprod_s = reinterpret_cast<int*>(prods + kMaxProd + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x % kGroups, tile = blockIdx.x / kGroups;
+  const int s = s0 + blockIdx.y;
+  const int2 ij = tiles[tile];  // (I: 128-column block, J: 256-column block)
+  int whi, wlo;
+  group_weights(g, whi, wlo);
+  const long long c0 = scb[s], c1 = scb[s + 1];
+  // exact-accumulation span: <= 2^17 / (products per weight) rows
+  const int maxpairs = whi - 1 < 11 ? whi - 1 : (23 - whi < 11 ? 23 - whi : 11);
+  int span = 1;
+  while (span * 2 * kKC * maxpairs <= (1 << 17)) span *= 2;
+  if (span > span_cap) span = span_cap;
+  const long long nspan = (c1 - c0 + span - 1) / span;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kAS; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < kBS; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // products (p ascending, q descending): every A plane's uses are
+    // adjacent, B plane q is used at p = w_lo - q and p = w_hi - q
+    int np = 0;
+    for (int p = 1; p <= kL; ++p)
+      for (int k = 0; k < 2; ++k) {
+        const int w = k == 0 ? whi : wlo;
+        if (w == 0) continue;
+        const int q = w - p;
+        if (q < 1 || q > kL) continue;
+        OzProduct pr;
+        pr.p = (signed char)p;
+        pr.q = (signed char)q;
+        pr.acc = (signed char)(w == whi ? 1 : 0);  // acc 0: w_lo (more significant), acc 1: w_hi
+        pr.flags = 0;
+        prods[np++] = pr;
+      }
+    for (int i = 0; i < np; ++i) {
+      int fa = 1, la = 1, fb = 1, lb = 1;
+      for (int j = 0; j < np; ++j) {
+        if (prods[j].p == prods[i].p) {
+          if (j < i) fa = 0;
+          if (j > i) la = 0;
+        }
+        if (prods[j].q == prods[i].q) {
+          if (j < i) fb = 0;
+          if (j > i) lb = 0;
+        }
+      }
+      prods[i].flags = (signed char)(fa | (la << 1) | (fb << 2) | (lb << 3));
+    }
+    *nprod_s = np;
+  }
+  if (warp >= 2) {
+    for (int c = threadIdx.x - 64; c < 256; c += 128) {
+      const int gj = ij.y * 256 + c;
+      ej[c] = gj < n ? e_cols[(long long)s * n + gj] : 0;
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int np = *nprod_s;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      unsigned long long ga = 0, gb = 0;
+      for (long long ch = c0; ch < c1; ++ch) {
+        const unsigned char* chunk = digits + (ch * kL) * ncb2 * (long long)kPlane;
+        for (int i = 0; i < np; ++i) {
+          const OzProduct pr = prods[i];
+          if (pr.flags & 1) {
+            const int sl = (int)(ga % kAS);
+            mbar_wait(&a_empty[sl], (unsigned)(((ga / kAS) & 1) ^ 1));
+            mbar_expect_tx(&a_full[sl], kPlane);
+            bulk_g2s(aring + sl * kPlane, chunk + ((long long)(pr.p - 1) * ncb2 + ij.x) * kPlane, kPlane, &a_full[sl]);
+            ++ga;
+          }
+          if (pr.flags & 4) {
+            const int sl = (int)(gb % kBS);
+            mbar_wait(&b_empty[sl], (unsigned)(((gb / kBS) & 1) ^ 1));
+            mbar_expect_tx(&b_full[sl], 2 * kPlane);
+            bulk_g2s(bring + sl * 2 * kPlane, chunk + ((long long)(pr.q - 1) * ncb2 + 2 * ij.y) * kPlane,
+                     2 * kPlane, &b_full[sl]);
+            ++gb;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // D s32, A s8, B s8, both K-major, N = 256, M = 128
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      unsigned long long ga = 0, gb = 0;
+      int aslot[kL + 1], bslot[kL + 1];
+      long long ch = c0;
+      for (long long sp = 0; sp < nspan; ++sp) {
+        mbar_wait(acc_empty, (unsigned)((sp & 1) ^ 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        long long ce = ch + span;
+        if (ce > c1) ce = c1;
+        unsigned fresh = 3u;
+        for (; ch < ce; ++ch) {
+          for (int i = 0; i < np; ++i) {
+            const OzProduct pr = prods[i];
+            if (pr.flags & 1) {
+              const int sl = (int)(ga % kAS);
+              mbar_wait(&a_full[sl], (unsigned)((ga / kAS) & 1));
+              aslot[pr.p] = sl;
+              ++ga;
+            }
+            if (pr.flags & 4) {
+              const int sl = (int)(gb % kBS);
+              mbar_wait(&b_full[sl], (unsigned)((gb / kBS) & 1));
+              bslot[pr.q] = sl;
+              ++gb;
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint64_t ad = kdesc(saddr(aring + aslot[pr.p] * kPlane));
+            const uint64_t bd = kdesc(saddr(bring + bslot[pr.q] * 2 * kPlane));
+            const unsigned acc = (unsigned)pr.acc;
+            umma_i8(tmem + acc * 256u, ad, bd, idesc, (fresh >> acc) & 1u ? 0u : 1u);
+            fresh &= ~(1u << acc);
+            if (pr.flags & 2) umma_commit(&a_empty[aslot[pr.p]]);
+            if (pr.flags & 8) umma_commit(&b_empty[bslot[pr.q]]);
+          }
+        }
+        umma_commit(acc_full);
+      }
+    }
+  } else {
+    // drain: TMEM lane quarter q = warp % 4, thread = tile row
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int gi = ij.x * kCB + r;
+    const int ei = gi < n ? e_cols[(long long)s * n + gi] : 0;
+    const int ti = gi >> 6;
+    const long long slot = (long long)s * kGroups + g;
+    auto out_ptr = [&](int c) -> double2* {
+      const int gj = ij.y * 256 + c, tj = gj >> 6;
+      if (ti > tj || tj >= T64) return nullptr;
+      const int tp = ti * T64 - (ti * (ti - 1)) / 2 + (tj - ti);
+      return partials + (slot * ntp64 + tp) * 4096 + (gi & 63) * 64 + (gj & 63);
+    };
+    if (nspan == 0) {
+      for (int c = 0; c < 256; ++c) {
+        double2* o = out_ptr(c);
+        if (o) *o = make_double2(0.0, 0.0);
+      }
+    }
+    for (long long sp = 0; sp < nspan; ++sp) {
+      mbar_wait(acc_full, (unsigned)(sp & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      for (int c0 = 0; c0 < 256; c0 += 16) {
+        uint32_t v0[16], v1[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(v0[0]), "=r"(v0[1]), "=r"(v0[2]), "=r"(v0[3]), "=r"(v0[4]), "=r"(v0[5]), "=r"(v0[6]),
+              "=r"(v0[7]), "=r"(v0[8]), "=r"(v0[9]), "=r"(v0[10]), "=r"(v0[11]), "=r"(v0[12]), "=r"(v0[13]),
+              "=r"(v0[14]), "=r"(v0[15])
+            : "r"(taddr));
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+            : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]), "=r"(v1[6]),
+              "=r"(v1[7]), "=r"(v1[8]), "=r"(v1[9]), "=r"(v1[10]), "=r"(v1[11]), "=r"(v1[12]), "=r"(v1[13]),
+              "=r"(v1[14]), "=r"(v1[15])
+            : "r"(taddr + 256u));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll 4
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c = c0 + jj;
+          double2* o = out_ptr(c);
+          if (!o) continue;
+          // acc 0 = w_lo (unused for the single-weight group), acc 1 = w_hi
+          const long long vlo = wlo ? (long long)(int)v0[jj] : 0ll;
+          const long long v = vlo * 256 + (long long)(int)v1[jj];
+          const double hi = (double)v;
+          const double lo = (double)(v - (long long)hi);
+          const int e2 = ej[c];
+          dd t;
+          if (ei == kBad || e2 == kBad) {
+            t = dd_make(__longlong_as_double(0x7ff8000000000000ll), 0.0);
+          } else {
+            const int sc = ei + e2 + 4 - 8 * whi;
+            t = dd_make(scalbn(hi, sc), scalbn(lo, sc));
+          }
+          if (sp > 0) {
+            const double2 old = *o;
+            t = dd_add(dd_make(old.x, old.y), t);
+          }
+          *o = make_double2(t.hi, t.lo);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+// ---------------------------------------------------------------------------
+size_t ozaki_digit_bytes(long long m, int n) {
+  const long long nch = (m + oz::kKC - 1) / oz::kKC;
+  const long long ncb2 = ((n + 255) / 256) * 2;
+  return (size_t)nch * oz::kL * ncb2 * oz::kPlane;
+}
+int ozaki_groups() { return oz::kGroups; }
+
+void ozaki_tiles(int n, std::vector<int2>& tiles) {
+  tiles.clear();
+  const int TI = (n + 127) / 128, TJ = (n + 255) / 256;
+  for (int J = 0; J < TJ; ++J)
+    for (int I = 0; I < TI; ++I)
+      if (I * 128 <= J * 256 + 255) tiles.push_back(make_int2(I, J));
+}
+
+static size_t ozaki_smem() {
+  return (size_t)oz::kAS * oz::kPlane + (size_t)oz::kBS * 2 * oz::kPlane + 2 * (oz::kAS + oz::kBS) * 8 + 16 + 16 +
+         256 * 4 + (oz::kMaxProd + 3) * 4 + 64;
+}
+
+cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
+                              const int* scb_host, int nsplit_total, int s0, int ns, const int2* tiles, int ntiles,
+                              int* e_cols, unsigned char* digits, double2* partials, int ntp64, int sm_count,
+                              cudaStream_t st) {
+  if (ns <= 0) return cudaSuccess;
+  const int T64 = (n + 63) / 64;
+  const int ncb2 = ((n + 255) / 256) * 2;
+  // test hook: chunks per exact-accumulation span (read per launch)
+  const char* span_env = getenv("MPSVD_OZAKI_SPAN");
+  const int span_cap = span_env && atoi(span_env) > 0 ? atoi(span_env) : 1 << 20;
+  dim3 gce((n + 7) / 8, ns);
+  ozaki_colexp<<<gce, 256, 0, st>>>(a, lda, m, n, scb_dev, s0, e_cols);
+  const long long ch0 = scb_host[s0], ch1 = scb_host[s0 + ns];
+  const long long units = (ch1 - ch0) * ncb2;
+  if (units > 0) {
+    long long grid = units < (long long)sm_count * 8 ? units : (long long)sm_count * 8;
+    ozaki_slice<<<(int)grid, 256, 0, st>>>(a, lda, m, n, e_cols, scb_dev, nsplit_total, ch0, ch1, ncb2, digits);
+  }
+  static bool configured = false;
+  const size_t smem = ozaki_smem();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gram_dd_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(ntiles * oz::kGroups, ns);
+  gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
+                                                  span_cap);
+  return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace mpsvd

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <vector>
+
 namespace mpsvd {
 namespace dev {
 
@@ -25,6 +27,17 @@ cudaError_t launch_gram_combine_dd(const double2* partials, int ntp, int n, cons
                                    int nblocks, double2* sums, double2* m_out, cudaStream_t st);
 cudaError_t launch_mirror_upper(double* m, int n, cudaStream_t st);
 cudaError_t launch_block_tree(const void* blocks, int nblocks, int n, void* m_out, bool dd,
+                              cudaStream_t st);
+
+// gram_ozaki.cu: K2z, the double-double Gram on the int8 tensor cores.
+// Splits are whole 32-row chunks: split s holds chunks [scb[s], scb[s + 1]).
+// Partial slots: split * ozaki_groups() + group, K2's tile layout.
+size_t ozaki_digit_bytes(long long m, int n);
+int ozaki_groups();
+void ozaki_tiles(int n, std::vector<int2>& tiles);  // (128-column block I, 256-column block J)
+cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
+                              const int* scb_host, int nsplit_total, int s0, int ns, const int2* tiles, int ntiles,
+                              int* e_cols, unsigned char* digits, double2* partials, int ntp64, int sm_count,
                               cudaStream_t st);
 
 // jacobi.cu ------------------------------------------------------------------

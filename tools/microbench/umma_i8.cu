@@ -167,7 +167,161 @@ __global__ void rate(int N, int iters, int a_tmem, int ksteps, unsigned long lon
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
 }
 
+
+// rate with `nacc` accumulators used round-robin (128 columns apart) and
+// either the no-swizzle layout (sw = 0) or the 128-byte-swizzle K-major
+// layout (sw = 1: 8-row x 128-byte atoms, 16-byte chunks XOR row % 8, SBO
+// 1024, K advanced by 32 bytes in the start address)
+__global__ void rate2(int N, int iters, int nacc, int sw, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (M + 256) * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(M, N, 1, 1);
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int kk = it & 3, acc = it % nacc;
+      uint64_t ad, bd;
+      if (sw) {
+        ad = desc(sa(sm) + kk * 32, 16, 1024) | (2ull << 61);
+        bd = desc(sa(sm) + M * 128 + kk * 32, 16, 1024) | (2ull << 61);
+      } else {
+        ad = desc(sa(sm) + kk * 2 * 128, 128, 1024);
+        bd = desc(sa(sm) + M * 128 + kk * 2 * 128, 128, 1024);
+      }
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tm + (uint32_t)(acc * (512 / nacc))), "l"(ad), "l"(bd), "r"(id), "r"(1u));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(sa(&bar)));
+    mbar_wait(&bar, 0);
+    const unsigned long long t1 = clock64();
+    if (blockIdx.x == 0) *cyc = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
+}
+
+// swizzle-128 correctness: A [128][128] and B [N][128] int8, K = 128 (4 MMAs)
+__global__ void check_sw(const int8_t* ga, const int8_t* gb, int* gd, int N) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  unsigned char* a = sm;
+  unsigned char* b = sm + 128 * 128;
+  auto off = [](int row, int k) { return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((((k >> 4) ^ (row & 7)) << 4) | (k & 15))); };
+  for (int e = tid; e < 128 * 128; e += blockDim.x) a[off(e / 128, e % 128)] = (unsigned char)ga[e];
+  for (int e = tid; e < N * 128; e += blockDim.x) b[off(e / 128, e % 128)] = (unsigned char)gb[e];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(128, N, 1, 1);
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint64_t ad = desc(sa(a) + kk * 32, 16, 1024) | (2ull << 61);
+      const uint64_t bd = desc(sa(b) + kk * 32, 16, 1024) | (2ull << 61);
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tm), "l"(ad), "l"(bd), "r"(id), "r"((uint32_t)(kk > 0)));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(sa(&bar)));
+  }
+  mbar_wait(&bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  if (warp < 4) {
+    const int row = warp * 32 + (tid & 31);
+    for (int c0 = 0; c0 < N; c0 += 8) {
+      uint32_t r[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(tm + ((uint32_t)(warp * 32) << 16) + c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      for (int j = 0; j < 8; ++j) gd[row * N + c0 + j] = (int)r[j];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
+}
+
+int main2() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  CK(cudaFuncSetAttribute(rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  CK(cudaFuncSetAttribute(check_sw, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+  {
+    int8_t *ha = new int8_t[128 * 128], *hb = new int8_t[256 * 128];
+    int* out = new int[128 * 256];
+    for (int i = 0; i < 128 * 128; ++i) ha[i] = (int8_t)(rand() & 0xFF);
+    for (int i = 0; i < 256 * 128; ++i) hb[i] = (int8_t)(rand() & 0xFF);
+    int8_t *da, *db; int* dd;
+    CK(cudaMalloc(&da, 128 * 128)); CK(cudaMalloc(&db, 256 * 128)); CK(cudaMalloc(&dd, 128 * 256 * 4));
+    CK(cudaMemcpy(da, ha, 128 * 128, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(db, hb, 256 * 128, cudaMemcpyHostToDevice));
+    for (int N = 128; N <= 256; N += 128) {
+      check_sw<<<1, 128, 64 * 1024>>>(da, db, dd, N);
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(out, dd, 128 * N * 4, cudaMemcpyDeviceToHost));
+      long long bad = 0;
+      for (int i = 0; i < 128; ++i)
+        for (int j = 0; j < N; ++j) {
+          long long r = 0;
+          for (int k = 0; k < 128; ++k) r += (long long)ha[i * 128 + k] * hb[j * 128 + k];
+          bad += (r != out[i * N + j]);
+        }
+      printf("check_sw N=%d: mismatches %lld / %d\n", N, bad, 128 * N);
+    }
+  }
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, 8));
+  for (int sw = 0; sw < 2; ++sw)
+    for (int N = 128; N <= 256; N += 128)
+      for (int nacc = 1; nacc <= 4; nacc *= 2) {
+        if (N == 256 && nacc == 4) continue;
+        const int iters = 4096;
+        rate2<<<sms, 128, 64 * 1024>>>(N, iters, nacc, sw, dc);
+        CK(cudaDeviceSynchronize());
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        rate2<<<sms, 128, 64 * 1024>>>(N, iters, nacc, sw, dc);
+        cudaEventRecord(e1);
+        CK(cudaDeviceSynchronize());
+        float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long c = 0; CK(cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost));
+        printf("rate2 N=%3d nacc=%d %s: %.1f cycles/MMA, %.0f TOPS\n", N, nacc, sw ? "sw128" : "nosw ", (double)c / iters,
+               2.0 * M * N * 32 * (double)iters * sms / (ms * 1e-3) / 1e12);
+      }
+  return 0;
+}
+
 int main() {
+  if (getenv("PROBE2")) return main2();
   int8_t *ha = new int8_t[M * K], *hb = new int8_t[256 * K];
   int* out = new int[M * 256];
   int8_t *da, *db;
