@@ -26,6 +26,7 @@ from .api import (  # noqa: F401
     device_available,
     fp64_peak_tflops,
     gram,
+    gram_schedule,
     max_rel_sv_error,
     mp_cholesky_qr,
     mp_thin_svd,

@@ -37,6 +37,7 @@
 // every ~152 cycles for any N <= 256 (s8 x s8), so N = 256 runs at 83% of
 // the nominal 4.5 POPS and N = 128 at half of that.
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -52,9 +53,8 @@ constexpr int kCB = 128;               // columns per digit block = UMMA M
 constexpr int kPlane = kCB * kKC;      // 4096 bytes
 constexpr int kGroups = 6;
 constexpr int kBad = 1 << 20;          // E sentinel: the column holds inf/NaN
-constexpr int kAS = 16, kBS = 16;      // A (4 KB) and B (8 KB) plane ring slots
-constexpr int kThreads = 192;          // warp 0 loader, warp 1 MMA, warps 2-5 drain
-constexpr int kMaxProd = 21;
+constexpr int kRing = 16;              // step slots: A plane (4 KB) + B plane (8 KB) each
+constexpr int kThreads = 320;          // warps 0-1 loaders, 2-5 drain, 6-9 MMA issuers
 
 // weights {w_hi, w_lo} per group (w_lo = 0: a single weight)
 __host__ __device__ __forceinline__ void group_weights(int g, int& whi, int& wlo) {
@@ -100,6 +100,50 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t ad, uint64_t b
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+// zero 16 TMEM columns of this warp's lane quarter
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr),
+      "r"(0u));
+}
+// Warp-converged issue: every lane runs the issuing loop (so its values stay
+// in uniform registers) and only the leader lane's instruction is enabled.
+__device__ __forceinline__ void umma_i8_lead(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
+                                             uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred p, l;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 l, %5, 0;\n"
+      "@l tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(lead));
+}
+__device__ __forceinline__ void umma_commit_lead(uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %1, 0;\n"
+      "@l tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(saddr(bar)),
+      "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_lead(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                              uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %4, 0;\n"
+      "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+      "@l cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar)), "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s2_lead(void* dst0, const void* src0, unsigned bytes0, void* dst1,
+                                               const void* src1, unsigned bytes1, uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %7, 0;\n"
+      "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%6], %8;\n"
+      "@l cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%6];\n"
+      "@l cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%3], [%4], %5, [%6];\n}\n" ::"r"(
+          saddr(dst0)),
+      "l"(src0), "r"(bytes0), "r"(saddr(dst1)), "l"(src1), "r"(bytes1), "r"(saddr(bar)), "r"(lead),
+      "r"(bytes0 + bytes1)
+      : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(saddr(bar))
@@ -239,29 +283,28 @@ ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, con
 //     its last product, so the next chunk streams in behind the current one;
 //   warps 2-5: drain (thread = tile row, tcgen05.ld 32x32b) into the
 //     double-double partial tile.
-struct OzProduct {
-  signed char p, q, acc, flags;  // flags: 1 A first use, 2 A last use, 4 B first, 8 B last
-};
+// MPSVD_OZAKI_PROF=1: per weight group, summed over CTAs: [0] CTAs, [1] MMA
+// thread cycles, [2] of which waiting for planes, [3] waiting for the drain,
+// [4] loader waiting for free slots, [5] drain cycles, [6] drain waiting
+__device__ unsigned long long g_oz_prof[6][8];
+
 
 __global__ void __launch_bounds__(oz::kThreads, 1)
 gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
               const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
-              double2* __restrict__ partials, int span_cap) {
+              double2* __restrict__ partials, int span_cap, int prof, int dbg) {
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
-  unsigned char* bring = aring + kAS * kPlane;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kBS * 2 * kPlane);
-  uint64_t* a_full = bars;
-  uint64_t* a_empty = a_full + kAS;
-  uint64_t* b_full = a_empty + kAS;
-  uint64_t* b_empty = b_full + kBS;
-  uint64_t* acc_full = b_empty + kBS;
+  unsigned char* bring = aring + kRing * kPlane;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kRing * 2 * kPlane);
+  uint64_t* a_full = bars;  // one full barrier per step slot (A and B plane)
+  uint64_t* a_empty = a_full + kRing;
+  uint64_t* b_empty = a_empty + kRing;
+  uint64_t* acc_full = b_empty + kRing;
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   int* ej = reinterpret_cast<int*>(tmem_slot + 4);              // 256 column exponents of block J
-  OzProduct* prods = reinterpret_cast<OzProduct*>(ej + 256);   // kMaxProd
-  int* nprod_s = reinterpret_cast<int*>(prods + kMaxProd + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x % kGroups, tile = blockIdx.x / kGroups;
@@ -276,58 +319,27 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   while (span * 2 * kKC * maxpairs <= (1 << 17)) span *= 2;
   if (span > span_cap) span = span_cap;
   const long long nspan = (c1 - c0 + span - 1) / span;
+  const int nrel = wlo ? 2 : 1;                // issuers releasing each plane
+  const int nissue = wlo ? 4 : 2;              // active issuer warps
+  const int D = whi - 1 < kL ? whi - 1 : kL;   // steps per chunk
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kAS; ++i) {
+    for (int i = 0; i < kRing; ++i) {
       mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], 1);
+      mbar_init(&a_empty[i], nrel);
+      mbar_init(&b_empty[i], nrel);
     }
-    for (int i = 0; i < kBS; ++i) {
-      mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], 1);
-    }
-    mbar_init(acc_full, 1);
+    mbar_init(acc_full, nissue);
     mbar_init(acc_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    // products (p ascending, q descending): every A plane's uses are
-    // adjacent, B plane q is used at p = w_lo - q and p = w_hi - q
-    int np = 0;
-    for (int p = 1; p <= kL; ++p)
-      for (int k = 0; k < 2; ++k) {
-        const int w = k == 0 ? whi : wlo;
-        if (w == 0) continue;
-        const int q = w - p;
-        if (q < 1 || q > kL) continue;
-        OzProduct pr;
-        pr.p = (signed char)p;
-        pr.q = (signed char)q;
-        pr.acc = (signed char)(w == whi ? 1 : 0);  // acc 0: w_lo (more significant), acc 1: w_hi
-        pr.flags = 0;
-        prods[np++] = pr;
-      }
-    for (int i = 0; i < np; ++i) {
-      int fa = 1, la = 1, fb = 1, lb = 1;
-      for (int j = 0; j < np; ++j) {
-        if (prods[j].p == prods[i].p) {
-          if (j < i) fa = 0;
-          if (j > i) la = 0;
-        }
-        if (prods[j].q == prods[i].q) {
-          if (j < i) fb = 0;
-          if (j > i) lb = 0;
-        }
-      }
-      prods[i].flags = (signed char)(fa | (la << 1) | (fb << 2) | (lb << 3));
-    }
-    *nprod_s = np;
   }
-  if (warp >= 2) {
+  if (warp >= 2 && warp < 6) {
     for (int c = threadIdx.x - 64; c < 256; c += 128) {
       const int gj = ij.y * 256 + c;
       ej[c] = gj < n ? e_cols[(long long)s * n + gj] : 0;
     }
   }
-  if (warp == 1) {
+  if (warp == 6) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -336,76 +348,95 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const int np = *nprod_s;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      unsigned long long ga = 0, gb = 0;
+  // Steps. Chunk step p = 1..D (global step t, ring slot t % kRing) brings
+  // A_p (digit p of block I) and B_{D+1-p} (digit D+1-p of block J) and
+  // issues two products: X: (p, D+1-p) of weight w_hi (A_p, B from slot t)
+  // and Y: (p-1, D+1-p) of weight w_lo (A_{p-1} from slot t-1, B from slot t).
+  // A_p's last users are X at step t and Y at step t+1; B's are X and Y at
+  // step t. Loaders and issuers are split by the parity of t (two loader
+  // warps; issuer warps X0, X1, Y0, Y1), so per-MMA issue latency overlaps;
+  // the integer accumulation makes MMA order irrelevant (accumulators are
+  // zeroed by the drain warps, every MMA accumulates).
+  if (warp < 2) {
+    // loader of the steps with t % 2 == warp
+    if (!(dbg & 1)) {
+      const uint32_t lead = lane == 0;
+      const unsigned par = (unsigned)warp;
+      unsigned t = 0;
+      unsigned long long tw = 0;
       for (long long ch = c0; ch < c1; ++ch) {
         const unsigned char* chunk = digits + (ch * kL) * ncb2 * (long long)kPlane;
-        for (int i = 0; i < np; ++i) {
-          const OzProduct pr = prods[i];
-          if (pr.flags & 1) {
-            const int sl = (int)(ga % kAS);
-            mbar_wait(&a_empty[sl], (unsigned)(((ga / kAS) & 1) ^ 1));
-            mbar_expect_tx(&a_full[sl], kPlane);
-            bulk_g2s(aring + sl * kPlane, chunk + ((long long)(pr.p - 1) * ncb2 + ij.x) * kPlane, kPlane, &a_full[sl]);
-            ++ga;
-          }
-          if (pr.flags & 4) {
-            const int sl = (int)(gb % kBS);
-            mbar_wait(&b_empty[sl], (unsigned)(((gb / kBS) & 1) ^ 1));
-            mbar_expect_tx(&b_full[sl], 2 * kPlane);
-            bulk_g2s(bring + sl * 2 * kPlane, chunk + ((long long)(pr.q - 1) * ncb2 + 2 * ij.y) * kPlane,
-                     2 * kPlane, &b_full[sl]);
-            ++gb;
-          }
+        for (int p = 1; p <= D; ++p, ++t) {
+          if ((t & 1u) != par) continue;
+          const int sl = (int)(t % kRing);
+          const unsigned ph = ((t / kRing) & 1u) ^ 1u;
+          const unsigned long long t0 = prof ? clock64() : 0;
+          mbar_wait(&a_empty[sl], ph);
+          mbar_wait(&b_empty[sl], ph);
+          if (prof) tw += clock64() - t0;
+          bulk_g2s2_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
+                         bring + (size_t)sl * 2 * kPlane,
+                         chunk + ((long long)(D - p) * ncb2 + 2 * ij.y) * kPlane, 2 * kPlane, &a_full[sl], lead);
         }
       }
+      if (prof && lead && warp == 0) atomicAdd(&g_oz_prof[g][4], tw);
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
+  } else if (warp >= 6) {
+    // issuers: warp 6 X0, 7 X1, 8 Y0, 9 Y1
+    const int role = (warp - 6) >> 1;          // 0: X (w_hi), 1: Y (w_lo)
+    const unsigned par = (unsigned)((warp - 6) & 1);
+    if (role == 0 || wlo) {
+      const uint32_t lead = lane == 0;
       // D s32, A s8, B s8, both K-major, N = 256, M = 128
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
-      unsigned long long ga = 0, gb = 0;
-      int aslot[kL + 1], bslot[kL + 1];
+      const uint32_t abase = saddr(aring), bbase = saddr(bring);
+      const uint32_t dacc = tmem + (role == 0 ? 256u : 0u);  // acc 0: w_lo (more significant), acc 1: w_hi
+      unsigned t = 0;
+      unsigned long long tacc = 0;
+      const unsigned long long tstart = prof ? clock64() : 0;
       long long ch = c0;
       for (long long sp = 0; sp < nspan; ++sp) {
-        mbar_wait(acc_empty, (unsigned)((sp & 1) ^ 1));
+        const unsigned long long t0 = prof ? clock64() : 0;
+        mbar_wait(acc_empty, (unsigned)(sp & 1));
+        if (prof) tacc += clock64() - t0;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         long long ce = ch + span;
         if (ce > c1) ce = c1;
-        unsigned fresh = 3u;
         for (; ch < ce; ++ch) {
-          for (int i = 0; i < np; ++i) {
-            const OzProduct pr = prods[i];
-            if (pr.flags & 1) {
-              const int sl = (int)(ga % kAS);
-              mbar_wait(&a_full[sl], (unsigned)((ga / kAS) & 1));
-              aslot[pr.p] = sl;
-              ++ga;
+          for (int p = 1; p <= D; ++p, ++t) {
+            if ((t & 1u) != par) continue;
+            const int sl = (int)(t % kRing);
+            const int slp = (int)((t + kRing - 1) % kRing);
+            if (!(dbg & 1)) mbar_wait(&a_full[sl], (t / kRing) & 1u);
+            if (role == 0) {
+              asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+              umma_i8_lead(dacc, kdesc(abase + (uint32_t)sl * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane), idesc,
+                           1u, lead && !(dbg & 2));
+              umma_commit_lead(&a_empty[sl], lead);
+              umma_commit_lead(&b_empty[sl], lead);
+            } else {
+              if (p >= 2) {
+                if (!(dbg & 1)) mbar_wait(&a_full[slp], ((t - 1) / kRing) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                umma_i8_lead(dacc, kdesc(abase + (uint32_t)slp * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
+                             idesc, 1u, lead && !(dbg & 2));
+              }
+              if (t > 0) umma_commit_lead(&a_empty[slp], lead);  // A_{p-1} (or the previous chunk's A_D)
+              umma_commit_lead(&b_empty[sl], lead);
             }
-            if (pr.flags & 4) {
-              const int sl = (int)(gb % kBS);
-              mbar_wait(&b_full[sl], (unsigned)((gb / kBS) & 1));
-              bslot[pr.q] = sl;
-              ++gb;
-            }
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint64_t ad = kdesc(saddr(aring + aslot[pr.p] * kPlane));
-            const uint64_t bd = kdesc(saddr(bring + bslot[pr.q] * 2 * kPlane));
-            const unsigned acc = (unsigned)pr.acc;
-            umma_i8(tmem + acc * 256u, ad, bd, idesc, (fresh >> acc) & 1u ? 0u : 1u);
-            fresh &= ~(1u << acc);
-            if (pr.flags & 2) umma_commit(&a_empty[aslot[pr.p]]);
-            if (pr.flags & 8) umma_commit(&b_empty[bslot[pr.q]]);
           }
         }
-        umma_commit(acc_full);
+        umma_commit_lead(acc_full, lead);
+      }
+      if (prof && lead && warp == 6) {
+        atomicAdd(&g_oz_prof[g][0], 1ull);
+        atomicAdd(&g_oz_prof[g][1], clock64() - tstart);
+        atomicAdd(&g_oz_prof[g][3], tacc);
       }
     }
-  } else {
+  } else if (warp < 6) {
     // drain: TMEM lane quarter q = warp % 4, thread = tile row
     const int q = warp & 3;
     const int r = q * 32 + lane;
@@ -425,8 +456,18 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
         if (o) *o = make_double2(0.0, 0.0);
       }
     }
+    // accumulators start at zero; every MMA accumulates
+    for (int c = 0; c < 512; c += 16) tmem_zero16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty);
+    unsigned long long tdr = 0, tdw = 0;
     for (long long sp = 0; sp < nspan; ++sp) {
+      const unsigned long long t0 = prof ? clock64() : 0;
       mbar_wait(acc_full, (unsigned)(sp & 1));
+      const unsigned long long t1 = prof ? clock64() : 0;
+      tdw += t1 - t0;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       for (int c0 = 0; c0 < 256; c0 += 16) {
         uint32_t v0[16], v1[16];
@@ -444,10 +485,21 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
               "=r"(v1[14]), "=r"(v1[15])
             : "r"(taddr + 256u));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll 4
+        tmem_zero16(taddr);
+        tmem_zero16(taddr + 256u);
+        // the running partials of the 16 columns are loaded together (one
+        // memory latency per group, not per entry)
+        double2* op[16];
+        double2 old[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          op[jj] = out_ptr(c0 + jj);
+          old[jj] = (sp > 0 && op[jj]) ? *op[jj] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           const int c = c0 + jj;
-          double2* o = out_ptr(c);
+          double2* o = op[jj];
           if (!o) continue;
           // acc 0 = w_lo (unused for the single-weight group), acc 1 = w_hi
           const long long vlo = wlo ? (long long)(int)v0[jj] : 0ll;
@@ -462,22 +514,25 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
             const int sc = ei + e2 + 4 - 8 * whi;
             t = dd_make(scalbn(hi, sc), scalbn(lo, sc));
           }
-          if (sp > 0) {
-            const double2 old = *o;
-            t = dd_add(dd_make(old.x, old.y), t);
-          }
+          if (sp > 0) t = dd_add(dd_make(old[jj].x, old[jj].y), t);
           *o = make_double2(t.hi, t.lo);
         }
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
+      if (prof) tdr += clock64() - t1;
+    }
+    if (prof && warp == 2 && lane == 0) {
+      atomicAdd(&g_oz_prof[g][5], tdr);
+      atomicAdd(&g_oz_prof[g][6], tdw);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  if (warp == 6) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
 }
 
 // ---------------------------------------------------------------------------
@@ -497,8 +552,7 @@ void ozaki_tiles(int n, std::vector<int2>& tiles) {
 }
 
 static size_t ozaki_smem() {
-  return (size_t)oz::kAS * oz::kPlane + (size_t)oz::kBS * 2 * oz::kPlane + 2 * (oz::kAS + oz::kBS) * 8 + 16 + 16 +
-         256 * 4 + (oz::kMaxProd + 3) * 4 + 64;
+  return (size_t)oz::kRing * 3 * oz::kPlane + 3 * oz::kRing * 8 + 16 + 16 + 256 * 4 + 64;
 }
 
 cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
@@ -526,9 +580,30 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  const char* prof_env = getenv("MPSVD_OZAKI_PROF");
+  const int prof = prof_env && prof_env[0] == '1';
+  const char* dbg_env = getenv("MPSVD_OZAKI_DBG");  // bit 0: no plane loads, bit 1: no MMAs (timing probes)
+  const int dbg = dbg_env ? atoi(dbg_env) : 0;
+  if (prof) {
+    unsigned long long z[48] = {};
+    cudaMemcpyToSymbolAsync(g_oz_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+  }
   dim3 grid(ntiles * oz::kGroups, ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
-                                                  span_cap);
+                                                  span_cap, prof, dbg);
+  if (prof) {
+    unsigned long long h[48];
+    cudaMemcpyFromSymbolAsync(h, g_oz_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    for (int g = 0; g < oz::kGroups; ++g) {
+      const double c = h[g * 8] ? (double)h[g * 8] : 1.0;
+      fprintf(stderr,
+              "ozaki prof g%d: CTAs %llu | per CTA (kcycles): mma %.1f (plane wait %.1f, drain wait %.1f) loader "
+              "slot wait %.1f | drain %.1f (acc wait %.1f)\n",
+              g, h[g * 8], h[g * 8 + 1] / c / 1e3, h[g * 8 + 2] / c / 1e3, h[g * 8 + 3] / c / 1e3, h[g * 8 + 4] / c / 1e3,
+              h[g * 8 + 5] / c / 1e3, h[g * 8 + 6] / c / 1e3);
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -320,7 +320,220 @@ int main2() {
   return 0;
 }
 
+// issue-loop overheads: mode bit 0: tcgen05.commit to an mbarrier after every
+// MMA; bit 1: tcgen05.fence::after_thread_sync before every MMA; bit 2: an
+// mbarrier try_wait (already complete) before every MMA; bit 3: A and B at a
+// different 4 KB / 8 KB slot every MMA (16 slots)
+__global__ void rate3(int iters, int mode, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar, bar2, done_bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (16 * 4096 + 8 * 8192) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&bar2)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&done_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(128, 256, 1, 1);
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (mode & 4) mbar_wait(&bar2, 1);  // parity 1 of a fresh barrier: complete
+      if (mode & 2) asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int sl = (mode & 8) ? (it & 7) : 0;
+      const uint64_t ad = desc(sa(sm) + sl * 4096 + (it & 1) * 256, 128, 256);
+      const uint64_t bd = desc(sa(sm) + 16 * 4096 + sl * 8192, 128, 256);
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tm + (uint32_t)((it & 1) * 256)), "l"(ad), "l"(bd), "r"(id), "r"(1u));
+      if (mode & 1) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(sa(&bar)));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(sa(&done_bar)));
+    mbar_wait(&done_bar, 0);
+    const unsigned long long t1 = clock64();
+    if (blockIdx.x == 0) *cyc = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
+}
+int main3() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  CK(cudaFuncSetAttribute(rate3, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, 8));
+  const int modes[8] = {0, 1, 2, 4, 8, 9, 15, 3};
+  for (int mi = 0; mi < 8; ++mi) {
+    rate3<<<sms, 128, 160 * 1024>>>(2048, modes[mi], dc);
+    CK(cudaDeviceSynchronize());
+    unsigned long long c = 0;
+    CK(cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost));
+    printf("rate3 mode=%2d (commit %d fence %d wait %d slots %d): %.1f cycles/MMA\n", modes[mi], modes[mi] & 1,
+           (modes[mi] >> 1) & 1, (modes[mi] >> 2) & 1, (modes[mi] >> 3) & 1, (double)c / 2048);
+  }
+  return 0;
+}
+
+// layout sweep: (LBO, SBO) of K-major no-swizzle operands; K = 32 per MMA
+__global__ void rate4(int iters, int lbo_a, int sbo_a, int lbo_b, int sbo_b, int kstep, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t done_bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < (160 * 1024) / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t*>(sm)[i] = (kstep < 0) ? h : 0x01010101u * (i & 3);
+  }
+  if (kstep < 0) kstep = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&done_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tm = tslot;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(128, 256, 1, 1);
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int k = it & 3;
+      const uint64_t ad = desc(sa(sm) + k * kstep, lbo_a, sbo_a);
+      const uint64_t bd = desc(sa(sm) + 64 * 1024 + k * kstep, lbo_b, sbo_b);
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tm + (uint32_t)((it & 1) * 256)), "l"(ad), "l"(bd), "r"(id), "r"(1u));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(sa(&done_bar)));
+    mbar_wait(&done_bar, 0);
+    const unsigned long long t1 = clock64();
+    if (blockIdx.x == 0) *cyc = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
+}
+int main4() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  CK(cudaFuncSetAttribute(rate4, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, 8));
+  // (lbo, sbo, kstep): kstep = start offset per K-step of 32
+  const int cfg[][3] = {{128, 256, 0}, {128, 256, -1}, {128, 256, 0}, {128, 256, -1}, {128, 1024, -1}};
+  for (auto& c : cfg) {
+    // B (N = 256) with the same pattern, its group stride scaled for 32 groups where SBO spans K
+    const int lbo_b = c[0] == 2048 ? 4096 : c[0] == 4096 ? 8192 : c[0] == 256 ? 256 : c[0];
+    for (int rep = 0; rep < 3; ++rep) rate4<<<sms, 128, 160 * 1024>>>(8192, c[0], c[1], lbo_b, c[1], c[2], dc);
+    CK(cudaDeviceSynchronize());
+    unsigned long long cy = 0;
+    CK(cudaMemcpy(&cy, dc, 8, cudaMemcpyDeviceToHost));
+    printf("rate4 A lbo=%4d sbo=%4d | B lbo=%4d sbo=%4d kstep=%4d (-1: random data): %.1f cycles/MMA\n", c[0], c[1], lbo_b, c[1], c[2],
+           (double)cy / 8192);
+  }
+  return 0;
+}
+
+// warp-converged issue loop (all 32 lanes run it, lane 0's MMA enabled):
+// mode bit 0: wait on a (complete) mbarrier per MMA, bit 1: the wait loop exits
+// on __all_sync, bit 2: tcgen05.commit per MMA, bit 3: ring slot per MMA (16)
+__global__ void rate5(int iters, int mode, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar[16], done_bar, cbar;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < (192 * 1024) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(sa(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 16; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&bar[i])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&done_bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sa(&cbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tm = tslot;
+  if (warp == 0) {
+    const uint32_t lead = lane == 0;
+    const uint32_t id = idesc_i8(128, 256, 1, 1);
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int sl = (mode & 8) ? (it & 15) : 0;
+      if (mode & 1) {
+        uint32_t done = 0;
+        if (mode & 2) {
+          do {
+            asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(done) : "r"(sa(&bar[sl])), "r"(1u) : "memory");
+          } while (!__all_sync(0xffffffffu, done));
+        } else {
+          mbar_wait(&bar[sl], 1);
+        }
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint64_t ad = desc(sa(sm) + sl * 4096, 128, 256);
+      const uint64_t bd = desc(sa(sm) + 64 * 1024 + sl * 8192, 128, 256);
+      asm volatile("{\n.reg .pred p, l;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 l, %5, 0;\n@l tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tm + (uint32_t)((it & 1) * 256)), "l"(ad), "l"(bd), "r"(id), "r"(1u), "r"(lead));
+      if (mode & 4)
+        asm volatile("{\n.reg .pred l;\nsetp.ne.b32 l, %1, 0;\n@l tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(sa(&cbar)), "r"(lead) : "memory");
+    }
+    if (lead) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(sa(&done_bar)));
+      mbar_wait(&done_bar, 0);
+      const unsigned long long t1 = clock64();
+      if (blockIdx.x == 0) *cyc = t1 - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
+}
+int main5() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  CK(cudaFuncSetAttribute(rate5, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024));
+  unsigned long long* dc;
+  CK(cudaMalloc(&dc, 8));
+  const int modes[] = {0, 8, 1, 9, 3, 11, 4, 12, 13, 15};
+  for (int md : modes) {
+    for (int rep = 0; rep < 2; ++rep) rate5<<<sms, 128, 192 * 1024>>>(4096, md, dc);
+    CK(cudaDeviceSynchronize());
+    unsigned long long c = 0;
+    CK(cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost));
+    printf("rate5 mode=%2d (wait %d all_sync %d commit %d slots %d): %.1f cycles/MMA\n", md, md & 1, (md >> 1) & 1,
+           (md >> 2) & 1, (md >> 3) & 1, (double)c / 4096);
+  }
+  return 0;
+}
+
 int main() {
+  if (getenv("PROBE5")) return main5();
+  if (getenv("PROBE4")) return main4();
+  if (getenv("PROBE3")) return main3();
   if (getenv("PROBE2")) return main2();
   int8_t *ha = new int8_t[M * K], *hb = new int8_t[256 * K];
   int* out = new int[M * 256];

@@ -14,7 +14,7 @@ def main():
     stage = sys.argv[1]
     cfg = inputs.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c2"]
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-    m = min(cfg.m, 1 << 16)
+    m = min(cfg.m, int(os.environ.get("PROF_M", 1 << 16)))
     a = inputs.make(cfg, seed=1, m=m)
     if stage == "jacobi":
         if cfg.working == "f32":
