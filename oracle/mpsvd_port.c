@@ -1065,12 +1065,28 @@ int port_dd_gram(const double* a, int64_t m, int64_t n, int threads, double* hi,
  * exact-accumulation span, their conversion to double-double
  * (V = acc_wlo 2^8 + acc_whi; (fl(V), V - fl(V)) scaled by
  * 2^(E_i + E_j + 4 - 8 w_hi)), the running dd_add per partial slot
- * (split * 6 + group), then the engine's combine: slots of a logical block
+ * (split * 12 + sub-group), then the engine's combine: slots of a logical block
  * summed in order from zero, blocks along the reference tree
  * (parallel_gram.cpp:93-102). Semantics follow dd_gram (dd.cpp:75-88) up to
  * the digit truncation. */
 #define OZ_L 11
-#define OZ_G 6
+#define OZ_G 12
+/* sub-group i: weights (whi, wlo) and steps [pa, pb] (gram_ozaki.cu sub_group) */
+static void oz_sub_group(int i, int* whi, int* wlo, int* pa, int* pb) {
+  for (int k = 0; k < 6; ++k) {
+    const int h = 12 - 2 * k, d = h - 1, parts = (d + 3) / 4;
+    if (i < parts) {
+      const int base = d / parts, extra = d % parts;
+      *pa = 1 + i * base + (i < extra ? i : extra);
+      *pb = *pa + base + (i < extra ? 1 : 0) - 1;
+      *whi = h;
+      *wlo = k == 5 ? 0 : h - 1;
+      return;
+    }
+    i -= parts;
+  }
+  *whi = *wlo = *pa = *pb = 0;
+}
 #define OZ_BAD (1 << 20)
 static void oz_fixed88(double x, int e_col, uint32_t w[3]) {
   uint64_t bits;
@@ -1138,10 +1154,11 @@ int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const 
   dd* part = (dd*)calloc((size_t)(nslot * n * n), sizeof(dd));
   for (int s = 0; s < nsplit; ++s)
     for (int g = 0; g < OZ_G; ++g) {
-      const int whi = 12 - 2 * g, wlo = g == 5 ? 0 : whi - 1;
-      const int maxpairs = whi - 1 < 11 ? whi - 1 : (23 - whi < 11 ? 23 - whi : 11);
+      int whi, wlo, pa, pb;
+      oz_sub_group(g, &whi, &wlo, &pa, &pb);
+      const int maxpairs = pb - pa + 1;
       int span = 1;
-      while (span * 2 * 32 * maxpairs <= (1 << 17)) span *= 2;
+      while (span * 2 * maxpairs < 4096) span *= 2;
       if (span > span_cap) span = span_cap;
       const int64_t c0 = scb[s], c1 = scb[s + 1];
       dd* P = part + ((int64_t)s * OZ_G + g) * n * n;
@@ -1155,10 +1172,9 @@ int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const 
             for (int64_t r = ch * 32; r < ce * 32 && r < m; ++r) {
               const int8_t* di = D + (r * n + i) * OZ_L - 1; /* di[p], p = 1..11 */
               const int8_t* dj = D + (r * n + j) * OZ_L - 1;
-              for (int p = 1; p <= OZ_L; ++p) {
-                const int qh = whi - p, ql = wlo - p;
-                if (qh >= 1 && qh <= OZ_L) ahi += (int64_t)di[p] * dj[qh];
-                if (wlo && ql >= 1 && ql <= OZ_L) alo += (int64_t)di[p] * dj[ql];
+              for (int p = pa; p <= pb; ++p) {
+                ahi += (int64_t)di[p] * dj[whi - p];                   /* X: (p, w_hi - p) */
+                if (wlo && p >= 2) alo += (int64_t)di[p - 1] * dj[whi - p]; /* Y: (p - 1, w_hi - p) */
               }
             }
             const int64_t v = alo * 256 + ahi;

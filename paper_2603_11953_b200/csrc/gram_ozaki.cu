@@ -51,15 +51,30 @@ constexpr int kL = 11;                 // digits per entry
 constexpr int kKC = 32;                // rows per chunk = UMMA K (int8)
 constexpr int kCB = 128;               // columns per digit block = UMMA M
 constexpr int kPlane = kCB * kKC;      // 4096 bytes
-constexpr int kGroups = 6;
+constexpr int kGroups = 12;             // weight-pair x step-range sub-groups (sub_group)
 constexpr int kBad = 1 << 20;          // E sentinel: the column holds inf/NaN
 constexpr int kRing = 16;              // step slots: A plane (4 KB) + B plane (8 KB) each
 constexpr int kThreads = 320;          // warps 0-1 loaders, 2-5 drain, 6-9 MMA issuers
 
-// weights {w_hi, w_lo} per group (w_lo = 0: a single weight)
-__host__ __device__ __forceinline__ void group_weights(int g, int& whi, int& wlo) {
-  whi = 12 - 2 * g;
-  wlo = g == 5 ? 0 : whi - 1;
+// Sub-group i: weights {w_hi, w_lo} (w_lo = 0: a single weight) of weight
+// pair k = 0..5 ({12,11} {10,9} {8,7} {6,5} {4,3} {2}) and its steps
+// [pa, pb] of 1..D (D = w_hi - 1), each pair's steps cut into ranges of at
+// most 4 so every CTA streams about the same planes per chunk: CTAs of one
+// split then move through the rows at the same rate and share planes in L2.
+__host__ __device__ __forceinline__ void sub_group(int i, int& whi, int& wlo, int& pa, int& pb) {
+  for (int k = 0; k < 6; ++k) {
+    const int h = 12 - 2 * k, d = h - 1, parts = (d + 3) / 4;
+    if (i < parts) {
+      const int base = d / parts, extra = d % parts;
+      pa = 1 + i * base + (i < extra ? i : extra);
+      pb = pa + base + (i < extra ? 1 : 0) - 1;
+      whi = h;
+      wlo = k == 5 ? 0 : h - 1;
+      return;
+    }
+    i -= parts;
+  }
+  whi = wlo = pa = pb = 0;
 }
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -286,13 +301,13 @@ ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, con
 // MPSVD_OZAKI_PROF=1: per weight group, summed over CTAs: [0] CTAs, [1] MMA
 // thread cycles, [2] of which waiting for planes, [3] waiting for the drain,
 // [4] loader waiting for free slots, [5] drain cycles, [6] drain waiting
-__device__ unsigned long long g_oz_prof[6][8];
+__device__ unsigned long long g_oz_prof[oz::kGroups][8];
 
 
 __global__ void __launch_bounds__(oz::kThreads, 1)
 gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
               const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
-              double2* __restrict__ partials, int span_cap, int prof, int dbg) {
+              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles) {
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
@@ -307,21 +322,28 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   int* ej = reinterpret_cast<int*>(tmem_slot + 4);              // 256 column exponents of block J
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x % kGroups, tile = blockIdx.x / kGroups;
-  const int s = s0 + blockIdx.y;
+  // linear order (tile fastest, then group, then split): co-resident CTAs are
+  // the tiles of one group and split, which run at the same rate and share
+  // the A planes (same I) or B planes (same J) through L2
+  const int tile = (int)(blockIdx.x % (unsigned)ntiles);
+  const int g = (int)((blockIdx.x / (unsigned)ntiles) % kGroups);
+  const int s = s0 + (int)(blockIdx.x / (unsigned)(ntiles * kGroups));
   const int2 ij = tiles[tile];  // (I: 128-column block, J: 256-column block)
-  int whi, wlo;
-  group_weights(g, whi, wlo);
+  int whi, wlo, pa, pb;
+  sub_group(g, whi, wlo, pa, pb);
   const long long c0 = scb[s], c1 = scb[s + 1];
-  // exact-accumulation span: <= 2^17 / (products per weight) rows
-  const int maxpairs = whi - 1 < 11 ? whi - 1 : (23 - whi < 11 ? 23 - whi : 11);
+  // exact-accumulation span: chunks x products per weight per chunk < 4096
+  // (|d_p d_q| <= 2^14, 32 rows per chunk: sums stay below 2^31)
+  const int maxpairs = pb - pa + 1;
   int span = 1;
-  while (span * 2 * kKC * maxpairs <= (1 << 17)) span *= 2;
+  while (span * 2 * maxpairs < 4096) span *= 2;
   if (span > span_cap) span = span_cap;
   const long long nspan = (c1 - c0 + span - 1) / span;
   const int nrel = wlo ? 2 : 1;                // issuers releasing each plane
   const int nissue = wlo ? 4 : 2;              // active issuer warps
-  const int D = whi - 1 < kL ? whi - 1 : kL;   // steps per chunk
+  const int D = whi - 1;                       // steps of the whole weight pair
+  const int pre = (wlo && pa >= 2) ? 1 : 0;    // leading A-only step (A_{pa-1} for Y)
+  const int L = pb - pa + 1 + pre;             // local steps per chunk
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
@@ -367,17 +389,22 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
       unsigned long long tw = 0;
       for (long long ch = c0; ch < c1; ++ch) {
         const unsigned char* chunk = digits + (ch * kL) * ncb2 * (long long)kPlane;
-        for (int p = 1; p <= D; ++p, ++t) {
+        for (int j = 0; j < L; ++j, ++t) {
           if ((t & 1u) != par) continue;
+          const int p = pa - pre + j;
           const int sl = (int)(t % kRing);
           const unsigned ph = ((t / kRing) & 1u) ^ 1u;
           const unsigned long long t0 = prof ? clock64() : 0;
           mbar_wait(&a_empty[sl], ph);
           mbar_wait(&b_empty[sl], ph);
           if (prof) tw += clock64() - t0;
-          bulk_g2s2_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
-                         bring + (size_t)sl * 2 * kPlane,
-                         chunk + ((long long)(D - p) * ncb2 + 2 * ij.y) * kPlane, 2 * kPlane, &a_full[sl], lead);
+          if (pre && j == 0)
+            bulk_g2s_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
+                          &a_full[sl], lead);
+          else
+            bulk_g2s2_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
+                           bring + (size_t)sl * 2 * kPlane,
+                           chunk + ((long long)(D - p) * ncb2 + 2 * ij.y) * kPlane, 2 * kPlane, &a_full[sl], lead);
         }
       }
       if (prof && lead && warp == 0) atomicAdd(&g_oz_prof[g][4], tw);
@@ -405,19 +432,23 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
         long long ce = ch + span;
         if (ce > c1) ce = c1;
         for (; ch < ce; ++ch) {
-          for (int p = 1; p <= D; ++p, ++t) {
+          for (int j = 0; j < L; ++j, ++t) {
             if ((t & 1u) != par) continue;
+            const int p = pa - pre + j;
+            const bool regular = !(pre && j == 0);  // the leading step only brings A_{pa-1}
             const int sl = (int)(t % kRing);
             const int slp = (int)((t + kRing - 1) % kRing);
-            if (!(dbg & 1)) mbar_wait(&a_full[sl], (t / kRing) & 1u);
+            if (regular && !(dbg & 1)) mbar_wait(&a_full[sl], (t / kRing) & 1u);
             if (role == 0) {
-              asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-              umma_i8_lead(dacc, kdesc(abase + (uint32_t)sl * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane), idesc,
-                           1u, lead && !(dbg & 2));
+              if (regular) {
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                umma_i8_lead(dacc, kdesc(abase + (uint32_t)sl * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
+                             idesc, 1u, lead && !(dbg & 2));
+              }
               umma_commit_lead(&a_empty[sl], lead);
               umma_commit_lead(&b_empty[sl], lead);
             } else {
-              if (p >= 2) {
+              if (regular && p >= 2) {
                 if (!(dbg & 1)) mbar_wait(&a_full[slp], ((t - 1) / kRing) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 umma_i8_lead(dacc, kdesc(abase + (uint32_t)slp * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
@@ -585,14 +616,14 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
   const char* dbg_env = getenv("MPSVD_OZAKI_DBG");  // bit 0: no plane loads, bit 1: no MMAs (timing probes)
   const int dbg = dbg_env ? atoi(dbg_env) : 0;
   if (prof) {
-    unsigned long long z[48] = {};
+    unsigned long long z[oz::kGroups * 8] = {};
     cudaMemcpyToSymbolAsync(g_oz_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
-  dim3 grid(ntiles * oz::kGroups, ns);
+  const unsigned grid = (unsigned)(ntiles * oz::kGroups * ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
-                                                  span_cap, prof, dbg);
+                                                  span_cap, prof, dbg, ntiles);
   if (prof) {
-    unsigned long long h[48];
+    unsigned long long h[oz::kGroups * 8];
     cudaMemcpyFromSymbolAsync(h, g_oz_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     for (int g = 0; g < oz::kGroups; ++g) {
