@@ -69,14 +69,26 @@ def config_dict(cfg, world: int, eig: int = 0):
             "parallelism": f"rows{world}", "eigensolver": EIG_NAME[eig]}
 
 
+OZ_PRODUCTS = 66                               # digit products p + q <= 12 of 11 digits (gram_ozaki.cu)
+I8_TOPS = 2 * 128 * 256 * 32 / 128 * 148 * 1.965e9 / 1e12  # 4.77 POPS (umma_i8 probe)
+
+
+def ozaki_gram(m_local: int) -> bool:
+    """The engine's double-double Gram choice (engine.cu Plan::Plan): K2z from
+    4096 local rows unless MPSVD_DD_GRAM forces one kernel."""
+    g = os.environ.get("MPSVD_DD_GRAM", "")
+    return g == "ozaki" or (g != "dot2" and m_local >= 4096)
+
+
 def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
     """Roofline of every pipeline phase of one SVD on one GPU.
 
     gram  f32: m n (n+1) flops on the DMMA pipe (K1; the phase also holds
                the two small combine kernels)
-    gram  f64: m n (n+1)/2 multiply-adds x 10 fp64 operations (Dot2:
-               two_prod 2, two_sum 6, error accumulation 2; c_dd = 10 as
-               SURVEY.md §8(d) defines it) on the fp64 pipe (K2)
+    gram  f64: K2z (>= 4096 rows): 66 int8 digit products per multiply-add
+               on the int8 tensor cores; K2 (Dot2): m n (n+1)/2
+               multiply-adds x 10 fp64 operations (two_prod 2, two_sum 6,
+               error accumulation 2; c_dd = 10 as SURVEY.md §8(d) defines it)
     eigen    : two-sided Jacobi, latency bound; 18 n flops per rotation
                (2 rows + 2 columns of M, 2 columns of V) against fp64 peak
     compute_u: f32: read A + write U (2 m n 4 bytes) against HBM (K7 on the
@@ -94,6 +106,16 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
         out["compute_u"] = {"kernel": "av_tc_f32 (tcgen05 bf16x3)", "bound": "hbm", "achieved": b, "peak": hbm,
                             "unit": "GB/s", "frac": b / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                             "algorithmic": "2*m*n*4 bytes (read A, write U) per SVD"}
+    elif ozaki_gram(m_local):
+        # K2z: 66 exact int8 digit products per entry of the upper triangle
+        ops = 2.0 * OZ_PRODUCTS * m_local * n * (n + 1) / 2
+        a = ops / (med["gram"] * 1e-3) / 1e12
+        out["gram"] = {"kernel": "gram_dd_ozaki (tcgen05 kind::i8) + ozaki_slice/colexp + combine", "bound": "tensor",
+                       "achieved": a, "peak": I8_TOPS, "unit": "TOPS", "frac": a / I8_TOPS,
+                       "peak_source": "tcgen05 kind::i8 probe: one M128 N256 K32 MMA per 128 cycles per SM "
+                                      "(tools/microbench/umma_i8.cu, profiles/r01_umma_i8.txt) x 148 SMs x 1965 MHz",
+                       "algorithmic": "2 x 66 int8 digit products x m x n(n+1)/2 (upper triangle) per SVD",
+                       "dd_equivalent_tops": m_local * n * (n + 1) / 2 * 10 / (med["gram"] * 1e-3) / 1e12}
     else:
         ops = m_local * n * (n + 1) / 2 * 10
         peak = DFMA_TFLOPS / 2

@@ -19,23 +19,29 @@
 //    groups 256 B apart), so the Gram kernel moves them with plain bulk copies.
 // 3. gram_dd_ozaki: for a 128 x 256 output tile, sum_k x_ki x_kj =
 //    2^(E_i + E_j - 172) sum_{p,q} 2^(8 (22 - p - q)) sum_k d_p(x_ki) d_q(x_kj).
-//    The digit products with p + q = w <= 12 are kept (dropped terms are
-//    below 2^-82 of |x_ki x_kj| per row); every product is an exact int8 MMA
-//    (tcgen05.mma kind::i8, M = 128, N = 256, K = 32) into an int32 TMEM
-//    accumulator per weight w. TMEM holds two 128 x 256 accumulators, so the
-//    weights are dealt to six CTAs per tile: {12,11} {10,9} {8,7} {6,5}
-//    {4,3} {2}. Accumulators stay exact (|d_p d_q| <= 2^14, at most 11
-//    products per weight and chunk, spans of <= 2^17 / 11 rows) and are
-//    drained every span into the CTA's double-double partial tile:
-//    V = acc_wlo * 2^8 + acc_whi (exact in int64), (hi, lo) = (fl(V), V - fl(V)),
-//    scaled by 2^(E_i + E_j + 4 - 8 w_hi) and added with dd_add.
+//    The digit products with p + q = w <= 12 are kept (66 of them; dropped
+//    terms are below 2^-82 of |x_ki x_kj| per row); every product is an
+//    exact int8 MMA (tcgen05.mma kind::i8, M = 128, N = 256, K = 32) into an
+//    int32 TMEM accumulator per weight. TMEM holds two 128 x 256
+//    accumulators, so the weight pairs {12,11} {10,9} {8,7} {6,5} {4,3} {2}
+//    are dealt to CTAs, each pair's steps cut into ranges of <= 4 (12
+//    sub-groups, sub_group()). Step p of pair (w_hi, w_lo) streams A_p and
+//    B_{w_hi - p} into one ring slot and issues (p, w_hi - p) and
+//    (p - 1, w_hi - p); two loader warps and four MMA-issuing warps split the
+//    steps by parity (one issuing thread could not keep up with the 128-cycle
+//    MMA: its wait / descriptor / commit chain took ~300 cycles per MMA).
+//    Accumulators stay exact (|d_p d_q| <= 2^14, span x products per weight
+//    per chunk < 4096 chunks) and are drained every span into the CTA's
+//    double-double partial tile: V = acc_wlo * 2^8 + acc_whi (exact in
+//    int64), (hi, lo) = (fl(V), V - fl(V)), scaled by 2^(E_i + E_j + 4 - 8 w_hi),
+//    added with dd_add; the drain warps then zero the accumulators (every MMA
+//    accumulates, so MMA order across issuers is irrelevant).
 //    Partials use K2's layout ([slot][64x64 tile pair][64x64] double2,
-//    slot = split * 6 + group), so the combine, the reference tree and the
-//    multi-GPU exchange are K2's.
+//    slot = split * 12 + sub-group), so the combine, the reference tree and
+//    the multi-GPU exchange are K2's.
 //
-// Measured on B200 (tools/microbench/umma_i8.cu): one kind::i8 MMA issues
-// every ~152 cycles for any N <= 256 (s8 x s8), so N = 256 runs at 83% of
-// the nominal 4.5 POPS and N = 128 at half of that.
+// Measured on B200 (tools/microbench/umma_i8.cu): an M128 N256 K32 kind::i8
+// MMA takes 128 cycles when issued back to back (4.77 POPS over 148 SMs).
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>

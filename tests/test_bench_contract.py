@@ -33,7 +33,9 @@ def test_phase_rooflines_f32_units_and_fractions():
     assert ph["eigen"]["bound"] == "latency"
 
 
-def test_phase_rooflines_dd_uses_c_dd_10():
+def test_phase_rooflines_dd_uses_c_dd_10(monkeypatch):
+    # K2 (Dot2, forced): c_dd = 10 fp64 operations per multiply-add
+    monkeypatch.setenv("MPSVD_DD_GRAM", "dot2")
     cfg = inputs.CONFIGS["c5"]
     med = {"gram": 1400.0, "eigen": 800.0, "compute_u": 270.0}
     ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info())
@@ -41,6 +43,20 @@ def test_phase_rooflines_dd_uses_c_dd_10():
     assert g["achieved"] == pytest.approx(cfg.m * cfg.n * (cfg.n + 1) / 2 * 10 / 1.4 / 1e12)
     assert g["peak"] == pytest.approx(bench.DFMA_TFLOPS / 2)
     assert ph["compute_u"]["bound"] == "tensor"
+
+
+def test_phase_rooflines_dd_ozaki_against_int8_peak(monkeypatch):
+    # K2z (the engine's choice from 4096 rows): 66 int8 digit products per
+    # multiply-add against the measured kind::i8 tensor peak
+    monkeypatch.delenv("MPSVD_DD_GRAM", raising=False)
+    cfg = inputs.CONFIGS["c5"]
+    med = {"gram": 236.0, "eigen": 800.0, "compute_u": 270.0}
+    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info())
+    g = ph["gram"]
+    assert g["achieved"] == pytest.approx(2 * 66 * cfg.m * cfg.n * (cfg.n + 1) / 2 / 0.236 / 1e12)
+    assert g["peak"] == pytest.approx(bench.I8_TOPS)
+    assert 4700 < bench.I8_TOPS < 4800
+    assert not bench.ozaki_gram(4095) and bench.ozaki_gram(4096)
 
 
 @pytest.mark.parametrize("name,world", [("c2", 1), ("c2", 8), ("c4", 4), ("c5", 2)])
