@@ -241,24 +241,60 @@ ozaki_colexp(const double* __restrict__ a, long long lda, long long m, int n, co
 // 2. digit planes: one (chunk, 128-column block) unit per iteration, 256
 // threads = 128 columns x 2 row halves; A staged through shared memory with
 // coalesced column reads.
-__global__ void __launch_bounds__(256)
+// A tile = 128 columns x 32 rows of fp64, staged by cp.async (16 bytes per
+// copy, 8 per thread) in a double buffer, so the next unit's loads are in
+// flight while this one is split; column stride 34 doubles (16-byte aligned
+// rows, 2-way bank conflicts at most on the reads).
+__global__ void __launch_bounds__(256, 2)
 ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, const int* __restrict__ e_cols,
             const int* __restrict__ scb, int nsplit, long long ch0, long long ch1, int ncb2,
             unsigned char* __restrict__ digits) {
-  __shared__ double st[oz::kCB * 33];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  extern __shared__ __align__(16) double st_dyn[];
+  constexpr int kLd = 34;
+  const int tid = threadIdx.x;
   const int col = tid & 127, half = tid >> 7;
   const long long units = (ch1 - ch0) * ncb2;
-  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+  const bool aligned = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(a) % 16 == 0);
+  // piece q = tid + 256 i (i < 8): column q >> 4, rows 2 (q & 15) .. + 1
+  auto issue = [&](long long u, int buf) {
     const long long ch = ch0 + u / ncb2;
     const int cb = (int)(u % ncb2);
     const long long r0 = ch * oz::kKC;
-#pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-      const int c = warp + 8 * i, gc = cb * oz::kCB + c;
-      const long long r = r0 + lane;
-      st[c * 33 + lane] = (gc < n && r < m) ? __ldg(a + (long long)gc * lda + r) : 0.0;
+    double* dst = st_dyn + buf * (oz::kCB * kLd);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int q = tid + 256 * i, c = q >> 4, rp = (q & 15) * 2;
+      const int gc = cb * oz::kCB + c;
+      const long long r = r0 + rp;
+      // bytes present: 16 (both rows), 8 (the last row of an odd m) or 0; the rest is zero-filled
+      const int bytes = gc < n && r < m ? (r + 1 < m ? 16 : 8) : 0;
+      if (aligned) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + c * kLd + rp);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                     "l"(bytes ? a + (long long)gc * lda + r : a), "r"(bytes)
+                     : "memory");
+      } else {  // odd lda or unaligned A: plain loads (visible after the __syncthreads)
+        const double* sp = a + (long long)gc * lda + r;
+        dst[c * kLd + rp] = bytes ? __ldg(sp) : 0.0;
+        dst[c * kLd + rp + 1] = bytes == 16 ? __ldg(sp + 1) : 0.0;
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  long long u = blockIdx.x;
+  int buf = 0;
+  if (u < units) issue(u, 0);
+  for (; u < units; u += gridDim.x, buf ^= 1) {
+    const long long un = u + gridDim.x;
+    if (un < units) {
+      issue(un, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const long long ch = ch0 + u / ncb2;
+    const int cb = (int)(u % ncb2);
     // split of this chunk: last s with scb[s] <= ch
     int lo = 0, hi = nsplit - 1;
     while (lo < hi) {
@@ -268,11 +304,11 @@ ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, con
     }
     const int gc = cb * oz::kCB + col;
     const int e_col = gc < n ? e_cols[(long long)lo * n + gc] : 0;
-    __syncthreads();
+    const double* src = st_dyn + buf * (oz::kCB * kLd) + col * kLd + 16 * half;
     uint32_t w[16][3];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      double x = st[col * 33 + 16 * half + r];
+      double x = src[r];
       if (e_col == oz::kBad) x = 0.0;
       oz::fixed88(x, e_col, w[r][0], w[r][1], w[r][2]);
     }
@@ -290,20 +326,16 @@ ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, con
       }
       *reinterpret_cast<uint4*>(base + (long long)(p - 1) * ncb2 * oz::kPlane) = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    __syncthreads();
+    __syncthreads();  // this buffer is refilled by the next iteration's issue
   }
 }
 
 // ---------------------------------------------------------------------------
-// 3. the Gram tiles. grid = (tiles x 6 groups, splits). Per CTA:
-//   warp 0 (one thread): streams digit planes in the order the MMAs use
-//     them into two rings: A planes (block I, 4 KB) and B planes (block J,
-//     two adjacent 128-column blocks, 8 KB);
-//   warp 1 (one thread): TMEM allocation, the product list, MMA issue; every
-//     plane is released (tcgen05.commit -> its empty barrier) right after
-//     its last product, so the next chunk streams in behind the current one;
-//   warps 2-5: drain (thread = tile row, tcgen05.ld 32x32b) into the
-//     double-double partial tile.
+// 3. the Gram tiles: one CTA per (tile, sub-group, split), linear order
+// tile fastest. Warps 0-1 load the steps (A plane 4 KB + B plane 8 KB per
+// ring slot) of even / odd global step, warps 6-9 issue the MMAs (X0, X1:
+// weight w_hi of even / odd steps; Y0, Y1: weight w_lo), warps 2-5 drain
+// (thread = tile row, tcgen05.ld 32x32b) into the double-double partial tile.
 // MPSVD_OZAKI_PROF=1: per weight group, summed over CTAs: [0] CTAs, [1] MMA
 // thread cycles, [2] of which waiting for planes, [3] waiting for the drain,
 // [4] loader waiting for free slots, [5] drain cycles, [6] drain waiting
@@ -607,8 +639,16 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
   const long long ch0 = scb_host[s0], ch1 = scb_host[s0 + ns];
   const long long units = (ch1 - ch0) * ncb2;
   if (units > 0) {
-    long long grid = units < (long long)sm_count * 8 ? units : (long long)sm_count * 8;
-    ozaki_slice<<<(int)grid, 256, 0, st>>>(a, lda, m, n, e_cols, scb_dev, nsplit_total, ch0, ch1, ncb2, digits);
+    static bool slice_configured = false;
+    if (!slice_configured) {
+      cudaError_t e = cudaFuncSetAttribute(ozaki_slice, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(2 * oz::kCB * 34 * sizeof(double)));
+      if (e != cudaSuccess) return e;
+      slice_configured = true;
+    }
+    long long grid = units < (long long)sm_count * 2 ? units : (long long)sm_count * 2;
+    ozaki_slice<<<(int)grid, 256, 2 * oz::kCB * 34 * sizeof(double), st>>>(a, lda, m, n, e_cols, scb_dev,
+                                                                           nsplit_total, ch0, ch1, ncb2, digits);
   }
   static bool configured = false;
   const size_t smem = ozaki_smem();
