@@ -151,6 +151,13 @@ mpsvd_status mpsvd_plan_wait(mpsvd_plan* p, mpsvd_exec_info* info);
 /* Timed region helpers for the dominant kernels (CUDA events, ms). */
 void mpsvd_plan_destroy(mpsvd_plan* p);
 
+/* Text wire format (proj/include/mpsvd.h:79-82): "m n f32|f64" header, then
+ * the column-major entries as shortest round-trip decimals, one column per
+ * line, so write-then-read is bit-exact. MPSVD_ERR_IO on a bad header, tag,
+ * short body, unparsable value or an unopenable file. Host-only. */
+mpsvd_status mpsvd_matrix_write_file(const char* path, const mpsvd_matrix* a);
+mpsvd_status mpsvd_matrix_read_file(const char* path, mpsvd_matrix** out);
+
 /* ---- ADDITIVE: stage entry points (host buffers; parity tests) ------------- */
 /* M = A^T A: prec WORKING -> f32 A, fp64 M (m_hi); HIGHER -> f64 A,
  * double-double M (m_hi + m_lo). */

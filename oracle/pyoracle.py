@@ -24,6 +24,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libmpsvd_ref.so")
 PORT_SO = os.path.join(HERE, "_port", "libmpsvd_port.so")
+REF_IO = os.path.join(HERE, "_ref", "ref_io")
 
 SEM_REFERENCE = 0
 SEM_DEVICE = 1
@@ -209,6 +210,15 @@ class Ref:
         q = np.zeros((m, n), np.float64, order="F")
         self._check(self.lib.refx_haar_orthonormal(_i64(m), _i64(n), C.c_uint64(seed), _d(q)))
         return q
+
+    @staticmethod
+    def io_roundtrip(src, dst) -> int:
+        """The reference's read_matrix_file(src) then write_matrix_file(dst)
+        (proj/src/io.cpp) in a child process (oracle/_ref/ref_io: the
+        reference's iostreams and this interpreter's libstdc++ do not mix);
+        returns its status (0 ok, 9 IoError)."""
+        import subprocess
+        return subprocess.run([REF_IO, str(src), str(dst)], capture_output=True).returncode
 
     def dd_gram(self, a):
         a = _fcol(a, np.float64)

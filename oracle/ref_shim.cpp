@@ -66,6 +66,9 @@ int run(F&& body) noexcept {
     t_index = e.index;
     t_value = e.value;
     return 7;
+  } catch (const IoError& e) {
+    t_msg = e.what();
+    return 9;
   } catch (const std::exception& e) {
     t_msg = e.what();
     return 10;

@@ -69,6 +69,8 @@ SIGNATURES = [
     ("mpsvd_plan_execute", C.c_int, [vp, vp, i64, vp, i64, vp, vp, vp]),
     ("mpsvd_plan_wait", C.c_int, [vp, C.POINTER(ExecInfo)]),
     ("mpsvd_plan_destroy", None, [vp]),
+    ("mpsvd_matrix_write_file", C.c_int, [C.c_char_p, vp]),
+    ("mpsvd_matrix_read_file", C.c_int, [C.c_char_p, C.POINTER(vp)]),
     ("mpsvd_stage_gram", C.c_int, [C.c_int, vp, i64, i64, dp, dp]),
     ("mpsvd_stage_gram_schedule", C.c_int, [i64, i64, C.c_int] + [C.POINTER(C.c_int)] * 5),
     ("mpsvd_stage_jacobi", C.c_int, [C.c_int, dp, dp, i64, C.c_double, C.c_int, dp, dp, dp, dp,

@@ -173,6 +173,18 @@ class Matrix:
     def bitwise_equal(self, other: "Matrix") -> bool:
         return bool(lib.mpsvd_matrix_bitwise_equal(self._h, other._h))
 
+    def write_file(self, path: str) -> None:
+        """Text wire format (mpsvd_matrix_write_file; proj/src/io.cpp)."""
+        _check(lib.mpsvd_matrix_write_file(str(path).encode(), self._h))
+
+    @classmethod
+    def read_file(cls, path: str) -> "Matrix":
+        """Parse the text wire format (mpsvd_matrix_read_file); IoError-backed
+        failures raise MpsvdError with status MPSVD_ERR_IO."""
+        h = C.c_void_p()
+        _check(lib.mpsvd_matrix_read_file(str(path).encode(), C.byref(h)))
+        return cls._adopt(h.value)
+
     def numpy(self) -> np.ndarray:
         """Zero-copy column-major view of the storage (valid while self lives)."""
         m, n = self.rows, self.cols

@@ -23,6 +23,7 @@
 #include "engine.h"
 #include "mpsvd.h"
 #include "mpsvd/metrics.hpp"
+#include "mpsvd/io.hpp"
 #include "mpsvd/thinsvd.hpp"
 #include "mpsvd/types.hpp"
 
@@ -909,6 +910,20 @@ mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, in
   return guarded([&] {
     require(a != nullptr && m_hi != nullptr, "null argument");
     mpsvd::gpu_gram_public(prec == MPSVD_PRECISION_HIGHER, a, m, n, m_hi, m_lo);
+  });
+}
+
+mpsvd_status mpsvd_matrix_write_file(const char* path, const mpsvd_matrix* a) {
+  return guarded([&] {
+    require(path != nullptr && a != nullptr, "null argument");
+    mpsvd::write_matrix_file(path, a->m);
+  });
+}
+
+mpsvd_status mpsvd_matrix_read_file(const char* path, mpsvd_matrix** out) {
+  return guarded([&] {
+    require(path != nullptr && out != nullptr, "null argument");
+    *out = new mpsvd_matrix{mpsvd::read_matrix_file(path)};
   });
 }
 
