@@ -345,7 +345,8 @@ __device__ unsigned long long g_oz_prof[oz::kGroups][8];
 __global__ void __launch_bounds__(oz::kThreads, 1)
 gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
               const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
-              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles) {
+              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles, int* progress,
+              int leash) {
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
@@ -425,8 +426,31 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
       const unsigned par = (unsigned)warp;
       unsigned t = 0;
       unsigned long long tw = 0;
+      // Leash (L2 reuse): every CTA of a split stays within `leash` chunks
+      // of the split's pace-setter, the tile-0 CTA of the sub-group with the
+      // most planes per chunk (steps 5-8 of {12,11}), which publishes its
+      // progress; CTAs of one split then stream the same rows at about the
+      // same time and share the digit planes in L2. The pace-setter never
+      // waits, and a CTA whose pace-setter has not started (or has finished)
+      // does not wait either, so the leash cannot deadlock.
+      const bool pacer = tile == 0 && g == 1;
+      int* prog = progress ? progress + s : nullptr;
       for (long long ch = c0; ch < c1; ++ch) {
         const unsigned char* chunk = digits + (ch * kL) * ncb2 * (long long)kPlane;
+        if (prog && ((ch - c0) & 7) == 0) {
+          if (pacer) {
+            if (warp == 0 && lead) atomicExch(prog, (int)(ch - c0));
+          } else if (leash > 0) {
+            bool go = false;
+            do {
+              int pp = 0;
+              if (lead) pp = atomicAdd(prog, 0);
+              pp = __shfl_sync(0xffffffffu, pp, 0);
+              go = pp < 0 || ch - c0 <= (long long)pp + leash;
+              if (!go) __nanosleep(500);
+            } while (!go);
+          }
+        }
         for (int j = 0; j < L; ++j, ++t) {
           if ((t & 1u) != par) continue;
           const int p = pa - pre + j;
@@ -445,6 +469,7 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
                            chunk + ((long long)(D - p) * ncb2 + 2 * ij.y) * kPlane, 2 * kPlane, &a_full[sl], lead);
         }
       }
+      if (pacer && prog && warp == 0 && lead) atomicExch(prog, 1 << 30);  // finished: nobody waits for it
       if (prof && lead && warp == 0) atomicAdd(&g_oz_prof[g][4], tw);
     }
   } else if (warp >= 6) {
@@ -476,7 +501,11 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
             const bool regular = !(pre && j == 0);  // the leading step only brings A_{pa-1}
             const int sl = (int)(t % kRing);
             const int slp = (int)((t + kRing - 1) % kRing);
-            if (regular && !(dbg & 1)) mbar_wait(&a_full[sl], (t / kRing) & 1u);
+            // every step waits for its slot's fill, the A-only leading step
+            // too: its releases must not run ahead of the loader, or a slot's
+            // empty barrier could complete two phases before the loader
+            // waits on the first (parity waits would then hang)
+            if (!(dbg & 1)) mbar_wait(&a_full[sl], (t / kRing) & 1u);
             if (role == 0) {
               if (regular) {
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -627,7 +656,7 @@ static size_t ozaki_smem() {
 cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
                               const int* scb_host, int nsplit_total, int s0, int ns, const int2* tiles, int ntiles,
                               int* e_cols, unsigned char* digits, double2* partials, int ntp64, int sm_count,
-                              cudaStream_t st) {
+                              int* progress, cudaStream_t st) {
   if (ns <= 0) return cudaSuccess;
   const int T64 = (n + 63) / 64;
   const int ncb2 = ((n + 255) / 256) * 2;
@@ -665,9 +694,14 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
     unsigned long long z[oz::kGroups * 8] = {};
     cudaMemcpyToSymbolAsync(g_oz_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
+  // pace-setter progress per split (-1: not started); MPSVD_OZAKI_LEASH:
+  // chunks of lead allowed (0: off)
+  if (progress) cudaMemsetAsync(progress + s0, 0xff, ns * sizeof(int), st);
+  const char* leash_env = getenv("MPSVD_OZAKI_LEASH");
+  const int leash = leash_env ? atoi(leash_env) : 32;
   const unsigned grid = (unsigned)(ntiles * oz::kGroups * ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
-                                                  span_cap, prof, dbg, ntiles);
+                                                  span_cap, prof, dbg, ntiles, progress, leash);
   if (prof) {
     unsigned long long h[oz::kGroups * 8];
     cudaMemcpyFromSymbolAsync(h, g_oz_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
