@@ -698,7 +698,7 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
   // chunks of lead allowed (0: off)
   if (progress) cudaMemsetAsync(progress + s0, 0xff, ns * sizeof(int), st);
   const char* leash_env = getenv("MPSVD_OZAKI_LEASH");
-  const int leash = leash_env ? atoi(leash_env) : 32;
+  const int leash = leash_env ? atoi(leash_env) : 0;  // measured: no gain on c3/c5
   const unsigned grid = (unsigned)(ntiles * oz::kGroups * ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
                                                   span_cap, prof, dbg, ntiles, progress, leash);
