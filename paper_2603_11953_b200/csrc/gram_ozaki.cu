@@ -368,6 +368,12 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   const int g = (int)((blockIdx.x / (unsigned)ntiles) % kGroups);
   const int s = s0 + (int)(blockIdx.x / (unsigned)(ntiles * kGroups));
   const int2 ij = tiles[tile];  // (I: 128-column block, J: 256-column block)
+  // I = 2J + 1: the left half of block J lies below the diagonal for every
+  // row of the tile, so only its right half (128-column block I itself) is
+  // computed: N = 128, B planes of 4 KB
+  const bool half = ij.x == 2 * ij.y + 1;
+  const int col0 = half ? ij.x * kCB : ij.y * 256;  // first output column
+  const int ncol = half ? 128 : 256;
   int whi, wlo, pa, pb;
   sub_group(g, whi, wlo, pa, pb);
   const long long c0 = scb[s], c1 = scb[s + 1];
@@ -396,8 +402,8 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   }
   if (warp >= 2 && warp < 6) {
     for (int c = threadIdx.x - 64; c < 256; c += 128) {
-      const int gj = ij.y * 256 + c;
-      ej[c] = gj < n ? e_cols[(long long)s * n + gj] : 0;
+      const int gj = col0 + c;
+      ej[c] = (c < ncol && gj < n) ? e_cols[(long long)s * n + gj] : 0;
     }
   }
   if (warp == 6) {
@@ -466,7 +472,8 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
           else
             bulk_g2s2_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
                            bring + (size_t)sl * 2 * kPlane,
-                           chunk + ((long long)(D - p) * ncb2 + 2 * ij.y) * kPlane, 2 * kPlane, &a_full[sl], lead);
+                           chunk + ((long long)(D - p) * ncb2 + (half ? ij.x : 2 * ij.y)) * kPlane,
+                           (half ? 1 : 2) * kPlane, &a_full[sl], lead);
         }
       }
       if (pacer && prog && warp == 0 && lead) atomicExch(prog, 1 << 30);  // finished: nobody waits for it
@@ -478,8 +485,8 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
     const unsigned par = (unsigned)((warp - 6) & 1);
     if (role == 0 || wlo) {
       const uint32_t lead = lane == 0;
-      // D s32, A s8, B s8, both K-major, N = 256, M = 128
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+      // D s32, A s8, B s8, both K-major, N = 256 (128 for half tiles), M = 128
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ncol >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       const uint32_t abase = saddr(aring), bbase = saddr(bring);
       const uint32_t dacc = tmem + (role == 0 ? 256u : 0u);  // acc 0: w_lo (more significant), acc 1: w_hi
@@ -543,7 +550,8 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
     const int ti = gi >> 6;
     const long long slot = (long long)s * kGroups + g;
     auto out_ptr = [&](int c) -> double2* {
-      const int gj = ij.y * 256 + c, tj = gj >> 6;
+      const int gj = col0 + c, tj = gj >> 6;
+      if (c >= ncol) return nullptr;
       if (ti > tj || tj >= T64) return nullptr;
       const int tp = ti * T64 - (ti * (ti - 1)) / 2 + (tj - ti);
       return partials + (slot * ntp64 + tp) * 4096 + (gi & 63) * 64 + (gj & 63);
@@ -567,7 +575,7 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
       const unsigned long long t1 = prof ? clock64() : 0;
       tdw += t1 - t0;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      for (int c0 = 0; c0 < 256; c0 += 16) {
+      for (int c0 = 0; c0 < ncol; c0 += 16) {
         uint32_t v0[16], v1[16];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
         asm volatile(
