@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(oz::kThreads, 1)
 gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
               const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
               double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles, int* progress,
-              int leash) {
+              int leash, int pf) {
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
@@ -455,6 +455,27 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
               go = pp < 0 || ch - c0 <= (long long)pp + leash;
               if (!go) __nanosleep(500);
             } while (!go);
+          }
+        }
+        if (pf > 0 && ch + pf < c1) {
+          // L2 prefetch of this loader's planes `pf` chunks ahead: the ring
+          // (16 slots) holds ~1.5 chunks, too little to cover DRAM latency
+          const unsigned char* fut = digits + ((ch + pf) * kL) * ncb2 * (long long)kPlane;
+          unsigned tf = t + (unsigned)(pf * L);
+          for (int j = 0; j < L; ++j, ++tf) {
+            if ((tf & 1u) != par) continue;
+            const int p = pa - pre + j;
+            if (lead) {
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(
+                               fut + ((long long)(p - 1) * ncb2 + ij.x) * kPlane),
+                           "r"((unsigned)kPlane)
+                           : "memory");
+              if (!(pre && j == 0))
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(
+                                 fut + ((long long)(D - p) * ncb2 + (half ? ij.x : 2 * ij.y)) * kPlane),
+                             "r"((unsigned)((half ? 1 : 2) * kPlane))
+                             : "memory");
+            }
           }
         }
         for (int j = 0; j < L; ++j, ++t) {
@@ -707,9 +728,11 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
   if (progress) cudaMemsetAsync(progress + s0, 0xff, ns * sizeof(int), st);
   const char* leash_env = getenv("MPSVD_OZAKI_LEASH");
   const int leash = leash_env ? atoi(leash_env) : 0;  // measured: no gain on c3/c5
+  const char* pf_env = getenv("MPSVD_OZAKI_PF");  // chunks of L2 prefetch ahead (0: off)
+  const int pf = pf_env ? atoi(pf_env) : 0;  // measured slower (c3 27 -> 35 ms, c5 236 -> 292 ms)
   const unsigned grid = (unsigned)(ntiles * oz::kGroups * ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
-                                                  span_cap, prof, dbg, ntiles, progress, leash);
+                                                  span_cap, prof, dbg, ntiles, progress, leash, pf);
   if (prof) {
     unsigned long long h[oz::kGroups * 8];
     cudaMemcpyFromSymbolAsync(h, g_oz_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
