@@ -540,8 +540,10 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
                 umma_i8_lead(dacc, kdesc(abase + (uint32_t)sl * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
                              idesc, 1u, lead && !(dbg & 2));
               }
-              umma_commit_lead(&a_empty[sl], lead);
-              umma_commit_lead(&b_empty[sl], lead);
+              if (!(dbg & 8)) {  // bit 3 (with bit 0 only): no slot releases, to time the bare MMA stream
+                umma_commit_lead(&a_empty[sl], lead);
+                umma_commit_lead(&b_empty[sl], lead);
+              }
             } else {
               if (regular && p >= 2) {
                 if (!(dbg & 1)) mbar_wait(&a_full[slp], ((t - 1) / kRing) & 1u);
@@ -549,8 +551,10 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
                 umma_i8_lead(dacc, kdesc(abase + (uint32_t)slp * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
                              idesc, 1u, lead && !(dbg & 2));
               }
-              if (t > 0) umma_commit_lead(&a_empty[slp], lead);  // A_{p-1} (or the previous chunk's A_D)
-              umma_commit_lead(&b_empty[sl], lead);
+              if (!(dbg & 8)) {
+                if (t > 0) umma_commit_lead(&a_empty[slp], lead);  // A_{p-1} (or the previous chunk's A_D)
+                umma_commit_lead(&b_empty[sl], lead);
+              }
             }
           }
         }
@@ -717,7 +721,8 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
   }
   const char* prof_env = getenv("MPSVD_OZAKI_PROF");
   const int prof = prof_env && prof_env[0] == '1';
-  const char* dbg_env = getenv("MPSVD_OZAKI_DBG");  // bit 0: no plane loads, bit 1: no MMAs (timing probes)
+  const char* dbg_env = getenv("MPSVD_OZAKI_DBG");  // bit 0: no plane loads, bit 1: no MMAs, bit 3: no releases
+  // (timing probes; bit 3 only together with bit 0)
   const int dbg = dbg_env ? atoi(dbg_env) : 0;
   if (prof) {
     unsigned long long z[oz::kGroups * 8] = {};
