@@ -106,3 +106,51 @@ def test_two_rank_sharded_pipeline(tmp_path, port):
     err = np.abs((res[0]["ddh"] - hh) + (res[0]["ddl"] - ll))
     assert np.all(err <= 4 * (m * 2.0 ** -53) ** 2 * np.outer(an, an) + 2.0 ** -100 * np.abs(hh))
     assert np.array_equal(res[0]["ddh"], res[1]["ddh"]) and np.array_equal(res[0]["ddl"], res[1]["ddl"])
+
+
+def _worker_ozaki(rank, world, port, out_dir):
+    # K2z on the sharded path: every rank slices its own rows with its own
+    # column exponents (the restatement stands in for gram_dd_ozaki), then
+    # the dd exchange of the library (all-gather + rank-ordered dd_add)
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), HERE]
+    import pyoracle
+    from paper_2603_11953_b200 import sharding
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    P = pyoracle.Port()
+    m, n = 10001, 20
+    r0, r1 = sharding.local_rows(m, world, rank)
+    a64 = _matrix(m, n, np.float64, seed=7)
+    loc = np.asfortranarray(a64[r0:r1])
+    nch = (r1 - r0 + 31) // 32
+    scb = np.linspace(0, nch, 9).astype(np.int32)  # 8 chunk-aligned splits
+    bsb = np.array([0, 2, 4, 6, 8], np.int32)       # 4 logical blocks
+    hi, lo = P.gram_dd_ozaki(loc, scb, bsb, span_cap=5)
+    pair = torch.from_numpy(np.stack([hi, lo]))
+    gath = [torch.zeros_like(pair) for _ in range(world)]
+    dist.all_gather(gath, pair)
+    acc_h, acc_l = gath[0][0].numpy().copy(), gath[0][1].numpy().copy()
+    for rr in range(1, world):
+        gh, gl = gath[rr][0].numpy(), gath[rr][1].numpy()
+        for idx in np.ndindex(acc_h.shape):
+            acc_h[idx], acc_l[idx] = P.dd_op("add", (acc_h[idx], acc_l[idx]), (gh[idx], gl[idx]))
+    np.savez(os.path.join(out_dir, f"oz{rank}.npz"), h=acc_h, l=acc_l)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_ozaki_gram_exchange(tmp_path, port):
+    world = 2
+    mp.start_processes(_worker_ozaki, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    res = [dict(np.load(tmp_path / f"oz{r}.npz")) for r in range(world)]
+    assert np.array_equal(res[0]["h"], res[1]["h"]) and np.array_equal(res[0]["l"], res[1]["l"])
+    m, n = 10001, 20
+    a64 = _matrix(m, n, np.float64, seed=7)
+    hh, ll = port.dd_gram(a64, threads=4)
+    an = np.linalg.norm(a64, axis=0)
+    err = np.abs((res[0]["h"] - hh) + (res[0]["l"] - ll)) / np.outer(an, an)
+    # the K2z error level (rank-local exponents change nothing about it)
+    assert err.max() <= 2.0 ** -80
+    assert np.array_equal(res[0]["h"], res[0]["h"].T)
