@@ -233,6 +233,13 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     const char* g = getenv("MPSVD_DD_GRAM");
     const std::string gs = g ? g : "";
     ozaki = gs == "ozaki" || (gs != "dot2" && m >= 4096);
+    if (ozaki && gs != "ozaki") {
+      // K2z partials: at least 16 splits x sub-groups x the upper 64x64 tile
+      // pairs in double-double; keep K2 when that alone passes 8 GB (n > ~2300)
+      const long long T64 = (n + 63) / 64;
+      const long long slot_bytes = T64 * (T64 + 1) / 2 * 64 * 64 * 16;
+      if (16LL * dev::ozaki_groups() * slot_bytes > (8LL << 30)) ozaki = false;
+    }
     if (ozaki) {  // the digit planes (11 bytes per entry); K2 when they do not fit
       void* ptr = nullptr;
       if (cudaMalloc(&ptr, dev::ozaki_digit_bytes(m, (int)n)) == cudaSuccess) {
