@@ -1063,29 +1063,30 @@ int port_dd_gram(const double* a, int64_t m, int64_t n, int threads, double* hi,
  * per-split column exponents, the 11 balanced 8-bit digits of
  * trunc(x 2^(86 - E)), the exact integer digit-product sums per weight and
  * exact-accumulation span, their conversion to double-double
- * (V = acc_wlo 2^8 + acc_whi; (fl(V), V - fl(V)) scaled by
- * 2^(E_i + E_j + 4 - 8 w_hi)), the running dd_add per partial slot
- * (split * 12 + sub-group), then the engine's combine: slots of a logical block
+ * (V = sum_k acc_k 2^(8k), acc_k of weight w_hi - k; (fl(V), V - fl(V))
+ * scaled by 2^(E_i + E_j + 4 - 8 w_hi)), the running dd_add per partial
+ * slot (split * 6 + sub-group), then the engine's combine: slots of a logical block
  * summed in order from zero, blocks along the reference tree
  * (parallel_gram.cpp:93-102). Semantics follow dd_gram (dd.cpp:75-88) up to
  * the digit truncation. */
 #define OZ_L 11
-#define OZ_G 12
-/* sub-group i: weights (whi, wlo) and steps [pa, pb] (gram_ozaki.cu sub_group) */
-static void oz_sub_group(int i, int* whi, int* wlo, int* pa, int* pb) {
-  for (int k = 0; k < 6; ++k) {
-    const int h = 12 - 2 * k, d = h - 1, parts = (d + 3) / 4;
+#define OZ_G 6
+/* sub-group i: weight quad (w_hi, nw weights w_hi - k) and steps [pa, pb]
+ * (gram_ozaki.cu sub_group) */
+static void oz_sub_group(int i, int* whi, int* nw, int* pa, int* pb) {
+  for (int q = 0; q < 3; ++q) {
+    const int h = 12 - 4 * q, d = h - 1, parts = (d + 3) / 4;
     if (i < parts) {
       const int base = d / parts, extra = d % parts;
       *pa = 1 + i * base + (i < extra ? i : extra);
       *pb = *pa + base + (i < extra ? 1 : 0) - 1;
       *whi = h;
-      *wlo = k == 5 ? 0 : h - 1;
+      *nw = q == 2 ? 3 : 4;
       return;
     }
     i -= parts;
   }
-  *whi = *wlo = *pa = *pb = 0;
+  *whi = *nw = *pa = *pb = 0;
 }
 #define OZ_BAD (1 << 20)
 static void oz_fixed88(double x, int e_col, uint32_t w[3]) {
@@ -1154,8 +1155,8 @@ int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const 
   dd* part = (dd*)calloc((size_t)(nslot * n * n), sizeof(dd));
   for (int s = 0; s < nsplit; ++s)
     for (int g = 0; g < OZ_G; ++g) {
-      int whi, wlo, pa, pb;
-      oz_sub_group(g, &whi, &wlo, &pa, &pb);
+      int whi, nw, pa, pb;
+      oz_sub_group(g, &whi, &nw, &pa, &pb);
       const int maxpairs = pb - pa + 1;
       int span = 1;
       while (span * 2 * maxpairs < 4096) span *= 2;
@@ -1168,16 +1169,15 @@ int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const 
           const int ei = E[s * n + i], ej = E[s * n + j];
           for (int64_t ch = c0; ch < c1; ch += span) {
             const int64_t ce = ch + span < c1 ? ch + span : c1;
-            int64_t ahi = 0, alo = 0;
+            int64_t acc[4] = {0, 0, 0, 0};
             for (int64_t r = ch * 32; r < ce * 32 && r < m; ++r) {
               const int8_t* di = D + (r * n + i) * OZ_L - 1; /* di[p], p = 1..11 */
               const int8_t* dj = D + (r * n + j) * OZ_L - 1;
-              for (int p = pa; p <= pb; ++p) {
-                ahi += (int64_t)di[p] * dj[whi - p];                   /* X: (p, w_hi - p) */
-                if (wlo && p >= 2) alo += (int64_t)di[p - 1] * dj[whi - p]; /* Y: (p - 1, w_hi - p) */
-              }
+              for (int p = pa; p <= pb; ++p)
+                for (int k = 0; k < nw; ++k)
+                  if (p - k >= 1) acc[k] += (int64_t)di[p - k] * dj[whi - p]; /* W_k: (p - k, w_hi - p) */
             }
-            const int64_t v = alo * 256 + ahi;
+            const int64_t v = acc[0] + acc[1] * 256 + acc[2] * 65536 + acc[3] * 16777216;
             const double h = (double)v;
             const double l = (double)(v - (int64_t)h);
             dd t;

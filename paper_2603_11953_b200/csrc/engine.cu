@@ -235,7 +235,7 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     ozaki = gs == "ozaki" || (gs != "dot2" && m >= 4096);
     if (ozaki && gs != "ozaki") {
       // K2z partials: at least 16 splits x sub-groups x the upper 64x64 tile
-      // pairs in double-double; keep K2 when that alone passes 8 GB (n > ~2300)
+      // pairs in double-double; keep K2 when that alone passes 8 GB (n > ~3300)
       const long long T64 = (n + 63) / 64;
       const long long slot_bytes = T64 * (T64 + 1) / 2 * 64 * 64 * 16;
       if (16LL * dev::ozaki_groups() * slot_bytes > (8LL << 30)) ozaki = false;
@@ -282,7 +282,6 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     d_bsb_oz = dalloc<int>(b6.size(), owned);
     check(cudaMemcpy(d_bsb_oz, b6.data(), b6.size() * sizeof(int), cudaMemcpyHostToDevice), "H2D bsb");
     d_oz_e = dalloc<int>(splits.size() * (size_t)n, owned);
-    d_oz_progress = dalloc<int>(splits.size() + 1, owned);
   }
   d_bsums = dalloc<double>((size_t)(nblocks > 0 ? nblocks : 1) * tiles.size() * 64 * 64 * esz, owned);
   d_m = dalloc<double>(nn * esz, owned);
@@ -462,7 +461,7 @@ void Plan::gram_dd_splits(const void* d_a, long long lda, int sb, int cnt, cudaS
   if (ozaki) {
     check(dev::launch_gram_ozaki((const double*)d_a, lda, m, (int)n, d_scb, scb.data(), (int)splits.size(), sb, cnt,
                                  d_oz_tiles, (int)oz_tiles.size(), d_oz_e, d_digits, (double2*)d_partials, ntp,
-                                 sm_count, d_oz_progress, st),
+                                 sm_count, st),
           "gram_ozaki");
     launches += 3;
   } else {

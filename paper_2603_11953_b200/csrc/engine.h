@@ -81,7 +81,6 @@ class Plan {
   int* d_scb = nullptr;
   int* d_bsb_oz = nullptr;  // block_split_begin x ozaki_groups()
   int* d_oz_e = nullptr;    // column exponents per split
-  int* d_oz_progress = nullptr;  // pace-setter progress per split (K2z L2 leash)
   unsigned char* d_digits = nullptr;
 
   int2* d_tiles = nullptr;

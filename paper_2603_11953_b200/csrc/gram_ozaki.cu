@@ -17,31 +17,32 @@
 //    images: [32-row chunk][digit][128-column block] x 4 KB, K-major,
 //    no swizzle (8x16-byte core matrices; K neighbours 128 B apart, 8-row
 //    groups 256 B apart), so the Gram kernel moves them with plain bulk copies.
-// 3. gram_dd_ozaki: for a 128 x 256 output tile, sum_k x_ki x_kj =
+// 3. gram_dd_ozaki: for a 128 x 128 output tile (I <= J), sum_k x_ki x_kj =
 //    2^(E_i + E_j - 172) sum_{p,q} 2^(8 (22 - p - q)) sum_k d_p(x_ki) d_q(x_kj).
 //    The digit products with p + q = w <= 12 are kept (66 of them; dropped
 //    terms are below 2^-82 of |x_ki x_kj| per row); every product is an
-//    exact int8 MMA (tcgen05.mma kind::i8, M = 128, N = 256, K = 32) into an
-//    int32 TMEM accumulator per weight. TMEM holds two 128 x 256
-//    accumulators, so the weight pairs {12,11} {10,9} {8,7} {6,5} {4,3} {2}
-//    are dealt to CTAs, each pair's steps cut into ranges of <= 4 (12
-//    sub-groups, sub_group()). Step p of pair (w_hi, w_lo) streams A_p and
-//    B_{w_hi - p} into one ring slot and issues (p, w_hi - p) and
-//    (p - 1, w_hi - p); two loader warps and four MMA-issuing warps split the
-//    steps by parity (one issuing thread could not keep up with the 128-cycle
-//    MMA: its wait / descriptor / commit chain took ~300 cycles per MMA).
+//    exact int8 MMA (tcgen05.mma kind::i8, M = 128, N = 128, K = 32) into an
+//    int32 TMEM accumulator per weight. TMEM holds four 128 x 128
+//    accumulators, so the weight quads {12,11,10,9} {8,7,6,5} {4,3,2} are
+//    dealt to CTAs, each quad's steps cut into ranges of <= 4 (6 sub-groups,
+//    sub_group()). Step p of a quad streams A_p and B_{w_hi - p} (4 KB each)
+//    into one ring slot (24 slots) and issuer W_k multiplies A_{p-k} by it
+//    (weight w_hi - k); two loader warps and eight issuing warps (W_k x step
+//    parity) share the steps — one issuing thread could not keep up with the
+//    MMA: its wait / descriptor / commit chain took ~300 cycles per MMA.
 //    Accumulators stay exact (|d_p d_q| <= 2^14, span x products per weight
 //    per chunk < 4096 chunks) and are drained every span into the CTA's
-//    double-double partial tile: V = acc_wlo * 2^8 + acc_whi (exact in
-//    int64), (hi, lo) = (fl(V), V - fl(V)), scaled by 2^(E_i + E_j + 4 - 8 w_hi),
+//    double-double partial tile: V = sum_k acc_k 2^(8k) (exact in int64),
+//    (hi, lo) = (fl(V), V - fl(V)), scaled by 2^(E_i + E_j + 4 - 8 w_hi),
 //    added with dd_add; the drain warps then zero the accumulators (every MMA
 //    accumulates, so MMA order across issuers is irrelevant).
 //    Partials use K2's layout ([slot][64x64 tile pair][64x64] double2,
-//    slot = split * 12 + sub-group), so the combine, the reference tree and
+//    slot = split * 6 + sub-group), so the combine, the reference tree and
 //    the multi-GPU exchange are K2's.
 //
-// Measured on B200 (tools/microbench/umma_i8.cu): an M128 N256 K32 kind::i8
-// MMA takes 128 cycles when issued back to back (4.77 POPS over 148 SMs).
+// Measured on B200 (tools/microbench/umma_i8.cu): an M128 K32 kind::i8 MMA
+// takes 128 cycles at N = 256 and 64 at N = 128 when issued back to back
+// (4.77 POPS over 148 SMs).
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -57,30 +58,28 @@ constexpr int kL = 11;                 // digits per entry
 constexpr int kKC = 32;                // rows per chunk = UMMA K (int8)
 constexpr int kCB = 128;               // columns per digit block = UMMA M
 constexpr int kPlane = kCB * kKC;      // 4096 bytes
-constexpr int kGroups = 12;             // weight-pair x step-range sub-groups (sub_group)
+constexpr int kGroups = 6;              // weight-quad x step-range sub-groups (sub_group)
 constexpr int kBad = 1 << 20;          // E sentinel: the column holds inf/NaN
-constexpr int kRing = 16;              // step slots: A plane (4 KB) + B plane (8 KB) each (18 measured no better)
-constexpr int kThreads = 320;          // warps 0-1 loaders, 2-5 drain, 6-9 MMA issuers
+constexpr int kRing = 24;              // step slots: A plane (4 KB) + B plane (4 KB) each
+constexpr int kThreads = 448;          // warps 0-1 loaders, 2-5 drain, 6-13 MMA issuers (weight k, parity)
 
-// Sub-group i: weights {w_hi, w_lo} (w_lo = 0: a single weight) of weight
-// pair k = 0..5 ({12,11} {10,9} {8,7} {6,5} {4,3} {2}) and its steps
-// [pa, pb] of 1..D (D = w_hi - 1), each pair's steps cut into ranges of at
-// most 4 so every CTA streams about the same planes per chunk: CTAs of one
-// split then move through the rows at the same rate and share planes in L2.
-__host__ __device__ __forceinline__ void sub_group(int i, int& whi, int& wlo, int& pa, int& pb) {
-  for (int k = 0; k < 6; ++k) {
-    const int h = 12 - 2 * k, d = h - 1, parts = (d + 3) / 4;
+// Sub-group i: weight quad q ({12,11,10,9}, {8,7,6,5}, {4,3,2}: w_hi and
+// nw weights w_hi - k, k < nw) and its steps [pa, pb] of 1..D (D = w_hi - 1),
+// each quad's steps cut into ranges of at most 4 (6 sub-groups).
+__host__ __device__ __forceinline__ void sub_group(int i, int& whi, int& nw, int& pa, int& pb) {
+  for (int q = 0; q < 3; ++q) {
+    const int h = 12 - 4 * q, d = h - 1, parts = (d + 3) / 4;
     if (i < parts) {
       const int base = d / parts, extra = d % parts;
       pa = 1 + i * base + (i < extra ? i : extra);
       pb = pa + base + (i < extra ? 1 : 0) - 1;
       whi = h;
-      wlo = k == 5 ? 0 : h - 1;
+      nw = q == 2 ? 3 : 4;
       return;
     }
     i -= parts;
   }
-  whi = wlo = pa = pb = 0;
+  whi = nw = pa = pb = 0;
 }
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -332,10 +331,10 @@ ozaki_slice(const double* __restrict__ a, long long lda, long long m, int n, con
 
 // ---------------------------------------------------------------------------
 // 3. the Gram tiles: one CTA per (tile, sub-group, split), linear order
-// tile fastest. Warps 0-1 load the steps (A plane 4 KB + B plane 8 KB per
-// ring slot) of even / odd global step, warps 6-9 issue the MMAs (X0, X1:
-// weight w_hi of even / odd steps; Y0, Y1: weight w_lo), warps 2-5 drain
-// (thread = tile row, tcgen05.ld 32x32b) into the double-double partial tile.
+// tile fastest. Warps 0-1 load the steps (A plane + B plane, 4 KB each, per
+// ring slot) of even / odd global step, warps 6-13 issue the MMAs (W_k x
+// step parity), warps 2-5 drain (thread = tile row, tcgen05.ld 32x32b) into
+// the double-double partial tile.
 // MPSVD_OZAKI_PROF=1: per weight group, summed over CTAs: [0] CTAs, [1] MMA
 // thread cycles, [2] of which waiting for planes, [3] waiting for the drain,
 // [4] loader waiting for free slots, [5] drain cycles, [6] drain waiting
@@ -345,37 +344,29 @@ __device__ unsigned long long g_oz_prof[oz::kGroups][8];
 __global__ void __launch_bounds__(oz::kThreads, 1)
 gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
               const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
-              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles, int* progress,
-              int leash, int pf) {
+              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles) {
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
   unsigned char* bring = aring + kRing * kPlane;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kRing * 2 * kPlane);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kRing * kPlane);
   uint64_t* a_full = bars;  // one full barrier per step slot (A and B plane)
   uint64_t* a_empty = a_full + kRing;
   uint64_t* b_empty = a_empty + kRing;
   uint64_t* acc_full = b_empty + kRing;
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-  int* ej = reinterpret_cast<int*>(tmem_slot + 4);              // 256 column exponents of block J
+  int* ej = reinterpret_cast<int*>(tmem_slot + 4);              // column exponents of block J
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // linear order (tile fastest, then group, then split): co-resident CTAs are
-  // the tiles of one group and split, which run at the same rate and share
-  // the A planes (same I) or B planes (same J) through L2
+  // linear order (tile fastest, then sub-group, then split)
   const int tile = (int)(blockIdx.x % (unsigned)ntiles);
   const int g = (int)((blockIdx.x / (unsigned)ntiles) % kGroups);
   const int s = s0 + (int)(blockIdx.x / (unsigned)(ntiles * kGroups));
-  const int2 ij = tiles[tile];  // (I: 128-column block, J: 256-column block)
-  // I = 2J + 1: the left half of block J lies below the diagonal for every
-  // row of the tile, so only its right half (128-column block I itself) is
-  // computed: N = 128, B planes of 4 KB
-  const bool half = ij.x == 2 * ij.y + 1;
-  const int col0 = half ? ij.x * kCB : ij.y * 256;  // first output column
-  const int ncol = half ? 128 : 256;
-  int whi, wlo, pa, pb;
-  sub_group(g, whi, wlo, pa, pb);
+  const int2 ij = tiles[tile];  // (I, J): 128-column blocks, I <= J
+  const int col0 = ij.y * kCB, ncol = kCB;
+  int whi, nw, pa, pb;
+  sub_group(g, whi, nw, pa, pb);
   const long long c0 = scb[s], c1 = scb[s + 1];
   // exact-accumulation span: chunks x products per weight per chunk < 4096
   // (|d_p d_q| <= 2^14, 32 rows per chunk: sums stay below 2^31)
@@ -384,26 +375,23 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   while (span * 2 * maxpairs < 4096) span *= 2;
   if (span > span_cap) span = span_cap;
   const long long nspan = (c1 - c0 + span - 1) / span;
-  const int nrel = wlo ? 2 : 1;                // issuers releasing each plane
-  const int nissue = wlo ? 4 : 2;              // active issuer warps
-  const int D = whi - 1;                       // steps of the whole weight pair
-  const int pre = (wlo && pa >= 2) ? 1 : 0;    // leading A-only step (A_{pa-1} for Y)
-  const int L = pb - pa + 1 + pre;             // local steps per chunk
+  const int npre = (pa - 1 < nw - 1) ? pa - 1 : nw - 1;  // leading A-only steps (A_{pa-npre} .. A_{pa-1})
+  const int L = pb - pa + 1 + npre;                       // local steps per chunk
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], nrel);
-      mbar_init(&b_empty[i], nrel);
+      mbar_init(&a_empty[i], nw);
+      mbar_init(&b_empty[i], nw);
     }
-    mbar_init(acc_full, nissue);
+    mbar_init(acc_full, 2 * nw);
     mbar_init(acc_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp >= 2 && warp < 6) {
-    for (int c = threadIdx.x - 64; c < 256; c += 128) {
+    for (int c = threadIdx.x - 64; c < kCB; c += 128) {
       const int gj = col0 + c;
-      ej[c] = (c < ncol && gj < n) ? e_cols[(long long)s * n + gj] : 0;
+      ej[c] = gj < n ? e_cols[(long long)s * n + gj] : 0;
     }
   }
   if (warp == 6) {
@@ -416,101 +404,53 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  // Steps. Chunk step p = 1..D (global step t, ring slot t % kRing) brings
-  // A_p (digit p of block I) and B_{D+1-p} (digit D+1-p of block J) and
-  // issues two products: X: (p, D+1-p) of weight w_hi (A_p, B from slot t)
-  // and Y: (p-1, D+1-p) of weight w_lo (A_{p-1} from slot t-1, B from slot t).
-  // A_p's last users are X at step t and Y at step t+1; B's are X and Y at
-  // step t. Loaders and issuers are split by the parity of t (two loader
-  // warps; issuer warps X0, X1, Y0, Y1), so per-MMA issue latency overlaps;
-  // the integer accumulation makes MMA order irrelevant (accumulators are
-  // zeroed by the drain warps, every MMA accumulates).
+  // Steps. Local step j of a chunk (global step t, slot t % kRing) covers
+  // digit p = pa - npre + j: it brings A_p (block I) and, for p >= pa, B_q
+  // with q = w_hi - p (block J). Issuer W_k (weight w_hi - k) multiplies
+  // A_{p-k} (slot t - k) by B_q (slot t). Every issuer waits for both slots'
+  // fills and then releases A of slot t - k and B of slot t at every step,
+  // so each slot's empty barriers count nw arrivals per use and no release
+  // can run ahead of the loader. Loaders and issuers split steps by the
+  // parity of t; the integer accumulation makes MMA order irrelevant.
   if (warp < 2) {
-    // loader of the steps with t % 2 == warp
     if (!(dbg & 1)) {
       const uint32_t lead = lane == 0;
       const unsigned par = (unsigned)warp;
       unsigned t = 0;
       unsigned long long tw = 0;
-      // Leash (L2 reuse): every CTA of a split stays within `leash` chunks
-      // of the split's pace-setter, the tile-0 CTA of the sub-group with the
-      // most planes per chunk (steps 5-8 of {12,11}), which publishes its
-      // progress; CTAs of one split then stream the same rows at about the
-      // same time and share the digit planes in L2. The pace-setter never
-      // waits, and a CTA whose pace-setter has not started (or has finished)
-      // does not wait either, so the leash cannot deadlock.
-      const bool pacer = tile == 0 && g == 1;
-      int* prog = progress ? progress + s : nullptr;
       for (long long ch = c0; ch < c1; ++ch) {
         const unsigned char* chunk = digits + (ch * kL) * ncb2 * (long long)kPlane;
-        if (prog && ((ch - c0) & 7) == 0) {
-          if (pacer) {
-            if (warp == 0 && lead) atomicExch(prog, (int)(ch - c0));
-          } else if (leash > 0) {
-            bool go = false;
-            do {
-              int pp = 0;
-              if (lead) pp = atomicAdd(prog, 0);
-              pp = __shfl_sync(0xffffffffu, pp, 0);
-              go = pp < 0 || ch - c0 <= (long long)pp + leash;
-              if (!go) __nanosleep(500);
-            } while (!go);
-          }
-        }
-        if (pf > 0 && ch + pf < c1) {
-          // L2 prefetch of this loader's planes `pf` chunks ahead: the ring
-          // (16 slots) holds ~1.5 chunks, too little to cover DRAM latency
-          const unsigned char* fut = digits + ((ch + pf) * kL) * ncb2 * (long long)kPlane;
-          unsigned tf = t + (unsigned)(pf * L);
-          for (int j = 0; j < L; ++j, ++tf) {
-            if ((tf & 1u) != par) continue;
-            const int p = pa - pre + j;
-            if (lead) {
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(
-                               fut + ((long long)(p - 1) * ncb2 + ij.x) * kPlane),
-                           "r"((unsigned)kPlane)
-                           : "memory");
-              if (!(pre && j == 0))
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(
-                                 fut + ((long long)(D - p) * ncb2 + (half ? ij.x : 2 * ij.y)) * kPlane),
-                             "r"((unsigned)((half ? 1 : 2) * kPlane))
-                             : "memory");
-            }
-          }
-        }
         for (int j = 0; j < L; ++j, ++t) {
           if ((t & 1u) != par) continue;
-          const int p = pa - pre + j;
+          const int p = pa - npre + j;
           const int sl = (int)(t % kRing);
           const unsigned ph = ((t / kRing) & 1u) ^ 1u;
           const unsigned long long t0 = prof ? clock64() : 0;
           mbar_wait(&a_empty[sl], ph);
           mbar_wait(&b_empty[sl], ph);
           if (prof) tw += clock64() - t0;
-          if (pre && j == 0)
+          if (p < pa)
             bulk_g2s_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
                           &a_full[sl], lead);
           else
             bulk_g2s2_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
-                           bring + (size_t)sl * 2 * kPlane,
-                           chunk + ((long long)(D - p) * ncb2 + (half ? ij.x : 2 * ij.y)) * kPlane,
-                           (half ? 1 : 2) * kPlane, &a_full[sl], lead);
+                           bring + (size_t)sl * kPlane,
+                           chunk + ((long long)(whi - p - 1) * ncb2 + ij.y) * kPlane, kPlane, &a_full[sl], lead);
         }
       }
-      if (pacer && prog && warp == 0 && lead) atomicExch(prog, 1 << 30);  // finished: nobody waits for it
       if (prof && lead && warp == 0) atomicAdd(&g_oz_prof[g][4], tw);
     }
   } else if (warp >= 6) {
-    // issuers: warp 6 X0, 7 X1, 8 Y0, 9 Y1
-    const int role = (warp - 6) >> 1;          // 0: X (w_hi), 1: Y (w_lo)
+    // issuers: warp 6 + 2k + par = W_k (weight w_hi - k) of the steps with t % 2 == par
+    const int k = (warp - 6) >> 1;
     const unsigned par = (unsigned)((warp - 6) & 1);
-    if (role == 0 || wlo) {
+    if (k < nw) {
       const uint32_t lead = lane == 0;
-      // D s32, A s8, B s8, both K-major, N = 256 (128 for half tiles), M = 128
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(ncol >> 3) << 17) |
+      // D s32, A s8, B s8, both K-major, N = 128, M = 128
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kCB >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       const uint32_t abase = saddr(aring), bbase = saddr(bring);
-      const uint32_t dacc = tmem + (role == 0 ? 256u : 0u);  // acc 0: w_lo (more significant), acc 1: w_hi
+      const uint32_t dacc = tmem + (uint32_t)(k * kCB);
       unsigned t = 0;
       unsigned long long tacc = 0;
       const unsigned long long tstart = prof ? clock64() : 0;
@@ -525,42 +465,26 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
         for (; ch < ce; ++ch) {
           for (int j = 0; j < L; ++j, ++t) {
             if ((t & 1u) != par) continue;
-            const int p = pa - pre + j;
-            const bool regular = !(pre && j == 0);  // the leading step only brings A_{pa-1}
+            const int p = pa - npre + j;
             const int sl = (int)(t % kRing);
-            const int slp = (int)((t + kRing - 1) % kRing);
-            // every step waits for its slot's fill, the A-only leading step
-            // too: its releases must not run ahead of the loader, or a slot's
-            // empty barrier could complete two phases before the loader
-            // waits on the first (parity waits would then hang)
             if (!(dbg & 1)) mbar_wait(&a_full[sl], (t / kRing) & 1u);
-            if (role == 0) {
-              if (regular) {
-                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                umma_i8_lead(dacc, kdesc(abase + (uint32_t)sl * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
-                             idesc, 1u, lead && !(dbg & 2));
-              }
-              if (!(dbg & 8)) {  // bit 3 (with bit 0 only): no slot releases, to time the bare MMA stream
-                umma_commit_lead(&a_empty[sl], lead);
-                umma_commit_lead(&b_empty[sl], lead);
-              }
-            } else {
-              if (regular && p >= 2) {
-                if (!(dbg & 1)) mbar_wait(&a_full[slp], ((t - 1) / kRing) & 1u);
-                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                umma_i8_lead(dacc, kdesc(abase + (uint32_t)slp * kPlane), kdesc(bbase + (uint32_t)sl * 2 * kPlane),
-                             idesc, 1u, lead && !(dbg & 2));
-              }
-              if (!(dbg & 8)) {
-                if (t > 0) umma_commit_lead(&a_empty[slp], lead);  // A_{p-1} (or the previous chunk's A_D)
-                umma_commit_lead(&b_empty[sl], lead);
-              }
+            const bool has_a = t >= (unsigned)k;
+            const int sla = (int)((t + kRing - (unsigned)k) % kRing);
+            if (has_a && k > 0 && !(dbg & 1)) mbar_wait(&a_full[sla], ((t - (unsigned)k) / kRing) & 1u);
+            if (p >= pa && p - k >= 1) {
+              asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+              umma_i8_lead(dacc, kdesc(abase + (uint32_t)sla * kPlane), kdesc(bbase + (uint32_t)sl * kPlane), idesc,
+                           1u, lead && !(dbg & 2));
+            }
+            if (!(dbg & 8)) {
+              if (has_a) umma_commit_lead(&a_empty[sla], lead);
+              umma_commit_lead(&b_empty[sl], lead);
             }
           }
         }
         umma_commit_lead(acc_full, lead);
       }
-      if (prof && lead && warp == 6) {
+      if (prof && lead && k == 0 && par == 0) {
         atomicAdd(&g_oz_prof[g][0], 1ull);
         atomicAdd(&g_oz_prof[g][1], clock64() - tstart);
         atomicAdd(&g_oz_prof[g][3], tacc);
@@ -582,7 +506,7 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
       return partials + (slot * ntp64 + tp) * 4096 + (gi & 63) * 64 + (gj & 63);
     };
     if (nspan == 0) {
-      for (int c = 0; c < 256; ++c) {
+      for (int c = 0; c < ncol; ++c) {
         double2* o = out_ptr(c);
         if (o) *o = make_double2(0.0, 0.0);
       }
@@ -600,43 +524,45 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
       const unsigned long long t1 = prof ? clock64() : 0;
       tdw += t1 - t0;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      for (int c0 = 0; c0 < ncol; c0 += 16) {
-        uint32_t v0[16], v1[16];
+      for (int c0 = 0; c0 < ncol; c0 += 8) {
+        uint32_t v[4][8];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-            : "=r"(v0[0]), "=r"(v0[1]), "=r"(v0[2]), "=r"(v0[3]), "=r"(v0[4]), "=r"(v0[5]), "=r"(v0[6]),
-              "=r"(v0[7]), "=r"(v0[8]), "=r"(v0[9]), "=r"(v0[10]), "=r"(v0[11]), "=r"(v0[12]), "=r"(v0[13]),
-              "=r"(v0[14]), "=r"(v0[15])
-            : "r"(taddr));
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-            : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]), "=r"(v1[6]),
-              "=r"(v1[7]), "=r"(v1[8]), "=r"(v1[9]), "=r"(v1[10]), "=r"(v1[11]), "=r"(v1[12]), "=r"(v1[13]),
-              "=r"(v1[14]), "=r"(v1[15])
-            : "r"(taddr + 256u));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k < nw)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                         : "=r"(v[k][0]), "=r"(v[k][1]), "=r"(v[k][2]), "=r"(v[k][3]), "=r"(v[k][4]), "=r"(v[k][5]),
+                           "=r"(v[k][6]), "=r"(v[k][7])
+                         : "r"(taddr + (uint32_t)(k * kCB)));
+          else
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) v[k][jj] = 0u;
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        tmem_zero16(taddr);
-        tmem_zero16(taddr + 256u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
+                           taddr + (uint32_t)(k * kCB)),
+                       "r"(0u));
         // the running partials of the 16 columns are loaded together (one
         // memory latency per group, not per entry)
-        double2* op[16];
-        double2 old[16];
+        double2* op[8];
+        double2 old[8];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
+        for (int jj = 0; jj < 8; ++jj) {
           op[jj] = out_ptr(c0 + jj);
           old[jj] = (sp > 0 && op[jj]) ? *op[jj] : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
+        for (int jj = 0; jj < 8; ++jj) {
           const int c = c0 + jj;
           double2* o = op[jj];
           if (!o) continue;
-          // acc 0 = w_lo (unused for the single-weight group), acc 1 = w_hi
-          const long long vlo = wlo ? (long long)(int)v0[jj] : 0ll;
-          const long long v = vlo * 256 + (long long)(int)v1[jj];
-          const double hi = (double)v;
-          const double lo = (double)(v - (long long)hi);
+          // acc k holds weight w_hi - k, worth 2^(8k) of weight w_hi: exact in int64
+          const long long vv = (long long)(int)v[0][jj] + (long long)(int)v[1][jj] * 256 +
+                               (long long)(int)v[2][jj] * 65536 + (long long)(int)v[3][jj] * 16777216;
+          const double hi = (double)vv;
+          const double lo = (double)(vv - (long long)hi);
           const int e2 = ej[c];
           dd t;
           if (ei == kBad || e2 == kBad) {
@@ -674,22 +600,22 @@ size_t ozaki_digit_bytes(long long m, int n) {
 }
 int ozaki_groups() { return oz::kGroups; }
 
+// Tiles (I, J) of 128-column blocks with I <= J (the upper triangle)
 void ozaki_tiles(int n, std::vector<int2>& tiles) {
   tiles.clear();
-  const int TI = (n + 127) / 128, TJ = (n + 255) / 256;
-  for (int J = 0; J < TJ; ++J)
-    for (int I = 0; I < TI; ++I)
-      if (I * 128 <= J * 256 + 255) tiles.push_back(make_int2(I, J));
+  const int T = (n + 127) / 128;
+  for (int J = 0; J < T; ++J)
+    for (int I = 0; I <= J; ++I) tiles.push_back(make_int2(I, J));
 }
 
 static size_t ozaki_smem() {
-  return (size_t)oz::kRing * 3 * oz::kPlane + 3 * oz::kRing * 8 + 16 + 16 + 256 * 4 + 64;
+  return (size_t)oz::kRing * 2 * oz::kPlane + 3 * oz::kRing * 8 + 16 + 16 + 128 * 4 + 64;
 }
 
 cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
                               const int* scb_host, int nsplit_total, int s0, int ns, const int2* tiles, int ntiles,
                               int* e_cols, unsigned char* digits, double2* partials, int ntp64, int sm_count,
-                              int* progress, cudaStream_t st) {
+                              cudaStream_t st) {
   if (ns <= 0) return cudaSuccess;
   const int T64 = (n + 63) / 64;
   const int ncb2 = ((n + 255) / 256) * 2;
@@ -728,16 +654,9 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
     unsigned long long z[oz::kGroups * 8] = {};
     cudaMemcpyToSymbolAsync(g_oz_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
-  // pace-setter progress per split (-1: not started); MPSVD_OZAKI_LEASH:
-  // chunks of lead allowed (0: off)
-  if (progress) cudaMemsetAsync(progress + s0, 0xff, ns * sizeof(int), st);
-  const char* leash_env = getenv("MPSVD_OZAKI_LEASH");
-  const int leash = leash_env ? atoi(leash_env) : 0;  // measured: no gain on c3/c5
-  const char* pf_env = getenv("MPSVD_OZAKI_PF");  // chunks of L2 prefetch ahead (0: off)
-  const int pf = pf_env ? atoi(pf_env) : 0;  // measured slower (c3 27 -> 35 ms, c5 236 -> 292 ms)
   const unsigned grid = (unsigned)(ntiles * oz::kGroups * ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
-                                                  span_cap, prof, dbg, ntiles, progress, leash, pf);
+                                                  span_cap, prof, dbg, ntiles);
   if (prof) {
     unsigned long long h[oz::kGroups * 8];
     cudaMemcpyFromSymbolAsync(h, g_oz_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);

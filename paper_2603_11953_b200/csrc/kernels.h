@@ -38,7 +38,7 @@ void ozaki_tiles(int n, std::vector<int2>& tiles);  // (128-column block I, 256-
 cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
                               const int* scb_host, int nsplit_total, int s0, int ns, const int2* tiles, int ntiles,
                               int* e_cols, unsigned char* digits, double2* partials, int ntp64, int sm_count,
-                              int* progress, cudaStream_t st);  // progress: nsplit_total ints (the L2 leash)
+                              cudaStream_t st);
 
 // jacobi.cu ------------------------------------------------------------------
 // A (n x n, full symmetric, column-major; f64 or dd=double2) is overwritten:

@@ -386,6 +386,7 @@ int main3() {
 }
 
 // layout sweep: (LBO, SBO) of K-major no-swizzle operands; K = 32 per MMA
+__device__ int g_n = 256;
 __global__ void rate4(int iters, int lbo_a, int sbo_a, int lbo_b, int sbo_b, int kstep, unsigned long long* cyc) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t tslot;
@@ -413,7 +414,7 @@ __global__ void rate4(int iters, int lbo_a, int sbo_a, int lbo_b, int sbo_b, int
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tm = tslot;
   if (tid == 0) {
-    const uint32_t id = idesc_i8(128, 256, 1, 1);
+    const uint32_t id = idesc_i8(128, g_n, 1, 1);
     const unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       const int k = it & 3;
@@ -432,6 +433,11 @@ __global__ void rate4(int iters, int lbo_a, int sbo_a, int lbo_b, int sbo_b, int
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm), "n"(512));
 }
 int main4() {
+  if (getenv("PROBE4_N")) {
+    const int nn = atoi(getenv("PROBE4_N"));
+    CK(cudaMemcpyToSymbol(g_n, &nn, sizeof(int)));
+    printf("N = %d\n", nn);
+  }
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   CK(cudaFuncSetAttribute(rate4, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
