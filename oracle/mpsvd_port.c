@@ -1116,6 +1116,8 @@ static void oz_fixed88(double x, int e_col, uint32_t w[3]) {
   w[2] = (uint32_t)rhi;
 }
 
+void port_oz_sub_group(int i, int* whi, int* nw, int* pa, int* pb) { oz_sub_group(i, whi, nw, pa, pb); }
+
 int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const int* scb, int nblocks,
                        const int* bsb, int span_cap, double* out_hi, double* out_lo) {
   if (m < 1 || n < 1 || nsplit < 1 || nblocks < 1 || nblocks > 16) return ST_INVALID;

@@ -90,6 +90,8 @@ void port_dd_sqrt(double ah, double al, double* rh, double* rl);
 /* G = A^T A, exact products + double-double accumulation (dd.cpp:75-88 order). */
 int port_dd_gram(const double* a, int64_t m, int64_t n, int threads, double* hi,
                  double* lo);
+/* K2z sub-group i: weight quad (w_hi, nw weights w_hi - k) and steps [pa, pb] */
+void port_oz_sub_group(int i, int* whi, int* nw, int* pa, int* pb);
 /* K2z (csrc/gram_ozaki.cu) replayed bit for bit on the schedule scb / bsb */
 int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const int* scb, int nblocks,
                        const int* bsb, int span_cap, double* out_hi, double* out_lo);

@@ -399,6 +399,12 @@ class Port:
             raise OracleError(st)
         return hi, lo
 
+    def oz_sub_group(self, i):
+        """K2z sub-group i: (w_hi, nw, pa, pb)."""
+        v = [C.c_int(0) for _ in range(4)]
+        self.lib.port_oz_sub_group(C.c_int(i), *[C.byref(x) for x in v])
+        return tuple(x.value for x in v)
+
     def gram_dd_ozaki(self, a, scb, bsb, span_cap=1 << 20):
         """K2z's double-double Gram (csrc/gram_ozaki.cu) on the split schedule
         scb (chunks) / bsb (logical blocks), bit for bit."""

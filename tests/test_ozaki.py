@@ -102,6 +102,24 @@ def test_port_ozaki_scale_invariance(port):
     assert _scaled_err(h3, l3, rh, rl, a) <= 2.0 ** -80
 
 
+def test_sub_groups_cover_every_digit_product_once(port):
+    # the 6 sub-groups' products (p - k, w_hi - p), k < nw, p in [pa, pb],
+    # p - k >= 1, are exactly the 66 digit pairs (a, b) with a + b <= 12
+    seen = {}
+    for i in range(6):
+        whi, nw, pa, pb = port.oz_sub_group(i)
+        assert 1 <= pa <= pb <= whi - 1 and pb - pa + 1 <= 4 and nw in (3, 4)
+        for p in range(pa, pb + 1):
+            for k in range(nw):
+                if p - k >= 1:
+                    pair = (p - k, whi - p)
+                    assert pair not in seen
+                    seen[pair] = i
+    want = {(a, b) for a in range(1, 12) for b in range(1, 12) if a + b <= 12}
+    assert set(seen) == want and len(want) == 66
+    assert port.oz_sub_group(6) == (0, 0, 0, 0)
+
+
 # ---------------------------------------------------------------- GPU
 
 @pytest.mark.gpu
