@@ -344,7 +344,7 @@ __device__ unsigned long long g_oz_prof[oz::kGroups][8];
 __global__ void __launch_bounds__(oz::kThreads, 1)
 gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __restrict__ e_cols, int n,
               const int2* __restrict__ tiles, const int* __restrict__ scb, int s0, int T64, int ntp64,
-              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles) {
+              double2* __restrict__ partials, int span_cap, int prof, int dbg, int ntiles, int ord) {
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
@@ -359,9 +359,13 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   int* ej = reinterpret_cast<int*>(tmem_slot + 4);              // column exponents of block J
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // linear order (tile fastest, then sub-group, then split)
-  const int tile = (int)(blockIdx.x % (unsigned)ntiles);
-  const int g = (int)((blockIdx.x / (unsigned)ntiles) % kGroups);
+  // linear order: MPSVD_OZAKI_ORDER=1 sub-group fastest (the sub-groups of
+  // one tile, which read the same two column blocks, run together), else
+  // tile fastest; then split
+  const unsigned inner = ord ? (unsigned)kGroups : (unsigned)ntiles;
+  const unsigned a0 = blockIdx.x % inner, a1 = (blockIdx.x / inner) % (unsigned)(ntiles * kGroups / inner);
+  const int tile = (int)(ord ? a1 : a0);
+  const int g = (int)(ord ? a0 : a1);
   const int s = s0 + (int)(blockIdx.x / (unsigned)(ntiles * kGroups));
   const int2 ij = tiles[tile];  // (I, J): 128-column blocks, I <= J
   const int col0 = ij.y * kCB, ncol = kCB;
@@ -654,9 +658,11 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
     unsigned long long z[oz::kGroups * 8] = {};
     cudaMemcpyToSymbolAsync(g_oz_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   }
+  const char* ord_env = getenv("MPSVD_OZAKI_ORDER");
+  const int ord = ord_env ? atoi(ord_env) : 0;
   const unsigned grid = (unsigned)(ntiles * oz::kGroups * ns);
   gram_dd_ozaki<<<grid, oz::kThreads, smem, st>>>(digits, ncb2, e_cols, n, tiles, scb_dev, s0, T64, ntp64, partials,
-                                                  span_cap, prof, dbg, ntiles);
+                                                  span_cap, prof, dbg, ntiles, ord);
   if (prof) {
     unsigned long long h[oz::kGroups * 8];
     cudaMemcpyFromSymbolAsync(h, g_oz_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
