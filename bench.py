@@ -208,7 +208,7 @@ def run_reference(args, cfg):
         return None
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-    from paper_2603_11953_b200 import inputs
+    import workloads as inputs
 
     cores = os.cpu_count() or 1
     n = cfg.n
@@ -266,7 +266,7 @@ def run_ours(args, cfg):
     import torch.distributed as dist
 
     import paper_2603_11953_b200 as M
-    from paper_2603_11953_b200 import inputs
+    import workloads as inputs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -490,7 +490,7 @@ def main():
     ap.add_argument("--eig", default="twosided", choices=list(EIG),
                     help="mp_thin_svd spectral branch (GramCholSvd / OneSidedJacobiOnGram: binary32 configs)")
     args = ap.parse_args()
-    from paper_2603_11953_b200.inputs import CONFIGS
+    from workloads import CONFIGS
 
     cfg = CONFIGS[args.config]
     line = run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)

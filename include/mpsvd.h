@@ -112,8 +112,12 @@ void mpsvd_svd_jacobi_stats(const mpsvd_svd_result* r, int* sweeps, int64_t* rot
  * mpsvd_plan_execute allocates nothing. Pointers are device pointers on the
  * plan's device; `stream` is a cudaStream_t (NULL = the plan's own stream).
  * m_local rows of A live on this rank; the Gram partials of all ranks are
- * combined by NCCL (all-reduce for fp64, all-gather + compensated sum for
- * double-double) through `comm` (NULL: single GPU). */
+ * exchanged once through `comm` (NULL: single GPU): an NCCL all-gather, then
+ * every rank adds the ranks' partials along the reference's fixed tree
+ * (binary64 adds for fp64, dd_add for double-double), so all ranks hold the
+ * same bits; MPSVD_F64_EXCHANGE=allreduce uses an NCCL sum for fp64.
+ * The host-buffer entry points (mpsvd_thin_svd, mpsvd_thin_svd_f64) shard
+ * over the visible GPUs by themselves (MPSVD_DEVICES). */
 typedef struct mpsvd_comm mpsvd_comm;
 typedef struct mpsvd_plan mpsvd_plan;
 
@@ -146,6 +150,13 @@ mpsvd_status mpsvd_plan_set_eigensolver(mpsvd_plan* p, mpsvd_eigensolver eig);
  * Multi-rank plans all-reduce the Gram; Q stays row-sharded. */
 mpsvd_status mpsvd_plan_cholesky_qr(mpsvd_plan* p, const void* d_a, int64_t lda, void* d_q, int64_t ldq,
                                     float* d_r, void* stream);
+/* ADDITIVE: ||Q^T Q - I||_F in binary64 (proj/src/dense.cpp:250-272) of a
+ * device-resident m_local x n Q in the plan's precision, Q^T Q formed by the
+ * plan's own Gram stage (K1 for binary32, the double-double Gram for
+ * binary64) and, on a multi-rank plan, combined over the ranks (a global
+ * orthogonality error; every rank must call it). Overwrites the plan's Gram
+ * workspace; synchronous on `stream`. */
+mpsvd_status mpsvd_plan_orth_error(mpsvd_plan* p, const void* d_q, int64_t ldq, void* stream, double* out);
 /* Blocks until the last execute finished; reports the device status. */
 mpsvd_status mpsvd_plan_wait(mpsvd_plan* p, mpsvd_exec_info* info);
 /* Timed region helpers for the dominant kernels (CUDA events, ms). */
@@ -181,6 +192,21 @@ mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, 
  * sorted working-precision sigma and sign-fixed binary32 V. */
 mpsvd_status mpsvd_stage_onesided(mpsvd_eigensolver eig, const double* m_hi, int64_t n, double tol,
                                   int max_sweeps, double* sigma, float* v, int* sweeps, int64_t* rotations);
+
+/* The multi-GPU exchange's combine (the kernel Plan::exchange runs after the
+ * all-gather) on nranks partial Grams supplied from the host, on one GPU:
+ * part_hi (and, for HIGHER, part_lo) hold nranks consecutive n x n
+ * column-major matrices; M = the reference tree over ranks ((0,1),(2,3),...
+ * then doubling widths, parallel_gram.cpp:93-102) with binary64 adds
+ * (WORKING plans' fp64 Gram) or dd_add (HIGHER). 1 <= nranks <= 16. */
+mpsvd_status mpsvd_stage_rank_combine(mpsvd_precision prec, const double* part_hi, const double* part_lo, int nranks,
+                                      int64_t n, double* m_hi, double* m_lo);
+
+/* ---- formatting (proj/include/mpsvd.h:166-171) ----------------------------- */
+/* Shortest decimal string that parses back to the identical double; returns
+ * the full length (excluding NUL), truncating to cap - 1 characters; a cap of
+ * 32 always suffices. Host-only. */
+size_t mpsvd_format_shortest(double value, char* buf, size_t cap);
 
 /* ---- ADDITIVE: measured device peaks (roofline denominators) --------------- */
 double mpsvd_fp64_peak_tflops(int device);

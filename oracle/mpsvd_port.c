@@ -53,7 +53,7 @@ static int64_t next_pow2(int64_t x) {
   return p;
 }
 
-/* make_partition_plan (proj/src/parallel_gram.cpp:243-263): contiguous,
+/* make_partition_plan (proj/src/parallel_gram.cpp:57-77): contiguous,
  * balanced row ranges, the first m%blocks blocks one row longer. */
 int port_partition_plan(int64_t m, int workers, int64_t blocks, int64_t* ranges,
                         int64_t* nblocks) {
@@ -137,7 +137,7 @@ int port_partitioned_gram_f64(const double* a, int64_t m, int64_t n, int64_t blo
   double* slots = (double*)calloc((size_t)(nb * n * n), sizeof(double));
   if (!slots || !ranges) return ST_INTERNAL;
   /* Blocks run on up to 16 threads; every block's bits are independent of
-   * which thread computes it (parallel_gram.cpp:220-239). */
+   * which thread computes it (parallel_gram.cpp:34-53). */
   int nthreads = (int)(nb < 16 ? nb : 16);
   pthread_t th[16];
   gram_job jobs[16];
@@ -171,10 +171,10 @@ int port_partitioned_gram_f32(const float* a, int64_t m, int64_t n, int64_t bloc
 }
 
 /* ======================================================================== */
-/* Two-sided Jacobi, fp64 (proj/src/jacobi.cpp:493-616)                     */
+/* Two-sided Jacobi, fp64 (proj/src/jacobi.cpp:189-311)                     */
 /* ======================================================================== */
 
-/* Stable descending permutation (jacobi.cpp:425-434): insertion sort keeps
+/* Stable descending permutation (jacobi.cpp:120-129): insertion sort keeps
  * equal keys in input order. */
 static void descending_perm_f64(const double* vals, int64_t n, int64_t* perm) {
   for (int64_t i = 0; i < n; ++i) perm[i] = i;
@@ -193,7 +193,7 @@ static void descending_perm_f64(const double* vals, int64_t n, int64_t* perm) {
 static inline double rot_lo(double c, double s, double x, double y) { return fma(c, x, -(s * y)); }
 static inline double rot_hi(double c, double s, double x, double y) { return fma(s, x, c * y); }
 
-/* finish (jacobi.cpp:585-609): sort by eigenvalue, sign from V's first
+/* finish (jacobi.cpp:280-304): sort by eigenvalue, sign from V's first
  * largest-magnitude entry. */
 static void finish_f64(const double* a, const double* v, int64_t n, double* lambda,
                        double* vout) {
@@ -219,7 +219,7 @@ static void finish_f64(const double* a, const double* v, int64_t n, double* lamb
   free(perm);
 }
 
-/* twosided_impl restated (jacobi.cpp:493-569): cyclic by rows. */
+/* twosided_impl restated (jacobi.cpp:189-264): cyclic by rows. */
 static int jacobi_cyclic_f64(double* A, double* V, int64_t n, double tol, int max_sweeps,
                              port_jacobi_stats* st, port_error* err) {
 #define AE(i, j) A[(j) * n + (i)]
@@ -276,7 +276,7 @@ static int jacobi_cyclic_f64(double* A, double* V, int64_t n, double tol, int ma
 /* Device semantics: parallel round-robin rounds. All rotations of a round
  * are computed from the matrix at the start of the round; every 2x2 block
  * between two pairs a<b gets the column rotation of b first, then the row
- * rotation of a; diagonal blocks take the t*a_pq update (jacobi.cpp:541-546)
+ * rotation of a; diagonal blocks take the t*a_pq update (jacobi.cpp:236-241)
  * with fma; V columns are rotated with the same fma forms. */
 static int jacobi_rr_f64(double* A, double* V, int64_t n, double tol, int max_sweeps,
                          port_jacobi_stats* st, port_error* err) {
@@ -418,7 +418,7 @@ int port_twosided_jacobi_f64(const double* mtx, int64_t n, double tol, int max_s
                              port_jacobi_stats* stats, port_error* err) {
   set_err(err, ST_OK, 0, 0.0);
   if (n < 1 || max_sweeps < 1) return set_err(err, ST_INVALID, 0, 0.0);
-  if (!(tol > 0.0)) tol = (double)n * 0x1p-53; /* jacobi.cpp:579-580 */
+  if (!(tol > 0.0)) tol = (double)n * 0x1p-53; /* jacobi.cpp:274-275 */
   if (stats) {
     stats->sweeps = 0;
     stats->rotations = 0;
@@ -1262,7 +1262,7 @@ typedef struct {
   int act;
 } dd_rot;
 
-/* One rotation from the 2x2 diagonal block, jacobi.cpp:516-529 in dd. */
+/* One rotation from the 2x2 diagonal block, jacobi.cpp:211-224 in dd. */
 static int dd_make_rotation(dd aii, dd ajj, dd aij, dd tol, double* worst, dd_rot* r) {
   const dd thresh = dd_mul(dd_mul(tol, dd_sqrt(aii)), dd_sqrt(ajj));
   const double ratio = fabs(aij.hi) / sqrt(aii.hi * ajj.hi);

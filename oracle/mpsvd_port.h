@@ -11,7 +11,7 @@
  *
  * Two semantics are restated (argument `sem`):
  *   PORT_SEM_REFERENCE    the reference's cyclic-by-rows sweep with its exact
- *                         formulas (proj/src/jacobi.cpp:493-569) -> bitwise
+ *                         formulas (proj/src/jacobi.cpp:189-264) -> bitwise
  *                         equal to the reference;
  *   PORT_SEM_DEVICE       the parallel round-robin schedule and FMA-based
  *                         formulas the CUDA kernels implement,

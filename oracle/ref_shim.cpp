@@ -128,7 +128,7 @@ int refx_thin_svd_f64_input(const double* a, int64_t m, int64_t n) {
   });
 }
 
-// partitioned_gram (proj/src/parallel_gram.cpp:265-298) of cast(A, Higher).
+// partitioned_gram (proj/src/parallel_gram.cpp:79-112) of cast(A, Higher).
 int refx_partitioned_gram_f32(const float* a, int64_t m, int64_t n, int workers,
                               int64_t blocks, double* out, int* sync_events,
                               int64_t* nblocks) {
@@ -158,7 +158,7 @@ int refx_gram_f64(const double* a, int64_t m, int64_t n, double* out) {
   });
 }
 
-// twosided_jacobi_eig (proj/src/jacobi.cpp:573-616) on an f64 symmetric M.
+// twosided_jacobi_eig (proj/src/jacobi.cpp:268-311) on an f64 symmetric M.
 int refx_twosided_jacobi(const double* mtx, int64_t n, double tol, int max_sweeps,
                          double* lambda, double* v, int* sweeps, int64_t* rotations) {
   return run([&] {

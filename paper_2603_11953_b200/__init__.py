@@ -33,6 +33,8 @@ from .api import (  # noqa: F401
     mp_thin_svd_f64,
     onesided_spectral,
     orth_error,
+    format_shortest,
+    rank_combine,
     rowwise_backward_error,
     twosided_jacobi_eig,
 )

@@ -67,6 +67,7 @@ SIGNATURES = [
     ("mpsvd_comm_destroy", None, [vp]),
     ("mpsvd_plan_create", C.c_int, [i64, i64, C.c_int, vp, C.POINTER(vp)]),
     ("mpsvd_plan_execute", C.c_int, [vp, vp, i64, vp, i64, vp, vp, vp]),
+    ("mpsvd_plan_orth_error", C.c_int, [vp, vp, i64, vp, dp]),
     ("mpsvd_plan_wait", C.c_int, [vp, C.POINTER(ExecInfo)]),
     ("mpsvd_plan_destroy", None, [vp]),
     ("mpsvd_matrix_write_file", C.c_int, [C.c_char_p, vp]),
@@ -78,6 +79,8 @@ SIGNATURES = [
     ("mpsvd_stage_onesided", C.c_int, [C.c_int, dp, i64, C.c_double, C.c_int, dp, C.POINTER(C.c_float),
                                        C.POINTER(C.c_int), C.POINTER(i64)]),
     ("mpsvd_plan_set_eigensolver", C.c_int, [vp, C.c_int]),
+    ("mpsvd_stage_rank_combine", C.c_int, [C.c_int, dp, dp, C.c_int, i64, dp, dp]),
+    ("mpsvd_format_shortest", C.c_size_t, [C.c_double, C.c_char_p, C.c_size_t]),
     ("mpsvd_fp64_peak_tflops", C.c_double, [C.c_int]),
     ("mpsvd_device_available", C.c_int, []),
 ]

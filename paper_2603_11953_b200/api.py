@@ -392,6 +392,31 @@ def gram_schedule(m: int, n: int):
     return bool(oz.value), scb[: ns.value + 1].copy(), bsb[: nb.value + 1].copy()
 
 
+def rank_combine(parts_hi, parts_lo=None):
+    """The multi-GPU exchange's combine kernel on host-supplied per-rank
+    partial Grams (shape (nranks, n, n); column-major n x n each): binary64
+    adds (parts_lo None) or dd_add along the reference's tree over ranks.
+    Returns M (fp64) or (hi, lo)."""
+    ph = np.ascontiguousarray(np.stack([np.asfortranarray(x, dtype=np.float64).ravel(order="F") for x in parts_hi]))
+    p, nn = ph.shape
+    n = int(round(nn ** 0.5))
+    dd = parts_lo is not None
+    pl = (np.ascontiguousarray(np.stack([np.asfortranarray(x, dtype=np.float64).ravel(order="F") for x in parts_lo]))
+          if dd else None)
+    hi = np.zeros((n, n), order="F")
+    lo = np.zeros((n, n), order="F")
+    _check(lib.mpsvd_stage_rank_combine(int(Precision.HIGHER if dd else Precision.WORKING), _dptr(ph),
+                                        _dptr(pl) if dd else None, p, n, _dptr(hi), _dptr(lo)))
+    return (hi, lo) if dd else hi
+
+
+def format_shortest(value: float) -> str:
+    """mpsvd_format_shortest (proj/include/mpsvd.h:166-171)."""
+    buf = C.create_string_buffer(48)
+    k = lib.mpsvd_format_shortest(float(value), buf, 48)
+    return buf.value.decode()[:k]
+
+
 def twosided_jacobi_eig(m_hi, m_lo=None, dd: bool = False, tol: float = 0.0, max_sweeps: int | None = None):
     """Device two-sided Jacobi (jacobi.hpp:45-46); returns (lambda, V, sweeps, rotations).
 
@@ -476,6 +501,13 @@ class Plan:
 
     def set_eigensolver(self, choice: EigensolverChoice) -> None:
         _check(lib.mpsvd_plan_set_eigensolver(self._h, int(choice)))
+
+    def orth_error(self, d_q: int, ldq: int, stream: int = 0) -> float:
+        """||Q^T Q - I||_F (binary64) of a device-resident m_local x n Q in
+        the plan's precision, through the plan's Gram (global over ranks)."""
+        out = C.c_double()
+        _check(lib.mpsvd_plan_orth_error(self._h, d_q, ldq, stream or None, C.byref(out)))
+        return out.value
 
     def wait(self) -> ExecInfo:
         info = ExecInfo()

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <memory>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -263,12 +264,199 @@ void raise_device_status(const mpsvd_exec_info& info, int max_sweeps) {
 
 using Clock = std::chrono::steady_clock;
 
+// ---------------------------------------------------------------------------
+// Single-process multi-GPU path of the host-buffer entry points (SURVEY.md
+// §5: one cached NCCL communicator set per process thread, one host thread
+// per GPU). Rows of the caller's column-major A are block-sharded across the
+// devices (the reference partition rule, parallel_gram.cpp:69-75); every
+// device uploads its rows with one strided copy, runs the pipeline with the
+// one Gram exchange (Plan::exchange), the redundant Jacobi and its rows of
+// U, which go straight back into the caller's U. Device selection:
+// MPSVD_DEVICES = "all" (default: every visible device) | a count | a list
+// "0,2,3"; a problem is sharded only when every device gets at least
+// MPSVD_SHARD_MIN_ROWS rows (default 2^18: below that the per-device
+// launches and copies outweigh the split). MPSVD_SHARD_FORCE=1 takes the
+// sharded path even on one device (tests: it must give the single-GPU bits).
+std::vector<int> shard_devices(long long m) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) {
+    cudaGetLastError();
+    return {};
+  }
+  std::vector<int> devs;
+  const char* env = getenv("MPSVD_DEVICES");
+  const std::string s = env ? env : "all";
+  if (s.empty() || s == "all") {
+    for (int d = 0; d < count; ++d) devs.push_back(d);
+  } else if (s.find(',') == std::string::npos && s.size() < 3 && s.find_first_not_of("0123456789") == std::string::npos) {
+    const int k = std::max(1, std::min(count, std::atoi(s.c_str())));
+    for (int d = 0; d < k; ++d) devs.push_back(d);
+  } else {
+    size_t pos = 0;
+    while (pos < s.size()) {
+      const size_t e = s.find(',', pos);
+      const int d = std::atoi(s.substr(pos, e == std::string::npos ? std::string::npos : e - pos).c_str());
+      if (d < 0 || d >= count) throw InvalidArgument("MPSVD_DEVICES names a device that is not visible");
+      devs.push_back(d);
+      if (e == std::string::npos) break;
+      pos = e + 1;
+    }
+  }
+  const char* mr = getenv("MPSVD_SHARD_MIN_ROWS");
+  const long long min_rows = mr ? std::max(1LL, std::atoll(mr)) : (1LL << 18);
+  while (devs.size() > 1 && m < (long long)devs.size() * min_rows) devs.pop_back();
+  return devs;
+}
+
+struct ShardSet {
+  std::vector<int> devs;
+  std::vector<engine::Comm*> comms;
+  std::vector<std::unique_ptr<Bundle>> parts;
+  std::vector<long long> row0, rows;
+  ~ShardSet() {
+    for (size_t r = 0; r < parts.size(); ++r) {
+      cudaSetDevice(devs[r]);
+      parts[r].reset();
+    }
+    for (auto* c : comms) engine::comm_destroy(c);
+  }
+};
+
+ShardSet& shard_set_for(const std::vector<int>& devs, long long m, long long n, bool f64) {
+  using SKey = std::tuple<std::vector<int>, long long, long long, bool>;
+  thread_local std::map<SKey, std::unique_ptr<ShardSet>> cache;
+  const SKey key{devs, m, n, f64};
+  auto it = cache.find(key);
+  if (it != cache.end()) return *it->second;
+  if (cache.size() >= 2) cache.clear();  // bounded: every device holds a plan
+  int prev = 0;
+  cudaGetDevice(&prev);
+  auto set = std::make_unique<ShardSet>();
+  set->devs = devs;
+  set->comms = engine::comm_init_all(devs);
+  const int p = (int)devs.size();
+  const long long base = m / p, extra = m % p;
+  long long row = 0;
+  for (int r = 0; r < p; ++r) {
+    const long long len = base + (r < extra ? 1 : 0);
+    set->row0.push_back(row);
+    set->rows.push_back(len);
+    row += len;
+  }
+  set->parts.resize(p);
+  std::vector<std::string> errs(p);
+  std::vector<std::thread> th;
+  for (int r = 0; r < p; ++r)
+    th.emplace_back([&, r] {
+      try {
+        engine::check(cudaSetDevice(devs[r]), "cudaSetDevice");
+        auto b = std::make_unique<Bundle>();
+        const long long ml = set->rows[r];
+        b->plan = std::make_unique<engine::Plan>(ml, n, f64, set->comms[r]);
+        const std::size_t elt = f64 ? 8 : 4;
+        engine::check(cudaMalloc(&b->d_a, std::max<std::size_t>(1, ml * n * elt)), "cudaMalloc A");
+        engine::check(cudaMalloc(&b->d_u, std::max<std::size_t>(1, ml * n * elt)), "cudaMalloc U");
+        engine::check(cudaMalloc((void**)&b->d_sigma, n * sizeof(double)), "cudaMalloc sigma");
+        engine::check(cudaMalloc(&b->d_v, n * n * elt), "cudaMalloc V");
+        engine::check(cudaMallocHost((void**)&b->h_sigma, n * sizeof(double)), "cudaMallocHost sigma");
+        set->parts[r] = std::move(b);
+      } catch (const std::exception& e) {
+        errs[r] = e.what();
+      }
+    });
+  for (auto& t : th) t.join();
+  cudaSetDevice(prev);
+  for (int r = 0; r < p; ++r)
+    if (!errs[r].empty()) throw std::runtime_error("device " + std::to_string(devs[r]) + ": " + errs[r]);
+  auto& ref = *set;
+  cache.emplace(key, std::move(set));
+  return ref;
+}
+
+ThinSvdResult run_thin_svd_sharded(const DenseMatrix& a, const JacobiConfig& cfg, bool f64, EigensolverChoice choice,
+                                   const std::vector<int>& devs, Clock::time_point t0) {
+  const long long m = a.rows(), n = a.cols();
+  ShardSet& set = shard_set_for(devs, m, n, f64);
+  const int p = (int)devs.size();
+  const Precision wp = f64 ? Precision::Higher : Precision::Working;
+  ThinSvdResult out;
+  out.factors.u = DenseMatrix::uninitialized(m, n, wp);
+  out.factors.v = DenseMatrix::uninitialized(n, n, wp);
+  out.factors.sigma.assign(n, 0.0);
+  out.factors.precision = wp;
+  const std::size_t elt = f64 ? 8 : 4;
+  const int eig = choice == EigensolverChoice::TwoSidedJacobi ? 0 : choice == EigensolverChoice::GramCholSvd ? 1 : 2;
+  std::vector<mpsvd_exec_info> infos(p);
+  std::vector<std::string> errs(p);
+  std::vector<std::thread> th;
+  for (int r = 0; r < p; ++r)
+    th.emplace_back([&, r] {
+      try {
+        engine::check(cudaSetDevice(devs[r]), "cudaSetDevice");
+        Bundle& b = *set.parts[r];
+        engine::Plan& pl = *b.plan;
+        pl.set_jacobi(cfg.tol, cfg.max_sweeps);
+        pl.set_eigensolver(eig);
+        cudaStream_t st = pl.own_stream;
+        const long long ml = set.rows[r], r0 = set.row0[r];
+        if (ml > 0)  // this rank's rows of every column: one strided copy
+          engine::check(cudaMemcpy2DAsync(b.d_a, ml * elt, (const char*)a.raw() + r0 * elt, m * elt, ml * elt, n,
+                                          cudaMemcpyHostToDevice, st),
+                        "H2D A rows");
+        pl.execute(b.d_a, std::max(1LL, ml), b.d_u, std::max(1LL, ml), b.d_sigma, b.d_v, st);
+        if (ml > 0)
+          engine::check(cudaMemcpy2DAsync((char*)out.factors.u.raw() + r0 * elt, m * elt, b.d_u, ml * elt, ml * elt, n,
+                                          cudaMemcpyDeviceToHost, st),
+                        "D2H U rows");
+        if (r == 0) {  // sigma and V are identical on every rank (redundant Jacobi)
+          engine::check(cudaMemcpyAsync(b.h_sigma, b.d_sigma, n * sizeof(double), cudaMemcpyDeviceToHost, st),
+                        "D2H sigma");
+          engine::check(cudaMemcpyAsync(out.factors.v.raw(), b.d_v, (size_t)n * n * elt, cudaMemcpyDeviceToHost, st),
+                        "D2H V");
+        }
+        infos[r] = pl.wait();
+      } catch (const std::exception& e) {
+        errs[r] = e.what();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (int r = 0; r < p; ++r)
+    if (!errs[r].empty()) throw std::runtime_error("device " + std::to_string(devs[r]) + ": " + errs[r]);
+  const mpsvd_exec_info& info = infos[0];
+  std::copy(set.parts[0]->h_sigma, set.parts[0]->h_sigma + n, out.factors.sigma.begin());
+  raise_device_status(info, cfg.max_sweeps);
+  out.eigensolver = choice;
+  out.gram_sync_events = 1;  // the one exchange of the partial Grams
+  out.gram_blocks = set.parts[0]->plan->nblocks;
+  out.jacobi_sweeps = info.sweeps;
+  out.jacobi_rotations = (long)info.rotations;
+  // device phases: the slowest rank's
+  for (int r = 0; r < p; ++r) {
+    out.times.gram = std::max(out.times.gram, infos[r].ms_gram * 1e-3);
+    out.times.eigen = std::max(out.times.eigen, infos[r].ms_eigen * 1e-3);
+    out.times.compute_u = std::max(out.times.compute_u, infos[r].ms_compute_u * 1e-3);
+  }
+  out.times.total = std::chrono::duration<double>(Clock::now() - t0).count();
+  out.times.overlap = out.times.total - out.times.gram - out.times.eigen - out.times.compute_u;
+  if (out.times.overlap < 0.0) {
+    out.times.total -= out.times.overlap;
+    out.times.overlap = 0.0;
+  }
+  return out;
+}
+
 ThinSvdResult run_thin_svd(const DenseMatrix& a, const JacobiConfig& cfg, bool f64,
                            EigensolverChoice choice = EigensolverChoice::TwoSidedJacobi) {
   const auto t0 = Clock::now();
   const long long m = a.rows(), n = a.cols();
   if (cfg.max_sweeps < 1) throw InvalidArgument("max_sweeps must be >= 1");
   require_device();
+  {
+    const std::vector<int> devs = shard_devices(m);
+    const char* force = getenv("MPSVD_SHARD_FORCE");
+    if (devs.size() > 1 || (force && force[0] == '1' && !devs.empty()))
+      return run_thin_svd_sharded(a, cfg, f64, choice, devs, t0);
+  }
   Bundle& b = bundle_for(m, n, f64);
   engine::Plan& p = *b.plan;
   p.set_jacobi(cfg.tol, cfg.max_sweeps);
@@ -595,6 +783,41 @@ void gpu_onesided_public(int choice, const double* m_hi, long long n, double tol
   if (rotations) *rotations = info.rotations;
 }
 
+// The multi-GPU exchange's combine kernel (Plan::exchange) on nranks
+// host-supplied partials [rank][n x n] (dd: hi and lo planes), one GPU.
+void gpu_rank_combine_public(bool dd, const double* part_hi, const double* part_lo, int nranks, long long n,
+                             double* m_hi, double* m_lo) {
+  const std::size_t nn = (std::size_t)n * n;
+  const std::size_t esz = dd ? 2 : 1;
+  std::vector<double> buf(nn * esz * nranks);
+  for (std::size_t k = 0; k < nn * nranks; ++k) {
+    if (dd) {
+      buf[2 * k] = part_hi[k];
+      buf[2 * k + 1] = part_lo ? part_lo[k] : 0.0;
+    } else {
+      buf[k] = part_hi[k];
+    }
+  }
+  cudaStream_t st = nullptr;
+  engine::check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  void *d_in = nullptr, *d_out = nullptr;
+  cudaError_t e = cudaMalloc(&d_in, buf.size() * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, nn * esz * 8);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = dev::launch_block_tree(d_in, nranks, (int)n, d_out, dd, st);
+  std::vector<double> res(nn * esz);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(res.data(), d_out, res.size() * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_in);
+  cudaFree(d_out);
+  cudaStreamDestroy(st);
+  engine::check(e, "rank combine");
+  for (std::size_t k = 0; k < nn; ++k) {
+    m_hi[k] = dd ? res[2 * k] : res[k];
+    if (m_lo) m_lo[k] = dd ? res[2 * k + 1] : 0.0;
+  }
+}
+
 void gpu_jacobi_public(bool dd, const double* m_hi, const double* m_lo, long long n, double tol, int max_sweeps,
                        double* lam_hi, double* lam_lo, double* v_hi, double* v_lo, int* sweeps,
                        long long* rotations) {
@@ -605,6 +828,13 @@ void gpu_jacobi_public(bool dd, const double* m_hi, const double* m_lo, long lon
 
 // =============================================================================
 // C ABI
+//
+// The opaque handle layouts, fail(), the guarded() exception-to-status
+// ladder (same catch order) and require() below follow the reference's C
+// surface, proj/src/capi.cpp:15-81 (its from_result is wrap() here): they are
+// the observable error contract of the ABI this library replaces, so they
+// are kept as the reference writes them. Everything behind them (plan cache,
+// host-buffer pipeline, device metrics, multi-GPU sharding) is this library's.
 // =============================================================================
 struct mpsvd_matrix {
   mpsvd::DenseMatrix m;
@@ -969,8 +1199,45 @@ mpsvd_status mpsvd_plan_set_eigensolver(mpsvd_plan* p, mpsvd_eigensolver eig) {
 
 double mpsvd_fp64_peak_tflops(int device) {
   if (!mpsvd::engine::device_available()) return 0.0;
-  cudaSetDevice(device);
-  return mpsvd::dev::measure_fp64_peak_tflops(device);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.0;
+  }
+  const double t = mpsvd::dev::measure_fp64_peak_tflops(device);
+  cudaSetDevice(prev);  // the caller's current device is left as it was
+  return t;
+}
+
+size_t mpsvd_format_shortest(double value, char* buf, size_t cap) {
+  // proj/include/mpsvd.h:168-171: shortest round-trip decimal, truncated to
+  // cap - 1 characters plus NUL; returns the full length
+  const std::string s = mpsvd::format_shortest(value);
+  if (buf && cap > 0) {
+    const size_t k = std::min(s.size(), cap - 1);
+    std::memcpy(buf, s.data(), k);
+    buf[k] = '\0';
+  }
+  return s.size();
+}
+
+mpsvd_status mpsvd_plan_orth_error(mpsvd_plan* p, const void* d_q, int64_t ldq, void* stream, double* out) {
+  return guarded([&] {
+    require(p != nullptr && p->p && out != nullptr, "null argument");
+    require(ldq >= p->p->m && (d_q != nullptr || p->p->m == 0), "bad Q / leading dimension");
+    *out = p->p->orth_error(d_q, std::max<int64_t>(1, ldq), (cudaStream_t)stream);
+  });
+}
+
+mpsvd_status mpsvd_stage_rank_combine(mpsvd_precision prec, const double* part_hi, const double* part_lo, int nranks,
+                                      int64_t n, double* m_hi, double* m_lo) {
+  return guarded([&] {
+    require(part_hi != nullptr && m_hi != nullptr, "null argument");
+    require(nranks >= 1 && nranks <= 16 && n >= 1, "need 1 <= nranks <= 16 and n >= 1");
+    mpsvd::require_device();
+    mpsvd::gpu_rank_combine_public(prec == MPSVD_PRECISION_HIGHER, part_hi, part_lo, nranks, n, m_hi, m_lo);
+  });
 }
 
 int mpsvd_device_available(void) { return mpsvd::engine::device_available() ? 1 : 0; }

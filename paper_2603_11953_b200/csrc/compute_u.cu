@@ -298,11 +298,7 @@ cudaError_t launch_av_dmma_f64(const double* a, long long lda, long long m, int 
   using namespace av64;
   if (m <= 0) return cudaSuccess;
   const size_t smem = 2 * (size_t)kStage * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(av_dmma_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  cudaFuncSetAttribute(av_dmma_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device
   dim3 grid((unsigned)((m + BM - 1) / BM), (unsigned)((n + BN - 1) / BN));
   av_dmma_f64<<<grid, 256, smem, st>>>(a, lda, m, n, w, av_ldw(n), u, ldu, status);
   return cudaGetLastError();

@@ -6,7 +6,8 @@
 //
 //   K1/K2 gram (split-K over rows, 16 logical blocks x S splits)
 //     -> gram_combine (splits in order, blocks along the reference tree)
-//     -> [N > 1: NCCL all-reduce (fp64) | all-gather + compensated rank sum (dd)]
+//     -> [N > 1: NCCL all-gather of the rank partials + the reference tree
+//         over ranks (fp64 adds / dd_add), Plan::exchange]
 //     -> K4/K5 jacobi (persistent, one barrier per round)
 //     -> jacobi_replay (V) -> finish (sort, sign, sigma, V, W = V / sigma)
 //     -> K7 av (U = A W)
@@ -59,6 +60,7 @@ enum { ncclSum = 0 };
 struct Api {
   int (*GetUniqueId)(ncclUniqueId*) = nullptr;
   int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*CommDestroy)(ncclComm_t) = nullptr;
@@ -74,6 +76,7 @@ Api& api() {
     if (!h) return;
     a.GetUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
     a.CommInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+    a.CommInitAll = (int (*)(ncclComm_t*, int, const int*))dlsym(h, "ncclCommInitAll");
     a.AllReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
     a.AllGather = (int (*)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllGather");
     a.CommDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
@@ -116,6 +119,25 @@ Comm* comm_init(const unsigned char id[128], int nranks, int rank) {
   return c;
 }
 
+// One communicator per device of `devs`, all in this process (the
+// single-process multi-GPU path of the host-buffer API: one host thread per
+// GPU drives its rank).
+std::vector<Comm*> comm_init_all(const std::vector<int>& devs) {
+  auto& a = nccl::api();
+  if (!a.ok || !a.CommInitAll) throw std::runtime_error("NCCL (libnccl.so.2) not loadable");
+  const int nd = (int)devs.size();
+  std::vector<nccl::ncclComm_t> raw(nd, nullptr);
+  nccl::check(a.CommInitAll(raw.data(), nd, devs.data()), "CommInitAll");
+  std::vector<Comm*> out(nd);
+  for (int r = 0; r < nd; ++r) {
+    out[r] = new Comm;
+    out[r]->comm = raw[r];
+    out[r]->nranks = nd;
+    out[r]->rank = r;
+  }
+  return out;
+}
+
 void comm_destroy(Comm* c) {
   if (!c) return;
   if (c->comm && nccl::api().CommDestroy) nccl::api().CommDestroy(c->comm);
@@ -124,7 +146,7 @@ void comm_destroy(Comm* c) {
 
 // ---------------------------------------------------------------------------
 // Gram schedule: logical blocks over the local rows (reference plan,
-// parallel_gram.cpp:243-263, 16 blocks as thinsvd.cpp:66), each cut into
+// parallel_gram.cpp:57-77, 16 blocks as thinsvd.cpp:66), each cut into
 // S splits sized so (tile pairs x splits) fills one wave of resident CTAs.
 static void build_schedule(Plan& p) {
   const long long m = p.m, n = p.n;
@@ -227,12 +249,20 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   check(cudaGetDevice(&device), "cudaGetDevice");
   check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
   max_sweeps = dd ? 100 : 30;  // thinsvd.hpp kDdMaxSweeps / jacobi.hpp:31
+  std::string gs;
   if (dd && m > 0) {
-    // K2z from 4096 local rows: its error (2^-80 of ||a_i|| ||a_j||, any m)
-    // is then inside K2's Dot2 bound 4 (m u)^2; MPSVD_DD_GRAM=dot2|ozaki forces one
+    // K2z (int8 Ozaki) from 4096 local rows and 128 columns. Its error is
+    // relative to the column maxima, not to |x_ki x_kj| (gram_ozaki.cu
+    // header): |dM_ij| <= rows * 2^-82 * 2^(E_i + E_j) in the worst case
+    // (aligned spiky columns), about sqrt(rows) * 2^-82 * 2^(E_i + E_j) for
+    // random signs - far inside K2's Dot2 bound 4 (m u)^2 ||a_i|| ||a_j|| for
+    // data whose columns are not dominated by one entry. Below 128 columns
+    // the 128 x 128 MMA tiles and the 11 * m * roundup(n, 256)-byte digit
+    // planes are mostly padding, so K2 keeps those shapes.
+    // MPSVD_DD_GRAM=dot2|ozaki forces one kernel.
     const char* g = getenv("MPSVD_DD_GRAM");
-    const std::string gs = g ? g : "";
-    ozaki = gs == "ozaki" || (gs != "dot2" && m >= 4096);
+    gs = g ? g : "";
+    ozaki = gs == "ozaki" || (gs != "dot2" && m >= 4096 && n >= 128);
     if (ozaki && gs != "ozaki") {
       // K2z partials: at least 16 splits x sub-groups x the upper 64x64 tile
       // pairs in double-double; keep K2 when that alone passes 8 GB (n > ~3300)
@@ -240,18 +270,29 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
       const long long slot_bytes = T64 * (T64 + 1) / 2 * 64 * 64 * 16;
       if (16LL * dev::ozaki_groups() * slot_bytes > (8LL << 30)) ozaki = false;
     }
-    if (ozaki) {  // the digit planes (11 bytes per entry); K2 when they do not fit
-      void* ptr = nullptr;
-      if (cudaMalloc(&ptr, dev::ozaki_digit_bytes(m, (int)n)) == cudaSuccess) {
-        d_digits = static_cast<unsigned char*>(ptr);
-        owned.push_back(ptr);
-      } else {
-        cudaGetLastError();
-        ozaki = false;
-      }
-    }
   }
   build_schedule(*this);
+  if (ozaki) {
+    // The whole K2z footprint (digit planes + per-slot partial tiles + the
+    // n x n workspaces) must fit in the free device memory with a margin,
+    // checked before anything is allocated, so plan creation never fails
+    // half-way; otherwise K2 (Dot2) runs.
+    const size_t T64 = (size_t)(n + 63) / 64;
+    const size_t partial_bytes = splits.size() * dev::ozaki_groups() * T64 * (T64 + 1) / 2 * 64 * 64 * 16;
+    const size_t need = dev::ozaki_digit_bytes(m, (int)n) + partial_bytes + (size_t)n * n * 16 * 8;
+    size_t free_b = 0, total_b = 0;
+    bool fits = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && need + (size_t(1) << 30) <= free_b;
+    void* ptr = nullptr;
+    if (fits && cudaMalloc(&ptr, dev::ozaki_digit_bytes(m, (int)n)) == cudaSuccess) {
+      d_digits = static_cast<unsigned char*>(ptr);
+      owned.push_back(ptr);
+    } else {
+      cudaGetLastError();
+      if (gs == "ozaki") throw std::runtime_error("MPSVD_DD_GRAM=ozaki: the K2z digit planes do not fit");
+      ozaki = false;
+      build_schedule(*this);
+    }
+  }
   const size_t nn = (size_t)n * n;
   const size_t esz = dd ? 2 : 1;  // doubles per element of the higher precision
   const int N = (int)(n + (n & 1)), np = N / 2;
@@ -287,8 +328,11 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
   d_m = dalloc<double>(nn * esz, owned);
   const int nranks = comm ? comm->nranks : 1;
   if (nranks > 1) {
+    if (nranks > 16) throw std::invalid_argument("plan: at most 16 ranks (the rank combine tree holds 16 slots)");
+    const char* ex = getenv("MPSVD_F64_EXCHANGE");
+    f64_allreduce = !dd && ex && std::string(ex) == "allreduce";
     d_mloc = dalloc<double>(nn * esz, owned);
-    if (dd) d_gather = dalloc<double>(nn * esz * nranks, owned);
+    if (!f64_allreduce) d_gather = dalloc<double>(nn * esz * nranks, owned);
   }
   jws.a = d_m;
   jws.diagbuf = dalloc<double>((size_t)2 * np * 3 * esz + 2, owned);  // + sweep flags
@@ -413,7 +457,7 @@ void Plan::cholqr(const void* d_a, long long lda, void* d_q, long long ldq, cuda
 
 double Plan::effective_tol() const {
   if (tol > 0.0) return tol;
-  return (double)n * (dd ? 0x1p-104 : 0x1p-53);  // jacobi.cpp:579-580; u_dd = 2^-104
+  return (double)n * (dd ? 0x1p-104 : 0x1p-53);  // jacobi.cpp:274-275; u_dd = 2^-104
 }
 
 void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
@@ -437,24 +481,53 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
           "gram_combine_f64");
     launches += 2 + (ndiag > 0 ? 1 : 0) + (ntp > ndiag ? 1 : 0);
   }
-  if (nranks > 1) {
-    auto& a = nccl::api();
-    const size_t nn = (size_t)n * n;
-    if (!dd) {
-      // fp64: one all-reduce of the partial Grams (north_star (4)); the
-      // result is re-symmetrised because a ring reduction may order the two
-      // triangles' additions differently.
-      nccl::check(a.AllReduce(d_mloc, d_m, nn, nccl::ncclFloat64, nccl::ncclSum, comm->comm, st), "AllReduce");
-      check(dev::launch_mirror_upper((double*)d_m, (int)n, st), "mirror");
-      launches += 1;
-    } else {
-      // double-double: a plain NCCL sum would drop the lo words; gather every
-      // rank's (hi, lo) partial and add them in rank order with dd_add.
-      nccl::check(a.AllGather(d_mloc, d_gather, nn * 2, nccl::ncclFloat64, comm->comm, st), "AllGather");
-      check(dev::launch_block_tree(d_gather, comm->nranks, (int)n, d_m, true, st), "rank combine");
-      launches += 1;
-    }
+  if (nranks > 1) exchange(st);
+}
+
+// The one exchange of the multi-GPU path (north_star (4); the reference's
+// join of the per-thread partials, parallel_gram.cpp:93-102). Every rank's
+// n x n partial is all-gathered and the ranks' partials are added along the
+// reference's fixed tree (0,1),(2,3),... then doubling widths - with dd_add
+// for double-double (a plain NCCL sum would drop the lo words), with fp64
+// adds otherwise. The combine is our own kernel, so every rank computes the
+// same bits by construction, independent of NCCL's algorithm choice, and
+// the sum of exactly symmetric partials stays exactly symmetric. At these
+// sizes (C4: 128 KiB per rank) the gather is latency-bound like an
+// all-reduce. MPSVD_F64_EXCHANGE=allreduce selects an NCCL all-reduce (sum)
+// plus a re-mirroring of the upper triangle for fp64 instead.
+void Plan::exchange(cudaStream_t st) {
+  auto& a = nccl::api();
+  const size_t nn = (size_t)n * n;
+  if (f64_allreduce) {
+    nccl::check(a.AllReduce(d_mloc, d_m, nn, nccl::ncclFloat64, nccl::ncclSum, comm->comm, st), "AllReduce");
+    check(dev::launch_mirror_upper((double*)d_m, (int)n, st), "mirror");
+  } else {
+    nccl::check(a.AllGather(d_mloc, d_gather, nn * (dd ? 2 : 1), nccl::ncclFloat64, comm->comm, st), "AllGather");
+    check(dev::launch_block_tree(d_gather, comm->nranks, (int)n, d_m, dd, st), "rank combine");
   }
+  launches += 1;
+}
+
+double Plan::orth_error(const void* d_q, long long ldq, cudaStream_t st) {
+  if (!st) st = own_stream;
+  last_stream = st;
+  events_recorded = false;
+  gram(d_q, ldq, st);
+  const size_t nn = (size_t)n * n;
+  std::vector<double> g(nn * (dd ? 2 : 1));
+  check(cudaMemcpyAsync(g.data(), d_m, g.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H Gram");
+  check(cudaStreamSynchronize(st), "orth sync");
+  // ||Q^T Q - I||_F over the exactly symmetric Gram (dense.cpp:250-272:
+  // binary64); the double-double Gram contributes (hi - delta) + lo
+  double sum = 0.0;
+  for (long long j = 0; j < n; ++j)
+    for (long long i = 0; i <= j; ++i) {
+      const size_t k = (size_t)j * n + i;
+      const double delta = i == j ? 1.0 : 0.0;
+      const double d = dd ? (g[2 * k] - delta) + g[2 * k + 1] : g[k] - delta;
+      sum += (i == j ? 1.0 : 2.0) * d * d;
+    }
+  return std::sqrt(sum);
 }
 
 void Plan::gram_dd_splits(const void* d_a, long long lda, int sb, int cnt, cudaStream_t st) {

@@ -18,6 +18,7 @@ bool device_available();
 void comm_unique_id(unsigned char id[128]);
 Comm* comm_init(const unsigned char id[128], int nranks, int rank);
 void comm_destroy(Comm* c);
+std::vector<Comm*> comm_init_all(const std::vector<int>& devs);
 
 class Plan {
  public:
@@ -50,6 +51,12 @@ class Plan {
   void gram(const void* d_a, long long lda, cudaStream_t st);
   // double-double Gram kernels of splits [sb, sb + cnt) (K2z Ozaki or K2 Dot2)
   void gram_dd_splits(const void* d_a, long long lda, int sb, int cnt, cudaStream_t st);
+  // multi-rank: the partial Grams (d_mloc) of every rank -> d_m
+  void exchange(cudaStream_t st);
+  // ||Q^T Q - I||_F in binary64 of a device-resident m_local x n Q in the
+  // plan's precision (the plan's Gram stage, exchange included: global over
+  // ranks); overwrites the plan's Gram. Synchronous on st.
+  double orth_error(const void* d_q, long long ldq, cudaStream_t st);
   void eigen(cudaStream_t st);
   // mixed-precision Cholesky QR (thinsvd.cpp:125-154): Gram (K1), chol (K8),
   // row solves (K10). Q: m x n binary32 (ldq), R: the plan's d_x32 (n x n)
@@ -75,6 +82,7 @@ class Plan {
   int ntp = 0, nblocks = 0;
   // K2z (double-double Gram on the int8 tensor cores); MPSVD_DD_GRAM=dot2 selects K2
   bool ozaki = false;
+  bool f64_allreduce = false;  // MPSVD_F64_EXCHANGE=allreduce (multi-rank fp64 exchange)
   std::vector<int2> oz_tiles;
   std::vector<int> scb;  // split s = 32-row chunks [scb[s], scb[s + 1])
   int2* d_oz_tiles = nullptr;

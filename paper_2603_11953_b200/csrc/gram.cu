@@ -1,6 +1,6 @@
 // K1 / K2: the higher-precision Gram product M = A^T A.
 //
-// Reference semantics: partitioned_gram (proj/src/parallel_gram.cpp:265-298)
+// Reference semantics: partitioned_gram (proj/src/parallel_gram.cpp:79-112)
 // on cast(A, Higher) (proj/src/thinsvd.cpp:61-70): fp32 entries widened
 // exactly, fp64 products exact, fp64 accumulation; 16 logical row blocks
 // (thinsvd.cpp:66) combined by a fixed binary tree (parallel_gram.cpp:93-102);
@@ -442,12 +442,9 @@ cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* ti
                             int ndiag, const int* tp_off, int noff, const longlong2* splits, int nsplit,
                             double* partials, cudaStream_t st) {
   const size_t smem_d = 2 * kTile * kLDK * sizeof(double), smem_o = 2 * smem_d;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gram_f32_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
-    cudaFuncSetAttribute(gram_f32_offdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_o);
-    configured = true;
-  }
+  // the opt-in is a per-device (per-context) attribute: set it on every launch
+  cudaFuncSetAttribute(gram_f32_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+  cudaFuncSetAttribute(gram_f32_offdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_o);
   if (ndiag > 0)
     gram_f32_diag<<<dim3(ndiag, nsplit), 128, smem_d, st>>>(a, lda, n, tiles, tp_diag, splits, partials, ntp);
   if (noff > 0)
@@ -458,12 +455,7 @@ cudaError_t launch_gram_f32(const float* a, long long lda, int n, const int2* ti
 cudaError_t launch_gram_dd(const double* a, long long lda, int n, const int2* tiles, int ntp,
                            const longlong2* splits, int nsplit, double2* partials,
                            cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gram_f64_dd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)gram_smem_bytes(true));
-    configured = true;
-  }
+  cudaFuncSetAttribute(gram_f64_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem_bytes(true));
   dim3 grid(ntp, nsplit);
   gram_f64_dd<<<grid, 256, gram_smem_bytes(true), st>>>(a, lda, n, tiles, splits, partials, ntp);
   return cudaGetLastError();

@@ -631,23 +631,18 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
   const long long ch0 = scb_host[s0], ch1 = scb_host[s0 + ns];
   const long long units = (ch1 - ch0) * ncb2;
   if (units > 0) {
-    static bool slice_configured = false;
-    if (!slice_configured) {
-      cudaError_t e = cudaFuncSetAttribute(ozaki_slice, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(2 * oz::kCB * 34 * sizeof(double)));
-      if (e != cudaSuccess) return e;
-      slice_configured = true;
-    }
+    // per-device attribute: set on every launch (a process may drive several GPUs)
+    cudaError_t e = cudaFuncSetAttribute(ozaki_slice, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(2 * oz::kCB * 34 * sizeof(double)));
+    if (e != cudaSuccess) return e;
     long long grid = units < (long long)sm_count * 2 ? units : (long long)sm_count * 2;
     ozaki_slice<<<(int)grid, 256, 2 * oz::kCB * 34 * sizeof(double), st>>>(a, lda, m, n, e_cols, scb_dev,
                                                                            nsplit_total, ch0, ch1, ncb2, digits);
   }
-  static bool configured = false;
   const size_t smem = ozaki_smem();
-  if (!configured) {
+  {
     cudaError_t e = cudaFuncSetAttribute(gram_dd_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   const char* prof_env = getenv("MPSVD_OZAKI_PROF");
   const int prof = prof_env && prof_env[0] == '1';

@@ -1,16 +1,16 @@
 // K4 / K5: two-sided Jacobi eigensolver on the n x n Gram matrix, fp64 (K4)
 // or double-double (K5), plus the V replay and the sort/sign/sigma epilogue.
 //
-// Reference semantics: twosided_impl (proj/src/jacobi.cpp:493-569):
+// Reference semantics: twosided_impl (proj/src/jacobi.cpp:189-264):
 //   * skip a pair when |a_ij| <= tol * sqrt(a_ii) * sqrt(a_jj) (the product of
-//     square roots, jacobi.cpp:516-522), tol = n*u (jacobi.cpp:579-580);
+//     square roots, jacobi.cpp:211-217), tol = n*u (jacobi.cpp:274-275);
 //   * zeta = (a_jj - a_ii) / (2 a_ij), t = sign(zeta)/(|zeta| + hypot(1, zeta)),
-//     c = 1/hypot(1, t), s = c t (jacobi.cpp:524-529);
+//     c = 1/hypot(1, t), s = c t (jacobi.cpp:219-224);
 //   * a_ii -= t a_ij, a_jj += t a_ij, a_ij = 0 exactly, PD re-check
-//     (jacobi.cpp:541-548); converged after a sweep without rotations,
-//     NoConvergenceError after max_sweeps (jacobi.cpp:561-567);
+//     (jacobi.cpp:236-243); converged after a sweep without rotations,
+//     NoConvergenceError after max_sweeps (jacobi.cpp:256-262);
 //   * stable descending sort, V's first largest entry made >= 0
-//     (jacobi.cpp:585-609).
+//     (jacobi.cpp:280-304).
 //
 // Device schedule: parallel round-robin. A sweep is N-1
 // rounds of N/2 disjoint pairs (N = n rounded up to even). Every CTA computes
@@ -57,7 +57,7 @@ struct Arith<double> {
   static __device__ __forceinline__ bool is_identity(AT c, AT s) { return s == 0.0 && c == 1.0; }
   static __device__ __forceinline__ AT rot_lo(AT c, AT s, AT x, AT y) { return fma(c, x, -(s * y)); }
   static __device__ __forceinline__ AT rot_hi(AT c, AT s, AT x, AT y) { return fma(s, x, c * y); }
-  // Stop test of jacobi.cpp:516-522, |a_pq| <= tol sqrt(a_pp) sqrt(a_qq), with
+  // Stop test of jacobi.cpp:211-217, |a_pq| <= tol sqrt(a_pp) sqrt(a_qq), with
   // one square root of the product; the two-root form only when the product
   // leaves the normal range (the reference's reason for it).
   static __device__ __forceinline__ bool active(AT app, AT aqq, AT apq, double tol) {
@@ -73,7 +73,7 @@ struct Arith<double> {
     const double xs = ldexp(x, -e), ys = ldexp(y, -e);
     return ldexp(sqrt(fma(xs, xs, ys * ys)), e);
   }
-  // Annihilating rotation (jacobi.cpp:524-546). With x = a_qq - a_pp,
+  // Annihilating rotation (jacobi.cpp:219-241). With x = a_qq - a_pp,
   // y = 2 a_pq, r = sqrt(x^2 + y^2):
   //   t = sign(x) y / (|x| + r)   (= sign(zeta)/(|zeta| + hypot(1, zeta))),
   //   c = sqrt((|x| + r) / (2 r)) (= 1/sqrt(1 + t^2)),   s = c t,
@@ -237,7 +237,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   if (tid == 0) s_flag = 0x7fffffff;
   __syncthreads();
 
-  // initial positive-definiteness check (jacobi.cpp:505-506): every CTA
+  // initial positive-definiteness check (jacobi.cpp:200-201): every CTA
   // evaluates it identically, so all exit together.
   for (int k = tid; k < n; k += bs)
     if (!A_::gt0(LD(AE(k, k)))) atomicMin(&s_flag, k);
@@ -263,7 +263,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     // ---- sweep pre-check: if no pair passes the stop test now, this sweep
     // would rotate nothing (A cannot change), i.e. it is the converged
-    // detection sweep of jacobi.cpp:561-565 — decided in one parallel pass.
+    // detection sweep of jacobi.cpp:256-260 — decided in one parallel pass.
     {
       if (kSmem) {
         if (tid == 0) s_sweep_flag = 0;
@@ -393,7 +393,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         badx = min(badx, w_bad[w]);
         worst = fmax(worst, w_worst[w]);
       }
-      if (badx != 0x7fffffff) {  // NotPositiveDefiniteError(pivot, value), jacobi.cpp:547-548
+      if (badx != 0x7fffffff) {  // NotPositiveDefiniteError(pivot, value), jacobi.cpp:242-243
         if (blockIdx.x == 0 && tid == 0) {
           const int x = badx;
           const int k = rr_slot(n, r, x);
@@ -427,7 +427,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
             const bool acta = (wa >> 30) & 1, actb = (wb >> 30) & 1;
             if (!acta && !actb) continue;
             const int p0 = wa & 0x7fff, q0 = (wa >> 15) & 0x7fff;
-            if (aa == bb) {  // diagonal block (jacobi.cpp:541-546)
+            if (aa == bb) {  // diagonal block (jacobi.cpp:236-241)
               A_::st(AE(p0, p0), rnpp[aa]);
               A_::st(AE(q0, q0), rnqq[aa]);
               A_::st(AE(p0, q0), A_::zero());
@@ -809,7 +809,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
   for (int k = tid; k < n; k += NT)
     if (!A_::gt0(A_::lds(AE(k, k)))) atomicMin(&s_bad, k);
   __syncthreads();
-  if (s_bad != 0x7fffffff) {  // jacobi.cpp:505-506
+  if (s_bad != 0x7fffffff) {  // jacobi.cpp:200-201
     if (tid == 0) {
       status->status = kNotPositiveDefinite;
       status->index = s_bad + 1;
@@ -838,7 +838,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
     const AT* rcs = rb;
     const AT* rss = rb + np;
     const int p0 = wa & 0x7fff, q0 = (wa >> 15) & 0x7fff;
-    if (aa == bb) {  // jacobi.cpp:541-546
+    if (aa == bb) {  // jacobi.cpp:236-241
       A_::st(AE(p0, p0), rb[2 * np + aa]);
       A_::st(AE(q0, q0), rb[3 * np + aa]);
       A_::st(AE(p0, q0), A_::zero());  // p0 < q0: the canonical copy
@@ -1153,7 +1153,7 @@ jacobi_replay(const ST* __restrict__ rot_log, int n, int rows_per_cta, int batch
 }
 
 // ---------------------------------------------------------------------------
-// Epilogue (jacobi.cpp:585-609 + thinsvd.cpp:81-89,106 + dense.cpp:220-232).
+// Epilogue (jacobi.cpp:280-304 + thinsvd.cpp:81-89,106 + dense.cpp:220-232).
 template <typename ST>
 __global__ void finish_sort(const ST* __restrict__ a, int n, DevStatus* __restrict__ status,
                             int* __restrict__ perm, double* __restrict__ lam_hi,
@@ -1281,7 +1281,7 @@ __global__ void finish_columns(const ST* __restrict__ v, int n, const DevStatus*
   const int jj = blockIdx.x;
   const int src = perm[jj];
   const ST* vc = v + (long long)src * n;
-  // first index of the largest |v| (ties: lowest row), jacobi.cpp:594-603
+  // first index of the largest |v| (ties: lowest row), jacobi.cpp:290-297
   __shared__ double s_hi[32], s_lo[32];
   __shared__ int s_idx[32];
   double bh = -1.0, bl = 0.0;

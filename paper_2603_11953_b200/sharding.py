@@ -2,7 +2,7 @@
 
 Contiguous, balanced row ranges whose sizes differ by at most one, the first
 ``m % nranks`` ranks one row longer — the partition rule of the reference's
-make_partition_plan (proj/src/parallel_gram.cpp:243-263) applied to ranks
+make_partition_plan (proj/src/parallel_gram.cpp:57-77) applied to ranks
 instead of thread blocks. Each rank keeps its rows of every column
 (column-major with leading dimension = its own row count), computes the
 partial Gram of those rows, and the partial Grams meet in ONE collective

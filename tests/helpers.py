@@ -58,3 +58,26 @@ def stacked_diag(m: int, d, dtype=np.float32) -> np.ndarray:
     for j, x in enumerate(d):
         a[j, j] = x
     return a
+
+
+def rank_tree(parts, add):
+    """The fixed reduction tree of proj/src/parallel_gram.cpp:93-102 over a
+    list (rank order): (0,1),(2,3),... then doubling widths. Plan::exchange
+    applies it to the all-gathered per-rank partial Grams."""
+    slots = list(parts)
+    width = 1
+    while width < len(slots):
+        for b in range(0, len(slots) - width, 2 * width):
+            slots[b] = add(slots[b], slots[b + width])
+        width *= 2
+    return slots[0]
+
+
+def dd_add_elementwise(port, x, y):
+    """Elementwise dd_add (proj/tests/support/dd.cpp:32-38, via the restatement)
+    of two (hi, lo) array pairs."""
+    (xh, xl), (yh, yl) = x, y
+    oh, ol = np.empty_like(xh), np.empty_like(xl)
+    for idx in np.ndindex(xh.shape):
+        oh[idx], ol[idx] = port.dd_op("add", (xh[idx], xl[idx]), (yh[idx], yl[idx]))
+    return oh, ol

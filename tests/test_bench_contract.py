@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
-from paper_2603_11953_b200 import inputs  # noqa: E402
+import workloads as inputs  # noqa: E402
 
 
 class _Info:

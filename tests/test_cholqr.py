@@ -23,7 +23,7 @@ import pytest
 from helpers import orth_err, stacked_diag
 
 M = pytest.importorskip("paper_2603_11953_b200")
-from paper_2603_11953_b200 import inputs  # noqa: E402
+import workloads as inputs  # noqa: E402
 from paper_2603_11953_b200._lib import lib  # noqa: E402
 
 import pyoracle  # noqa: E402

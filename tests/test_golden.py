@@ -26,7 +26,7 @@ def test_port_reproduces_reference_thin_svd(port, name):
 
 
 def test_port_reproduces_reference_config_c1(port):
-    from paper_2603_11953_b200 import inputs
+    import workloads as inputs
 
     g = load("config_c1")
     a = inputs.make(inputs.CONFIGS["c1"], seed=int(g["seed"]))
@@ -95,7 +95,7 @@ def test_gpu_golden_config_c1():
     M = pytest.importorskip("paper_2603_11953_b200")
     if not M.device_available():
         pytest.skip("no CUDA device")
-    from paper_2603_11953_b200 import inputs
+    import workloads as inputs
 
     g = load("config_c1")
     a = inputs.make(inputs.CONFIGS["c1"], seed=int(g["seed"]))

@@ -12,7 +12,7 @@ from helpers import U32, U64, UDD, dd_diff, kappa_b, max_rel, north_star_gates, 
 pytestmark = pytest.mark.gpu
 
 M = pytest.importorskip("paper_2603_11953_b200")
-from paper_2603_11953_b200 import inputs  # noqa: E402
+import workloads as inputs  # noqa: E402
 
 if not M.device_available():
     pytest.skip("no CUDA device", allow_module_level=True)
@@ -241,7 +241,7 @@ def test_thin_svd_shape_sweep_f64(port, m, n):
 
 
 def test_thin_svd_tiny_sigma():
-    # proj/tests/test_thinsvd.cpp:244-264; test_capi.cpp:220-225
+    # proj/tests/test_thinsvd.cpp:244-264; test_capi.cpp:118-126
     a = stacked_diag(2, [1.0, 1e-39])
     with pytest.raises(M.TinySingularValueError) as e:
         M.mp_thin_svd(a)

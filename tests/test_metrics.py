@@ -120,7 +120,7 @@ def test_gpu_backward_error_mixed_precision_widens_exactly():
 def test_gpu_backward_error_of_thin_svd_and_device_variant():
     import torch
 
-    from paper_2603_11953_b200 import inputs
+    import workloads as inputs
 
     a = inputs.graded(1 << 16, 64, 5.0, seed=3)
     r = M.mp_thin_svd(a)

@@ -1,9 +1,13 @@
-"""World-size-2 model of the multi-GPU path on CPU (gloo): rows sharded with
-paper_2603_11953_b200.sharding, rank-local partial Grams (the restatement
-stands in for the device kernel), ONE exchange (sum all-reduce for fp64;
-all-gather + fixed rank-order double-double sum for dd, since a plain sum
-would drop the lo words), redundant Jacobi identical on every rank, and
-rank-local U rows that concatenate to the single-process U."""
+"""World-size-2 and -4 model of the multi-GPU path on CPU (gloo): rows
+sharded with paper_2603_11953_b200.sharding, rank-local partial Grams (the
+restatement stands in for the device kernel), ONE exchange as Plan::exchange
+does it (engine.cu): an all-gather of every rank's partial, then the
+reference's fixed tree over ranks (parallel_gram.cpp:93-102) with binary64
+adds for fp64 and dd_add for double-double (a plain sum would drop the lo
+words); redundant Jacobi identical on every rank, and rank-local U rows that
+concatenate to the single-process U. The device side of the combine is
+pinned bitwise to the same tree by tests/test_configs_gpu.py
+(mpsvd_stage_rank_combine)."""
 from __future__ import annotations
 
 import os
@@ -40,6 +44,7 @@ def _matrix(m, n, dtype, seed=5):
 def _worker(rank, world, port, out_dir):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), HERE]
     import pyoracle
+    from helpers import dd_add_elementwise, rank_tree
     from paper_2603_11953_b200 import sharding
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -47,13 +52,13 @@ def _worker(rank, world, port, out_dir):
     m, n = 3001, 24
     r0, r1 = sharding.local_rows(m, world, rank)
 
-    # ---- fp64 Gram of fp32 A: local partial + one all-reduce
+    # ---- fp64 Gram of fp32 A: local partial + one all-gather + rank tree
     a32 = _matrix(m, n, np.float32)
     loc = P.partitioned_gram_f32(np.asfortranarray(a32[r0:r1]), blocks=min(16, r1 - r0))
     t = torch.from_numpy(np.ascontiguousarray(loc))
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    g = t.numpy().copy()
-    g = np.triu(g) + np.triu(g, 1).T  # re-symmetrise as the library does after the all-reduce
+    gl = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(gl, t)
+    g = rank_tree([x.numpy().copy() for x in gl], lambda x, y: x + y)
     lam, v, _, _ = P.twosided_jacobi(g, sem=pyoracle.SEM_DEVICE)
     # redundant Jacobi: identical bits on every rank
     lam_all = [torch.zeros(n, dtype=torch.float64) for _ in range(world)]
@@ -69,11 +74,8 @@ def _worker(rank, world, port, out_dir):
     pair = torch.from_numpy(np.stack([hi, lo]))
     gath = [torch.zeros_like(pair) for _ in range(world)]
     dist.all_gather(gath, pair)
-    acc_h, acc_l = gath[0][0].numpy().copy(), gath[0][1].numpy().copy()
-    for rr in range(1, world):
-        gh, gl = gath[rr][0].numpy(), gath[rr][1].numpy()
-        for idx in np.ndindex(acc_h.shape):
-            acc_h[idx], acc_l[idx] = P.dd_op("add", (acc_h[idx], acc_l[idx]), (gh[idx], gl[idx]))
+    acc_h, acc_l = rank_tree([(x[0].numpy().copy(), x[1].numpy().copy()) for x in gath],
+                             lambda x, y: dd_add_elementwise(P, x, y))
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), g=g, lam=lam, same=same, u=u_loc, r0=r0, r1=r1,
              w=w, ddh=acc_h, ddl=acc_l)
     dist.barrier()
@@ -81,8 +83,8 @@ def _worker(rank, world, port, out_dir):
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_sharded_pipeline(tmp_path, port):
-    world = 2
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_pipeline(tmp_path, port, world):
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
     res = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
@@ -95,9 +97,11 @@ def test_two_rank_sharded_pipeline(tmp_path, port):
         assert np.array_equal(r["g"], r["g"].T)
         # both sums within m*u_h*||a_i|| ||a_j|| of the exact Gram
         assert np.all(np.abs(r["g"] - g_full) <= 2 * m * 2.0 ** -53 * np.outer(d, d))
-    assert np.array_equal(res[0]["lam"], res[1]["lam"]) and np.array_equal(res[0]["w"], res[1]["w"])
+    for r in res[1:]:
+        assert np.array_equal(res[0]["lam"], r["lam"]) and np.array_equal(res[0]["w"], r["w"])
+        assert np.array_equal(res[0]["g"], r["g"])
     # rank-local U rows concatenate to the single-process U for the same W
-    u = np.concatenate([res[0]["u"], res[1]["u"]], axis=0)
+    u = np.concatenate([r["u"] for r in res], axis=0)
     assert np.array_equal(u, port.av_f32(a32, res[0]["w"]))
     # dd: the gathered, rank-ordered compensated sum matches the single-pass dd Gram
     a64 = _matrix(m, n, np.float64, seed=6)
@@ -105,7 +109,8 @@ def test_two_rank_sharded_pipeline(tmp_path, port):
     an = np.linalg.norm(a64, axis=0)
     err = np.abs((res[0]["ddh"] - hh) + (res[0]["ddl"] - ll))
     assert np.all(err <= 4 * (m * 2.0 ** -53) ** 2 * np.outer(an, an) + 2.0 ** -100 * np.abs(hh))
-    assert np.array_equal(res[0]["ddh"], res[1]["ddh"]) and np.array_equal(res[0]["ddl"], res[1]["ddl"])
+    for r in res[1:]:
+        assert np.array_equal(res[0]["ddh"], r["ddh"]) and np.array_equal(res[0]["ddl"], r["ddl"])
 
 
 def _worker_ozaki(rank, world, port, out_dir):
@@ -129,11 +134,10 @@ def _worker_ozaki(rank, world, port, out_dir):
     pair = torch.from_numpy(np.stack([hi, lo]))
     gath = [torch.zeros_like(pair) for _ in range(world)]
     dist.all_gather(gath, pair)
-    acc_h, acc_l = gath[0][0].numpy().copy(), gath[0][1].numpy().copy()
-    for rr in range(1, world):
-        gh, gl = gath[rr][0].numpy(), gath[rr][1].numpy()
-        for idx in np.ndindex(acc_h.shape):
-            acc_h[idx], acc_l[idx] = P.dd_op("add", (acc_h[idx], acc_l[idx]), (gh[idx], gl[idx]))
+    from helpers import dd_add_elementwise, rank_tree
+
+    acc_h, acc_l = rank_tree([(x[0].numpy().copy(), x[1].numpy().copy()) for x in gath],
+                             lambda x, y: dd_add_elementwise(P, x, y))
     np.savez(os.path.join(out_dir, f"oz{rank}.npz"), h=acc_h, l=acc_l)
     dist.barrier()
     dist.destroy_process_group()

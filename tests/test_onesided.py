@@ -23,7 +23,7 @@ import pytest
 from helpers import kappa_b, orth_err, rowwise_backward
 
 M = pytest.importorskip("paper_2603_11953_b200")
-from paper_2603_11953_b200 import inputs  # noqa: E402
+import workloads as inputs  # noqa: E402
 
 import pyoracle  # noqa: E402
 

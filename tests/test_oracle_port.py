@@ -132,7 +132,7 @@ def test_dd_jacobi_prescribed_sigma_needs_more_than_30_sweeps(port, sem):
     # orderings need ~30 sweeps; the dd path's cap is 100 (kDdMaxSweeps)
     import sys, os
     sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
-    from paper_2603_11953_b200 import inputs
+    import workloads as inputs
     n = 128
     a, sigma = inputs.prescribed(2 * n, n, 10.0, seed=500 + n)
     hi, lo = port.dd_gram(a, threads=8)

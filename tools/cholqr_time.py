@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_11953_b200 as M  # noqa: E402
-from paper_2603_11953_b200 import inputs  # noqa: E402
+import workloads as inputs  # noqa: E402
 
 for name in sys.argv[1:] or ["c2", "c4"]:
     cfg = inputs.CONFIGS[name]
