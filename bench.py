@@ -1,19 +1,24 @@
 """Benchmark: one step = one full thin SVD (Gram + Jacobi + U) of one
 synthetic matrix of a BASELINE.json configuration, device-resident.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
-N=1 runs configs[1] (c2: m=2^20, n=64, fp32, Gram/Jacobi fp64). For N>1 the
-driver launches one process per GPU (torchrun); rows are block-sharded, the
-partial Grams combined by NCCL inside the library (all-reduce for fp64,
-all-gather + compensated sum for double-double), Jacobi replicated, U
-rank-local. c2 scales weakly (2^20 rows per rank); c4 strongly (2^26 rows in
-total). Rank 0 prints ONE JSON line.
+The default workload is c4 (m=2^26, n=128, fp32 working, Gram in fp64,
+Gaussian A): the largest single-GPU configuration of BASELINE.json's
+binary32 path, the one its north_star quotes the >= 60 % roofline and the
+>= 6x 8-GPU scaling targets on. For N>1 the driver launches one process per
+GPU (torchrun); the 2^26 rows are block-sharded (strong scaling), each rank
+forms its partial Gram, the partials meet in ONE NCCL all-gather followed by
+the reference's fixed tree over ranks inside the library, the Jacobi is
+replicated and U stays rank-local. (c2 runs weak scaling: 2^20 rows per
+rank.) Rank 0 prints ONE JSON line.
 
 `--impl reference` times the reference's own CPU implementation (the
 unmodified reference compiled in place, oracle/_ref; the C restatement
-oracle/_port when the reference is absent or has no path, i.e. the
-double-double configs) on the host cores, on a bounded row sample.
+oracle/_port when the reference has no path, i.e. the double-double
+configs) on the host cores, on a row sample sized so the whole run stays
+within a few minutes. That arm imports only oracle/ and workloads.py, never
+the product library.
 """
 from __future__ import annotations
 
@@ -136,6 +141,45 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
     return out
 
 
+def latency_probe():
+    """Measured latency floors (tools/microbench/rot_latency.cu on the B200,
+    committed as profiles/r02_latency_probe.json): cycles of one dependent
+    fp64 rotation (stop test + rotation), one 512-thread __syncthreads
+    hand-off, one 148-CTA cooperative grid.sync."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_latency_probe.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def jacobi_latency(n: int, info, eigen_ms: float, dd: bool, clock_mhz: float = 1965.0):
+    """The two-sided Jacobi against its latency floor: every parallel round is
+    one dependent rotation evaluation followed by one hand-off (a CTA barrier
+    for the single-CTA solver, n <= 128 fp64 / <= 100 dd; a grid barrier for
+    the cooperative solver), so T_floor = rounds x (rotation chain +
+    barrier). The eigen phase also holds the V replay / finish kernels."""
+    rounds = int(getattr(info, "rounds", 0) or 0)
+    out = {"kernel": "jacobi_smem" if n <= (100 if dd else 128) else "jacobi_kernel (cooperative grid)",
+           "bound": "latency", "sweeps": int(info.sweeps), "rounds": rounds, "eigen_ms": eigen_ms}
+    if rounds <= 0:
+        return out
+    cyc = eigen_ms * 1e-3 * clock_mhz * 1e6 / rounds
+    out["cycles_per_round"] = cyc
+    pr = latency_probe()
+    chain = pr.get("rotation_chain_cycles")
+    bar = pr.get("grid_sync_cycles") if out["kernel"].startswith("jacobi_kernel") else pr.get("syncthreads_cycles")
+    if chain and bar:
+        floor = chain + bar
+        out["floor_cycles_per_round"] = floor
+        out["floor_ms"] = rounds * floor / (clock_mhz * 1e3)
+        out["frac"] = floor / cyc
+        out["floor_definition"] = ("rounds x (one dependent fp64 rotation chain + one barrier hand-off), "
+                                   "profiles/r02_latency_probe.json" + (" (fp64 chain: a lower bound for the dd solver)"
+                                                                        if dd else ""))
+    return out
+
+
 def traffic_for(kernel: str, config: str):
     """DRAM bytes per launch of `kernel` from a committed ncu --set full
     capture (profiles/r01_traffic.json), or None."""
@@ -201,8 +245,26 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def run_reference(args, cfg):
-    """CPU reference arm: rank 0 only, bounded row sample, all host threads."""
+def _sample_rows(cfg, fn_for, budget_s: float, runs: int):
+    """Largest power-of-two row count (<= cfg.m, >= 2^12) whose run fits
+    budget_s / runs seconds, from one timed calibration run on 2^14 rows
+    (the CPU path is linear in m at fixed n)."""
+    m0 = min(cfg.m, 1 << 14)
+    fn = fn_for(m0)
+    fn()  # page-in / thread-pool start-up
+    t0 = time.perf_counter()
+    fn()
+    t = max(time.perf_counter() - t0, 1e-4)
+    per_run = budget_s / max(runs, 1)
+    m_s = m0
+    while m_s * 2 <= cfg.m and (m_s * 2) / m0 * t <= per_run:
+        m_s *= 2
+    return m_s
+
+
+def run_reference(args, cfg, budget_s: float = 150.0):
+    """CPU reference arm: rank 0 only, all host threads, a row sample of the
+    workload sized so warm-up + timed runs take about budget_s seconds."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
@@ -213,20 +275,41 @@ def run_reference(args, cfg):
     cores = os.cpu_count() or 1
     n = cfg.n
     eig = EIG[args.eig]
+    runs = args.steps + args.warmup
+    what = f"mp_thin_svd {EIG_NAME[eig]}"
     if cfg.working == "f32":
-        m_s = min(cfg.m, 1 << 18)
-        a = inputs.make(cfg, seed=1, m=m_s)
-        if pyoracle.ref_available():
-            lib, kind = pyoracle.Ref(), "reference"
-            fn = lambda: lib.thin_svd(a, threads=cores, choice=eig)  # noqa: E731
-        else:
-            lib, kind = pyoracle.Port(), "port"
-            fn = lambda: lib.thin_svd(a, threads=cores, choice=eig)  # noqa: E731
-    else:
-        m_s = min(cfg.m, 1 << 13)
-        a = inputs.make(cfg, seed=1, m=m_s)
+        lib = pyoracle.Ref() if pyoracle.ref_available() else pyoracle.Port()
+        kind = "reference" if pyoracle.ref_available() else "port"
+
+        def fn_for(m_s):
+            a = inputs.make(cfg, seed=1, m=m_s)
+            return lambda: lib.thin_svd(a, threads=cores, choice=eig)
+        flops_fn = flops
+    elif cfg.n <= 256:
+        # no reference path for binary64 input (thinsvd.cpp:52-53): the
+        # restated double-double oracle, whole pipeline (dd Gram + dd Jacobi + U)
         lib, kind = pyoracle.Port(), "port"
-        fn = lambda: lib.thin_svd_f64dd(a, threads=cores)  # noqa: E731
+        what = "restated double-double thin SVD (dd Gram + dd two-sided Jacobi + U), not reference code"
+
+        def fn_for(m_s):
+            a = inputs.make(cfg, seed=1, m=m_s)
+            return lambda: lib.thin_svd_f64dd(a, threads=cores)
+        flops_fn = flops
+    else:
+        # c5 (n = 1024): the restated dd Jacobi alone is hours of CPU time
+        # (O(n^3) double-double work per sweep, ~45 sweeps), so the sample
+        # times the Gram-phase oracle only - the dd Gram of the reference's
+        # test support (dd.cpp:75-88), restated - and prices it with the
+        # Gram flops alone (the metric's F_gram part)
+        lib, kind = pyoracle.Port(), "port"
+        what = "restated double-double Gram only (dd_gram, dd.cpp:75-88), not reference code; Jacobi and U not run"
+
+        def fn_for(m_s):
+            a = inputs.make(cfg, seed=1, m=m_s)
+            return lambda: lib.dd_gram(a, threads=cores)
+        flops_fn = lambda m, nn: (float(m) * nn * (nn + 1), 0.0)  # noqa: E731
+    m_s = _sample_rows(cfg, fn_for, budget_s, runs)
+    fn = fn_for(m_s)
     for _ in range(args.warmup):
         fn()
     times = []
@@ -235,11 +318,11 @@ def run_reference(args, cfg):
         fn()
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
-    fg, fa = flops(m_s, n)
+    fg, fa = flops_fn(m_s, n)
     value = (fg + fa) / t / 1e12
-    sample = (f"{cfg.name} distribution with m={m_s} rows (of {cfg.m}), n={n}; median of {args.steps} "
-              f"after {args.warmup} warm-up; mp_thin_svd {EIG_NAME[eig]}"
-              + ("" if kind == "reference" else " (restated double-double oracle, reference has no fp64 path)"))
+    sample = (f"{cfg.name} distribution with m={m_s} rows (of {cfg.m}; the largest power of two fitting "
+              f"~{budget_s:.0f} s of CPU for the whole run), n={n}; median of {args.steps} after {args.warmup} "
+              f"warm-up; {what}; {cores} threads")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
@@ -254,9 +337,10 @@ def run_reference(args, cfg):
 
 
 def cpu_baseline(cfg, eig="twosided"):
-    """Reported baseline (not the target): same sample as the reference arm."""
+    """Reported baseline (not the target): the reference arm's measurement
+    on a smaller sample (~25 s of CPU work) so the default run stays short."""
     ns = argparse.Namespace(steps=3, warmup=1, gpus=1, eig=eig)
-    line = run_reference(ns, cfg)
+    line = run_reference(ns, cfg, budget_s=25.0)
     return line["cpu_baseline"] if line else None
 
 
@@ -362,11 +446,26 @@ def run_ours(args, cfg):
         ms = float(t.item())
 
     # full-size validation of the factorisation just timed, on the device
-    # (SURVEY.md §8(f)-2): max row-wise backward error, max over ranks
+    # (SURVEY.md §8(f)-2): max row-wise backward error (max over ranks), the
+    # north_star orthogonality gates ||U^T U - I||_F (U^T U by the plan's own
+    # Gram stage, exchange included, so it is global over ranks) and
+    # ||V^T V - I||_F, and for c5 sigma against the prescribed values
     bw = M.backward_error_device(a_t.T, u_t.T, sig_t, v_t.T, stream)
+    u_w = 2.0 ** -24 if cfg.working == "f32" else 2.0 ** -53
+    orth_u = plan.orth_error(u_t.data_ptr(), m_local, sptr)
+    v64 = v_t.double().cpu().numpy().T  # (n, n) column-major V
+    orth_v = float(np.linalg.norm(v64.T @ v64 - np.eye(n)))
     validation = {"rowwise_backward_error": bw.max_rel, "skipped_rows": bw.skipped_rows,
-                  "unit_roundoff": 2.0 ** -24 if cfg.working == "f32" else 2.0 ** -53,
-                  "definition": "max_i ||(U diag(s) V^T - A)(i,:)|| / ||A(i,:)||, binary64 (metrics.cpp:40-70)"}
+                  "unit_roundoff": u_w,
+                  "definition": "max_i ||(U diag(s) V^T - A)(i,:)|| / ||A(i,:)||, binary64 (metrics.cpp:40-70)",
+                  "orth_u": orth_u, "orth_v": orth_v, "orth_gate": 10.0 * n * u_w,
+                  "orth_definition": "||Q^T Q - I||_F in binary64 (dense.cpp:250-272); gate 10*n*u (north_star)"}
+    if cfg.kind == "prescribed":
+        want = 10.0 ** (-cfg.decades * np.arange(n) / max(n - 1, 1))
+        got = sig_t.cpu().numpy()
+        validation["sigma_vs_prescribed_max_rel"] = float(np.max(np.abs(got - want) / want))
+        validation["sigma_note"] = ("A = U0 diag(sigma) V0^T is formed in binary64, which perturbs sigma_i by "
+                                    "about u*sigma_1/sigma_i (up to ~1e-6 relative at sigma_n = 1e-10)")
     if world > 1:
         t = torch.tensor([bw.max_rel, float(bw.skipped_rows)], dtype=torch.float64)
         dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
@@ -380,8 +479,13 @@ def run_ours(args, cfg):
     # --- e2e through the reference-facing C ABI with host buffers -----------
     e2e = None
     if world == 1:
+        # the public host-buffer API on this GPU only (MPSVD_DEVICES: it would
+        # otherwise shard over every visible GPU of the node)
+        os.environ["MPSVD_DEVICES"] = str(local)
         host = M.Matrix(m_local, n, working)
-        host.numpy()[...] = a_t.cpu().numpy().T
+        # A straight into the page-locked host matrix: its (n, m) transpose
+        # view is the same column-major memory as a_t
+        torch.from_numpy(host.numpy().T).copy_(a_t)
         # free the device-resident arm before the API allocates its own buffers
         del plan, a_t, u_t, v_t, sig_t
         torch.cuda.empty_cache()
@@ -442,13 +546,18 @@ def run_ours(args, cfg):
     pk = peaks()
     fp64_peak = M.fp64_peak_tflops(local)
     hbm = pk.get("hbm_gbs", 6650.0)
-    # per-phase rooflines (DESIGN.md §4): algorithmic work per launch over
-    # the phase's CUDA-event time on the plan's stream; the dominant phase is
-    # the headline `roofline`
+    # per-phase rooflines (DESIGN.md §7): algorithmic work per launch over
+    # the phase's CUDA-event time on the plan's stream. The headline
+    # `roofline` is the dominant throughput kernel of the Gram+AV pair (the
+    # north_star's roofline scope), each against its own bound: K1 on the
+    # DMMA pipe, K2z on the int8 tensor cores, K7 f32 on HBM, K7 f64 on
+    # DMMA. The Jacobi is latency-bound and reported beside it (`jacobi`).
     phases = phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info)
-    dom = max(med, key=med.get)
+    dom = max(("gram", "compute_u"), key=lambda k: med[k])
     roof = dict(phases[dom])
+    roof["phase"] = dom
     roof["traffic"] = traffic_for(roof["kernel"], cfg.name)
+    jac = jacobi_latency(n, info, med["eigen"], cfg.working != "f32")
     # north_star roofline for the whole Gram+AV pair
     t_hbm = 2.0 * m_global / world * n * esz / (hbm * 1e9)
     t_cmp = (fg + fa) / world / (fp64_peak * 1e12) if cfg.working == "f32" else (fg * 5 + fa) / world / (fp64_peak * 1e12)
@@ -464,6 +573,7 @@ def run_ours(args, cfg):
         "phase_ms": med,
         "roofline": roof,
         "roofline_phases": phases,
+        "jacobi": jac,
         "svd_roofline": {"definition": "max(2*m*n*s/HBM, F_gram/P_gram + F_AV/P_fp64) (north_star)",
                          "t_roof_ms": t_roof * 1e3, "gram_plus_av_ms": gram_av_ms,
                          "frac": (t_roof * 1e3) / gram_av_ms if gram_av_ms > 0 else None,
@@ -484,7 +594,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eig", default="twosided", choices=list(EIG),

@@ -129,6 +129,7 @@ typedef struct mpsvd_exec_info {
   int64_t rotations;
   double ms_gram, ms_eigen, ms_compute_u; /* CUDA-event device times */
   int kernel_launches; /* kernels of this library launched by one execute */
+  int64_t rounds;      /* parallel Jacobi rounds executed (two-sided solver) */
 } mpsvd_exec_info;
 
 mpsvd_status mpsvd_comm_unique_id(unsigned char id[128]);

@@ -28,6 +28,7 @@ class ExecInfo(C.Structure):
         ("ms_eigen", C.c_double),
         ("ms_compute_u", C.c_double),
         ("kernel_launches", C.c_int),
+        ("rounds", i64),
     ]
 
 

@@ -63,5 +63,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+C_SRC = os.path.join(ROOT, "tests", "c", "capi_ref.c")
+C_BIN = os.path.join(ROOT, "tests", "c", "_bin")
+
+
+def build_c_consumers() -> list[str]:
+    """The C consumer tests/c/capi_ref.c, linked to the library, compiled
+    twice: against the reference's own C header (capi_ref; only where
+    /root/reference exists - the binary then travels with the repo) and
+    against this repo's include/mpsvd.h (capi_own)."""
+    os.makedirs(C_BIN, exist_ok=True)
+    out = []
+    targets = [("capi_own", os.path.join(ROOT, "include"))]
+    if os.path.isfile(os.path.join(REF_INCLUDE, "mpsvd.h")):
+        targets.insert(0, ("capi_ref", REF_INCLUDE))
+    for name, inc in targets:
+        exe = os.path.join(C_BIN, name)
+        cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Werror", f"-I{inc}", C_SRC, "-o", exe, f"-L{HERE}",
+               "-l:libmpsvd_b200.so", "-Wl,-rpath,$ORIGIN/../../../paper_2603_11953_b200", "-lm"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"C consumer {name} failed to build:\n{' '.join(cmd)}\n{r.stdout}{r.stderr}")
+        out.append(exe)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -272,8 +272,8 @@ using Clock = std::chrono::steady_clock;
 // device uploads its rows with one strided copy, runs the pipeline with the
 // one Gram exchange (Plan::exchange), the redundant Jacobi and its rows of
 // U, which go straight back into the caller's U. Device selection:
-// MPSVD_DEVICES = "all" (default: every visible device) | a count | a list
-// "0,2,3"; a problem is sharded only when every device gets at least
+// MPSVD_DEVICES = "all" (default: every visible device) | a comma-separated
+// device list ("0", "0,2,3"); a problem is sharded only when every device gets at least
 // MPSVD_SHARD_MIN_ROWS rows (default 2^18: below that the per-device
 // launches and copies outweigh the split). MPSVD_SHARD_FORCE=1 takes the
 // sharded path even on one device (tests: it must give the single-GPU bits).
@@ -288,10 +288,9 @@ std::vector<int> shard_devices(long long m) {
   const std::string s = env ? env : "all";
   if (s.empty() || s == "all") {
     for (int d = 0; d < count; ++d) devs.push_back(d);
-  } else if (s.find(',') == std::string::npos && s.size() < 3 && s.find_first_not_of("0123456789") == std::string::npos) {
-    const int k = std::max(1, std::min(count, std::atoi(s.c_str())));
-    for (int d = 0; d < k; ++d) devs.push_back(d);
   } else {
+    if (s.find_first_not_of("0123456789,") != std::string::npos)
+      throw InvalidArgument("MPSVD_DEVICES must be \"all\" or a comma-separated device list");
     size_t pos = 0;
     while (pos < s.size()) {
       const size_t e = s.find(',', pos);

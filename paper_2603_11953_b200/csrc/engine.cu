@@ -792,6 +792,7 @@ mpsvd_exec_info Plan::wait() {
   info.error_value = h_status->value;
   info.sweeps = h_status->sweeps;
   info.rotations = h_status->rotations;
+  info.rounds = h_status->rounds;
   if (events_recorded) {
     float ms = 0;
     check(cudaEventElapsedTime(&ms, ev[0], ev[1]), "event time");

@@ -1,6 +1,7 @@
 // Latency of one fp64 Jacobi rotation (the formula of csrc/jacobi.cu) for one
 // warp, dependent chain, vs the pieces (sqrt, div) on their own.
 #include <cstdio>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 __device__ __noinline__ double scaled_hypot(double x, double y, double big) {
@@ -56,6 +57,32 @@ __global__ void dfma_chain(double* out, int iters) {
   if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / iters; out[1] = v; }
 }
 
+// one 512-thread block: dependent __syncthreads hand-offs (a value written
+// by one warp is read by another after every barrier)
+__global__ void sync_chain(double* out, int iters) {
+  __shared__ volatile int flag[2];
+  if (threadIdx.x == 0) flag[0] = 0;
+  __syncthreads();
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    if (threadIdx.x == (unsigned)((i & 15) * 32)) flag[i & 1] = flag[(i + 1) & 1] + 1;
+    __syncthreads();
+  }
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / iters; out[1] = flag[0]; }
+}
+
+// cooperative grid barrier, one 512-thread CTA per SM (the multi-CTA solver's shape)
+__global__ void grid_chain(double* out, int iters) {
+  namespace cg = cooperative_groups;
+  cg::grid_group g = cg::this_grid();
+  g.sync();
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) g.sync();
+  unsigned long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (double)(t1 - t0) / iters;
+}
+
 int main() {
   double* d;
   cudaMalloc(&d, 16);
@@ -74,5 +101,25 @@ int main() {
   dfma_chain<<<1, 32>>>(d, it);
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
   printf("dfma chain: %.1f cycles\n", h[0]);
+  double rot = 0;
+  rot_chain<<<1, 32>>>(d, it, 64 * 0x1p-53);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  rot = h[0];
+  sync_chain<<<1, 512>>>(d, it);
+  sync_chain<<<1, 512>>>(d, it);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  const double syn = h[0];
+  printf("__syncthreads hand-off (512 threads): %.1f cycles\n", syn);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int git = 500;
+  void* args[] = {&d, &git};
+  cudaLaunchCooperativeKernel((void*)grid_chain, sms, 512, args, 0, nullptr);
+  cudaLaunchCooperativeKernel((void*)grid_chain, sms, 512, args, 0, nullptr);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  const double gs = h[0];
+  printf("grid.sync (%d CTAs x 512): %.1f cycles\n", sms, gs);
+  printf("JSON {\"rotation_chain_cycles\": %.1f, \"syncthreads_cycles\": %.1f, \"grid_sync_cycles\": %.1f, "
+         "\"sms\": %d, \"source\": \"tools/microbench/rot_latency.cu\"}\n", rot, syn, gs, sms);
   return 0;
 }
