@@ -140,10 +140,13 @@ static void thin_svd_surface(void) {
   mpsvd_matrix* g = NULL;
   const int64_t m = 4096, n = 24;
   CHECK(mpsvd_matrix_create(m, n, MPSVD_PRECISION_WORKING, &g) == MPSVD_OK);
+  uint64_t st = 0x9E3779B97F4A7C15ull;  /* full-rank pseudo-random entries in [-1, 1), graded columns */
   for (int64_t j = 0; j < n; ++j)
-    for (int64_t i = 0; i < m; ++i)
-      CHECK(mpsvd_matrix_set(g, i, j, sin(0.37 * (double)i + 1.9 * (double)j) * pow(10.0, -3.0 * j / (n - 1))) ==
-            MPSVD_OK);
+    for (int64_t i = 0; i < m; ++i) {
+      st = st * 6364136223846793005ull + 1442695040888963407ull;
+      const double u = (double)(st >> 40) / (double)(1ull << 23) - 1.0;
+      CHECK(mpsvd_matrix_set(g, i, j, u * pow(10.0, -3.0 * j / (n - 1))) == MPSVD_OK);
+    }
   for (int eig = 0; eig < 3; ++eig) {
     mpsvd_svd_result *r1 = NULL, *r8 = NULL;
     CHECK(mpsvd_thin_svd(g, (mpsvd_eigensolver)eig, 1, &r1) == MPSVD_OK);
