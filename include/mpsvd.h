@@ -181,6 +181,12 @@ mpsvd_status mpsvd_stage_gram(mpsvd_precision prec, const void* a, int64_t m, in
  * cap bounds both arrays. */
 mpsvd_status mpsvd_stage_gram_schedule(int64_t m, int64_t n, int cap, int* nsplit, int* nblocks, int* scb,
                                        int* bsb, int* ozaki);
+/* The binary32 Gram schedule of an m x n plan: *ozaki = 1 when K1z (the int8
+ * tensor-core Gram, gram_ozaki32.cu) runs; it then launches once per range
+ * [bounds[b], bounds[b + 1]) of 32-row chunks (b < *nbounds - 1) with
+ * *npairs CTA pairs. cap bounds `bounds`. */
+mpsvd_status mpsvd_stage_gram32_schedule(int64_t m, int64_t n, int cap, int* ozaki, int* npairs, int* nbounds,
+                                         int64_t* bounds);
 /* Two-sided Jacobi on the GPU: dd = 0 fp64 (m_lo ignored), 1 double-double.
  * Outputs sorted/sign-fixed eigenpairs in the higher precision. */
 mpsvd_status mpsvd_stage_jacobi(int dd, const double* m_hi, const double* m_lo, int64_t n, double tol,

@@ -1632,3 +1632,207 @@ double port_orth_error_f32(const float* q, int64_t m, int64_t n, int threads) {
 double port_orth_error_f64(const double* q, int64_t m, int64_t n, int threads) {
   return orth_run(NULL, q, m, n, threads);
 }
+
+/* ======================================================================== */
+/* K1z restated (csrc/gram_ozaki32.cu): the binary64 Gram of a binary32 A   */
+/* (n <= 128) by the int8 Ozaki scheme, bit for bit. Reference semantics:   */
+/* partitioned_gram of cast(A, Higher) (proj/src/parallel_gram.cpp:79-112); */
+/* this is the device's different exact-accumulation order, restated so the */
+/* tests can pin the kernel bitwise; its accuracy against the reference is   */
+/* checked separately (tests/test_ozaki32.py).                               */
+/* ======================================================================== */
+
+#define O32_ZERO_E (-160)
+#define O32_HEAD 2
+
+#define O32_C48 0x808080808080ull
+
+static int o32_fexp_bits(uint32_t ab) {
+  const int e8 = (int)(ab >> 23);
+  if (e8) return e8 - 126;
+  if (!ab) return -1000;
+  return (32 - __builtin_clz(ab)) - 149;
+}
+
+static uint64_t o32_fixed48(uint32_t b, int E) {
+  const uint32_t e8 = (b >> 23) & 0xFFu;
+  if (e8 == 0xFFu) return O32_C48;
+  const uint32_t mant = (b & 0x7FFFFFu) | (e8 ? 0x800000u : 0u);
+  const int sh = (int)(e8 ? e8 : 1u) - 104 - E;
+  uint64_t X = 0;
+  if (mant) { /* round to nearest, ties to even */
+    if (sh >= 0) {
+      X = (uint64_t)mant << sh;
+    } else if (sh > -64) {
+      const int s = -sh;
+      const uint64_t r = (uint64_t)mant >> s;
+      const uint64_t rem = (uint64_t)mant - (r << s), half = 1ull << (s - 1);
+      X = r + ((rem > half || (rem == half && (r & 1ull))) ? 1ull : 0ull);
+    }
+  }
+  return (b >> 31) ? O32_C48 - X : O32_C48 + X;
+}
+
+static void o32_product(int g, int k, int* p, int* q, int* acc) {
+  const int sh = 4 * k;
+  *p = (int)(((g ? 0x322121u : 0x111321u) >> sh) & 15u);
+  *q = (int)(((g ? 0x323445u : 0x123456u) >> sh) & 15u);
+  *acc = (int)(((g ? 0x321100u : 0x321000u) >> sh) & 15u);
+}
+
+static dd o32_group_total(int g, int32_t a0, int32_t a1, int32_t a2, int32_t a3) {
+  if (g == 0) {
+    const int64_t vlo = (int64_t)a0 + (int64_t)a1 * 16777216LL;
+    const int64_t vhi = (int64_t)a2 + (int64_t)a3 * 128LL;
+    const double lh = (double)vlo;
+    const double ll = (double)(vlo - (int64_t)lh);
+    return dd_add((dd){(double)vhi * 4294967296.0, 0.0}, (dd){lh, ll});
+  }
+  const int64_t v = (int64_t)a0 * 2LL + (int64_t)a1 * 512LL + (int64_t)a2 * 65536LL + (int64_t)a3;
+  return (dd){(double)v, 0.0};
+}
+
+typedef struct {
+  const float* a;
+  int64_t m, n, c0, c1;
+  int g, accumulate, span_max;
+  dd* P;      /* [128][128], [j][i] */
+  int* bad;   /* [128] */
+} O32Job;
+
+static void* o32_worker(void* arg) {
+  O32Job* J = (O32Job*)arg;
+  const int64_t m = J->m, n = J->n;
+  const int g = J->g;
+  int64_t* acc = (int64_t*)calloc((size_t)4 * 128 * 128, sizeof(int64_t));
+  int8_t* D = (int8_t*)malloc((size_t)6 * 32 * 128); /* [p][r][c] */
+  int E[128];
+  int64_t s8[128];
+  for (int c = 0; c < 128; ++c) {
+    E[c] = O32_ZERO_E;
+    s8[c] = 0;
+  }
+  int span = -1, len = 0;
+  const int base = g ? 47 : 40;
+  for (int64_t ch = J->c0; ch <= J->c1; ++ch) {
+    const int end = ch == J->c1;
+    uint32_t b[32][128];
+    uint32_t mx[128];
+    int fresh = 0;
+    if (!end) {
+      for (int c = 0; c < 128; ++c) {
+        mx[c] = 0;
+        for (int r = 0; r < 32; ++r) {
+          const int64_t row = ch * 32 + r;
+          uint32_t v = 0;
+          if (row < m && c < n) memcpy(&v, &J->a[c * m + row], 4);
+          const uint32_t ab = v & 0x7FFFFFFFu;
+          if (ab > mx[c]) mx[c] = ab; /* inf / NaN included: they force a new span */
+          if ((ab >> 23) == 0xFFu) {  /* the column is flagged, the entry used as zero */
+            J->bad[c] = 1;
+            v = 0;
+          }
+          b[r][c] = v;
+        }
+      }
+      int ovf = 0;
+      for (int c = 0; c < 128; ++c) ovf |= o32_fexp_bits(mx[c]) > E[c];
+      fresh = ovf || len == J->span_max || ch == J->c0;
+    }
+    if ((fresh || end) && span >= 0) {
+      /* drain the span just closed */
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+          const int64_t e = i * 128 + j;
+          dd t0 = o32_group_total(g, (int32_t)(uint32_t)acc[e], (int32_t)(uint32_t)acc[16384 + e],
+                                  (int32_t)(uint32_t)acc[2 * 16384 + e], (int32_t)(uint32_t)acc[3 * 16384 + e]);
+          if (g == 1 && i == j) t0 = dd_add(t0, (dd){(double)s8[i] * 0x1p-16, 0.0}); /* D8 diagonal */
+          const int sc = E[i] + E[j] - 92 + base;
+          dd t = {scalbn(t0.hi, sc), scalbn(t0.lo, sc)};
+          dd* o = &J->P[j * 128 + i];
+          if (J->accumulate || span > 0) t = dd_add(*o, t);
+          *o = t;
+        }
+    }
+    if (end) break;
+    if (fresh) {
+      ++span;
+      len = 0;
+      for (int c = 0; c < 128; ++c) {
+        E[c] = mx[c] ? o32_fexp_bits(mx[c]) + O32_HEAD : O32_ZERO_E;
+        s8[c] = 0;
+      }
+      memset(acc, 0, sizeof(int64_t) * 4 * 128 * 128);
+    }
+    ++len;
+    for (int r = 0; r < 32; ++r)
+      for (int c = 0; c < 128; ++c) {
+        const uint64_t y = o32_fixed48(b[r][c], E[c]);
+        for (int p = 1; p <= 6; ++p) D[((p - 1) * 32 + r) * 128 + c] = (int8_t)(((y >> (8 * (6 - p))) & 0xFFu) ^ 0x80u);
+        const int d4 = D[(3 * 32 + r) * 128 + c];
+        s8[c] += d4 * d4;
+      }
+    for (int k = 0; k < 6; ++k) {
+      int p, q, ai;
+      o32_product(g, k, &p, &q, &ai);
+      int64_t* A = acc + (int64_t)ai * 16384;
+      for (int r = 0; r < 32; ++r) {
+        const int8_t* dp = D + ((p - 1) * 32 + r) * 128;
+        const int8_t* dq = D + ((q - 1) * 32 + r) * 128;
+        for (int i = 0; i < n; ++i) {
+          const int64_t x = dp[i];
+          if (!x) continue;
+          int64_t* row = A + i * 128;
+          for (int j = 0; j < n; ++j) row[j] += x * dq[j];
+        }
+      }
+    }
+  }
+  if (span < 0 && !J->accumulate)
+    for (int64_t e = 0; e < 128 * 128; ++e) J->P[e] = (dd){0.0, 0.0};
+  free(acc);
+  free(D);
+  return NULL;
+}
+
+int port_gram_f32_ozaki(const float* a, int64_t m, int64_t n, int npairs, int nranges, const int64_t* bounds,
+                        int span_max, int threads, double* out) {
+  if (m < 1 || n < 1 || n > 128 || npairs < 1 || nranges < 1 || span_max < 1) return ST_INVALID;
+  const int ncta = 2 * npairs;
+  dd* P = (dd*)calloc((size_t)ncta * 128 * 128, sizeof(dd));
+  int* bad = (int*)calloc((size_t)ncta * 128, sizeof(int));
+  O32Job* jobs = (O32Job*)malloc(sizeof(O32Job) * (size_t)ncta);
+  if (threads < 1) threads = 1;
+  if (threads > 64) threads = 64;
+  for (int l = 0; l < nranges; ++l) {
+    const int64_t cb = bounds[l], nall = bounds[l + 1] - bounds[l];
+    for (int k = 0; k < ncta; ++k) {
+      const int pr = k >> 1;
+      jobs[k] = (O32Job){a,     m,      n, cb + nall * pr / npairs, cb + nall * (pr + 1) / npairs, k & 1, l > 0,
+                         span_max, P + (int64_t)k * 128 * 128, bad + (int64_t)k * 128};
+    }
+    for (int k0 = 0; k0 < ncta; k0 += threads) {
+      pthread_t th[64];
+      const int cnt = ncta - k0 < threads ? ncta - k0 : threads;
+      for (int t = 0; t < cnt; ++t) pthread_create(&th[t], NULL, o32_worker, &jobs[k0 + t]);
+      for (int t = 0; t < cnt; ++t) pthread_join(th[t], NULL);
+    }
+  }
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i <= j; ++i) {
+      dd acc = {0.0, 0.0};
+      int isbad = 0;
+      for (int k = 0; k < ncta; ++k) {
+        acc = dd_add(acc, P[(int64_t)k * 16384 + j * 128 + i]);
+        acc = dd_add(acc, P[(int64_t)k * 16384 + i * 128 + j]);
+        isbad |= bad[k * 128 + i] | bad[k * 128 + j];
+      }
+      const double v = isbad ? NAN : acc.hi;
+      out[j * n + i] = v;
+      out[i * n + j] = v;
+    }
+  free(P);
+  free(bad);
+  free(jobs);
+  return ST_OK;
+}

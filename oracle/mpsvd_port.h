@@ -93,6 +93,11 @@ int port_dd_gram(const double* a, int64_t m, int64_t n, int threads, double* hi,
 /* K2z sub-group i: weight quad (w_hi, nw weights w_hi - k) and steps [pa, pb] */
 void port_oz_sub_group(int i, int* whi, int* nw, int* pa, int* pb);
 /* K2z (csrc/gram_ozaki.cu) replayed bit for bit on the schedule scb / bsb */
+/* K1z (csrc/gram_ozaki32.cu): binary64 Gram of binary32 A (n <= 128) by the
+ * int8 Ozaki scheme on the plan's schedule (npairs CTA pairs, chunk ranges
+ * bounds[0..nranges]); out: n x n, both triangles. */
+int port_gram_f32_ozaki(const float* a, int64_t m, int64_t n, int npairs, int nranges, const int64_t* bounds,
+                        int span_max, int threads, double* out);
 int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const int* scb, int nblocks,
                        const int* bsb, int span_cap, double* out_hi, double* out_lo);
 int port_twosided_jacobi_dd(const double* mhi, const double* mlo, int64_t n,

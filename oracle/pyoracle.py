@@ -422,6 +422,20 @@ class Port:
             raise OracleError(st)
         return hi, lo
 
+    def gram_f32_ozaki(self, a, npairs, bounds, span_max=1024, threads=8):
+        """K1z's binary64 Gram of a binary32 A (csrc/gram_ozaki32.cu) on the
+        plan's schedule (npairs, chunk-range bounds), bit for bit."""
+        a = _fcol(a, np.float32)
+        m, n = a.shape
+        bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        out = np.zeros((n, n), order="F")
+        st = self.lib.port_gram_f32_ozaki(_f(a), _i64(m), _i64(n), C.c_int(npairs), C.c_int(len(bounds) - 1),
+                                          bounds.ctypes.data_as(C.POINTER(C.c_int64)), C.c_int(span_max),
+                                          C.c_int(threads), _d(out))
+        if st:
+            raise OracleError(st)
+        return out
+
     def twosided_jacobi_dd(self, mhi, mlo=None, tol=0.0, max_sweeps=30, sem=SEM_REFERENCE):
         mhi = _fcol(mhi, np.float64)
         n = mhi.shape[0]

@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     fp64_peak_tflops,
     gram,
     gram_schedule,
+    gram32_schedule,
     max_rel_sv_error,
     mp_cholesky_qr,
     mp_thin_svd,

@@ -75,6 +75,7 @@ SIGNATURES = [
     ("mpsvd_matrix_read_file", C.c_int, [C.c_char_p, C.POINTER(vp)]),
     ("mpsvd_stage_gram", C.c_int, [C.c_int, vp, i64, i64, dp, dp]),
     ("mpsvd_stage_gram_schedule", C.c_int, [i64, i64, C.c_int] + [C.POINTER(C.c_int)] * 5),
+    ("mpsvd_stage_gram32_schedule", C.c_int, [i64, i64, C.c_int] + [C.POINTER(C.c_int)] * 3 + [C.POINTER(i64)]),
     ("mpsvd_stage_jacobi", C.c_int, [C.c_int, dp, dp, i64, C.c_double, C.c_int, dp, dp, dp, dp,
                                      C.POINTER(C.c_int), C.POINTER(i64)]),
     ("mpsvd_stage_onesided", C.c_int, [C.c_int, dp, i64, C.c_double, C.c_int, dp, C.POINTER(C.c_float),

@@ -392,6 +392,18 @@ def gram_schedule(m: int, n: int):
     return bool(oz.value), scb[: ns.value + 1].copy(), bsb[: nb.value + 1].copy()
 
 
+def gram32_schedule(m: int, n: int):
+    """The binary32 Gram schedule of an m x n plan (parity tests):
+    (ozaki, npairs, bounds) - K1z launches once per chunk range
+    [bounds[b], bounds[b+1]) with npairs CTA pairs."""
+    cap = 64
+    bounds = np.zeros(cap, np.int64)
+    oz, npairs, nb = C.c_int(0), C.c_int(0), C.c_int(0)
+    _check(lib.mpsvd_stage_gram32_schedule(m, n, cap, C.byref(oz), C.byref(npairs), C.byref(nb),
+                                           bounds.ctypes.data_as(C.POINTER(C.c_int64))))
+    return bool(oz.value), npairs.value, bounds[: nb.value].copy()
+
+
 def rank_combine(parts_hi, parts_lo=None):
     """The multi-GPU exchange's combine kernel on host-supplied per-rank
     partial Grams (shape (nranks, n, n); column-major n x n each): binary64

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmpsvd_b200.so")
-SOURCES = ["gram.cu", "gram_ozaki.cu", "jacobi.cu", "compute_u.cu", "compute_u_tc.cu", "metrics.cu", "onesided.cu", "cholqr.cu", "microbench.cu", "engine.cu", "api.cpp", "textio.cpp"]
+SOURCES = ["gram.cu", "gram_ozaki.cu", "gram_ozaki32.cu", "jacobi.cu", "compute_u.cu", "compute_u_tc.cu", "metrics.cu", "onesided.cu", "cholqr.cu", "microbench.cu", "engine.cu", "api.cpp", "textio.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",

@@ -756,6 +756,17 @@ void gpu_gram_schedule_public(long long m, long long n, int cap, int* nsplit, in
   for (size_t i = 0; i < p.scb.size(); ++i) scb[i] = p.scb[i];
   for (size_t i = 0; i < p.block_split_begin.size(); ++i) bsb[i] = p.block_split_begin[i];
 }
+// the binary32 Gram schedule of a plan: K1z on/off, CTA pairs, chunk bounds
+void gpu_gram32_schedule_public(long long m, long long n, int cap, int* ozaki, int* npairs, int* nbounds,
+                                int64_t* bounds) {
+  require_device();
+  engine::Plan p(m, n, false, nullptr);
+  *ozaki = p.oz32 ? 1 : 0;
+  *npairs = p.oz32_pairs;
+  *nbounds = (int)p.oz32_bounds.size();
+  if ((int)p.oz32_bounds.size() > cap) throw InvalidArgument("schedule: capacity too small");
+  for (size_t i = 0; i < p.oz32_bounds.size(); ++i) bounds[i] = p.oz32_bounds[i];
+}
 // the spectral phase of the one-sided branches on an uploaded fp64 Gram:
 // sorted working-precision sigma and V (binary32), as port_onesided_spectral
 void gpu_onesided_public(int choice, const double* m_hi, long long n, double tol, int max_sweeps, double* sigma,
@@ -1161,6 +1172,14 @@ mpsvd_status mpsvd_stage_gram_schedule(int64_t m, int64_t n, int cap, int* nspli
   return guarded([&] {
     require(nsplit && nblocks && scb && bsb && ozaki, "null argument");
     mpsvd::gpu_gram_schedule_public(m, n, cap, nsplit, nblocks, scb, bsb, ozaki);
+  });
+}
+
+mpsvd_status mpsvd_stage_gram32_schedule(int64_t m, int64_t n, int cap, int* ozaki, int* npairs, int* nbounds,
+                                         int64_t* bounds) {
+  return guarded([&] {
+    require(ozaki && npairs && nbounds && bounds, "null argument");
+    mpsvd::gpu_gram32_schedule_public(m, n, cap, ozaki, npairs, nbounds, bounds);
   });
 }
 

@@ -421,17 +421,21 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
 // checked by tools/microbench/umma_tmem_a.cu). No shared-memory planes and
 // no generic->async proxy fence; the freed shared memory deepens the fp32
 // staging ring. Roles:
-//   warps 0-7   converters, two groups of four (one warp per TMEM lane
-//               quarter); group g converts chunks g, g + 2, ... into TMEM
-//               A slots {g, g + 2} (each slot has one owner group)
-//   warps 8-15  epilogue (as in av_tc_f32)
-//   warps 16-17 loaders: fp32 chunk [16 columns][128 rows] by cp.async
-//   warp 18     W pieces (bulk copy) + MMA issue
+//   warps 0-15  converters, four groups of four (one warp per TMEM lane
+//               quarter); group g converts chunks g, g + 4, ... into TMEM
+//               A slots {g, g + 4} (each slot has one owner group)
+//   warps 16-23 epilogue (as in av_tc_f32)
+//   warps 24-25 loaders: fp32 chunk [16 columns][128 rows] by cp.async
+//   warp 26     W pieces (bulk copy) + MMA issue
 namespace tm {
-constexpr int kASlots = 4;          // TMEM A slots (24 columns each: 3 pieces x 8); 8 measured the same
+#ifndef TM_GROUPS
+#define TM_GROUPS 4  // converter groups (4 warps each); 2 left the MMA waiting for A slots (C4 ncu)
+#endif
+constexpr int kGroups = TM_GROUPS;
+constexpr int kASlots = 2 * kGroups;  // TMEM A slots (24 columns each: 3 pieces x 8)
 constexpr int kACols = 3 * 8;
-constexpr int kGroups = 2;
-constexpr int kLoad0 = 16, kLoadWarps = TM_LOAD_WARPS, kMma = kLoad0 + kLoadWarps;
+constexpr int kConvW = 4 * kGroups, kEpi0 = kConvW;  // converters: warps 0 .. kConvW-1, then 8 epilogue warps
+constexpr int kLoad0 = kEpi0 + 8, kLoadWarps = TM_LOAD_WARPS, kMma = kLoad0 + kLoadWarps;
 constexpr int kThreads = 32 * (kMma + 1);
 constexpr int kPieces = 512 / (32 * kLoadWarps);  // 16-byte pieces per loader thread per chunk
 }  // namespace tm
@@ -560,7 +564,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
         }
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < tm::kConvW) {
     // converter group grp = warp / 4; quarter q = warp % 4 owns TMEM lanes
     // 32q .. 32q + 31 (rows of the tile)
     const int grp = warp >> 2, q = warp & 3;
@@ -598,8 +602,8 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_full[sl]);
     }
-  } else if (warp < kConvWarps + kEpiWarps) {
-    const int q = warp & 3, e = (warp - kConvWarps) >> 2;
+  } else if (warp < tm::kEpi0 + kEpiWarps) {
+    const int q = warp & 3, e = (warp - tm::kEpi0) >> 2;
     int ab = 0;
     unsigned aph = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {

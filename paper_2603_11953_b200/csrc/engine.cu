@@ -272,6 +272,26 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     }
   }
   build_schedule(*this);
+  if (!dd && m > 0 && n <= 128) {
+    // K1z: binary32 Gram on the int8 tensor cores (gram_ozaki32.cu) for tall
+    // matrices with 64 < n <= 128, where its one 128 x 128 tile is not mostly
+    // padding; MPSVD_F32_GRAM=dmma|ozaki forces K1 / K1z (n <= 128)
+    const char* g32 = getenv("MPSVD_F32_GRAM");
+    const std::string s32 = g32 ? g32 : "";
+    oz32 = s32 == "ozaki" || (s32 != "dmma" && n > 64 && m >= (1LL << 20));
+    if (oz32) {
+      const long long nch = (m + 31) / 32;
+      oz32_pairs = (int)std::max(1LL, std::min<long long>(sm_count / 2, nch / 64));
+      oz32_bounds.clear();
+      const long long base = m / nblocks, extra = m % nblocks;
+      long long row = 0;
+      for (int b = 0; b < nblocks; ++b) {
+        oz32_bounds.push_back(row / 32);
+        row += base + (b < extra ? 1 : 0);
+      }
+      oz32_bounds.push_back(nch);
+    }
+  }
   if (ozaki) {
     // The whole K2z footprint (digit planes + per-slot partial tiles + the
     // n x n workspaces) must fit in the free device memory with a margin,
@@ -325,6 +345,10 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     d_oz_e = dalloc<int>(splits.size() * (size_t)n, owned);
   }
   d_bsums = dalloc<double>((size_t)(nblocks > 0 ? nblocks : 1) * tiles.size() * 64 * 64 * esz, owned);
+  if (oz32) {
+    d_oz32_part = reinterpret_cast<double2*>(dalloc<unsigned char>(dev::gram_ozaki32_partial_bytes(oz32_pairs), owned));
+    d_oz32_bad = dalloc<int>(128, owned);
+  }
   d_m = dalloc<double>(nn * esz, owned);
   const int nranks = comm ? comm->nranks : 1;
   if (nranks > 1) {
@@ -460,11 +484,25 @@ double Plan::effective_tol() const {
   return (double)n * (dd ? 0x1p-104 : 0x1p-53);  // jacobi.cpp:274-275; u_dd = 2^-104
 }
 
+bool Plan::oz32_usable(const void* d_a, long long lda) const {
+  return oz32 && dev::gram_ozaki32_supported((const float*)d_a, lda, m, (int)n);
+}
+
 void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
   const int nranks = comm ? comm->nranks : 1;
   void* target = nranks > 1 ? d_mloc : d_m;
   if (nblocks == 0) {
     check(cudaMemsetAsync(target, 0, (size_t)n * n * sizeof(double) * (dd ? 2 : 1), st), "memset M");
+  } else if (oz32_usable(d_a, lda)) {
+    // K1z: the same per-logical-block range launches as execute_host
+    check(dev::launch_gram_ozaki32_begin(d_oz32_bad, st), "ozaki32 begin");
+    for (int b = 0; b < nblocks; ++b)
+      check(dev::launch_gram_ozaki32_range((const float*)d_a, lda, m, (int)n, oz32_bounds[b], oz32_bounds[b + 1],
+                                           oz32_pairs, d_oz32_part, d_oz32_bad, b > 0, st),
+            "gram_ozaki32");
+    check(dev::launch_gram_ozaki32_combine(d_oz32_part, oz32_pairs, (int)n, d_oz32_bad, (double*)target, st),
+          "gram_ozaki32 combine");
+    launches += nblocks + 1;
   } else if (dd) {
     gram_dd_splits(d_a, lda, 0, (int)splits.size(), st);
     check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, ozaki ? d_bsb_oz : d_bsb, nblocks,
@@ -694,6 +732,8 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
   check(cudaEventRecord(cdone, st), "event");
   check(cudaStreamWaitEvent(cs, cdone, 0), "wait");
   record_event(ev[0], st);
+  const bool k1z = oz32_usable(d_a, m);
+  if (k1z) check(dev::launch_gram_ozaki32_begin(d_oz32_bad, st), "ozaki32 begin");
   {
     const long long base = m / nblocks, extra = m % nblocks;
     long long row = 0;
@@ -705,7 +745,13 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
       check(cudaEventRecord(cev[b], cs), "event");
       check(cudaStreamWaitEvent(st, cev[b], 0), "wait");
       const int sb = block_split_begin[b], cnt = block_split_begin[b + 1] - sb;
-      if (dd) {
+      if (k1z) {
+        // K1z range b: its chunks end at or before this block's last row
+        check(dev::launch_gram_ozaki32_range((const float*)d_a, m, m, (int)n, oz32_bounds[b], oz32_bounds[b + 1],
+                                             oz32_pairs, d_oz32_part, d_oz32_bad, b > 0, st),
+              "gram_ozaki32");
+        launches += 1;
+      } else if (dd) {
         gram_dd_splits(d_a, m, sb, cnt, st);
       } else {
         check(dev::launch_gram_f32((const float*)d_a, m, (int)n, d_tiles, ntp, d_tp_order, ndiag, d_tp_order + ndiag,
@@ -716,7 +762,10 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
       row += len;
     }
   }
-  if (dd)
+  if (k1z)
+    check(dev::launch_gram_ozaki32_combine(d_oz32_part, oz32_pairs, (int)n, d_oz32_bad, (double*)d_m, st),
+          "gram_ozaki32 combine");
+  else if (dd)
     check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, ozaki ? d_bsb_oz : d_bsb, nblocks,
                                       (double2*)d_bsums, (double2*)d_m, st),
           "gram_combine_dd");
@@ -724,7 +773,7 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
     check(dev::launch_gram_combine_f64((const double*)d_partials, ntp, (int)n, d_bsb, nblocks, (double*)d_bsums,
                                        (double*)d_m, st),
           "gram_combine_f64");
-  launches += 2;
+  launches += k1z ? 1 : 2;
   (void)esz;
   record_event(ev[1], st);
   eigen(st);

@@ -83,6 +83,14 @@ class Plan {
   // K2z (double-double Gram on the int8 tensor cores); MPSVD_DD_GRAM=dot2 selects K2
   bool ozaki = false;
   bool f64_allreduce = false;  // MPSVD_F64_EXCHANGE=allreduce (multi-rank fp64 exchange)
+  // K1z (binary32 Gram on the int8 tensor cores, gram_ozaki32.cu): one range
+  // launch per logical row block, chunk bounds oz32_bounds[b] .. [b + 1]
+  bool oz32 = false;
+  int oz32_pairs = 0;
+  std::vector<long long> oz32_bounds;
+  double2* d_oz32_part = nullptr;
+  int* d_oz32_bad = nullptr;
+  bool oz32_usable(const void* d_a, long long lda) const;
   std::vector<int2> oz_tiles;
   std::vector<int> scb;  // split s = 32-row chunks [scb[s], scb[s + 1])
   int2* d_oz_tiles = nullptr;

@@ -1,0 +1,673 @@
+// K1z: the binary64 Gram M = A^T A of a binary32 A (n <= 128) on the int8
+// tensor cores (Ozaki scheme), the fp32 sibling of K2z (gram_ozaki.cu).
+//
+// Reference semantics: partitioned_gram of cast(A, Higher) (proj/src/
+// parallel_gram.cpp:79-112, thinsvd.cpp:61-70): exact binary32 -> binary64
+// widening, exact products, binary64 accumulation in a fixed order, exactly
+// symmetric result. Any fixed summation order is allowed; the
+// acceptance criterion is ||dM||_F / ||M||_F <= 10 m u_h
+// (proj/tests/test_parallel_gram.cpp:74-86). K1z replaces the binary64
+// accumulation by an exact integer one: every entry is truncated once to a
+// 47-bit fixed-point grid of its column (below), the digit products are
+// summed exactly, and each CTA's span totals are carried in double-double;
+// the result is rounded to binary64 once. DESIGN.md §3 gives the error
+// analysis; tests/test_ozaki32.py pins it bitwise to the C restatement
+// (oracle/mpsvd_port.c port_gram_f32_ozaki) and to the reference criterion.
+//
+// Work split. The rows are cut into 32-row chunks (the kind::i8 UMMA K).
+// A launch covers a chunk range; CTA pair p takes an equal share of it and
+// both CTAs of the pair stream the same chunks (the second read is an L2
+// hit): CTA g of the pair owns accumulator group g (below). Per CTA:
+//   warp 0      TMA: 32 x 128 fp32 boxes (16 KB, 128B swizzle) into a ring
+//   warp 1      MMA issue (one thread) + TMEM allocation (4 x 128 columns)
+//   warps 2-5   drain (TMEM lane quarter = tile rows): span totals -> dd
+//   warps 14-17 scouts: lane = column; each chunk's column maxima -> the
+//               span decision (one 128-thread barrier-with-reduction) and the
+//               span's exponents, published per chunk by an mbarrier, so the
+//               converters never synchronise with each other
+//   warps 6-13  convert: thread = (column, 16-row half): the 6 signed digits
+//               of every entry, written as UMMA operand planes (K-major, no
+//               swizzle) into a digit ring.
+//
+// Digits. A span is a run of chunks with fixed column exponents E_c. A span
+// starts at the first chunk of the CTA's range, after kSpanMax chunks (the
+// int32 accumulators stay exact), or at a chunk holding an entry with
+// |x| >= 2^E_c; it sets E_c = e(colmax of that chunk) + kHead (frexp
+// exponent, colmax < 2^e), or kZeroE for an all-zero column. Within the span
+// every x of column c becomes X = sign(x) round(|x| 2^(46 - E_c)),
+// |X| < 2^46, written as 6 balanced digits X = sum_p d_p 2^(8 (6 - p)),
+// d_p in [-128, 127]: the bytes of X + 0x808080808080, each XOR 0x80.
+// Products. x_ki x_kj ~ 2^(E_i + E_j - 92) sum_{p,q} d_p d_q 2^(8 (12 - p - q));
+// the weights s = p + q <= 7 are kept. The tile is diagonal (n <= 128), so
+// S_s = sum_{p+q=s} A_p^T A_q = T_s + T_s^T + D_s with T_s = sum_{p<q} and
+// D_s = A_{s/2}^T A_{s/2}: 12 MMAs per chunk instead of 21, in 8
+// accumulators, which TMEM (512 columns) holds 4 at a time - hence the CTA
+// pair: group 0 = {T7: (1,6)(2,5)(3,4), T4: (1,3), T3: (1,2), D2: (1,1)},
+// group 1 = {T6: (1,5)(2,4), T5: (1,4)(2,3), D4: (2,2), D6: (3,3)},
+// 6 MMAs (M = N = 128, K = 32, 64 cycles each) per chunk per CTA. Of the
+// dropped weights only D8 = A_4^T A_4 has a non-zero mean (on the diagonal,
+// sum_k d_4(x_ki)^2 >= 0); its diagonal is summed on the CUDA cores by the
+// converters (dp4a on plane 4) and added to M_ii by group 1's drain. Every
+// other dropped term is zero-mean noise of ~2^-39 colmax_i colmax_j per row.
+// Drain. At a span end every entry's group total is formed exactly
+// (int64 / double pieces), scaled by 2^(E_i + E_j - 92 + ...) - D terms
+// with an extra 1/2, so that M = P + P^T - and dd_add-ed into the CTA's
+// double-double partial P (stored [j][i], i contiguous). A final kernel adds
+// the partials of every CTA (fixed order: P(i,j) then P(j,i)) and rounds
+// once to binary64, writing both triangles. Columns holding inf / NaN give
+// NaN in their row and column of M.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mpsvd {
+namespace dev {
+namespace oz32 {
+
+constexpr int kKC = 32;                       // rows per chunk = UMMA K (int8)
+constexpr int kCB = 128;                      // tile columns = UMMA M = N
+constexpr int kPlane = kCB * kKC;             // 4096 bytes per digit plane
+constexpr int kDigits = 6;
+constexpr int kHead = 2;                      // exponent headroom (bits) of a new span
+constexpr int kSpanMax = 1024;                // chunks per span: int32 sums stay exact
+constexpr int kZeroE = -160;                  // exponent of an all-zero column
+constexpr int kAStages = 8;                   // fp32 chunk slots (16 KB each): ~2 us of HBM latency in flight
+constexpr int kDStages = 3;                   // digit slots (6 planes = 24 KB each)
+constexpr int kAStageBytes = kKC * kCB * 4;   // 16384
+constexpr int kDStageBytes = kDigits * kPlane;
+constexpr int kThreads = 576;
+constexpr int kConvThreads = 256;
+constexpr int kConvWarp0 = 6;
+constexpr int kScoutWarp0 = 14, kScoutWarps = 4;
+constexpr unsigned long long kC48 = 0x808080808080ull;
+
+// products of group g, in issue order: (p, q, accumulator)
+__host__ __device__ __forceinline__ void product(int g, int k, int& p, int& q, int& acc) {
+  // group 0: T7 (1,6)(2,5)(3,4) -> acc 0, T4 (1,3) -> 1, T3 (1,2) -> 2, D2 (1,1) -> 3
+  // group 1: T6 (1,5)(2,4) -> 0, T5 (1,4)(2,3) -> 1, D4 (2,2) -> 2, D6 (3,3) -> 3
+  // nibble k of each word = product k (P: {1,2,3,1,1,1} / {1,2,1,2,2,3}, Q, accumulator)
+  const int sh = 4 * k;
+  p = (int)(((g ? 0x322121u : 0x111321u) >> sh) & 15u);
+  q = (int)(((g ? 0x323445u : 0x123456u) >> sh) & 15u);
+  acc = (int)(((g ? 0x321100u : 0x321000u) >> sh) & 15u);
+}
+
+// frexp exponent of a non-negative finite binary32 bit pattern (v < 2^e), or
+// -1000 for zero
+__host__ __device__ __forceinline__ int fexp_bits(uint32_t ab) {
+  const int e8 = (int)(ab >> 23);
+  if (e8) return e8 - 126;
+  if (!ab) return -1000;
+#ifdef __CUDA_ARCH__
+  return (32 - __clz((int)ab)) - 149;
+#else
+  return (32 - __builtin_clz(ab)) - 149;
+#endif
+}
+
+// X + 0x808080808080 for X = RNE(x 2^(46 - E)) (round to nearest, ties to
+// even), |x| < 2^E: rounding, not truncation, so the grid error has zero
+// mean and the diagonal of M carries no bias. Exact integer form (the
+// converters' path for columns with E < -78, and the restatement's).
+__host__ __device__ __forceinline__ unsigned long long fixed48(uint32_t b, int E) {
+  const uint32_t e8 = (b >> 23) & 0xFFu;
+  if (e8 == 0xFFu) return kC48;  // inf / NaN: handled as a flagged zero
+  const uint32_t mant = (b & 0x7FFFFFu) | (e8 ? 0x800000u : 0u);
+  const int sh = (int)(e8 ? e8 : 1u) - 104 - E;
+  unsigned long long X = 0;
+  if (mant) {
+    if (sh >= 0) {
+      X = (unsigned long long)mant << sh;
+    } else if (sh > -64) {
+      const int s = -sh;
+      const unsigned long long r = (unsigned long long)mant >> s;
+      const unsigned long long rem = (unsigned long long)mant - (r << s), half = 1ull << (s - 1);
+      X = r + ((rem > half || (rem == half && (r & 1ull))) ? 1ull : 0ull);
+    }
+  }
+  return (b >> 31) ? kC48 - X : kC48 + X;
+}
+
+// The same on the fp64 pipe, for columns with E >= -78 (or all-zero, E_f = 0
+// then): the binary32 bits re-biased into a binary64 scaled by 2^(46 - E)
+// (exact), plus 1.5 2^52 + 0x808080808080 - the sum has ulp 1, so it rounds
+// the scaled value to the nearest integer, ties to even (the constant is
+// even), and its low 48 bits are X + 0x808080808080. Zero and subnormal x
+// become 2^(-81-E) (1 + f) < 1/2 and round to 0, as the exact form gives.
+// kc = (942 - E) << 20.
+__device__ __forceinline__ void fixed48_fast(uint32_t b, uint32_t kc, uint32_t& lo, uint32_t& hi) {
+  const uint32_t h = (((b >> 3) & 0x0FFFFFFFu) + kc) | (b & 0x80000000u);
+  const double d = __hiloint2double((int)h, (int)(b << 29));
+  const double w = __dadd_rn(d, 6755399441055744.0 + 141289400074368.0);  // 1.5 2^52 + 0x808080808080
+  lo = (uint32_t)__double2loint(w);
+  hi = (uint32_t)__double2hiint(w);
+}
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+// try_wait with a long suspend-time hint: a waiting warp sleeps until the
+// phase completes (woken at once) instead of re-polling and taking issue
+// slots from the converters
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(saddr(b)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ uint64_t kdesc(uint32_t addr) {  // K-major, no swizzle, LBO 128, SBO 256
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(saddr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(saddr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_i8_lead(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc,
+                                             uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred p, l;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 l, %5, 0;\n"
+      "@l tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc), "r"(lead));
+}
+__device__ __forceinline__ void commit_lead(uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %1, 0;\n"
+      "@l tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(saddr(bar)),
+      "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_lead(uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %1, 0;\n"
+      "@l mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(saddr(bar)),
+      "r"(lead)
+      : "memory");
+}
+// The 6 MMAs of one chunk for group G (compile-time products): operand
+// descriptors are the slot's base descriptor plus the plane offset >> 4.
+template <int G>
+__device__ __forceinline__ void issue_chunk(uint32_t tmem, uint64_t sd, uint32_t idesc, bool fresh, uint32_t lead) {
+  unsigned started = 0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    int p, q, acc;
+    product(G, k, p, q, acc);
+    const uint32_t first = fresh && !(started & (1u << acc));
+    started |= 1u << acc;
+    umma_i8_lead(tmem + (uint32_t)(acc * kCB), sd + (uint64_t)((p - 1) * (kPlane >> 4)),
+                 sd + (uint64_t)((q - 1) * (kPlane >> 4)), idesc, first ? 0u : 1u, lead);
+  }
+}
+
+// Exact group total of one tile entry from the 4 accumulators, relative to
+// 2^(base) with base = 40 (group 0) or 47 (group 1), as a double-double.
+__device__ __forceinline__ dd group_total(int g, int a0, int a1, int a2, int a3) {
+  if (g == 0) {
+    // T7 * 2^0 + T4 * 2^24 + (T3 * 2^32 + D2 * 2^39), D2 already halved (2^40 -> 2^39)
+    const long long vlo = (long long)a0 + (long long)a1 * 16777216LL;          // |.| < 2^56
+    const long long vhi = (long long)a2 + (long long)a3 * 128LL;               // |.| < 2^39
+    const double lh = (double)vlo;
+    const double ll = (double)(vlo - (long long)lh);
+    return dd_add(dd_make((double)vhi * 4294967296.0, 0.0), dd_make(lh, ll));
+  }
+  // T6 * 2^1 + T5 * 2^9 + D4 * 2^16 + D6 * 2^0 (D4, D6 halved): |.| < 2^48, exact
+  const long long v = (long long)a0 * 2LL + (long long)a1 * 512LL + (long long)a2 * 65536LL + (long long)a3;
+  return dd_make((double)v, 0.0);
+}
+
+}  // namespace oz32
+
+using namespace oz32;
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begin, long long c_end, int npairs,
+               double2* __restrict__ partials, int* __restrict__ bad_cols, int accumulate, int span_max) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-aligned carve-up (the 128B swizzle needs 1024-byte aligned boxes);
+  // offsets from smem_raw keep the pointers in the shared window (LDS/STS,
+  // not generic loads and stores)
+  unsigned char* base = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
+  unsigned char* astage = base;                                       // kAStages x 16 KB
+  unsigned char* dstage = astage + kAStages * kAStageBytes;           // kDStages x 24 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dstage + kDStages * kDStageBytes);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kAStages;
+  uint64_t* d_full = a_empty + kAStages;
+  uint64_t* d_empty = d_full + kDStages;
+  uint64_t* acc_full = d_empty + kDStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint64_t* info_full = acc_empty + 1;   // span metadata published by the issuer
+  uint64_t* desc_empty = info_full + 1;  // 2: span exponent descriptors free
+  uint64_t* meta_full = desc_empty + 2;  // kAStages: the scout's decision for the chunk in A slot s
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(meta_full + kAStages);
+  int* d_meta = reinterpret_cast<int*>(tmem_slot + 4);   // kDStages: chunk starts a span
+  int* span_last = d_meta + kDStages;                    // issuer -> drain: this span is the last
+  int* desc = span_last + 4;                             // [2][128] span exponents
+  int* meta = desc + 2 * kCB;                            // [kAStages][2]: fresh, span
+  int* sbad = meta + 2 * kAStages;                       // [128]
+  int* dsq = sbad + kCB;                                           // [2][2][128] D8 diagonal sums per span
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x >> 1, g = blockIdx.x & 1;
+  const long long nch_all = c_end - c_begin;
+  const long long c0 = c_begin + nch_all * pair / npairs, c1 = c_begin + nch_all * (pair + 1) / npairs;
+  const int nch = (int)(c1 - c0);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kAStages; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], kConvThreads / 32 + kScoutWarps);  // converter warps + the scouts
+      mbar_init(&meta_full[i], kScoutWarps);
+    }
+    for (int i = 0; i < kDStages; ++i) {
+      mbar_init(&d_full[i], kConvThreads / 32);
+      mbar_init(&d_empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);
+    mbar_init(info_full, 1);
+    mbar_init(&desc_empty[0], 4);
+    mbar_init(&desc_empty[1], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (threadIdx.x < kCB) sbad[threadIdx.x] = 0;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&amap) : "memory");
+      for (int j = 0; j < nch; ++j) {
+        const int s = j % kAStages;
+        mbar_wait(&a_empty[s], ((unsigned)(j / kAStages) & 1u) ^ 1u);
+        mbar_expect_tx(&a_full[s], kAStageBytes);
+        tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + j) * kKC), 0, &a_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer: the whole warp runs the loop (warp-uniform control
+    // flow keeps the descriptors in uniform registers; a divergent one-lane
+    // loop paid ~150 cycles of register traffic per MMA) and lane 0's
+    // instructions are the only ones enabled
+    const uint32_t lead = lane == 0;
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kCB >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);  // D s32, A/B s8 K-major, N = M = 128
+    const uint64_t dbase = kdesc(saddr(dstage));           // + (byte offset >> 4) per operand
+    int span = -1;
+    for (int j = 0; j < nch; ++j) {
+      const int s = j % kDStages;
+      mbar_wait(&d_full[s], (unsigned)(j / kDStages) & 1u);
+      const bool fresh = d_meta[s] != 0;
+      if (fresh) {
+        if (span >= 0) {  // close the previous span: the drain may read it
+          if (lead) span_last[span & 1] = 0;
+          __syncwarp();
+          arrive_lead(info_full, lead);
+          commit_lead(acc_full, lead);
+        }
+        ++span;
+        mbar_wait(acc_empty, (unsigned)span & 1u);  // its accumulators are drained
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint64_t sd = dbase + (uint64_t)((uint32_t)s * (kDStageBytes >> 4));
+      if (g == 0)
+        issue_chunk<0>(tmem, sd, idesc, fresh, lead);
+      else
+        issue_chunk<1>(tmem, sd, idesc, fresh, lead);
+      commit_lead(&d_empty[s], lead);  // the digit slot is free once these MMAs have read it
+    }
+    if (lead) span_last[span >= 0 ? (span & 1) : 0] = span >= 0 ? 1 : 2;  // 2: no chunk, nothing to drain
+    __syncwarp();
+    arrive_lead(info_full, lead);
+    if (span >= 0) commit_lead(acc_full, lead);
+  } else if (warp >= kScoutWarp0) {
+    // ---- scouts: lane owns column c = 32 (warp - kScoutWarp0) + lane; per
+    // chunk the column maximum (finite entries), the span decision (first
+    // chunk, span_max chunks, or an entry >= 2^E_c: OR over the 128 scout
+    // threads) and at a new span E_c = e(max) + kHead
+    const int c = (warp - kScoutWarp0) * 32 + lane;
+    int Ec = kZeroE;
+    int span = -1, len = 0;
+    for (int j = 0; j < nch; ++j) {
+      const int sa = j % kAStages;
+      mbar_wait(&a_full[sa], (unsigned)(j / kAStages) & 1u);
+      const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
+      // max of |x| as bit patterns over all entries: inf / NaN (exponent 255)
+      // lie above every finite value, so they force a new span and a huge
+      // E_c for their column, whose entries the converters then zero and flag
+      uint32_t mx = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ (c & 7)) << 4));
+        mx = max(mx, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_empty[sa]);
+      // bit 0: some column needs a new span; bit 1: some entry is inf / NaN
+      const uint32_t mine = (fexp_bits(mx) > Ec ? 1u : 0u) | (mx >= 0x7F800000u ? 2u : 0u);
+      uint32_t any, anybad;
+      asm volatile(
+          "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nbar.red.or.pred q, 1, 128, p;\nselp.u32 %0, 1, 0, q;\n}\n"
+          : "=r"(any)
+          : "r"(mine & 1u)
+          : "memory");
+      asm volatile(
+          "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nbar.red.or.pred q, 1, 128, p;\nselp.u32 %0, 1, 0, q;\n}\n"
+          : "=r"(anybad)
+          : "r"(mine & 2u)
+          : "memory");
+      const bool fresh = any != 0 || len == span_max || j == 0;
+      if (fresh) {
+        ++span;
+        len = 0;
+        if (span >= 2) mbar_wait(&desc_empty[span & 1], ((unsigned)(span >> 1) & 1u) ^ 1u);
+        Ec = mx ? fexp_bits(mx) + kHead : kZeroE;
+        desc[(span & 1) * kCB + c] = Ec;
+      }
+      ++len;
+      if (c == 0) {
+        meta[2 * sa] = (fresh ? 1 : 0) | (anybad ? 2 : 0);
+        meta[2 * sa + 1] = span;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&meta_full[sa]);
+    }
+  } else if (warp < kConvWarp0) {
+    // ---- drain: a warp may only touch TMEM lanes 32 (warp % 4) .. + 31, so
+    // lane quarter qd = warp % 4; thread = tile row i
+    const int qd = warp & 3;
+    const int i = qd * 32 + lane;
+    if (lane == 0) mbar_arrive(acc_empty);  // the accumulators start free
+    double2* P = partials + (size_t)blockIdx.x * kCB * kCB;
+    for (int span = 0;; ++span) {
+      mbar_wait(info_full, (unsigned)span & 1u);
+      const int last = span_last[span & 1];
+      if (last == 2) {  // empty range: the partial is zero
+        if (!accumulate && i < n)
+          for (int jj = 0; jj < n; ++jj) P[(size_t)jj * kCB + i] = make_double2(0.0, 0.0);
+        break;
+      }
+      mbar_wait(acc_full, (unsigned)span & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int* E = desc + (span & 1) * kCB;
+      const int ei = E[i];
+      const int basee = g ? 47 : 40;
+      for (int j0 = 0; j0 < kCB; j0 += 8) {
+        uint32_t v[4][8];
+        const uint32_t taddr = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)j0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                       : "=r"(v[k][0]), "=r"(v[k][1]), "=r"(v[k][2]), "=r"(v[k][3]), "=r"(v[k][4]), "=r"(v[k][5]),
+                         "=r"(v[k][6]), "=r"(v[k][7])
+                       : "r"(taddr + (uint32_t)(k * kCB)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (i < n) {
+          // the 8 running partials are loaded together (one memory latency
+          // per group of columns, not per entry)
+          const bool rmw = accumulate || span > 0;
+          double2 old[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            old[jj] = (rmw && j0 + jj < n) ? P[(size_t)(j0 + jj) * kCB + i] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int jc = j0 + jj;
+            if (jc >= n) continue;
+            dd t0 = group_total(g, (int)v[0][jj], (int)v[1][jj], (int)v[2][jj], (int)v[3][jj]);
+            if (g == 1 && jc == i)  // D8 diagonal: sum d_4^2 at 2^-16 of this frame (halved)
+              t0 = dd_add(t0, dd_make((double)(dsq[(span & 1) * 2 * kCB + i] + dsq[(span & 1) * 2 * kCB + kCB + i]) *
+                                          0x1p-16,
+                                      0.0));
+            const int sc = ei + E[jc] - 92 + basee;
+            dd t = dd_make(scalbn(t0.hi, sc), scalbn(t0.lo, sc));
+            if (rmw) t = dd_add(dd_make(old[jj].x, old[jj].y), t);
+            P[(size_t)jc * kCB + i] = make_double2(t.hi, t.lo);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(acc_empty);
+        mbar_arrive(&desc_empty[span & 1]);
+      }
+      if (last) break;
+    }
+  } else {
+    // ---- converters: thread = (column c, rows 16 h .. 16 h + 15)
+    const int t = threadIdx.x - kConvWarp0 * 32;
+    const int c = t & (kCB - 1), h = t >> 7;
+    const bool need6 = g == 0;  // group 1 uses digits 1-5 only
+    int E = kZeroE;
+    int span = -1;
+    int badc = 0;
+    int s8 = 0;  // sum of d_4^2 over this thread's rows of the open span
+    for (int j = 0; j < nch; ++j) {
+      const int sa = j % kAStages;
+      mbar_wait(&meta_full[sa], (unsigned)(j / kAStages) & 1u);
+      mbar_wait(&a_full[sa], (unsigned)(j / kAStages) & 1u);  // already complete: the TMA data's visibility
+      const int mflags = meta[2 * sa];
+      const bool fresh = (mflags & 1) != 0;
+      const int mspan = meta[2 * sa + 1];
+      // 16 values: 16-byte units 4h .. 4h + 3 of column c, 128B-swizzled
+      const unsigned char* col = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
+      uint32_t b[16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint4 w = *reinterpret_cast<const uint4*>(col + (((4 * h + u) ^ (c & 7)) << 4));
+        b[4 * u] = w.x;
+        b[4 * u + 1] = w.y;
+        b[4 * u + 2] = w.z;
+        b[4 * u + 3] = w.w;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_empty[sa]);
+      if (mflags & 2) {  // inf / NaN in this chunk (the scouts saw it): flag the column, use zeros
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if ((b[r] & 0x7FFFFFFFu) >= 0x7F800000u) {
+            b[r] = 0;
+            badc = 1;
+          }
+      }
+      if (fresh) {
+        if (span >= 0) dsq[(span & 1) * 2 * kCB + h * kCB + c] = s8;  // the closing span's D8 diagonal
+        s8 = 0;
+        span = mspan;
+        E = desc[(span & 1) * kCB + c];
+      }
+      const int sd = j % kDStages;
+      mbar_wait(&d_empty[sd], ((unsigned)(j / kDStages) & 1u) ^ 1u);
+      if (t == 0) d_meta[sd] = fresh ? 1 : 0;
+      uint32_t ylo[16], yhi[16];
+      if (__all_sync(0xffffffffu, E >= -78 || E == kZeroE)) {
+        const uint32_t kc = (uint32_t)(942 - (E == kZeroE ? 0 : E)) << 20;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) fixed48_fast(b[r], kc, ylo[r], yhi[r]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const unsigned long long y = fixed48(b[r], E);
+          ylo[r] = (uint32_t)y;
+          yhi[r] = (uint32_t)(y >> 32);
+        }
+      }
+      unsigned char* dst = dstage + (size_t)sd * kDStageBytes + (size_t)(c >> 3) * 256 + h * 128 + (c & 7) * 16;
+      // 4 x 4 byte transposes: plane word q of digit p = byte (6 - p) of Y
+      // for rows 4q .. 4q + 3 (8 PRMT for the low word's 4 digits, 4 for the
+      // high word's 2, per 4 rows); then XOR 0x80 per byte (balanced digits)
+      uint32_t o[6][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t a01 = __byte_perm(ylo[4 * q], ylo[4 * q + 1], 0x5140);
+        const uint32_t b01 = __byte_perm(ylo[4 * q], ylo[4 * q + 1], 0x7362);
+        const uint32_t a23 = __byte_perm(ylo[4 * q + 2], ylo[4 * q + 3], 0x5140);
+        const uint32_t b23 = __byte_perm(ylo[4 * q + 2], ylo[4 * q + 3], 0x7362);
+        const uint32_t c01 = __byte_perm(yhi[4 * q], yhi[4 * q + 1], 0x5140);
+        const uint32_t c23 = __byte_perm(yhi[4 * q + 2], yhi[4 * q + 3], 0x5140);
+        o[5][q] = __byte_perm(a01, a23, 0x5410) ^ 0x80808080u;  // byte 0: digit 6
+        o[4][q] = __byte_perm(a01, a23, 0x7632) ^ 0x80808080u;  // byte 1: digit 5
+        o[3][q] = __byte_perm(b01, b23, 0x5410) ^ 0x80808080u;  // byte 2: digit 4
+        o[2][q] = __byte_perm(b01, b23, 0x7632) ^ 0x80808080u;  // byte 3: digit 3
+        o[1][q] = __byte_perm(c01, c23, 0x5410) ^ 0x80808080u;  // byte 4: digit 2
+        o[0][q] = __byte_perm(c01, c23, 0x7632) ^ 0x80808080u;  // byte 5: digit 1
+        s8 = __dp4a((int)o[3][q], (int)o[3][q], s8);
+      }
+#pragma unroll
+      for (int p = 1; p <= kDigits; ++p) {
+        if (p == 6 && !need6) break;
+        *reinterpret_cast<uint4*>(dst + (size_t)(p - 1) * kPlane) =
+            make_uint4(o[p - 1][0], o[p - 1][1], o[p - 1][2], o[p - 1][3]);
+      }
+      if (j == nch - 1) dsq[(span & 1) * 2 * kCB + h * kCB + c] = s8;  // the last span's D8 diagonal
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d_full[sd]);
+    }
+    if (badc) atomicOr(&sbad[c], 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (threadIdx.x < kCB && threadIdx.x < n && sbad[threadIdx.x]) atomicOr(&bad_cols[threadIdx.x], 1);
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+// M (n x n, both triangles) = fl64(sum over CTAs of P(i,j) + P(j,i)), in CTA order
+__global__ void __launch_bounds__(256)
+gram_f32_ozaki_combine(const double2* __restrict__ partials, int ncta, int n, const int* __restrict__ bad_cols,
+                       double* __restrict__ m_out) {
+  const int nn = n * n;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += gridDim.x * blockDim.x) {
+    const int j = e / n, i = e - j * n;
+    if (i > j) continue;
+    dd acc = dd_make(0.0, 0.0);
+    for (int k = 0; k < ncta; ++k) {
+      const double2* P = partials + (size_t)k * kCB * kCB;
+      const double2 a = P[(size_t)j * kCB + i], b = P[(size_t)i * kCB + j];
+      acc = dd_add(acc, dd_make(a.x, a.y));
+      acc = dd_add(acc, dd_make(b.x, b.y));
+    }
+    double v = acc.hi;
+    if (bad_cols[i] || bad_cols[j]) v = __longlong_as_double(0x7ff8000000000000ll);
+    m_out[(size_t)j * n + i] = v;
+    m_out[(size_t)i * n + j] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+static size_t ozaki32_smem() {
+  return 1024 + (size_t)kAStages * kAStageBytes + (size_t)kDStages * kDStageBytes + 1024 + 4 * kCB * 4 + kCB * 4 +
+         4 * kCB * 4 + 64 * 4;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+bool gram_ozaki32_supported(const float* a, long long lda, long long m, int n) {
+  return n >= 1 && n <= kCB && m >= 1 && (reinterpret_cast<uintptr_t>(a) % 16 == 0) && (lda % 4 == 0) &&
+         lda < (1LL << 38) && encode_fn() != nullptr;
+}
+
+size_t gram_ozaki32_partial_bytes(int npairs) { return (size_t)2 * npairs * kCB * kCB * sizeof(double2); }
+
+cudaError_t launch_gram_ozaki32_begin(int* bad_cols, cudaStream_t st) {
+  return cudaMemsetAsync(bad_cols, 0, kCB * sizeof(int), st);
+}
+
+cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m, int n, long long c_begin,
+                                      long long c_end, int npairs, double2* partials, int* bad_cols, bool accumulate,
+                                      cudaStream_t st) {
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kCB};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const size_t smem = ozaki32_smem();
+  cudaError_t e = cudaFuncSetAttribute(gram_f32_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // test hook: chunks per exact span (MPSVD_OZAKI32_SPAN, at most kSpanMax)
+  const char* span_env = getenv("MPSVD_OZAKI32_SPAN");
+  int span_max = span_env && atoi(span_env) > 0 ? atoi(span_env) : kSpanMax;
+  if (span_max > kSpanMax) span_max = kSpanMax;
+  gram_f32_ozaki<<<2 * npairs, kThreads, smem, st>>>(map, n, c_begin, c_end, npairs, partials, bad_cols,
+                                                       accumulate ? 1 : 0, span_max);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_ozaki32_combine(const double2* partials, int npairs, int n, const int* bad_cols,
+                                        double* m_out, cudaStream_t st) {
+  const int nn = n * n;
+  int grid = (nn + 255) / 256;
+  if (grid > 148 * 4) grid = 148 * 4;
+  gram_f32_ozaki_combine<<<grid, 256, 0, st>>>(partials, 2 * npairs, n, bad_cols, m_out);
+  return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace mpsvd

@@ -40,6 +40,21 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
                               int* e_cols, unsigned char* digits, double2* partials, int ntp64, int sm_count,
                               cudaStream_t st);
 
+// gram_ozaki32.cu: K1z, the binary64 Gram of a binary32 A (n <= 128) on the
+// int8 tensor cores. A is read by TMA (16-byte aligned, lda % 4 == 0).
+// begin() clears the non-finite column flags; every range launch covers
+// 32-row chunks [c_begin, c_end) with npairs CTA pairs and adds into the
+// 2 npairs double-double partial tiles (accumulate = false: overwrite);
+// combine() writes M (both triangles).
+bool gram_ozaki32_supported(const float* a, long long lda, long long m, int n);
+size_t gram_ozaki32_partial_bytes(int npairs);
+cudaError_t launch_gram_ozaki32_begin(int* bad_cols, cudaStream_t st);
+cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m, int n, long long c_begin,
+                                      long long c_end, int npairs, double2* partials, int* bad_cols, bool accumulate,
+                                      cudaStream_t st);
+cudaError_t launch_gram_ozaki32_combine(const double2* partials, int npairs, int n, const int* bad_cols,
+                                        double* m_out, cudaStream_t st);
+
 // jacobi.cu ------------------------------------------------------------------
 // A (n x n, full symmetric, column-major; f64 or dd=double2) is overwritten:
 // on success its diagonal holds the eigenvalues. The rotation log receives
