@@ -78,62 +78,86 @@ OZ_PRODUCTS = 66                               # digit products p + q <= 12 of 1
 I8_TOPS = 2 * 128 * 256 * 32 / 128 * 148 * 1.965e9 / 1e12  # 4.77 POPS (umma_i8 probe)
 
 
-def ozaki_gram(m_local: int) -> bool:
-    """The engine's double-double Gram choice (engine.cu Plan::Plan): K2z from
-    4096 local rows unless MPSVD_DD_GRAM forces one kernel."""
-    g = os.environ.get("MPSVD_DD_GRAM", "")
-    return g == "ozaki" or (g != "dot2" and m_local >= 4096)
+K1Z_MMAS_PER_CHUNK = 12                        # 2 CTAs x 6 M128 N128 K32 int8 MMAs per 32-row chunk (gram_ozaki32.cu)
+NCU_NAME = {("gram", 0): "gram_f32_diag", ("gram", 1): "gram_f32_ozaki", ("gram", 2): "gram_f64_dd",
+            ("gram", 3): "gram_dd_ozaki", ("compute_u", 0): "av_kernel", ("compute_u", 1): "av_tc_tmem_f32",
+            ("compute_u", 2): "av_dmma_f64"}
+GRAM_KERNELS = {0: "K1 gram_f32_diag/offdiag (DMMA)", 1: "K1z gram_f32_ozaki (tcgen05 kind::i8, TMA)",
+                2: "K2 gram_f64_dd (Dot2, fp64 pipe)", 3: "K2z gram_dd_ozaki (tcgen05 kind::i8) + ozaki_slice/colexp"}
+AV_KERNELS = {0: "av_kernel (fp32 SIMT)", 1: "av_tc_tmem_f32 (tcgen05 bf16x3)", 2: "av_dmma_f64 (DMMA)"}
 
 
 def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
-    """Roofline of every pipeline phase of one SVD on one GPU.
+    """Roofline of every pipeline phase of one SVD on one GPU, each against
+    the bound of the kernel the plan actually ran (info.gram_kernel /
+    info.av_kernel, reported by the library):
 
-    gram  f32: m n (n+1) flops on the DMMA pipe (K1; the phase also holds
-               the two small combine kernels)
-    gram  f64: K2z (>= 4096 rows): 66 int8 digit products per multiply-add
-               on the int8 tensor cores; K2 (Dot2): m n (n+1)/2
-               multiply-adds x 10 fp64 operations (two_prod 2, two_sum 6,
-               error accumulation 2; c_dd = 10 as SURVEY.md §8(d) defines it)
-    eigen    : two-sided Jacobi, latency bound; 18 n flops per rotation
-               (2 rows + 2 columns of M, 2 columns of V) against fp64 peak
-    compute_u: f32: read A + write U (2 m n 4 bytes) against HBM (K7 on the
-               tensor cores, which are far from their bf16 bound);
-               f64: 2 m n^2 flops on the DMMA pipe (av_dmma_f64)
+    gram K1 : m n (n+1) flops on the DMMA pipe
+    gram K1z: 12 int8 MMAs (M = N = 128, K = 32) per 32-row chunk = 12 x 2 x
+              128 x 128 ops per row, against the int8 tensor peak; also
+              m n 4 bytes of A against HBM (hbm_frac)
+    gram K2 : m n (n+1)/2 multiply-adds x 10 fp64 operations (c_dd = 10,
+              SURVEY.md §8(d)) against the DFMA issue rate
+    gram K2z: 66 int8 digit products per multiply-add on the int8 tensor cores
+    eigen   : two-sided Jacobi, latency bound (see `jacobi`); 18 n flops per
+              rotation against fp64 peak for reference only
+    U  f32  : read A + write U (2 m n 4 bytes) against HBM (K7 on the tensor
+              cores, far from their bf16 bound)
+    U  f64  : 2 m n^2 flops on the DMMA pipe (av_dmma_f64)
     """
     out = {}
-    if cfg.working == "f32":
-        a = m_local * n * (n + 1) / (med["gram"] * 1e-3) / 1e12
-        out["gram"] = {"kernel": "gram_f32_diag/offdiag (DMMA)", "bound": "tensor", "achieved": a,
+    gk = int(getattr(info, "gram_kernel", -1))
+    ak = int(getattr(info, "av_kernel", -1))
+    t_g = med["gram"] * 1e-3
+    if gk == 1:
+        ops = float(m_local) * K1Z_MMAS_PER_CHUNK * 2 * 128 * 128
+        a = ops / t_g / 1e12
+        bw = m_local * n * 4 / t_g / 1e9
+        out["gram"] = {"kernel": GRAM_KERNELS[1], "bound": "tensor", "achieved": a, "peak": I8_TOPS,
+                       "unit": "TOPS", "frac": a / I8_TOPS,
+                       "peak_source": "tcgen05 kind::i8 probe: one M128 N256 K32 MMA per 128 cycles per SM "
+                                      "(tools/microbench/umma_i8.cu, profiles/r01_umma_i8.txt) x 148 SMs x 1965 MHz",
+                       "algorithmic": "12 x 2 x 128 x 128 int8 ops per row of A (2 CTA groups x 6 digit-product "
+                                      "MMAs per 32-row chunk)",
+                       "hbm_achieved_gbs": bw, "hbm_frac": bw / hbm,
+                       "fp64_equivalent_tflops": m_local * n * (n + 1) / t_g / 1e12}
+    elif gk == 0:
+        a = m_local * n * (n + 1) / t_g / 1e12
+        out["gram"] = {"kernel": GRAM_KERNELS[0], "bound": "tensor", "achieved": a,
                        "peak": fp64_peak, "unit": "TFLOP/s", "frac": a / fp64_peak,
                        "peak_source": "live DMMA m8n8k4 probe (MEASURED_PEAKS.json has no fp64 figure)",
                        "algorithmic": "m*n*(n+1) flops per SVD"}
-        b = 2.0 * m_local * n * 4 / (med["compute_u"] * 1e-3) / 1e9
-        out["compute_u"] = {"kernel": "av_tc_f32 (tcgen05 bf16x3)", "bound": "hbm", "achieved": b, "peak": hbm,
-                            "unit": "GB/s", "frac": b / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                            "algorithmic": "2*m*n*4 bytes (read A, write U) per SVD"}
-    elif ozaki_gram(m_local):
-        # K2z: 66 exact int8 digit products per entry of the upper triangle
+    elif gk == 3:
         ops = 2.0 * OZ_PRODUCTS * m_local * n * (n + 1) / 2
-        a = ops / (med["gram"] * 1e-3) / 1e12
-        out["gram"] = {"kernel": "gram_dd_ozaki (tcgen05 kind::i8) + ozaki_slice/colexp + combine", "bound": "tensor",
+        a = ops / t_g / 1e12
+        out["gram"] = {"kernel": GRAM_KERNELS[3], "bound": "tensor",
                        "achieved": a, "peak": I8_TOPS, "unit": "TOPS", "frac": a / I8_TOPS,
                        "peak_source": "tcgen05 kind::i8 probe: one M128 N256 K32 MMA per 128 cycles per SM "
                                       "(tools/microbench/umma_i8.cu, profiles/r01_umma_i8.txt) x 148 SMs x 1965 MHz",
                        "algorithmic": "2 x 66 int8 digit products x m x n(n+1)/2 (upper triangle) per SVD",
-                       "dd_equivalent_tops": m_local * n * (n + 1) / 2 * 10 / (med["gram"] * 1e-3) / 1e12}
+                       "dd_equivalent_tops": m_local * n * (n + 1) / 2 * 10 / t_g / 1e12}
     else:
         ops = m_local * n * (n + 1) / 2 * 10
         peak = DFMA_TFLOPS / 2
-        a = ops / (med["gram"] * 1e-3) / 1e12
-        out["gram"] = {"kernel": "gram_f64_dd (Dot2)", "bound": "fp64", "achieved": a, "peak": peak,
-                       "unit": "Tops/s", "frac": a / peak,
+        a = ops / t_g / 1e12
+        out["gram"] = {"kernel": GRAM_KERNELS.get(gk, "K2 gram_f64_dd"), "bound": "fp64", "achieved": a,
+                       "peak": peak, "unit": "Tops/s", "frac": a / peak,
                        "peak_source": "DFMA issue rate (profiles/r01_microbench.txt 34.2 TFLOP/s / 2)",
                        "algorithmic": "c_dd = 10 fp64 ops per multiply-add, m*n*(n+1)/2 multiply-adds"}
-        f = 2.0 * m_local * n * n / (med["compute_u"] * 1e-3) / 1e12
-        out["compute_u"] = {"kernel": "av_dmma_f64 (DMMA)", "bound": "tensor", "achieved": f,
+    t_u = med["compute_u"] * 1e-3
+    if cfg.working == "f32":
+        b = 2.0 * m_local * n * 4 / t_u / 1e9
+        out["compute_u"] = {"kernel": AV_KERNELS.get(ak, "av"), "bound": "hbm", "achieved": b, "peak": hbm,
+                            "unit": "GB/s", "frac": b / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                            "algorithmic": "2*m*n*4 bytes (read A, write U) per SVD"}
+    else:
+        f = 2.0 * m_local * n * n / t_u / 1e12
+        out["compute_u"] = {"kernel": AV_KERNELS.get(ak, "av_dmma_f64 (DMMA)"), "bound": "tensor", "achieved": f,
                             "peak": fp64_peak, "unit": "TFLOP/s", "frac": f / fp64_peak,
                             "peak_source": "live DMMA m8n8k4 probe",
                             "algorithmic": "2*m*n^2 flops per SVD"}
+    out["gram"]["ncu_kernel"] = NCU_NAME.get(("gram", gk))
+    out["compute_u"]["ncu_kernel"] = NCU_NAME.get(("compute_u", ak))
     jf = 18.0 * n * info.rotations / (med["eigen"] * 1e-3) / 1e12
     out["eigen"] = {"kernel": "jacobi_smem / jacobi_kernel", "bound": "latency", "achieved": jf,
                     "peak": DFMA_TFLOPS, "unit": "TFLOP/s", "frac": jf / DFMA_TFLOPS,
@@ -181,14 +205,19 @@ def jacobi_latency(n: int, info, eigen_ms: float, dd: bool, clock_mhz: float = 1
 
 
 def traffic_for(kernel: str, config: str):
-    """DRAM bytes per launch of `kernel` from a committed ncu --set full
-    capture (profiles/r01_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            t = json.load(f)
-        return t.get(config, {}).get(kernel)
-    except (OSError, ValueError):
-        return None
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
+    `kernel` (its ncu function name) from a committed ncu --set full capture
+    (profiles/r02_traffic.json, else r01), or None."""
+    for f in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", f)) as fh:
+                t = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        v = t.get(config, {}).get(kernel)
+        if v is not None:
+            return v
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -556,13 +585,20 @@ def run_ours(args, cfg):
     dom = max(("gram", "compute_u"), key=lambda k: med[k])
     roof = dict(phases[dom])
     roof["phase"] = dom
-    roof["traffic"] = traffic_for(roof["kernel"], cfg.name)
+    roof["traffic"] = traffic_for(roof.get("ncu_kernel") or "", cfg.name)
     jac = jacobi_latency(n, info, med["eigen"], cfg.working != "f32")
     # north_star roofline for the whole Gram+AV pair
     t_hbm = 2.0 * m_global / world * n * esz / (hbm * 1e9)
     t_cmp = (fg + fa) / world / (fp64_peak * 1e12) if cfg.working == "f32" else (fg * 5 + fa) / world / (fp64_peak * 1e12)
     t_roof = max(t_hbm, t_cmp)
     gram_av_ms = med["gram"] + med["compute_u"]
+    floor_ms = {}
+    for ph in ("gram", "compute_u"):
+        r = phases[ph]
+        t_ach = med[ph]
+        t_unit = t_ach * r["achieved"] / r["peak"]           # the kernel's work at its unit's peak
+        t_bytes = (m_local * n * esz * (1 if ph == "gram" else 2)) / (hbm * 1e9) * 1e3
+        floor_ms[ph] = max(t_unit, t_bytes)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -577,7 +613,12 @@ def run_ours(args, cfg):
         "svd_roofline": {"definition": "max(2*m*n*s/HBM, F_gram/P_gram + F_AV/P_fp64) (north_star)",
                          "t_roof_ms": t_roof * 1e3, "gram_plus_av_ms": gram_av_ms,
                          "frac": (t_roof * 1e3) / gram_av_ms if gram_av_ms > 0 else None,
-                         "p_fp64_tflops": fp64_peak},
+                         "p_fp64_tflops": fp64_peak,
+                         "per_kernel_floor_ms": floor_ms,
+                         "per_kernel_frac": sum(floor_ms.values()) / gram_av_ms if gram_av_ms > 0 else None,
+                         "per_kernel_definition": "each of the Gram and U kernels at the floor of the resource it "
+                                                  "runs on (the slower of its algorithmic work at that unit's "
+                                                  "peak and its HBM bytes at measured HBM), summed"},
         "gpu_launches": info.kernel_launches * args.steps,
         "clocks": clk,
         "e2e": e2e,

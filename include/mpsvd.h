@@ -130,6 +130,10 @@ typedef struct mpsvd_exec_info {
   double ms_gram, ms_eigen, ms_compute_u; /* CUDA-event device times */
   int kernel_launches; /* kernels of this library launched by one execute */
   int64_t rounds;      /* parallel Jacobi rounds executed (two-sided solver) */
+  int gram_kernel;     /* Gram kernel of the last execute: 0 K1 (DMMA), 1 K1z (int8 Ozaki),
+                          2 K2 (Dot2), 3 K2z (int8 Ozaki) */
+  int av_kernel;       /* U = A W kernel: 0 av_kernel (SIMT), 1 av_tc_f32 (tcgen05), 2 av_dmma_f64,
+                          -1 none */
 } mpsvd_exec_info;
 
 mpsvd_status mpsvd_comm_unique_id(unsigned char id[128]);

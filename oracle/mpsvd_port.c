@@ -1121,6 +1121,12 @@ void port_oz_sub_group(int i, int* whi, int* nw, int* pa, int* pb) { oz_sub_grou
 int port_gram_dd_ozaki(const double* a, int64_t m, int64_t n, int nsplit, const int* scb, int nblocks,
                        const int* bsb, int span_cap, double* out_hi, double* out_lo) {
   if (m < 1 || n < 1 || nsplit < 1 || nblocks < 1 || nblocks > 16) return ST_INVALID;
+  // the schedule must be a K2z chunk schedule covering every row exactly once
+  if (scb[0] != 0 || (int64_t)scb[nsplit] * 32 < m || bsb[0] != 0 || bsb[nblocks] != nsplit) return ST_INVALID;
+  for (int s = 0; s < nsplit; ++s)
+    if (scb[s + 1] < scb[s]) return ST_INVALID;
+  for (int b = 0; b < nblocks; ++b)
+    if (bsb[b + 1] < bsb[b]) return ST_INVALID;
   int* E = (int*)malloc(sizeof(int) * (size_t)(nsplit * n));
   for (int s = 0; s < nsplit; ++s) {
     const int64_t r0 = (int64_t)scb[s] * 32;

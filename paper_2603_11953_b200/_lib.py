@@ -29,6 +29,8 @@ class ExecInfo(C.Structure):
         ("ms_compute_u", C.c_double),
         ("kernel_launches", C.c_int),
         ("rounds", i64),
+        ("gram_kernel", C.c_int),
+        ("av_kernel", C.c_int),
     ]
 
 

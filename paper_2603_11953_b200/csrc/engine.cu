@@ -495,6 +495,7 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
     check(cudaMemsetAsync(target, 0, (size_t)n * n * sizeof(double) * (dd ? 2 : 1), st), "memset M");
   } else if (oz32_usable(d_a, lda)) {
     // K1z: the same per-logical-block range launches as execute_host
+    gram_kernel = 1;
     check(dev::launch_gram_ozaki32_begin(d_oz32_bad, st), "ozaki32 begin");
     for (int b = 0; b < nblocks; ++b)
       check(dev::launch_gram_ozaki32_range((const float*)d_a, lda, m, (int)n, oz32_bounds[b], oz32_bounds[b + 1],
@@ -504,12 +505,14 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
           "gram_ozaki32 combine");
     launches += nblocks + 1;
   } else if (dd) {
+    gram_kernel = ozaki ? 3 : 2;
     gram_dd_splits(d_a, lda, 0, (int)splits.size(), st);
     check(dev::launch_gram_combine_dd((const double2*)d_partials, ntp, (int)n, ozaki ? d_bsb_oz : d_bsb, nblocks,
                                       (double2*)d_bsums, (double2*)target, st),
           "gram_combine_dd");
     launches += 2;
   } else {
+    gram_kernel = 0;
     check(dev::launch_gram_f32((const float*)d_a, lda, (int)n, d_tiles, ntp, d_tp_order, ndiag,
                                d_tp_order + ndiag, ntp - ndiag, d_splits, (int)splits.size(), (double*)d_partials,
                                st),
@@ -683,7 +686,9 @@ void Plan::enqueue(const void* d_a, long long lda, void* d_u, long long ldu, voi
   void* vw = d_v ? d_v : d_vwork_tmp;
   finish(sig, vw, st);
   record_event(ev[2], st);
+  av_kernel = -1;
   if (d_u && m > 0) {
+    av_kernel = dd ? 2 : (d_wplanes && dev::av_tc_supported((const float*)d_a, lda, m, (int)n, ldu)) ? 1 : 0;
     if (dd)
       check(dev::launch_av_dmma_f64((const double*)d_a, lda, m, (int)n, (const double*)d_w, (double*)d_u, ldu,
                                     jws.status, st),
@@ -733,6 +738,7 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
   check(cudaStreamWaitEvent(cs, cdone, 0), "wait");
   record_event(ev[0], st);
   const bool k1z = oz32_usable(d_a, m);
+  gram_kernel = k1z ? 1 : dd ? (ozaki ? 3 : 2) : 0;
   if (k1z) check(dev::launch_gram_ozaki32_begin(d_oz32_bad, st), "ozaki32 begin");
   {
     const long long base = m / nblocks, extra = m % nblocks;
@@ -785,6 +791,7 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
   check(cudaMemcpyAsync(h_sigma, d_sigma, n * sizeof(double), cudaMemcpyDeviceToHost, cs), "D2H sigma");
   check(cudaMemcpyAsync(h_v, d_v, (size_t)n * n * elt, cudaMemcpyDeviceToHost, cs), "D2H V");
   const bool tc = !dd && d_wplanes && dev::av_tc_supported((const float*)d_a, m, m, (int)n, m);
+  av_kernel = dd ? 2 : tc ? 1 : 0;
   constexpr int kChunks = 16;
   long long r0 = 0;
   bool first = true;  // the first launched chunk splits W into its pieces
@@ -852,6 +859,8 @@ mpsvd_exec_info Plan::wait() {
     info.ms_compute_u = ms;
   }
   info.kernel_launches = launches;
+  info.gram_kernel = gram_kernel;
+  info.av_kernel = av_kernel;
   return info;
 }
 

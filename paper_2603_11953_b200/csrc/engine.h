@@ -86,6 +86,7 @@ class Plan {
   // K1z (binary32 Gram on the int8 tensor cores, gram_ozaki32.cu): one range
   // launch per logical row block, chunk bounds oz32_bounds[b] .. [b + 1]
   bool oz32 = false;
+  int gram_kernel = -1, av_kernel = -1;  // kernels of the last execute (mpsvd_exec_info)
   int oz32_pairs = 0;
   std::vector<long long> oz32_bounds;
   double2* d_oz32_part = nullptr;

@@ -19,44 +19,61 @@ import workloads as inputs  # noqa: E402
 class _Info:
     rotations = 1000
 
+    def __init__(self, gram_kernel=0, av_kernel=1):
+        self.gram_kernel, self.av_kernel = gram_kernel, av_kernel
+
 
 def test_phase_rooflines_f32_units_and_fractions():
+    # K1 (DMMA): m n (n+1) flops against the fp64 tensor peak; K7 on HBM
     cfg = inputs.CONFIGS["c2"]
     med = {"gram": 0.2, "eigen": 0.25, "compute_u": 0.13}
-    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info())
+    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info(0, 1))
     g = ph["gram"]
-    assert g["bound"] == "tensor" and g["unit"] == "TFLOP/s"
+    assert g["bound"] == "tensor" and g["unit"] == "TFLOP/s" and g["ncu_kernel"] == "gram_f32_diag"
     assert g["achieved"] == pytest.approx(cfg.m * cfg.n * (cfg.n + 1) / 0.2e-3 / 1e12)
     assert g["frac"] == pytest.approx(g["achieved"] / 37.0)
     u = ph["compute_u"]
     assert u["bound"] == "hbm" and u["achieved"] == pytest.approx(2 * cfg.m * cfg.n * 4 / 0.13e-3 / 1e9)
+    assert u["ncu_kernel"] == "av_tc_tmem_f32"
     assert ph["eigen"]["bound"] == "latency"
 
 
-def test_phase_rooflines_dd_uses_c_dd_10(monkeypatch):
-    # K2 (Dot2, forced): c_dd = 10 fp64 operations per multiply-add
-    monkeypatch.setenv("MPSVD_DD_GRAM", "dot2")
+def test_phase_rooflines_k1z_against_int8_peak():
+    # K1z: 12 int8 MMAs (M = N = 128, K = 32) per 32-row chunk against the
+    # kind::i8 peak, plus its A stream against HBM
+    cfg = inputs.CONFIGS["c4"]
+    med = {"gram": 24.0, "eigen": 2.7, "compute_u": 14.5}
+    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info(1, 1))
+    g = ph["gram"]
+    assert g["ncu_kernel"] == "gram_f32_ozaki" and g["unit"] == "TOPS"
+    assert g["achieved"] == pytest.approx(cfg.m * 12 * 2 * 128 * 128 / 24e-3 / 1e12)
+    assert g["peak"] == pytest.approx(bench.I8_TOPS)
+    assert g["hbm_achieved_gbs"] == pytest.approx(cfg.m * cfg.n * 4 / 24e-3 / 1e9)
+
+
+def test_phase_rooflines_dd_uses_c_dd_10():
+    # K2 (Dot2): c_dd = 10 fp64 operations per multiply-add
     cfg = inputs.CONFIGS["c5"]
     med = {"gram": 1400.0, "eigen": 800.0, "compute_u": 270.0}
-    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info())
+    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info(2, 2))
     g = ph["gram"]
     assert g["achieved"] == pytest.approx(cfg.m * cfg.n * (cfg.n + 1) / 2 * 10 / 1.4 / 1e12)
     assert g["peak"] == pytest.approx(bench.DFMA_TFLOPS / 2)
     assert ph["compute_u"]["bound"] == "tensor"
 
 
-def test_phase_rooflines_dd_ozaki_against_int8_peak(monkeypatch):
-    # K2z (the engine's choice from 4096 rows): 66 int8 digit products per
-    # multiply-add against the measured kind::i8 tensor peak
-    monkeypatch.delenv("MPSVD_DD_GRAM", raising=False)
+def test_phase_rooflines_dd_ozaki_against_int8_peak():
+    # K2z: 66 int8 digit products per multiply-add against the measured
+    # kind::i8 tensor peak; U on DMMA (c5's dominant phase: the line's
+    # headline roofline must exist for it)
     cfg = inputs.CONFIGS["c5"]
     med = {"gram": 236.0, "eigen": 800.0, "compute_u": 270.0}
-    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info())
+    ph = bench.phase_rooflines(cfg, cfg.m, cfg.n, med, 37.0, 6555.2, _Info(3, 2))
     g = ph["gram"]
     assert g["achieved"] == pytest.approx(2 * 66 * cfg.m * cfg.n * (cfg.n + 1) / 2 / 0.236 / 1e12)
     assert g["peak"] == pytest.approx(bench.I8_TOPS)
     assert 4700 < bench.I8_TOPS < 4800
-    assert not bench.ozaki_gram(4095) and bench.ozaki_gram(4096)
+    assert ph["compute_u"]["ncu_kernel"] == "av_dmma_f64"
 
 
 @pytest.mark.parametrize("name,world", [("c2", 1), ("c2", 8), ("c4", 4), ("c5", 2)])

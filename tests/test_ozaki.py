@@ -141,9 +141,11 @@ def test_gpu_ozaki_gram_bitwise_vs_restatement(port, m, n, decades, monkeypatch)
 def test_gpu_ozaki_short_spans_bitwise(port, monkeypatch):
     # several drains per CTA (MPSVD_OZAKI_SPAN: chunks per exact span)
     monkeypatch.setenv("MPSVD_OZAKI_SPAN", "3")
+    monkeypatch.setenv("MPSVD_DD_GRAM", "ozaki")  # the engine picks K2z itself only from n = 128
     m, n = 6000, 70
     a = _graded(m, n, 10, seed=2)
     oz, scb, bsb = M.gram_schedule(m, n)
+    assert oz
     hi, lo = M.gram(a)
     rh, rl = port.gram_dd_ozaki(a, scb, bsb, span_cap=3)
     assert np.array_equal(hi, rh) and np.array_equal(lo, rl)
@@ -154,6 +156,7 @@ def test_gpu_ozaki_matches_dot2_kernel(port, monkeypatch):
     # K2z against K2 (MPSVD_DD_GRAM=dot2) and the reference oracle
     m, n = 20000, 96
     a = _graded(m, n, 12, seed=9)
+    monkeypatch.setenv("MPSVD_DD_GRAM", "ozaki")
     hi, lo = M.gram(a)
     monkeypatch.setenv("MPSVD_DD_GRAM", "dot2")
     dh, dl = M.gram(a)
