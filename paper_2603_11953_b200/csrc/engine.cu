@@ -281,7 +281,9 @@ Plan::Plan(long long m_local, long long n_cols, bool f64_working, Comm* c)
     oz32 = s32 == "ozaki" || (s32 != "dmma" && n > 64 && m >= (1LL << 20));
     if (oz32) {
       const long long nch = (m + 31) / 32;
-      oz32_pairs = (int)std::max(1LL, std::min<long long>(sm_count / 2, nch / 64));
+      const int resident = dev::gram_ozaki32_max_pairs();
+      oz32_pairs = (int)std::max(1LL, std::min<long long>(std::min(sm_count / 2, resident > 0 ? resident : sm_count / 2),
+                                                          nch / 64));
       oz32_bounds.clear();
       const long long base = m / nblocks, extra = m % nblocks;
       long long row = 0;

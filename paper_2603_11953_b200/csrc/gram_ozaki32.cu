@@ -79,11 +79,11 @@ constexpr int kDigits = 6;
 constexpr int kHead = 2;                      // exponent headroom (bits) of a new span
 constexpr int kSpanMax = 1024;                // chunks per span: int32 sums stay exact
 constexpr int kZeroE = -160;                  // exponent of an all-zero column
-constexpr int kAStages = 8;                   // fp32 chunk slots (16 KB each): ~2 us of HBM latency in flight
-constexpr int kDStages = 3;                   // digit slots (6 planes = 24 KB each)
 constexpr int kAStageBytes = kKC * kCB * 4;   // 16384
 constexpr int kDStageBytes = kDigits * kPlane;
-constexpr int kThreads = 576;
+constexpr int kThreads = 608;
+constexpr int kWarpCopy = 18;                 // DSMEM bulk copies of this CTA's digit half to the peer
+constexpr int kHalfBytes = kDigits * 2048;    // one CTA's 16-row half of a digit slot: 6 planes x 2 KB
 constexpr int kConvThreads = 256;
 constexpr int kConvWarp0 = 6;
 constexpr int kScoutWarp0 = 14, kScoutWarps = 4;
@@ -161,9 +161,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes) : "memory");
 }
-// try_wait with a long suspend-time hint: a waiting warp sleeps until the
-// phase completes (woken at once) instead of re-polling and taking issue
-// slots from the converters
+// try_wait with a long suspend-time hint (wait mode 0). The hinted sleep
+// ends at any mbarrier activity of the CTA, so in this kernel (barriers
+// updated every few cycles) a waiting warp re-polls every ~20 ns: the drain
+// warps' span-long waits alone took 18% of all issue slots (ncu, c4). Wait
+// mode 2 polls once and then backs off by a per-site __nanosleep, long for
+// the waits that span many chunks (drain, accumulator hand-off), short or
+// none on the per-chunk hand-offs.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   uint32_t done = 0;
   do {
@@ -174,12 +178,104 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         : "memory");
   } while (!done);
 }
-__device__ __forceinline__ uint64_t kdesc(uint32_t addr) {  // K-major, no swizzle, LBO 128, SBO 256
+__device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(saddr(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(saddr(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+// Release an A slot after this warp's shared-memory loads of it (called by
+// every lane; dep = the lane's loaded data). The arrive must not overtake a
+// load still in flight, or the TMA refills the slot under it: measured, with
+// 4-7 A slots and a plain lane-0 arrive after __syncwarp, the converters'
+// second LDS of a chunk sometimes returned the next occupant's data
+// (tools/oz32_harness.cu). A zero derived from every lane's loaded registers
+// is OR-reduced over the warp (REDUX waits for all lanes' loads to return)
+// and lane 0's arrive count depends on it.
+// zmask is a runtime zero (a kernel argument's unused bits): ptxas folds an
+// AND with the constant 0 and the dependency with it.
+__device__ __forceinline__ void release_a(uint64_t* b, int lane, uint32_t dep, uint32_t zmask) {
+  uint32_t z = __reduce_or_sync(0xffffffffu, dep & zmask);
+  if (lane == 0)
+    asm volatile(
+        "{\n.reg .b32 cnt;\nadd.u32 cnt, %1, 1;\n"
+        "mbarrier.arrive.shared::cta.b64 _, [%0], cnt;\n}\n" ::"r"(saddr(b)),
+        "r"(z)
+        : "memory");
+}
+// cluster-scope acquire (the digit slots are also filled by the peer CTA's
+// converters, which arrive with release.cluster)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, unsigned parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(saddr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_v2(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// MMA completion -> the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void commit_lead_pair(uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %1, 0;\n"
+      "@l tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %2;\n}\n" ::
+          "r"(saddr(bar)),
+      "r"(lead), "h"((unsigned short)3)
+      : "memory");
+}
+// wmode 0: hinted try_wait; 1: un-hinted try_wait loop; 2: test_wait with
+// __nanosleep(ns) back-off (ns = 0: un-hinted try_wait loop)
+__device__ __forceinline__ void mbar_wait_m(uint64_t* b, unsigned parity, int wmode, unsigned ns) {
+  if (wmode == 0) {
+    mbar_wait(b, parity);
+  } else if (wmode == 1 || ns == 0) {
+    while (!mbar_try(b, parity)) {
+    }
+  } else {
+    while (!mbar_test(b, parity)) __nanosleep(ns);
+  }
+}
+// Digit slot layout: [K half h][digit p][16 column groups][8 columns x 16 B],
+// i.e. K-major, no swizzle, with the two 16-row K halves kHalfBytes apart
+// (LBO) and 8-column groups 128 B apart (SBO): each CTA's half of a slot is
+// one contiguous block, moved to the peer by a single bulk copy.
+__device__ __forceinline__ uint64_t kdesc(uint32_t addr) {
   uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)(128 >> 4) << 16;
-  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)(kHalfBytes >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   return d;
+}
+__device__ __forceinline__ void bulk_s2peer(uint32_t dst_cl, uint32_t src, unsigned bytes, uint32_t bar_cl) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   dst_cl),
+               "r"(src), "r"(bytes), "r"(bar_cl)
+               : "memory");
 }
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -231,8 +327,8 @@ __device__ __forceinline__ void issue_chunk(uint32_t tmem, uint64_t sd, uint32_t
     product(G, k, p, q, acc);
     const uint32_t first = fresh && !(started & (1u << acc));
     started |= 1u << acc;
-    umma_i8_lead(tmem + (uint32_t)(acc * kCB), sd + (uint64_t)((p - 1) * (kPlane >> 4)),
-                 sd + (uint64_t)((q - 1) * (kPlane >> 4)), idesc, first ? 0u : 1u, lead);
+    umma_i8_lead(tmem + (uint32_t)(acc * kCB), sd + (uint64_t)((p - 1) * (2048 >> 4)),
+                 sd + (uint64_t)((q - 1) * (2048 >> 4)), idesc, first ? 0u : 1u, lead);
   }
 }
 
@@ -256,10 +352,21 @@ __device__ __forceinline__ dd group_total(int g, int a0, int a1, int a2, int a3)
 
 using namespace oz32;
 
+// Debug hook (tools/oz32_harness.cu only; null in the library): per global
+// chunk, the digits the converters wrote ([chunk][digit][column][32 rows]
+// int8), the exponent each column used and the MMA's span-start flag.
+struct Oz32Dbg {
+  int8_t* digits;
+  short* E;
+  int* fresh;
+};
+__device__ Oz32Dbg g_oz32_dbg = {nullptr, nullptr, nullptr};
+
 // ---------------------------------------------------------------------------
+template <int kAStages, int kDStages>
 __global__ void __launch_bounds__(kThreads, 1)
 gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begin, long long c_end, int npairs,
-               double2* __restrict__ partials, int* __restrict__ bad_cols, int accumulate, int span_max) {
+               double2* __restrict__ partials, int* __restrict__ bad_cols, int accumulate, int span_max, int wmode) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-aligned carve-up (the 128B swizzle needs 1024-byte aligned boxes);
   // offsets from smem_raw keep the pointers in the shared window (LDS/STS,
@@ -277,16 +384,18 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   uint64_t* info_full = acc_empty + 1;   // span metadata published by the issuer
   uint64_t* desc_empty = info_full + 1;  // 2: span exponent descriptors free
   uint64_t* meta_full = desc_empty + 2;  // kAStages: the scout's decision for the chunk in A slot s
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(meta_full + kAStages);
+  uint64_t* half_full = meta_full + kAStages;  // kDStages: this CTA's half of the slot is written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(half_full + kDStages);
   int* d_meta = reinterpret_cast<int*>(tmem_slot + 4);   // kDStages: chunk starts a span
   int* span_last = d_meta + kDStages;                    // issuer -> drain: this span is the last
   int* desc = span_last + 4;                             // [2][128] span exponents
   int* meta = desc + 2 * kCB;                            // [kAStages][2]: fresh, span
   int* sbad = meta + 2 * kAStages;                       // [128]
-  int* dsq = sbad + kCB;                                           // [2][2][128] D8 diagonal sums per span
+  int* dsq = sbad + kCB;                                 // [2][2][128] D8 diagonal sums of this CTA's rows per span
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x >> 1, g = blockIdx.x & 1;
+  const uint32_t zmask = (uint32_t)wmode >> 8;  // 0 (wmode < 256), unknown to the compiler
   const long long nch_all = c_end - c_begin;
   const long long c0 = c_begin + nch_all * pair / npairs, c1 = c_begin + nch_all * (pair + 1) / npairs;
   const int nch = (int)(c1 - c0);
@@ -298,8 +407,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       mbar_init(&meta_full[i], kScoutWarps);
     }
     for (int i = 0; i < kDStages; ++i) {
-      mbar_init(&d_full[i], kConvThreads / 32);
-      mbar_init(&d_empty[i], 1);
+      mbar_init(&d_full[i], kConvThreads / 32);  // own converter warps (+ the peer's half: transaction bytes)
+      mbar_init(&d_empty[i], 2);                 // the MMAs of both CTAs have read the slot
+      mbar_init(&half_full[i], kConvThreads / 32);
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4);
@@ -316,6 +426,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / store
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -325,7 +436,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&amap) : "memory");
       for (int j = 0; j < nch; ++j) {
         const int s = j % kAStages;
-        mbar_wait(&a_empty[s], ((unsigned)(j / kAStages) & 1u) ^ 1u);
+        mbar_wait_m(&a_empty[s], ((unsigned)(j / kAStages) & 1u) ^ 1u, wmode, 64);
         mbar_expect_tx(&a_full[s], kAStageBytes);
         tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + j) * kKC), 0, &a_full[s]);
       }
@@ -342,8 +453,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     int span = -1;
     for (int j = 0; j < nch; ++j) {
       const int s = j % kDStages;
-      mbar_wait(&d_full[s], (unsigned)(j / kDStages) & 1u);
+      mbar_wait_cl(&d_full[s], (unsigned)(j / kDStages) & 1u);
       const bool fresh = d_meta[s] != 0;
+      if (g_oz32_dbg.fresh && lead) g_oz32_dbg.fresh[(c0 + j) * 2 + g] = fresh ? 1 : 0;
       if (fresh) {
         if (span >= 0) {  // close the previous span: the drain may read it
           if (lead) span_last[span & 1] = 0;
@@ -352,7 +464,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
           commit_lead(acc_full, lead);
         }
         ++span;
-        mbar_wait(acc_empty, (unsigned)span & 1u);  // its accumulators are drained
+        mbar_wait_m(acc_empty, (unsigned)span & 1u, wmode, 128);  // its accumulators are drained
       }
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint64_t sd = dbase + (uint64_t)((uint32_t)s * (kDStageBytes >> 4));
@@ -360,12 +472,30 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         issue_chunk<0>(tmem, sd, idesc, fresh, lead);
       else
         issue_chunk<1>(tmem, sd, idesc, fresh, lead);
-      commit_lead(&d_empty[s], lead);  // the digit slot is free once these MMAs have read it
+      commit_lead_pair(&d_empty[s], lead);  // the slot is free (in both CTAs) once these MMAs have read it
     }
     if (lead) span_last[span >= 0 ? (span & 1) : 0] = span >= 0 ? 1 : 2;  // 2: no chunk, nothing to drain
     __syncwarp();
     arrive_lead(info_full, lead);
     if (span >= 0) commit_lead(acc_full, lead);
+  } else if (warp == kWarpCopy) {
+    // ---- copier: once this CTA's converters have written their half of
+    // digit slot s, one bulk copy moves it into the peer's slot s, completing
+    // on the peer's d_full (transaction bytes). Group 1 does not use digit 6,
+    // so group 0 sends digits 1-5 only.
+    if (lane == 0) {
+      const uint32_t peer = (uint32_t)(g ^ 1);
+      const uint32_t src0 = saddr(dstage) + (uint32_t)(g * kHalfBytes);
+      const uint32_t dst0 = mapa(src0, peer);
+      const uint32_t bar0 = mapa(saddr(d_full), peer);
+      const unsigned bytes = g == 0 ? 5u * 2048u : 6u * 2048u;
+      for (int j = 0; j < nch; ++j) {
+        const int s = j % kDStages;
+        mbar_wait_m(&half_full[s], (unsigned)(j / kDStages) & 1u, wmode, 0);
+        bulk_s2peer(dst0 + (uint32_t)(s * kDStageBytes), src0 + (uint32_t)(s * kDStageBytes), bytes,
+                    bar0 + (uint32_t)(s * 8));
+      }
+    }
   } else if (warp >= kScoutWarp0) {
     // ---- scouts: lane owns column c = 32 (warp - kScoutWarp0) + lane; per
     // chunk the column maximum (finite entries), the span decision (first
@@ -376,7 +506,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     int span = -1, len = 0;
     for (int j = 0; j < nch; ++j) {
       const int sa = j % kAStages;
-      mbar_wait(&a_full[sa], (unsigned)(j / kAStages) & 1u);
+      mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 64);
       const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
       // max of |x| as bit patterns over all entries: inf / NaN (exponent 255)
       // lie above every finite value, so they force a new span and a huge
@@ -387,8 +517,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ (c & 7)) << 4));
         mx = max(mx, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a_empty[sa]);
+      release_a(&a_empty[sa], lane, mx, zmask);
       // bit 0: some column needs a new span; bit 1: some entry is inf / NaN
       const uint32_t mine = (fexp_bits(mx) > Ec ? 1u : 0u) | (mx >= 0x7F800000u ? 2u : 0u);
       uint32_t any, anybad;
@@ -406,7 +535,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       if (fresh) {
         ++span;
         len = 0;
-        if (span >= 2) mbar_wait(&desc_empty[span & 1], ((unsigned)(span >> 1) & 1u) ^ 1u);
+        if (span >= 2) mbar_wait_m(&desc_empty[span & 1], ((unsigned)(span >> 1) & 1u) ^ 1u, wmode, 256);
         Ec = mx ? fexp_bits(mx) + kHead : kZeroE;
         desc[(span & 1) * kCB + c] = Ec;
       }
@@ -426,14 +555,14 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     if (lane == 0) mbar_arrive(acc_empty);  // the accumulators start free
     double2* P = partials + (size_t)blockIdx.x * kCB * kCB;
     for (int span = 0;; ++span) {
-      mbar_wait(info_full, (unsigned)span & 1u);
+      mbar_wait_m(info_full, (unsigned)span & 1u, wmode, 2048);
       const int last = span_last[span & 1];
       if (last == 2) {  // empty range: the partial is zero
         if (!accumulate && i < n)
           for (int jj = 0; jj < n; ++jj) P[(size_t)jj * kCB + i] = make_double2(0.0, 0.0);
         break;
       }
-      mbar_wait(acc_full, (unsigned)span & 1u);
+      mbar_wait_m(acc_full, (unsigned)span & 1u, wmode, 256);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int* E = desc + (span & 1) * kCB;
       const int ei = E[i];
@@ -461,9 +590,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
             const int jc = j0 + jj;
             if (jc >= n) continue;
             dd t0 = group_total(g, (int)v[0][jj], (int)v[1][jj], (int)v[2][jj], (int)v[3][jj]);
-            if (g == 1 && jc == i)  // D8 diagonal: sum d_4^2 at 2^-16 of this frame (halved)
+            if (jc == i)  // D8 diagonal of this CTA's rows: sum d_4^2 at 2^-16 (group 1) / 2^-9 (group 0), halved
               t0 = dd_add(t0, dd_make((double)(dsq[(span & 1) * 2 * kCB + i] + dsq[(span & 1) * 2 * kCB + kCB + i]) *
-                                          0x1p-16,
+                                          (g ? 0x1p-16 : 0x1p-9),
                                       0.0));
             const int sc = ei + E[jc] - 92 + basee;
             dd t = dd_make(scalbn(t0.hi, sc), scalbn(t0.lo, sc));
@@ -481,101 +610,122 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       if (last) break;
     }
   } else {
-    // ---- converters: thread = (column c, rows 16 h .. 16 h + 15)
+    // ---- converters: thread = (column c, rows 16 g + 8 q .. + 7). Each CTA
+    // of the pair converts its own 16-row half of every chunk into its own
+    // digit slot; the copier moves that half into the peer's slot (one bulk
+    // copy through distributed shared memory), so the pair converts each
+    // chunk once. A slot is full when this CTA's converter warps have
+    // arrived and the peer's half has landed (transaction bytes), and free
+    // when both CTAs' MMAs have read it (multicast commit).
     const int t = threadIdx.x - kConvWarp0 * 32;
-    const int c = t & (kCB - 1), h = t >> 7;
-    const bool need6 = g == 0;  // group 1 uses digits 1-5 only
+    const int q = t & 1, c = t >> 1;  // lanes 2k, 2k + 1 store adjacent 8-byte pieces (no bank conflicts)
+    const uint32_t dloc = saddr(dstage) + (uint32_t)(g * kHalfBytes + (c >> 3) * 128 + (c & 7) * 16 + q * 8);
+    const unsigned in_bytes = g == 0 ? 6u * 2048u : 5u * 2048u;  // the peer's half (group 1 gets digits 1-5)
+    const int dsq_idx = q * kCB + c;
     int E = kZeroE;
     int span = -1;
     int badc = 0;
     int s8 = 0;  // sum of d_4^2 over this thread's rows of the open span
     for (int j = 0; j < nch; ++j) {
       const int sa = j % kAStages;
-      mbar_wait(&meta_full[sa], (unsigned)(j / kAStages) & 1u);
-      mbar_wait(&a_full[sa], (unsigned)(j / kAStages) & 1u);  // already complete: the TMA data's visibility
+      mbar_wait_m(&meta_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
+      mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);  // already complete: the TMA data's visibility
       const int mflags = meta[2 * sa];
       const bool fresh = (mflags & 1) != 0;
       const int mspan = meta[2 * sa + 1];
-      // 16 values: 16-byte units 4h .. 4h + 3 of column c, 128B-swizzled
+      // 8 values: 16-byte units 4 g + 2 q, + 1 of column c, 128B-swizzled
       const unsigned char* col = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
-      uint32_t b[16];
+      uint32_t b[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint4 w = *reinterpret_cast<const uint4*>(col + (((4 * h + u) ^ (c & 7)) << 4));
+      for (int u = 0; u < 2; ++u) {
+        const uint4 w = *reinterpret_cast<const uint4*>(col + (((4 * g + 2 * q + u) ^ (c & 7)) << 4));
         b[4 * u] = w.x;
         b[4 * u + 1] = w.y;
         b[4 * u + 2] = w.z;
         b[4 * u + 3] = w.w;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a_empty[sa]);
+      release_a(&a_empty[sa], lane, b[0] | b[4] | (uint32_t)mflags, zmask);
       if (mflags & 2) {  // inf / NaN in this chunk (the scouts saw it): flag the column, use zeros
 #pragma unroll
-        for (int r = 0; r < 16; ++r)
+        for (int r = 0; r < 8; ++r)
           if ((b[r] & 0x7FFFFFFFu) >= 0x7F800000u) {
             b[r] = 0;
             badc = 1;
           }
       }
       if (fresh) {
-        if (span >= 0) dsq[(span & 1) * 2 * kCB + h * kCB + c] = s8;  // the closing span's D8 diagonal
+        if (span >= 0) dsq[(span & 1) * 2 * kCB + dsq_idx] = s8;  // the closing span's D8 diagonal
         s8 = 0;
         span = mspan;
         E = desc[(span & 1) * kCB + c];
       }
       const int sd = j % kDStages;
-      mbar_wait(&d_empty[sd], ((unsigned)(j / kDStages) & 1u) ^ 1u);
+      mbar_wait_m(&d_empty[sd], ((unsigned)(j / kDStages) & 1u) ^ 1u, wmode, 32);
       if (t == 0) d_meta[sd] = fresh ? 1 : 0;
-      uint32_t ylo[16], yhi[16];
+      uint32_t ylo[8], yhi[8];
       if (__all_sync(0xffffffffu, E >= -78 || E == kZeroE)) {
         const uint32_t kc = (uint32_t)(942 - (E == kZeroE ? 0 : E)) << 20;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) fixed48_fast(b[r], kc, ylo[r], yhi[r]);
+        for (int r = 0; r < 8; ++r) fixed48_fast(b[r], kc, ylo[r], yhi[r]);
       } else {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
+        for (int r = 0; r < 8; ++r) {
           const unsigned long long y = fixed48(b[r], E);
           ylo[r] = (uint32_t)y;
           yhi[r] = (uint32_t)(y >> 32);
         }
       }
-      unsigned char* dst = dstage + (size_t)sd * kDStageBytes + (size_t)(c >> 3) * 256 + h * 128 + (c & 7) * 16;
-      // 4 x 4 byte transposes: plane word q of digit p = byte (6 - p) of Y
-      // for rows 4q .. 4q + 3 (8 PRMT for the low word's 4 digits, 4 for the
+      // 4 x 4 byte transposes: plane word w of digit p = byte (6 - p) of Y
+      // for rows 4w .. 4w + 3 (8 PRMT for the low word's 4 digits, 4 for the
       // high word's 2, per 4 rows); then XOR 0x80 per byte (balanced digits)
-      uint32_t o[6][4];
+      uint32_t o[6][2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t a01 = __byte_perm(ylo[4 * q], ylo[4 * q + 1], 0x5140);
-        const uint32_t b01 = __byte_perm(ylo[4 * q], ylo[4 * q + 1], 0x7362);
-        const uint32_t a23 = __byte_perm(ylo[4 * q + 2], ylo[4 * q + 3], 0x5140);
-        const uint32_t b23 = __byte_perm(ylo[4 * q + 2], ylo[4 * q + 3], 0x7362);
-        const uint32_t c01 = __byte_perm(yhi[4 * q], yhi[4 * q + 1], 0x5140);
-        const uint32_t c23 = __byte_perm(yhi[4 * q + 2], yhi[4 * q + 3], 0x5140);
-        o[5][q] = __byte_perm(a01, a23, 0x5410) ^ 0x80808080u;  // byte 0: digit 6
-        o[4][q] = __byte_perm(a01, a23, 0x7632) ^ 0x80808080u;  // byte 1: digit 5
-        o[3][q] = __byte_perm(b01, b23, 0x5410) ^ 0x80808080u;  // byte 2: digit 4
-        o[2][q] = __byte_perm(b01, b23, 0x7632) ^ 0x80808080u;  // byte 3: digit 3
-        o[1][q] = __byte_perm(c01, c23, 0x5410) ^ 0x80808080u;  // byte 4: digit 2
-        o[0][q] = __byte_perm(c01, c23, 0x7632) ^ 0x80808080u;  // byte 5: digit 1
-        s8 = __dp4a((int)o[3][q], (int)o[3][q], s8);
+      for (int w = 0; w < 2; ++w) {
+        const uint32_t a01 = __byte_perm(ylo[4 * w], ylo[4 * w + 1], 0x5140);
+        const uint32_t b01 = __byte_perm(ylo[4 * w], ylo[4 * w + 1], 0x7362);
+        const uint32_t a23 = __byte_perm(ylo[4 * w + 2], ylo[4 * w + 3], 0x5140);
+        const uint32_t b23 = __byte_perm(ylo[4 * w + 2], ylo[4 * w + 3], 0x7362);
+        const uint32_t c01 = __byte_perm(yhi[4 * w], yhi[4 * w + 1], 0x5140);
+        const uint32_t c23 = __byte_perm(yhi[4 * w + 2], yhi[4 * w + 3], 0x5140);
+        o[5][w] = __byte_perm(a01, a23, 0x5410) ^ 0x80808080u;  // byte 0: digit 6
+        o[4][w] = __byte_perm(a01, a23, 0x7632) ^ 0x80808080u;  // byte 1: digit 5
+        o[3][w] = __byte_perm(b01, b23, 0x5410) ^ 0x80808080u;  // byte 2: digit 4
+        o[2][w] = __byte_perm(b01, b23, 0x7632) ^ 0x80808080u;  // byte 3: digit 3
+        o[1][w] = __byte_perm(c01, c23, 0x5410) ^ 0x80808080u;  // byte 4: digit 2
+        o[0][w] = __byte_perm(c01, c23, 0x7632) ^ 0x80808080u;  // byte 5: digit 1
+        s8 = __dp4a((int)o[3][w], (int)o[3][w], s8);
       }
+      const uint32_t so = dloc + (uint32_t)(sd * kDStageBytes);
 #pragma unroll
-      for (int p = 1; p <= kDigits; ++p) {
-        if (p == 6 && !need6) break;
-        *reinterpret_cast<uint4*>(dst + (size_t)(p - 1) * kPlane) =
-            make_uint4(o[p - 1][0], o[p - 1][1], o[p - 1][2], o[p - 1][3]);
+      for (int p = 1; p <= kDigits; ++p) st_v2(so + (uint32_t)((p - 1) * 2048), o[p - 1][0], o[p - 1][1]);
+      if (g_oz32_dbg.digits) {
+        const long long gc = c0 + j;
+        for (int p = 1; p <= kDigits; ++p)
+          *reinterpret_cast<uint2*>(g_oz32_dbg.digits + ((gc * kDigits + p - 1) * kCB + c) * 32 + 16 * g + 8 * q) =
+              make_uint2(o[p - 1][0], o[p - 1][1]);
+        if (g == 0 && q == 0) g_oz32_dbg.E[gc * kCB + c] = (short)E;
       }
-      if (j == nch - 1) dsq[(span & 1) * 2 * kCB + h * kCB + c] = s8;  // the last span's D8 diagonal
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core reads
+      if (j == nch - 1) dsq[(span & 1) * 2 * kCB + dsq_idx] = s8;  // the last span's D8 diagonal
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core / bulk copy
       __syncwarp();
-      if (lane == 0) mbar_arrive(&d_full[sd]);
+      if (lane == 0) {
+        mbar_arrive(&half_full[sd]);
+        if (t == 0)
+          mbar_expect_tx(&d_full[sd], in_bytes);  // one of the arrivals also expects the peer's half
+        else
+          mbar_arrive(&d_full[sd]);
+      }
     }
+    // the peer's MMAs arrive (multicast) on this CTA's slot barriers: wait
+    // for the last arrivals before this CTA may exit
+    for (int jj = nch; jj < nch + kDStages; ++jj)
+      if (jj >= kDStages) mbar_wait_m(&d_empty[jj % kDStages], ((unsigned)(jj / kDStages) & 1u) ^ 1u, wmode, 32);
     if (badc) atomicOr(&sbad[c], 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  cluster_sync_all();  // no remote store or arrive targets this CTA after it exits
   if (threadIdx.x < kCB && threadIdx.x < n && sbad[threadIdx.x]) atomicOr(&bad_cols[threadIdx.x], 1);
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
 }
@@ -603,9 +753,31 @@ gram_f32_ozaki_combine(const double2* __restrict__ partials, int ncta, int n, co
 }
 
 // ---------------------------------------------------------------------------
-static size_t ozaki32_smem() {
-  return 1024 + (size_t)kAStages * kAStageBytes + (size_t)kDStages * kDStageBytes + 1024 + 4 * kCB * 4 + kCB * 4 +
+static size_t ozaki32_smem(int astages, int dstages) {
+  return 1024 + (size_t)astages * kAStageBytes + (size_t)dstages * kDStageBytes + 1024 + 4 * kCB * 4 + kCB * 4 +
          4 * kCB * 4 + 64 * 4;
+}
+
+// pipeline shape (MPSVD_OZ32_STAGES: "8x3" or "7x4" A x digit slots) and
+// wait mode (MPSVD_OZ32_WAIT: 0 hinted try_wait, 1 plain try_wait, 2
+// back-off), read once
+struct Oz32Cfg {
+  int astages = 8, dstages = 3;  // A x digit slots
+  int wmode = 2;
+};
+static const Oz32Cfg& oz32_cfg() {
+  static Oz32Cfg c;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* st = getenv("MPSVD_OZ32_STAGES");
+    if (st && st[0] >= '4' && st[0] <= '8' && st[1] == 'x' && st[2] >= '2' && st[2] <= '4') {
+      c.astages = st[0] - '0';
+      c.dstages = st[2] - '0';
+    }
+    const char* w = getenv("MPSVD_OZ32_WAIT");
+    if (w && w[0] >= '0' && w[0] <= '2') c.wmode = w[0] - '0';
+  });
+  return c;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -628,6 +800,50 @@ bool gram_ozaki32_supported(const float* a, long long lda, long long m, int n) {
          lda < (1LL << 38) && encode_fn() != nullptr;
 }
 
+// CTA pairs (clusters of 2) that can be resident at once: the launch must
+// fit one wave (a second wave of a few pairs would double the range's time)
+using Oz32Kern = void (*)(CUtensorMap, int, long long, long long, int, double2*, int*, int, int, int);
+static Oz32Kern oz32_kernel(const Oz32Cfg& c) {
+  const int k = c.astages * 10 + c.dstages;
+  switch (k) {
+    case 73: return gram_f32_ozaki<7, 3>;
+    case 74: return gram_f32_ozaki<7, 4>;
+    case 64: return gram_f32_ozaki<6, 4>;
+    case 63: return gram_f32_ozaki<6, 3>;
+    case 43: return gram_f32_ozaki<4, 3>;
+    case 53: return gram_f32_ozaki<5, 3>;
+    case 44: return gram_f32_ozaki<4, 4>;
+    default: return gram_f32_ozaki<8, 3>;
+  }
+}
+
+int gram_ozaki32_max_pairs() {
+  const Oz32Cfg& cfg = oz32_cfg();
+  auto kern = oz32_kernel(cfg);
+  const size_t smem = ozaki32_smem(cfg.astages, cfg.dstages);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(2);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, kern, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nc;
+}
+
 size_t gram_ozaki32_partial_bytes(int npairs) { return (size_t)2 * npairs * kCB * kCB * sizeof(double2); }
 
 cudaError_t launch_gram_ozaki32_begin(int* bad_cols, cudaStream_t st) {
@@ -648,16 +864,29 @@ cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const size_t smem = ozaki32_smem();
-  cudaError_t e = cudaFuncSetAttribute(gram_f32_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const Oz32Cfg& cfg = oz32_cfg();
+  auto kern = oz32_kernel(cfg);
+  const size_t smem = ozaki32_smem(cfg.astages, cfg.dstages);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // test hook: chunks per exact span (MPSVD_OZAKI32_SPAN, at most kSpanMax)
   const char* span_env = getenv("MPSVD_OZAKI32_SPAN");
   int span_max = span_env && atoi(span_env) > 0 ? atoi(span_env) : kSpanMax;
   if (span_max > kSpanMax) span_max = kSpanMax;
-  gram_f32_ozaki<<<2 * npairs, kThreads, smem, st>>>(map, n, c_begin, c_end, npairs, partials, bad_cols,
-                                                       accumulate ? 1 : 0, span_max);
-  return cudaGetLastError();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(2 * npairs);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;  // CTA pair = cluster of 2 (distributed shared memory)
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kern, map, n, c_begin, c_end, npairs, partials, bad_cols, accumulate ? 1 : 0,
+                            span_max, cfg.wmode);
 }
 
 cudaError_t launch_gram_ozaki32_combine(const double2* partials, int npairs, int n, const int* bad_cols,

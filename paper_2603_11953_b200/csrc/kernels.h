@@ -48,6 +48,7 @@ cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n
 // combine() writes M (both triangles).
 bool gram_ozaki32_supported(const float* a, long long lda, long long m, int n);
 size_t gram_ozaki32_partial_bytes(int npairs);
+int gram_ozaki32_max_pairs();
 cudaError_t launch_gram_ozaki32_begin(int* bad_cols, cudaStream_t st);
 cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m, int n, long long c_begin,
                                       long long c_end, int npairs, double2* partials, int* bad_cols, bool accumulate,
