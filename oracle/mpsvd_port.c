@@ -1752,8 +1752,7 @@ static void* o32_worker(void* arg) {
           const int64_t e = i * 128 + j;
           dd t0 = o32_group_total(g, (int32_t)(uint32_t)acc[e], (int32_t)(uint32_t)acc[16384 + e],
                                   (int32_t)(uint32_t)acc[2 * 16384 + e], (int32_t)(uint32_t)acc[3 * 16384 + e]);
-          /* D8 diagonal of this CTA's 16-row halves, in its group's frame */
-          if (i == j) t0 = dd_add(t0, (dd){(double)s8[i] * (g ? 0x1p-16 : 0x1p-9), 0.0});
+          if (g == 1 && i == j) t0 = dd_add(t0, (dd){(double)s8[i] * 0x1p-16, 0.0}); /* D8 diagonal */
           const int sc = E[i] + E[j] - 92 + base;
           dd t = {scalbn(t0.hi, sc), scalbn(t0.lo, sc)};
           dd* o = &J->P[j * 128 + i];
@@ -1777,7 +1776,7 @@ static void* o32_worker(void* arg) {
         const uint64_t y = o32_fixed48(b[r][c], E[c]);
         for (int p = 1; p <= 6; ++p) D[((p - 1) * 32 + r) * 128 + c] = (int8_t)(((y >> (8 * (6 - p))) & 0xFFu) ^ 0x80u);
         const int d4 = D[(3 * 32 + r) * 128 + c];
-        if ((r >> 4) == g) s8[c] += d4 * d4; /* each CTA of the pair converts (and sums) rows 16 g .. 16 g + 15 */
+        s8[c] += d4 * d4;
       }
     for (int k = 0; k < 6; ++k) {
       int p, q, ai;

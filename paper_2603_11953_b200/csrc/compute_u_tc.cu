@@ -465,6 +465,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
   const long long ntiles = (m + kBM - 1) / kBM;
   const int my_tiles = (int)(ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int nchunks = my_tiles * nkc;
+  const uint32_t zmask = (uint32_t)tcols >> 16;  // 0 (tcols <= 512), unknown to the compiler
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nstage; ++i) {
@@ -578,16 +579,30 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
       float v[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) v[c] = src[c * kBM + row];  // consecutive lanes: consecutive rows
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&stage_empty[slot]);
+      uint32_t hp[8], mp[8], lp[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) split3(v[2 * c], v[2 * c + 1], hp[c], mp[c], lp[c]);
+      // release the staging slot only once every lane's loads have returned:
+      // an arrive right after the loads (lane 0, after __syncwarp) can
+      // overtake loads still in flight, and the loaders then overwrite the
+      // slot under them (measured on K1z's identical ring, gram_ozaki32.cu
+      // release_a). The arrive count depends on a warp OR-reduction of a
+      // runtime zero derived from all 16 values (via the last pieces).
+      {
+        const uint32_t dep = (lp[0] | lp[1] | lp[2] | lp[3]) | (lp[4] | lp[5] | lp[6] | lp[7]);
+        const uint32_t z = __reduce_or_sync(0xffffffffu, dep & zmask);
+        if (lane == 0)
+          asm volatile(
+              "{\n.reg .b32 cnt;\nadd.u32 cnt, %1, 1;\n"
+              "mbarrier.arrive.shared::cta.b64 _, [%0], cnt;\n}\n" ::"r"(saddr(&stage_empty[slot])),
+              "r"(z)
+              : "memory");
+      }
       slot += kGroups;
       if (slot >= nstage) {
         slot -= nstage;
         sph ^= 1;
       }
-      uint32_t hp[8], mp[8], lp[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) split3(v[2 * c], v[2 * c + 1], hp[c], mp[c], lp[c]);
       mbar_wait(&a_empty[sl], (unsigned)(((g / kASlots) & 1) ^ 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_col0 + sl * kACols);

@@ -15,19 +15,32 @@
 // (oracle/mpsvd_port.c port_gram_f32_ozaki) and to the reference criterion.
 //
 // Work split. The rows are cut into 32-row chunks (the kind::i8 UMMA K).
-// A launch covers a chunk range; CTA pair p takes an equal share of it and
-// both CTAs of the pair stream the same chunks (the second read is an L2
+// A launch covers a chunk range; CTA pair p (a cluster of 2) takes an equal
+// share of it and both CTAs stream the same chunks (the second read is an L2
 // hit): CTA g of the pair owns accumulator group g (below). Per CTA:
-//   warp 0      TMA: 32 x 128 fp32 boxes (16 KB, 128B swizzle) into a ring
-//   warp 1      MMA issue (one thread) + TMEM allocation (4 x 128 columns)
-//   warps 2-5   drain (TMEM lane quarter = tile rows): span totals -> dd
-//   warps 14-17 scouts: lane = column; each chunk's column maxima -> the
-//               span decision (one 128-thread barrier-with-reduction) and the
-//               span's exponents, published per chunk by an mbarrier, so the
-//               converters never synchronise with each other
-//   warps 6-13  convert: thread = (column, 16-row half): the 6 signed digits
-//               of every entry, written as UMMA operand planes (K-major, no
-//               swizzle) into a digit ring.
+//   warp 0       TMA: 32 x 128 fp32 boxes (16 KB, 128B swizzle) into a ring
+//   warp 1       MMA issue (one thread) + TMEM allocation (4 x 128 columns);
+//                in group 1 the warp also sums the D8 diagonal (below)
+//   warps 2-5    drain (TMEM lane quarter = tile rows): span totals -> dd
+//   warps 6-21   convert, two groups of 8 warps taking alternate chunks;
+//                thread = (column, 8 rows of this CTA's 16-row half): the
+//                6 signed digits of every entry as UMMA operand planes
+//                (K-major, no swizzle) in this CTA's half of a digit slot
+//   warps 22-25  scouts: lane = column; each chunk's column maxima -> the
+//                span decision (one 128-thread barrier-with-reduction) and
+//                the span's exponents, published per chunk by an mbarrier
+//   warp 26      copier: one DSMEM bulk copy moves this CTA's half of each
+//                digit slot into the peer's slot (transaction bytes on the
+//                peer's slot barrier), so the pair converts each chunk once
+// A slot is released by the warps that read it only once every lane's loads
+// have returned (release_a: a plain lane-0 arrive after __syncwarp let the
+// TMA refill a slot under loads still in flight, tools/oz32_harness.cu).
+// Per role one warp polls an mbarrier and the role's other warps wait on a
+// named barrier. Measured (c4, ncu + harness stamps): ~1,300 cycles per
+// chunk; the SM's shared-memory bandwidth bounds it - the 6 MMAs read 48 KB
+// of operands per chunk (int8 M128 N128 K32 alone would need 128 B/clk),
+// plus 16 KB TMA, 16 KB scout and 8 KB converter reads, 12 KB digit writes
+// and 24 KB of DSMEM copies.
 //
 // Digits. A span is a run of chunks with fixed column exponents E_c. A span
 // starts at the first chunk of the CTA's range, after kSpanMax chunks (the
@@ -81,12 +94,14 @@ constexpr int kSpanMax = 1024;                // chunks per span: int32 sums sta
 constexpr int kZeroE = -160;                  // exponent of an all-zero column
 constexpr int kAStageBytes = kKC * kCB * 4;   // 16384
 constexpr int kDStageBytes = kDigits * kPlane;
-constexpr int kThreads = 608;
-constexpr int kWarpCopy = 18;                 // DSMEM bulk copies of this CTA's digit half to the peer
-constexpr int kHalfBytes = kDigits * 2048;    // one CTA's 16-row half of a digit slot: 6 planes x 2 KB
-constexpr int kConvThreads = 256;
+constexpr int kConvGroups = 2;                // converter groups: group G converts the chunks j = G mod 2
+constexpr int kConvThreads = 256 * kConvGroups;
 constexpr int kConvWarp0 = 6;
-constexpr int kScoutWarp0 = 14, kScoutWarps = 4;
+constexpr int kScoutWarp0 = kConvWarp0 + kConvThreads / 32, kScoutWarps = 4;
+constexpr int kWarpCopy = kScoutWarp0 + kScoutWarps;  // DSMEM bulk copies of this CTA's digit half to the peer
+constexpr int kThreads = 32 * (kWarpCopy + 1);
+constexpr int kGroupWarps = 8;                // converter warps per group (one chunk half: 128 columns x 2)
+constexpr int kHalfBytes = kDigits * 2048;    // one CTA's 16-row half of a digit slot: 6 planes x 2 KB
 constexpr unsigned long long kC48 = 0x808080808080ull;
 
 // products of group g, in issue order: (p, q, accumulator)
@@ -236,8 +251,24 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void st_v2(uint32_t addr, uint32_t a, uint32_t b) {
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
+// named barrier (hardware wait, no issue slots): one warp of a role polls the
+// mbarrier, the role's other warps block here until it has seen the phase
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// MMA completion -> the mbarrier at this offset in both CTAs of the pair,
+// issued only after `dep` (a runtime zero derived from loads that must have
+// returned first) is available
+__device__ __forceinline__ void commit_lead_pair_dep(uint64_t* bar, uint32_t lead, uint32_t dep) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %1, 0;\n"
+      "@l tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %2;\n}\n" ::
+          "r"(saddr(bar) + dep),
+      "r"(lead), "h"((unsigned short)3)
+      : "memory");
 }
 // MMA completion -> the mbarrier at this offset in both CTAs of the pair
 __device__ __forceinline__ void commit_lead_pair(uint64_t* bar, uint32_t lead) {
@@ -352,15 +383,26 @@ __device__ __forceinline__ dd group_total(int g, int a0, int a1, int a2, int a3)
 
 using namespace oz32;
 
-// Debug hook (tools/oz32_harness.cu only; null in the library): per global
-// chunk, the digits the converters wrote ([chunk][digit][column][32 rows]
-// int8), the exponent each column used and the MMA's span-start flag.
+// Debug hook, compiled only with -DOZ32_DEBUG (tools/oz32_harness.cu): per
+// global chunk, the digits the converters wrote ([chunk][digit][column][32
+// rows] int8), the exponent each column used, the MMA's span-start flag and
+// per-stage clock64 stamps of pair 0.
+#ifdef OZ32_DEBUG
 struct Oz32Dbg {
   int8_t* digits;
   short* E;
   int* fresh;
+  unsigned long long* prof;  // [cta 0/1 of pair 0][chunk][12] clock64 stamps
+  int prof_chunks;
 };
-__device__ Oz32Dbg g_oz32_dbg = {nullptr, nullptr, nullptr};
+__device__ Oz32Dbg g_oz32_dbg = {nullptr, nullptr, nullptr, nullptr, 0};
+__device__ __forceinline__ void oz32_stamp(const Oz32Dbg& d, int g, int pair, int j, int ev) {
+  if (d.prof && pair == 0 && j < d.prof_chunks) d.prof[((size_t)g * d.prof_chunks + j) * 12 + ev] = clock64();
+}
+#define OZ32_DBG(...) __VA_ARGS__
+#else
+#define OZ32_DBG(...)
+#endif
 
 // ---------------------------------------------------------------------------
 template <int kAStages, int kDStages>
@@ -391,11 +433,12 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   int* desc = span_last + 4;                             // [2][128] span exponents
   int* meta = desc + 2 * kCB;                            // [kAStages][2]: fresh, span
   int* sbad = meta + 2 * kAStages;                       // [128]
-  int* dsq = sbad + kCB;                                 // [2][2][128] D8 diagonal sums of this CTA's rows per span
+  int* dsq = sbad + kCB;                                 // [2][128] D8 diagonal sums per span (group 1's MMA warp)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x >> 1, g = blockIdx.x & 1;
   const uint32_t zmask = (uint32_t)wmode >> 8;  // 0 (wmode < 256), unknown to the compiler
+  OZ32_DBG(const Oz32Dbg dbg = g_oz32_dbg;)
   const long long nch_all = c_end - c_begin;
   const long long c0 = c_begin + nch_all * pair / npairs, c1 = c_begin + nch_all * (pair + 1) / npairs;
   const int nch = (int)(c1 - c0);
@@ -403,13 +446,13 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   if (threadIdx.x == 0) {
     for (int i = 0; i < kAStages; ++i) {
       mbar_init(&a_full[i], 1);
-      mbar_init(&a_empty[i], kConvThreads / 32 + kScoutWarps);  // converter warps + the scouts
+      mbar_init(&a_empty[i], kGroupWarps + kScoutWarps);  // the chunk's converter group + the scouts
       mbar_init(&meta_full[i], kScoutWarps);
     }
     for (int i = 0; i < kDStages; ++i) {
-      mbar_init(&d_full[i], kConvThreads / 32);  // own converter warps (+ the peer's half: transaction bytes)
-      mbar_init(&d_empty[i], 2);                 // the MMAs of both CTAs have read the slot
-      mbar_init(&half_full[i], kConvThreads / 32);
+      mbar_init(&d_full[i], kGroupWarps);  // own converter warps (+ the peer's half: transaction bytes)
+      mbar_init(&d_empty[i], 2);           // the MMAs of both CTAs have read the slot
+      mbar_init(&half_full[i], kGroupWarps);
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 4);
@@ -437,6 +480,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       for (int j = 0; j < nch; ++j) {
         const int s = j % kAStages;
         mbar_wait_m(&a_empty[s], ((unsigned)(j / kAStages) & 1u) ^ 1u, wmode, 64);
+        OZ32_DBG(oz32_stamp(dbg, g, pair, j, 0);)
         mbar_expect_tx(&a_full[s], kAStageBytes);
         tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + j) * kKC), 0, &a_full[s]);
       }
@@ -450,12 +494,24 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kCB >> 3) << 17) |
                            ((uint32_t)(128 >> 4) << 24);  // D s32, A/B s8 K-major, N = M = 128
     const uint64_t dbase = kdesc(saddr(dstage));           // + (byte offset >> 4) per operand
+    // D8 diagonal (group 1): sum over the chunk's 32 rows of d_4^2 per
+    // column, from digit plane 4 of both halves of the slot; lane l owns
+    // columns l + 32 k (each 8-lane group reads 128 contiguous bytes)
+    int s8[4] = {0, 0, 0, 0};
     int span = -1;
     for (int j = 0; j < nch; ++j) {
       const int s = j % kDStages;
       mbar_wait_cl(&d_full[s], (unsigned)(j / kDStages) & 1u);
       const bool fresh = d_meta[s] != 0;
-      if (g_oz32_dbg.fresh && lead) g_oz32_dbg.fresh[(c0 + j) * 2 + g] = fresh ? 1 : 0;
+      if (fresh && g == 1) {
+        if (span >= 0)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dsq[(span & 1) * kCB + lane + 32 * k] = s8[k];  // the closing span's D8
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s8[k] = 0;
+      }
+      OZ32_DBG(if (lead) oz32_stamp(dbg, g, pair, j, 5);)
+      OZ32_DBG(if (dbg.fresh && lead) dbg.fresh[(c0 + j) * 2 + g] = fresh ? 1 : 0;)
       if (fresh) {
         if (span >= 0) {  // close the previous span: the drain may read it
           if (lead) span_last[span & 1] = 0;
@@ -468,12 +524,32 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       }
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint64_t sd = dbase + (uint64_t)((uint32_t)s * (kDStageBytes >> 4));
-      if (g == 0)
+      uint32_t dep = 0;
+      if (g == 0) {
         issue_chunk<0>(tmem, sd, idesc, fresh, lead);
-      else
+      } else {
         issue_chunk<1>(tmem, sd, idesc, fresh, lead);
-      commit_lead_pair(&d_empty[s], lead);  // the slot is free (in both CTAs) once these MMAs have read it
+        const unsigned char* p4 = dstage + (size_t)s * kDStageBytes + 3 * 2048 + (lane >> 3) * 128 + (lane & 7) * 16;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint4 w = *reinterpret_cast<const uint4*>(p4 + h * kHalfBytes + k * 512);
+            s8[k] = __dp4a((int)w.x, (int)w.x, s8[k]);
+            s8[k] = __dp4a((int)w.y, (int)w.y, s8[k]);
+            s8[k] = __dp4a((int)w.z, (int)w.z, s8[k]);
+            s8[k] = __dp4a((int)w.w, (int)w.w, s8[k]);
+          }
+        // the slot may be refilled once the commit below lands: every lane's
+        // loads must have returned first (see release_a)
+        dep = __reduce_or_sync(0xffffffffu, (uint32_t)(s8[0] | s8[1] | s8[2] | s8[3]) & zmask);
+      }
+      commit_lead_pair_dep(&d_empty[s], lead, dep);  // the slot is free (in both CTAs) once these MMAs have read it
+      OZ32_DBG(if (lead) oz32_stamp(dbg, g, pair, j, 6);)
     }
+    if (g == 1 && span >= 0)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dsq[(span & 1) * kCB + lane + 32 * k] = s8[k];  // the last span's D8
     if (lead) span_last[span >= 0 ? (span & 1) : 0] = span >= 0 ? 1 : 2;  // 2: no chunk, nothing to drain
     __syncwarp();
     arrive_lead(info_full, lead);
@@ -492,6 +568,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       for (int j = 0; j < nch; ++j) {
         const int s = j % kDStages;
         mbar_wait_m(&half_full[s], (unsigned)(j / kDStages) & 1u, wmode, 0);
+        OZ32_DBG(oz32_stamp(dbg, g, pair, j, 4);)
         bulk_s2peer(dst0 + (uint32_t)(s * kDStageBytes), src0 + (uint32_t)(s * kDStageBytes), bytes,
                     bar0 + (uint32_t)(s * 8));
       }
@@ -506,7 +583,8 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     int span = -1, len = 0;
     for (int j = 0; j < nch; ++j) {
       const int sa = j % kAStages;
-      mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 64);
+      if (warp == kScoutWarp0) mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
+      nbar_sync(7, 128);
       const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
       // max of |x| as bit patterns over all entries: inf / NaN (exponent 255)
       // lie above every finite value, so they force a new span and a huge
@@ -546,6 +624,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&meta_full[sa]);
+      OZ32_DBG(if (threadIdx.x == kScoutWarp0 * 32) oz32_stamp(dbg, g, pair, j, 1);)
     }
   } else if (warp < kConvWarp0) {
     // ---- drain: a warp may only touch TMEM lanes 32 (warp % 4) .. + 31, so
@@ -555,7 +634,8 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     if (lane == 0) mbar_arrive(acc_empty);  // the accumulators start free
     double2* P = partials + (size_t)blockIdx.x * kCB * kCB;
     for (int span = 0;; ++span) {
-      mbar_wait_m(info_full, (unsigned)span & 1u, wmode, 2048);
+      if (warp == 2) mbar_wait_m(info_full, (unsigned)span & 1u, wmode, 0);
+      nbar_sync(6, 128);
       const int last = span_last[span & 1];
       if (last == 2) {  // empty range: the partial is zero
         if (!accumulate && i < n)
@@ -567,33 +647,32 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const int* E = desc + (span & 1) * kCB;
       const int ei = E[i];
       const int basee = g ? 47 : 40;
-      for (int j0 = 0; j0 < kCB; j0 += 8) {
-        uint32_t v[4][8];
+      // 4 columns per step (4 x 4 TMEM words, 4 running partials in flight):
+      // the kernel runs 27 warps, so the drain must fit in ~72 registers
+      for (int j0 = 0; j0 < kCB; j0 += 4) {
+        uint32_t v[4][4];
         const uint32_t taddr = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)j0;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                       : "=r"(v[k][0]), "=r"(v[k][1]), "=r"(v[k][2]), "=r"(v[k][3]), "=r"(v[k][4]), "=r"(v[k][5]),
-                         "=r"(v[k][6]), "=r"(v[k][7])
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                       : "=r"(v[k][0]), "=r"(v[k][1]), "=r"(v[k][2]), "=r"(v[k][3])
                        : "r"(taddr + (uint32_t)(k * kCB)));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         if (i < n) {
-          // the 8 running partials are loaded together (one memory latency
-          // per group of columns, not per entry)
+          // the running partials of the step are loaded together (one
+          // memory latency per group of columns, not per entry)
           const bool rmw = accumulate || span > 0;
-          double2 old[8];
+          double2 old[4];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
+          for (int jj = 0; jj < 4; ++jj)
             old[jj] = (rmw && j0 + jj < n) ? P[(size_t)(j0 + jj) * kCB + i] : make_double2(0.0, 0.0);
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
+          for (int jj = 0; jj < 4; ++jj) {
             const int jc = j0 + jj;
             if (jc >= n) continue;
             dd t0 = group_total(g, (int)v[0][jj], (int)v[1][jj], (int)v[2][jj], (int)v[3][jj]);
-            if (jc == i)  // D8 diagonal of this CTA's rows: sum d_4^2 at 2^-16 (group 1) / 2^-9 (group 0), halved
-              t0 = dd_add(t0, dd_make((double)(dsq[(span & 1) * 2 * kCB + i] + dsq[(span & 1) * 2 * kCB + kCB + i]) *
-                                          (g ? 0x1p-16 : 0x1p-9),
-                                      0.0));
+            if (g == 1 && jc == i)  // D8 diagonal: sum d_4^2 at 2^-16 of this frame (halved)
+              t0 = dd_add(t0, dd_make((double)dsq[(span & 1) * kCB + i] * 0x1p-16, 0.0));
             const int sc = ei + E[jc] - 92 + basee;
             dd t = dd_make(scalbn(t0.hi, sc), scalbn(t0.lo, sc));
             if (rmw) t = dd_add(dd_make(old[jj].x, old[jj].y), t);
@@ -617,19 +696,30 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     // chunk once. A slot is full when this CTA's converter warps have
     // arrived and the peer's half has landed (transaction bytes), and free
     // when both CTAs' MMAs have read it (multicast commit).
-    const int t = threadIdx.x - kConvWarp0 * 32;
+    // Two groups of 8 warps alternate chunks (group G takes j = G mod 2), so
+    // the per-chunk hand-off latencies of one group overlap the other's work.
+    const int grp = (threadIdx.x - kConvWarp0 * 32) >> 8;
+    const int t = (threadIdx.x - kConvWarp0 * 32) & 255;
     const int q = t & 1, c = t >> 1;  // lanes 2k, 2k + 1 store adjacent 8-byte pieces (no bank conflicts)
+    const int gw = t >> 5;            // warp within the group
     const uint32_t dloc = saddr(dstage) + (uint32_t)(g * kHalfBytes + (c >> 3) * 128 + (c & 7) * 16 + q * 8);
     const unsigned in_bytes = g == 0 ? 6u * 2048u : 5u * 2048u;  // the peer's half (group 1 gets digits 1-5)
-    const int dsq_idx = q * kCB + c;
     int E = kZeroE;
     int span = -1;
     int badc = 0;
-    int s8 = 0;  // sum of d_4^2 over this thread's rows of the open span
-    for (int j = 0; j < nch; ++j) {
+    for (int j = grp; j < nch; j += kConvGroups) {
       const int sa = j % kAStages;
-      mbar_wait_m(&meta_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
-      mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);  // already complete: the TMA data's visibility
+      OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 8);)  // iteration start
+      // one warp of the group polls; the group's other warps block on a
+      // named barrier (polling by all 16 converter warps took most of the
+      // SM's issue slots, ncu)
+      if (gw == 0) {
+        mbar_wait_m(&meta_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
+        mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
+      }
+      OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 9);)
+      nbar_sync(2 + 2 * grp, 256);
+      OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 10);)
       const int mflags = meta[2 * sa];
       const bool fresh = (mflags & 1) != 0;
       const int mspan = meta[2 * sa + 1];
@@ -645,6 +735,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         b[4 * u + 3] = w.w;
       }
       release_a(&a_empty[sa], lane, b[0] | b[4] | (uint32_t)mflags, zmask);
+      OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 11);)
       if (mflags & 2) {  // inf / NaN in this chunk (the scouts saw it): flag the column, use zeros
 #pragma unroll
         for (int r = 0; r < 8; ++r)
@@ -653,14 +744,15 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
             badc = 1;
           }
       }
-      if (fresh) {
-        if (span >= 0) dsq[(span & 1) * 2 * kCB + dsq_idx] = s8;  // the closing span's D8 diagonal
-        s8 = 0;
+      if (mspan != span) {  // this group's first chunk of a span (it may have skipped a short one)
         span = mspan;
         E = desc[(span & 1) * kCB + c];
       }
       const int sd = j % kDStages;
-      mbar_wait_m(&d_empty[sd], ((unsigned)(j / kDStages) & 1u) ^ 1u, wmode, 32);
+      OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 7);)  // A data in registers
+      if (gw == 0) mbar_wait_m(&d_empty[sd], ((unsigned)(j / kDStages) & 1u) ^ 1u, wmode, 0);
+      nbar_sync(3 + 2 * grp, 256);
+      OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 2);)
       if (t == 0) d_meta[sd] = fresh ? 1 : 0;
       uint32_t ylo[8], yhi[8];
       if (__all_sync(0xffffffffu, E >= -78 || E == kZeroE)) {
@@ -693,23 +785,22 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         o[2][w] = __byte_perm(b01, b23, 0x7632) ^ 0x80808080u;  // byte 3: digit 3
         o[1][w] = __byte_perm(c01, c23, 0x5410) ^ 0x80808080u;  // byte 4: digit 2
         o[0][w] = __byte_perm(c01, c23, 0x7632) ^ 0x80808080u;  // byte 5: digit 1
-        s8 = __dp4a((int)o[3][w], (int)o[3][w], s8);
       }
       const uint32_t so = dloc + (uint32_t)(sd * kDStageBytes);
 #pragma unroll
       for (int p = 1; p <= kDigits; ++p) st_v2(so + (uint32_t)((p - 1) * 2048), o[p - 1][0], o[p - 1][1]);
-      if (g_oz32_dbg.digits) {
+      OZ32_DBG(if (dbg.digits) {
         const long long gc = c0 + j;
         for (int p = 1; p <= kDigits; ++p)
-          *reinterpret_cast<uint2*>(g_oz32_dbg.digits + ((gc * kDigits + p - 1) * kCB + c) * 32 + 16 * g + 8 * q) =
+          *reinterpret_cast<uint2*>(dbg.digits + ((gc * kDigits + p - 1) * kCB + c) * 32 + 16 * g + 8 * q) =
               make_uint2(o[p - 1][0], o[p - 1][1]);
-        if (g == 0 && q == 0) g_oz32_dbg.E[gc * kCB + c] = (short)E;
-      }
-      if (j == nch - 1) dsq[(span & 1) * 2 * kCB + dsq_idx] = s8;  // the last span's D8 diagonal
+        if (g == 0 && q == 0) dbg.E[gc * kCB + c] = (short)E;
+      })
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core / bulk copy
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&half_full[sd]);
+        OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 3);)
         if (t == 0)
           mbar_expect_tx(&d_full[sd], in_bytes);  // one of the arrivals also expects the peer's half
         else
@@ -718,8 +809,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     }
     // the peer's MMAs arrive (multicast) on this CTA's slot barriers: wait
     // for the last arrivals before this CTA may exit
-    for (int jj = nch; jj < nch + kDStages; ++jj)
-      if (jj >= kDStages) mbar_wait_m(&d_empty[jj % kDStages], ((unsigned)(jj / kDStages) & 1u) ^ 1u, wmode, 32);
+    if (grp == 0)
+      for (int jj = nch; jj < nch + kDStages; ++jj)
+        if (jj >= kDStages) mbar_wait_m(&d_empty[jj % kDStages], ((unsigned)(jj / kDStages) & 1u) ^ 1u, wmode, 32);
     if (badc) atomicOr(&sbad[c], 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -762,7 +854,7 @@ static size_t ozaki32_smem(int astages, int dstages) {
 // wait mode (MPSVD_OZ32_WAIT: 0 hinted try_wait, 1 plain try_wait, 2
 // back-off), read once
 struct Oz32Cfg {
-  int astages = 8, dstages = 3;  // A x digit slots
+  int astages = 7, dstages = 4;  // A x digit slots (8x3, 7x4, 4x6 measured within 3% on c4)
   int wmode = 2;
 };
 static const Oz32Cfg& oz32_cfg() {
@@ -770,7 +862,7 @@ static const Oz32Cfg& oz32_cfg() {
   static std::once_flag once;
   std::call_once(once, [] {
     const char* st = getenv("MPSVD_OZ32_STAGES");
-    if (st && st[0] >= '4' && st[0] <= '8' && st[1] == 'x' && st[2] >= '2' && st[2] <= '4') {
+    if (st && st[0] >= '4' && st[0] <= '8' && st[1] == 'x' && st[2] >= '2' && st[2] <= '9') {
       c.astages = st[0] - '0';
       c.dstages = st[2] - '0';
     }
@@ -807,13 +899,13 @@ static Oz32Kern oz32_kernel(const Oz32Cfg& c) {
   const int k = c.astages * 10 + c.dstages;
   switch (k) {
     case 73: return gram_f32_ozaki<7, 3>;
-    case 74: return gram_f32_ozaki<7, 4>;
-    case 64: return gram_f32_ozaki<6, 4>;
-    case 63: return gram_f32_ozaki<6, 3>;
-    case 43: return gram_f32_ozaki<4, 3>;
-    case 53: return gram_f32_ozaki<5, 3>;
-    case 44: return gram_f32_ozaki<4, 4>;
-    default: return gram_f32_ozaki<8, 3>;
+    case 46: return gram_f32_ozaki<4, 6>;
+    case 55: return gram_f32_ozaki<5, 5>;
+    case 45: return gram_f32_ozaki<4, 5>;
+    case 37: return gram_f32_ozaki<3, 7>;
+    case 36: return gram_f32_ozaki<3, 6>;
+    case 83: return gram_f32_ozaki<8, 3>;
+    default: return gram_f32_ozaki<7, 4>;
   }
 }
 

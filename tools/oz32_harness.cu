@@ -7,6 +7,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false --expt-relaxed-constexpr \
 //     -I include -I paper_2603_11953_b200/csrc tools/oz32_harness.cu -lcuda -o tools/oz32_harness
 //   MPSVD_OZ32_STAGES=7x4 ./tools/oz32_harness 22
+#define OZ32_DEBUG 1
 #include "../paper_2603_11953_b200/csrc/gram_ozaki32.cu"
 
 #include <cmath>
@@ -57,7 +58,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&d_part, pbytes));
   int* d_bad;
   CK(cudaMalloc(&d_bad, 128 * 4));
-  Oz32Dbg dbg;
+  Oz32Dbg dbg = {};
   CK(cudaMalloc(&dbg.digits, (size_t)nch * 6 * 128 * 32));
   CK(cudaMalloc(&dbg.E, (size_t)nch * 128 * 2));
   CK(cudaMalloc(&dbg.fresh, (size_t)nch * 2 * 4));
@@ -71,12 +72,18 @@ int main(int argc, char** argv) {
     }
     bounds.push_back(nch);
   }
+  const int pch = 400;
+  dbg.prof_chunks = pch;
+  CK(cudaMalloc(&dbg.prof, (size_t)2 * pch * 12 * 8));
+  CK(cudaMemset(dbg.prof, 0, (size_t)2 * pch * 12 * 8));
   std::vector<double2> p0(pbytes / 16), p1(pbytes / 16);
   std::vector<int8_t> dig((size_t)nch * 6 * 128 * 32);
   std::vector<short> E((size_t)nch * 128);
   std::vector<int> fr((size_t)nch * 2);
   for (int run = 0; run < 3; ++run) {
-    CK(cudaMemcpyToSymbol(g_oz32_dbg, &dbg, sizeof(dbg)));
+    Oz32Dbg d2 = dbg;
+    if (getenv("H_NODIG")) d2.digits = nullptr, d2.E = nullptr;
+    CK(cudaMemcpyToSymbol(g_oz32_dbg, &d2, sizeof(d2)));
     CK(cudaMemset(dbg.digits, 0x55, (size_t)nch * 6 * 128 * 32));
     CK(cudaMemset(d_bad, 0, 128 * 4));
     cudaEvent_t e0, e1;
@@ -106,7 +113,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(E.data(), dbg.E, E.size() * 2, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(fr.data(), dbg.fresh, fr.size() * 4, cudaMemcpyDeviceToHost));
     long long bad = 0, shown = 0;
-    for (long long ch = 0; ch < nch; ++ch)
+    for (long long ch = 0; ch < (getenv("H_NODIG") ? 0 : nch); ++ch)
       for (int c = 0; c < n; ++c) {
         const int e = E[ch * 128 + c];
         for (int r = 0; r < 32; ++r) {
@@ -147,6 +154,31 @@ int main(int argc, char** argv) {
           }
         }
       }
+    if (run == 0) {
+      // pipeline timing of pair 0 over its first range (SM clock cycles): per event the mean gap to the
+      // previous event of the same chunk, and the mean chunk period of each event stream
+      std::vector<unsigned long long> pr((size_t)2 * pch * 12);
+      CK(cudaMemcpy(pr.data(), dbg.prof, pr.size() * 8, cudaMemcpyDeviceToHost));
+      const char* names[12] = {"tma issue", "scouts done", "conv: slot free", "conv: half done", "copier issue",
+                               "mma: slot full", "mma: committed", "conv: A in regs", "conv: iter start",
+                               "conv: meta ok", "conv: a_full ok", "conv: released"};
+      const long long nj = std::min<long long>(pch, bounds[1] / npairs);
+      for (int gg = 0; gg < 2; ++gg) {
+        printf("  CTA %d of pair 0, chunks 20..%lld:\n", gg, nj - 1);
+        for (int ev = 0; ev < 12; ++ev) {
+          double per = 0, lag = 0;
+          long long cnt = 0;
+          for (long long j = 21; j < nj; ++j) {
+            const unsigned long long* r = &pr[((size_t)gg * pch + j) * 12];
+            const unsigned long long* r0 = &pr[((size_t)gg * pch + j - 1) * 12];
+            per += (double)(r[ev] - r0[ev]);
+            lag += (double)r[ev] - (double)r[0];
+            ++cnt;
+          }
+          printf("    %-16s period %8.1f cyc   after tma issue %9.1f cyc\n", names[ev], per / cnt, lag / cnt);
+        }
+      }
+    }
     long long fmis = 0;
     for (long long ch = 0; ch < nch; ++ch)
       if (fr[2 * ch] != fr[2 * ch + 1]) ++fmis;
