@@ -415,6 +415,10 @@ av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np
 
 
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void nbar_sync_k7(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
 // K7, TMEM variant: the bf16 pieces of A are written to tensor memory with
 // tcgen05.st (thread = row) and fed to the MMA as its A operand (K-major in
 // TMEM, two K-neighbours per 32-bit column, low half = even k; encoding
@@ -465,7 +469,9 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
   const long long ntiles = (m + kBM - 1) / kBM;
   const int my_tiles = (int)(ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int nchunks = my_tiles * nkc;
-  const uint32_t zmask = (uint32_t)tcols >> 16;  // 0 (tcols <= 512), unknown to the compiler
+  const int kdbg = tcols >> 16;  // experiment switches (MPSVD_AV_DBG bits 4-6): 1 no MMA, 2 no U stores, 4 no split
+  tcols &= 0xFFFF;
+  const uint32_t zmask = (uint32_t)kdbg >> 8;  // 0 (kdbg < 256), unknown to the compiler
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nstage; ++i) {
@@ -550,6 +556,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
           const uint32_t at = tmem + (uint32_t)(a_col0 + sl * kACols);
 #pragma unroll
           for (int q = 0; q < 6; ++q) {
+            if (kdbg & 1) break;
             const uint64_t bd = umma_desc(wbase + (uint32_t)pw[q] * wplane + (uint32_t)kc * 2u * w_lbo, w_lbo, 128);
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -572,16 +579,25 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     const int row = q * 32 + lane;
     int slot = grp % nstage;
     unsigned sph = (unsigned)((grp / nstage) & 1);
+    // one warp of the group polls each mbarrier, the other three wait on the
+    // group's named barrier (all 16 converter warps polling took ~40% of the
+    // SM's issue slots, ncu c4)
     for (int g = grp; g < nchunks; g += kGroups) {
       const int sl = g % kASlots;
-      mbar_wait(&stage_full[slot], sph);
+      if (q == 0) mbar_wait(&stage_full[slot], sph);
+      nbar_sync_k7(1 + grp, 128);
       const float* src = reinterpret_cast<const float*>(ssm + slot * kStageBytes);
       float v[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) v[c] = src[c * kBM + row];  // consecutive lanes: consecutive rows
       uint32_t hp[8], mp[8], lp[8];
+      if (kdbg & 4) {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) split3(v[2 * c], v[2 * c + 1], hp[c], mp[c], lp[c]);
+        for (int c = 0; c < 8; ++c) hp[c] = mp[c] = lp[c] = __float_as_uint(v[2 * c]) ^ __float_as_uint(v[2 * c + 1]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) split3(v[2 * c], v[2 * c + 1], hp[c], mp[c], lp[c]);
+      }
       // release the staging slot only once every lane's loads have returned:
       // an arrive right after the loads (lane 0, after __syncwarp) can
       // overtake loads still in flight, and the loaders then overwrite the
@@ -603,7 +619,8 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
         slot -= nstage;
         sph ^= 1;
       }
-      mbar_wait(&a_empty[sl], (unsigned)(((g / kASlots) & 1) ^ 1));
+      if (q == 0) mbar_wait(&a_empty[sl], (unsigned)(((g / kASlots) & 1) ^ 1));
+      nbar_sync_k7(1 + grp, 128);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a_col0 + sl * kACols);
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta), "r"(hp[0]),
@@ -622,7 +639,8 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     int ab = 0;
     unsigned aph = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      mbar_wait(&acc_full[ab], aph);
+      if (warp == tm::kEpi0) mbar_wait(&acc_full[ab], aph);  // one poller, the epilogue waits on barrier 5
+      nbar_sync_k7(1 + kGroups, 32 * kEpiWarps);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const long long row = tile * kBM + q * 32 + lane;
       const bool row_ok = row < m;
@@ -637,7 +655,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
               "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (row_ok) {
+        if (row_ok && !(kdbg & 2)) {
           float* p = base + (long long)c0 * ldu;
           if (c0 + 16 <= n) {
 #pragma unroll
@@ -717,7 +735,8 @@ cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, 
     const int need = a_col0 + tm::kASlots * tm::kACols;
     const int tcols = need <= 128 ? 128 : need <= 256 ? 256 : 512;
     int nstage = (int)((kSmemLimit - wbytes - 1024) / kStageBytes);
-    if (nstage > 16) nstage = 16;
+    static const int stage_cap = getenv("MPSVD_AV_STAGES") ? atoi(getenv("MPSVD_AV_STAGES")) : 16;
+    if (nstage > stage_cap) nstage = stage_cap;
     if (nstage < tm::kGroups) return cudaErrorInvalidConfiguration;
     const size_t smem = wbytes + (size_t)nstage * kStageBytes + 1024;
     cudaError_t e = cudaFuncSetAttribute(av_tc_tmem_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -725,7 +744,8 @@ cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, 
     const long long ntiles = (m + kBM - 1) / kBM;
     const int grid = (int)(ntiles < sm_count ? ntiles : sm_count);
     av_tc_tmem_f32<<<grid, tm::kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const __nv_bfloat16*>(wplanes),
-                                                 u, ldu, status, nstage, acc_stride, a_col0, tcols);
+                                                 u, ldu, status, nstage, acc_stride, a_col0,
+                                                 tcols | (((g_av_dbg >> 4) & 7) << 16));
     return cudaGetLastError();
   }
   // one staging slot + one plane slot per active converter warp
