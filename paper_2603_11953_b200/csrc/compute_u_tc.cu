@@ -1,37 +1,41 @@
 // K7 on the 5th-generation tensor cores: U = A * W for fp32 A (m x n,
 // column-major) and n <= 128, W = V Sigma^-1 (thinsvd.cpp:110-113).
 //
-// fp32 operands are split into three bf16 pieces, x = x0 + x1 + x2 (each
-// piece the bf16 rounding of the remainder; 3 x 8 significand bits cover
-// fp32's 24), and U accumulates the six piece products whose weight is at
-// least 2^-16 of the leading one,
-//     A2W0 + A1W1 + A0W2 + A1W0 + A0W1 + A0W0,
-// in one fp32 TMEM accumulator. Every bf16 x bf16 product is exact; the
-// dropped terms (A1W2, A2W1, A2W2) are <= 2^-24 relative, the size of the
-// fp32 rounding the reference's own U accumulation commits per term
-// (dense.cpp:83-96), so U keeps working-precision accuracy.
+// A is split into two fp16 pieces and W into three, after an exact
+// power-of-two scaling: column c of A by 2^-s_c and row c of W by 2^s_c (2^s_c >= the
+// column norm sqrt(M_cc) / 2^14, so every scaled entry of A is < 2^14), and
+// column j of W by 2^-t_j (its largest scaled entry < 2^14) with U's column
+// j multiplied back by 2^t_j in the epilogue. a = a0 + a1 (a0 = fp16(a),
+// a1 = fp16(a - a0)) carries 22 significand bits, w = w0 + w1 + w2 all of
+// binary32's 24; U accumulates the four piece products A1 W0 + A0 W2 +
+// A0 W1 + A0 W0 in one fp32 TMEM accumulator. Every fp16 x fp16 product is
+// exact; the dropped A1 W1 and A1 W2 and A's representation error are
+// ~2^-22 relative per term, below the error of the reference's own fp32
+// accumulation (dense.cpp:83-96: up to n u with u = 2^-24), so U keeps
+// working-precision accuracy (tests bound it by 2 n u |A||W| elementwise),
+// and W is carried exactly, so an A whose entries fit 22 bits gives U =
+// fl(A W) like the reference (the stacked-diagonal known answer,
+// test_thinsvd.cpp: U = [I; 0] exactly). Entries below 2^-14 of the scaled
+// range become fp16 subnormals: their absolute error stays below
+// 2^-24 2^s_c, far under the bound. (The first version used three bf16
+// pieces of both operands and six products: 14.6 ms at c4 against 12.7 ms
+// with two fp16 pieces of each - which loses W's exactness.)
 //
-// Structure (one persistent CTA per SM, 19 warps, warp-specialised):
-//   warps 16-17 load  : stream fp32 A chunks (128 rows x 16 columns) with
-//                       16-byte cp.async, whole 128-byte lines per 8 lanes,
-//                       kDepth chunks ahead; completion is signalled with
-//                       cp.async.mbarrier.arrive (no thread waits on loads)
-//   warps 0-7 convert : staging fp32 -> three bf16 planes in the UMMA
-//                       MN-major no-swizzle layout (8x8 core matrices), one
-//                       generic->async proxy fence per chunk. The loads are
-//                       kept out of these warps: fence.proxy.async waits for
-//                       the issuing thread's outstanding cp.async, which
-//                       serialised converter warps that also loaded on the
-//                       full memory latency (profiles/r01_av_tc_notes.md).
-//   warp 18 MMA       : W pieces once (one bulk copy); one thread issues 6
-//                       tcgen05.mma (M=128, N=np, K=16)
-//                       per chunk into a double-buffered TMEM accumulator
-//   warps 8-15 epilogue: tcgen05.ld 32x32b -> coalesced column stores of U
-//                       (two warps per TMEM lane quarter, alternate 16-column
-//                       groups; branch-free strided stores for full groups)
+// Structure (one persistent CTA per SM, warp-specialised):
+//   warps 0-15  converters, four groups of four (one warp per TMEM lane
+//               quarter); group g converts chunks g, g + 4, ... (128 rows x
+//               16 columns: thread = row) into TMEM A slots {g, g + 4}
+//               (tcgen05.st, K-major A operand in TMEM; encoding checked by
+//               tools/microbench/umma_tmem_a.cu)
+//   warps 16-23 epilogue: tcgen05.ld 32x32b -> scaled, coalesced column
+//               stores of U (two warps per TMEM lane quarter, alternate
+//               16-column groups)
+//   warps 24-25 loaders: fp32 chunk [16 columns][128 rows] by cp.async
+//               (16 B per lane, a warp a whole 512-byte column segment)
+//   warp 26     W pieces + scales (one bulk copy) + MMA issue (one thread)
 // The encodings (descriptors, instruction descriptor, TMEM load shape) are
 // the ones checked by tools/microbench/umma_test.cu on the B200.
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -40,24 +44,19 @@
 #include "kernels.h"
 
 #ifndef TM_LOAD_WARPS
-#define TM_LOAD_WARPS 2  // loader warps of the TMEM variant (4 measured 5% slower)
+#define TM_LOAD_WARPS 2  // loader warps (4 measured 5% slower)
 #endif
 
 namespace mpsvd {
 namespace dev {
 namespace tc {
 
-constexpr int kBM = 128;                          // rows per tile = UMMA M
-constexpr int kKC = 16;                           // K per chunk = UMMA K
-constexpr int kMaxDepth = 8;                      // fp32 A chunks in flight per CTA (staging ring)
-constexpr int kStageBytes = kBM * kKC * 4;        // fp32 chunk: 8 KB
-constexpr int kPlaneBytes = kBM * kKC * 2;        // one bf16 piece of a chunk: 4096
-constexpr int kConvWarps = 8, kEpiWarps = 8;      // converters: warps 0-7; epilogue: warps 8-15
-constexpr int kLoadWarps = 2;                     // A loaders: warps 16-17
-constexpr int kWarpLoad0 = 16, kWarpMma = 18;
-constexpr int kThreads = 608;
-constexpr int kPlanes = 8;                        // max bf16 chunk slots = one per active converter warp
+constexpr int kBM = 128;                    // rows per tile = UMMA M
+constexpr int kKC = 16;                     // K per chunk = UMMA K
+constexpr int kStageBytes = kBM * kKC * 4;  // fp32 chunk: 8 KB
+constexpr int kEpiWarps = 8;
 constexpr int kSmemLimit = 227 * 1024;
+constexpr int kHead = 14;                   // scaled operands stay below 2^14 (fp16 max 65504)
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -105,27 +104,19 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint3
   d |= (uint64_t)1 << 46;  // sm100 descriptor version; base offset 0, no swizzle
   return d;
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
-}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(saddr(bar))
                : "memory");
 }
 
-// x = h + m + l, each a bf16 (rounded remainders); packs 2 values per word.
-__device__ __forceinline__ void split3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
-  const __nv_bfloat162 bh = __floats2bfloat162_rn(x0, x1);
-  const float2 fh = __bfloat1622float2(bh);
-  const float r0 = x0 - fh.x, r1 = x1 - fh.y;
-  const __nv_bfloat162 bm = __floats2bfloat162_rn(r0, r1);
-  const float2 fm = __bfloat1622float2(bm);
-  const __nv_bfloat162 bl = __floats2bfloat162_rn(r0 - fm.x, r1 - fm.y);
+
+// x = h + l, each an fp16 (the rounded remainder); packs 2 values per word
+// (low half = the even K index).
+__device__ __forceinline__ void split2h(float x0, float x1, uint32_t& h, uint32_t& l) {
+  const __half2 bh = __floats2half2_rn(x0, x1);
+  const float2 fh = __half22float2(bh);
+  const __half2 bl = __floats2half2_rn(x0 - fh.x, x1 - fh.y);
   h = *reinterpret_cast<const uint32_t*>(&bh);
-  m = *reinterpret_cast<const uint32_t*>(&bm);
   l = *reinterpret_cast<const uint32_t*>(&bl);
 }
 
@@ -136,308 +127,84 @@ __host__ __device__ __forceinline__ uint32_t mn_major_off(int mn, int k, int mn_
   return (uint32_t)((((k >> 3) * (mn_ext >> 3) + (mn >> 3)) << 7) + ((k & 7) << 4) + ((mn & 7) << 1));
 }
 
+// W pieces + scales: [3 fp16 planes np x np][np floats 2^-s_c][np floats 2^t_j]
+constexpr int kWPieces = 3;
+__host__ __device__ __forceinline__ size_t wplanes_bytes(int np) {
+  return (size_t)kWPieces * np * np * 2 + (size_t)2 * np * 4;
+}
+
 }  // namespace tc
 
-// W (n x n, fp32, row-major rows of ldw = W^T buffer of finish_columns) ->
-// three bf16 planes, each the np x np (K x N, N-major) smem image.
-__global__ void av_tc_prep_w(const float* __restrict__ w, int ldw, int n, int np, __nv_bfloat16* __restrict__ planes,
+// The Gram diagonal M_kk = ||a_k||^2, saved right after the Gram phase (the
+// Jacobi then works on M in place) behind the W pieces and scales.
+__global__ void av_tc_save_diag(const double* __restrict__ gram, int n, double* __restrict__ diag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) diag[k] = gram[(size_t)k * n + k];
+}
+
+// W (n x n, fp32, row-major rows of ldw = W^T buffer of finish_columns) and
+// the saved Gram diagonal -> the three fp16 planes of 2^s_k W_kj 2^-t_j, each
+// the np x np (K x N, N-major) smem image, and the column scales. One block
+// per column j, thread = k.
+__global__ void av_tc_prep_w(const float* __restrict__ w, int ldw, int n, int np, unsigned char* __restrict__ out,
                              const DevStatus* __restrict__ status) {
+  const double* __restrict__ diag = reinterpret_cast<const double*>(out + tc::wplanes_bytes(np));
   if (status && status->status != kOk) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= np * np) return;
-  const int k = idx / np, c = idx - k * np;
-  const float x = (k < n && c < n) ? w[(long long)k * ldw + c] : 0.0f;
-  uint32_t h, m, l;
-  tc::split3(x, 0.0f, h, m, l);
-  const uint32_t off = tc::mn_major_off(c, k, np) >> 1;  // in bf16 elements
-  const size_t plane = (size_t)np * np;
-  planes[off] = __ushort_as_bfloat16((unsigned short)(h & 0xFFFF));
-  planes[plane + off] = __ushort_as_bfloat16((unsigned short)(m & 0xFFFF));
-  planes[2 * plane + off] = __ushort_as_bfloat16((unsigned short)(l & 0xFFFF));
-}
-
-// dbg bit 2: CTA 0 accumulates per-phase cycle counts (converter warp 0,
-// MMA thread, epilogue warp 8) into g_av_prof
-__device__ unsigned long long g_av_prof[16];
-#define AVP_T0() _t0 = (prof ? clock64() : 0ull)
-#define AVP_ADD(i) do { if (prof) pacc[i] += clock64() - _t0; } while (0)
-
-__global__ void __launch_bounds__(tc::kThreads, 1)
-av_tc_f32(const float* __restrict__ a, long long lda, long long m, int n, int np,
-          const __nv_bfloat16* __restrict__ wplanes, float* __restrict__ u, long long ldu,
-          const DevStatus* __restrict__ status, int depth, int dbg) {
-  // `depth` = staging slots = bf16 plane slots = active converter warps (4 or
-  // 8): every slot belongs to one converter warp, so each mbarrier is waited
-  // on by a single consumer that is never more than one phase behind.
-  using namespace tc;
-  if (status && status->status != kOk) return;
-  extern __shared__ __align__(1024) unsigned char smem_tc[];
-  const int nkc = np / kKC;
-  const uint32_t wbytes = 3u * np * np * 2u;
-  unsigned char* wsm = smem_tc;
-  unsigned char* psm = wsm + ((wbytes + 1023) & ~1023u);
-  unsigned char* ssm = psm + depth * 3 * kPlaneBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ssm + depth * kStageBytes);
-  uint64_t* stage_full = bars;
-  uint64_t* stage_empty = stage_full + depth;
-  uint64_t* plane_full = stage_empty + depth;
-  uint64_t* plane_empty = plane_full + depth;
-  uint64_t* acc_full = plane_empty + depth;
-  uint64_t* acc_empty = acc_full + 2;
-  uint64_t* w_full = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long ntiles = (m + kBM - 1) / kBM;
-  const bool prof = (dbg & 4) && blockIdx.x == 0 && (lane == 0) && (warp == 0 || warp == kWarpMma || warp == 8);
-  const int my_tiles = (int)(ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
-  const int nchunks = my_tiles * nkc;
-  const unsigned long long t_start = prof ? clock64() : 0ull;
-  unsigned long long _t0 = 0, pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const uint32_t tcols = np * 2 <= 32 ? 32 : np * 2 <= 64 ? 64 : np * 2 <= 128 ? 128 : 256;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < depth; ++i) {
-      mbar_init(&stage_full[i], kLoadWarps * 32);  // one cp.async-completion arrive per loader thread
-      mbar_init(&stage_empty[i], 1);               // the converter warp of the chunk
+  __shared__ float red[4];
+  const int j = blockIdx.x, k = threadIdx.x;
+  int sk = 0;
+  if (k < n) {
+    const double d = diag[k];
+    if (d > 0.0 && d <= 1.7976931348623157e308) {
+      int e;
+      frexp(sqrt(d), &e);  // ||a_k|| < 2^e
+      sk = e - tc::kHead;
     }
-    for (int i = 0; i < depth; ++i) {
-      mbar_init(&plane_full[i], 1);
-      mbar_init(&plane_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], kEpiWarps);
-    }
-    mbar_init(w_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == kWarpMma) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
-                 "r"(tcols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  const float x = (k < n && j < n) ? ldexpf(w[(long long)k * ldw + j], sk) : 0.0f;
+  float mx = fabsf(x);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((k & 31) == 0) red[k >> 5] = mx;
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp >= kWarpLoad0 && warp < kWarpLoad0 + kLoadWarps) {
-    // loader thread lt fetches 16-byte pieces q = lt + 64 i (i < 8) of each
-    // chunk: column q / 32, rows 4 (q % 32) .. +3 (8 lanes read a whole
-    // 128-byte line); the piece is written where its converter lane reads
-    // it: [item][half][lane] x 16 B.
-    const int lt = threadIdx.x - kWarpLoad0 * 32;
-    int dst_off[8], col_off[8], row_off[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int q = lt + 64 * i, c = q >> 5, p = q & 31;
-      const int rg = p >> 1, half = p & 1, kg = c >> 3, kl = c & 7;
-      const int item = (rg >> 2) + 4 * kg, clane = (rg & 3) * 8 + kl;
-      dst_off[i] = ((item * 2 + half) * 32 + clane) * 16;
-      col_off[i] = c;
-      row_off[i] = p * 4;
-    }
-    long long row0 = (long long)blockIdx.x * kBM;
-    const long long row_step = (long long)gridDim.x * kBM;
-    int kc = 0, slot = 0;
-    unsigned ph = 0;
-    for (int g = 0; g < nchunks; ++g) {
-      mbar_wait(&stage_empty[slot], ph ^ 1);
-      unsigned char* dst = ssm + slot * kStageBytes;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int col = kc * kKC + col_off[i];
-        const long long row = row0 + row_off[i];
-        const bool ok = col < n && row < m;  // m % 4 == 0: a 16-byte piece is all in or all out
-        cp_async16_zfill(dst + dst_off[i], ok ? a + (long long)col * lda + row : a, ok);
-      }
-      cp_async_mbar_arrive(&stage_full[slot]);
-      if (++kc == nkc) {
-        kc = 0;
-        row0 += row_step;
-      }
-      if (++slot == depth) {
-        slot = 0;
-        ph ^= 1;
-      }
-    }
-    cp_async_wait<0>();
-  } else if (warp == kWarpMma) {
-    if (lane == 0) {
-      // D f32, A/B bf16, both MN-major, N = np, M = 128
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
-                             ((uint32_t)(np >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
-      const uint32_t a_lbo = (kBM / 8) * 128, w_lbo = (uint32_t)(np / 8) * 128;
-      const uint32_t wbase = saddr(wsm), pbase = saddr(psm);
-      const uint32_t wplane = (uint32_t)np * np * 2u;
-      // (A piece, W piece), smallest products first
-      const int pa[6] = {2, 1, 0, 1, 0, 0}, pw[6] = {0, 1, 2, 0, 1, 0};
-      mbar_expect_tx(w_full, wbytes);
-      bulk_g2s(wsm, wplanes, wbytes, w_full);
-      mbar_wait(w_full, 0);
-      int ps = 0, ab = 0;
-      unsigned pph = 0, aph = 0;
-      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        { AVP_T0(); mbar_wait(&acc_empty[ab], aph ^ 1); AVP_ADD(0); }
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t d = tmem + (uint32_t)ab * (tcols / 2);
-        for (int kc = 0; kc < nkc; ++kc) {
-          { AVP_T0(); mbar_wait(&plane_full[ps], pph); AVP_ADD(1); }
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-#pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            const uint64_t ad = umma_desc(pbase + (uint32_t)(ps * 3 + pa[q]) * kPlaneBytes, a_lbo, 128);
-            const uint64_t bd = umma_desc(wbase + (uint32_t)pw[q] * wplane + (uint32_t)kc * 2u * w_lbo, w_lbo, 128);
-            if (!(dbg & 2)) umma_bf16(d, ad, bd, idesc, (kc > 0 || q > 0) ? 1u : 0u);
-          }
-          umma_commit(&plane_empty[ps]);
-          if (++ps == depth) {
-            ps = 0;
-            pph ^= 1;
-          }
-        }
-        umma_commit(&acc_full[ab]);
-        if (++ab == 2) {
-          ab = 0;
-          aph ^= 1;
-        }
-      }
-    }
-  } else if (warp < kConvWarps) {
-    // Warp-per-chunk: converter warp w (< depth) converts chunks w, w + depth,
-    // ... from staging slot w into its own plane slot w, so the warps'
-    // barrier and proxy-fence latencies overlap instead of adding up per
-    // chunk. Lane (rgl, kl) handles items i = 0..7: 8 rows (row group
-    // rgl + 4 (i & 3)) of column 8 (i >> 2) + kl; reads are [item][half][lane]
-    // x 16 B and each 8-lane phase writes one contiguous 128-byte core-matrix
-    // row: conflict-free.
-    if (warp < depth) {
-      const int kl = lane & 7, rgl = lane >> 3;
-      unsigned char* dst = psm + warp * 3 * kPlaneBytes;
-      const unsigned char* src = ssm + warp * kStageBytes + lane * 16;
-      unsigned ph = 0;
-      for (int g = warp; g < nchunks; g += depth) {
-        { AVP_T0(); mbar_wait(&stage_full[warp], ph); mbar_wait(&plane_empty[warp], ph ^ 1); AVP_ADD(2); }
-        AVP_T0();
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float4 x[4], y[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int i = hh * 4 + j;
-            x[j] = *reinterpret_cast<const float4*>(src + (i * 2 + 0) * 512);
-            y[j] = *reinterpret_cast<const float4*>(src + (i * 2 + 1) * 512);
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int i = hh * 4 + j;
-            uint4 h, mm, l;
-            split3(x[j].x, x[j].y, h.x, mm.x, l.x);
-            split3(x[j].z, x[j].w, h.y, mm.y, l.y);
-            split3(y[j].x, y[j].y, h.z, mm.z, l.z);
-            split3(y[j].z, y[j].w, h.w, mm.w, l.w);
-            const uint32_t off = mn_major_off((rgl + 4 * (i & 3)) * 8, (i >> 2) * 8 + kl, kBM);
-            *reinterpret_cast<uint4*>(dst + off) = h;
-            *reinterpret_cast<uint4*>(dst + kPlaneBytes + off) = mm;
-            *reinterpret_cast<uint4*>(dst + 2 * kPlaneBytes + off) = l;
-          }
-        }
-        AVP_ADD(3);
-        AVP_T0();
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&stage_empty[warp]);
-          mbar_arrive(&plane_full[warp]);
-        }
-        ph ^= 1;
-        AVP_ADD(5);
-      }
-    }
-  } else if (warp < kConvWarps + kEpiWarps) {
-    // epilogue: TMEM lane quarter = warp % 4; e selects alternate 16-column groups
-    const int q = warp & 3, e = (warp - kConvWarps) >> 2;
-    int ab = 0;
-    unsigned aph = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      { AVP_T0(); mbar_wait(&acc_full[ab], aph); AVP_ADD(6); }
-      AVP_T0();
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const long long row = tile * kBM + q * 32 + lane;
-      const bool row_ok = row < m && !(dbg & 1);
-      float* base = u + row;
-      for (int c0 = 16 * e; c0 < np; c0 += 32) {
-        uint32_t r[16];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)ab * (tcols / 2) + (uint32_t)c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-            "[%16];\n"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (row_ok) {
-          float* p = base + (long long)c0 * ldu;
-          if (c0 + 16 <= n) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              *p = __uint_as_float(r[j]);
-              p += ldu;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < n) p[(long long)j * ldu] = __uint_as_float(r[j]);
-          }
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[ab]);
-      AVP_ADD(7);
-      if (++ab == 2) {
-        ab = 0;
-        aph ^= 1;
-      }
-    }
+  mx = red[0];
+  for (int i = 1; i < (int)((blockDim.x + 31) >> 5); ++i) mx = fmaxf(mx, red[i]);
+  int tj = 0;
+  if (mx > 0.0f && mx <= 3.4028235e38f) {
+    int e;
+    frexpf(mx, &e);  // max |2^s_k W_kj| < 2^e
+    tj = e - tc::kHead;
   }
-  if (prof) {
-    g_av_prof[8 + (warp == 0 ? 0 : warp == 8 ? 1 : 2)] = clock64() - t_start;
-    for (int i = 0; i < 8; ++i)
-      if (pacc[i]) g_av_prof[i] = pacc[i];
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == kWarpMma)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols));
+  if (k >= np) return;  // blockDim = max(np, 32): full warps for the shuffles
+  const float xs = ldexpf(x, -tj);
+  // w = w0 + w1 + w2 exactly (33 >= 24 bits) while w2 is a normal fp16, i.e.
+  // for |xs| >= 2^8 (the column maximum is near 2^14); smaller entries keep
+  // an absolute error below 2^-24 of the column maximum
+  const __half w0 = __float2half_rn(xs);
+  const float r1 = xs - __half2float(w0);
+  const __half w1 = __float2half_rn(r1);
+  const __half w2 = __float2half_rn(r1 - __half2float(w1));
+  __half* planes = reinterpret_cast<__half*>(out);
+  const uint32_t off = tc::mn_major_off(j, k, np) >> 1;  // in fp16 elements
+  planes[off] = w0;
+  planes[(size_t)np * np + off] = w1;
+  planes[(size_t)2 * np * np + off] = w2;
+  float* scl = reinterpret_cast<float*>(out + (size_t)tc::kWPieces * np * np * 2);
+  if (j == 0) scl[k] = k < n ? ldexpf(1.0f, -sk) : 0.0f;
+  if (k == 0) scl[np + j] = ldexpf(1.0f, tj);
 }
-
 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void nbar_sync_k7(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
-// K7, TMEM variant: the bf16 pieces of A are written to tensor memory with
-// tcgen05.st (thread = row) and fed to the MMA as its A operand (K-major in
-// TMEM, two K-neighbours per 32-bit column, low half = even k; encoding
-// checked by tools/microbench/umma_tmem_a.cu). No shared-memory planes and
-// no generic->async proxy fence; the freed shared memory deepens the fp32
-// staging ring. Roles:
-//   warps 0-15  converters, four groups of four (one warp per TMEM lane
-//               quarter); group g converts chunks g, g + 4, ... into TMEM
-//               A slots {g, g + 4} (each slot has one owner group)
-//   warps 16-23 epilogue (as in av_tc_f32)
-//   warps 24-25 loaders: fp32 chunk [16 columns][128 rows] by cp.async
-//   warp 26     W pieces (bulk copy) + MMA issue
 namespace tm {
 #ifndef TM_GROUPS
 #define TM_GROUPS 4  // converter groups (4 warps each); 2 left the MMA waiting for A slots (C4 ncu)
 #endif
 constexpr int kGroups = TM_GROUPS;
-constexpr int kASlots = 2 * kGroups;  // TMEM A slots (24 columns each: 3 pieces x 8)
-constexpr int kACols = 3 * 8;
+constexpr int kASlots = 2 * kGroups;  // TMEM A slots (16 columns each: 2 pieces x 8)
+constexpr int kACols = 2 * 8;
 constexpr int kConvW = 4 * kGroups, kEpi0 = kConvW;  // converters: warps 0 .. kConvW-1, then 8 epilogue warps
 constexpr int kLoad0 = kEpi0 + 8, kLoadWarps = TM_LOAD_WARPS, kMma = kLoad0 + kLoadWarps;
 constexpr int kThreads = 32 * (kMma + 1);
@@ -446,14 +213,16 @@ constexpr int kPieces = 512 / (32 * kLoadWarps);  // 16-byte pieces per loader t
 
 __global__ void __launch_bounds__(tm::kThreads, 1)
 av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, int np,
-               const __nv_bfloat16* __restrict__ wplanes, float* __restrict__ u, long long ldu,
+               const unsigned char* __restrict__ wplanes, float* __restrict__ u, long long ldu,
                const DevStatus* __restrict__ status, int nstage, int acc_stride, int a_col0, int tcols) {
   using namespace tc;
   using namespace tm;
   if (status && status->status != kOk) return;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   const int nkc = np / kKC;
-  const uint32_t wbytes = 3u * np * np * 2u;
+  const uint32_t wbytes = (uint32_t)wplanes_bytes(np);  // 3 fp16 W planes + A and U column scales
+  const float* a_scl = reinterpret_cast<const float*>(smem_tc + (uint32_t)kWPieces * np * np * 2u);  // 2^-s_c per column of A
+  const float* u_scl = a_scl + np;                                                    // 2^t_j per column of U
   unsigned char* wsm = smem_tc;
   unsigned char* ssm = wsm + ((wbytes + 1023) & ~1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ssm + nstage * kStageBytes);
@@ -469,7 +238,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
   const long long ntiles = (m + kBM - 1) / kBM;
   const int my_tiles = (int)(ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int nchunks = my_tiles * nkc;
-  const int kdbg = tcols >> 16;  // experiment switches (MPSVD_AV_DBG bits 4-6): 1 no MMA, 2 no U stores, 4 no split
+  const int kdbg = tcols >> 16;  // experiment switches (MPSVD_AV_DBG): 1 no MMA, 2 no U stores, 4 no split
   tcols &= 0xFFFF;
   const uint32_t zmask = (uint32_t)kdbg >> 8;  // 0 (kdbg < 256), unknown to the compiler
 
@@ -532,13 +301,15 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     cp_async_wait<0>();
   } else if (warp == tm::kMma) {
     if (lane == 0) {
-      // D f32, A bf16 K-major (TMEM), B bf16 MN-major (smem), N = np, M = 128
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(np >> 3) << 17) |
+      // D f32, A fp16 K-major (TMEM), B fp16 MN-major (smem), N = np, M = 128
+      const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | (1u << 16) | ((uint32_t)(np >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
       const uint32_t w_lbo = (uint32_t)(np / 8) * 128;
       const uint32_t wbase = saddr(wsm);
       const uint32_t wplane = (uint32_t)np * np * 2u;
-      const int pa[6] = {2, 1, 0, 1, 0, 0}, pw[6] = {0, 1, 2, 0, 1, 0};
+      // A1 W0 + A0 W2 + A0 W1 + A0 W0 (smallest first); A1 W1, A1 W2 (2^-22,
+      // 2^-33 relative) are dropped
+      const int pa[4] = {1, 0, 0, 0}, pw[4] = {0, 2, 1, 0};
       mbar_expect_tx(w_full, wbytes);
       bulk_g2s(wsm, wplanes, wbytes, w_full);
       mbar_wait(w_full, 0);
@@ -555,7 +326,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint32_t at = tmem + (uint32_t)(a_col0 + sl * kACols);
 #pragma unroll
-          for (int q = 0; q < 6; ++q) {
+          for (int q = 0; q < 4; ++q) {
             if (kdbg & 1) break;
             const uint64_t bd = umma_desc(wbase + (uint32_t)pw[q] * wplane + (uint32_t)kc * 2u * w_lbo, w_lbo, 128);
             asm volatile(
@@ -577,6 +348,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     // 32q .. 32q + 31 (rows of the tile)
     const int grp = warp >> 2, q = warp & 3;
     const int row = q * 32 + lane;
+    mbar_wait(w_full, 0);  // the column scales arrive with the W pieces
     int slot = grp % nstage;
     unsigned sph = (unsigned)((grp / nstage) & 1);
     // one warp of the group polls each mbarrier, the other three wait on the
@@ -590,13 +362,19 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
       float v[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) v[c] = src[c * kBM + row];  // consecutive lanes: consecutive rows
-      uint32_t hp[8], mp[8], lp[8];
+      // column scales of this chunk's 16 columns (same address in every lane: broadcast)
+      const float4* scl = reinterpret_cast<const float4*>(a_scl + (g % nkc) * kKC);
+      uint32_t hp[8], lp[8];
       if (kdbg & 4) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) hp[c] = mp[c] = lp[c] = __float_as_uint(v[2 * c]) ^ __float_as_uint(v[2 * c + 1]);
+        for (int c = 0; c < 8; ++c) hp[c] = lp[c] = __float_as_uint(v[2 * c]) ^ __float_as_uint(v[2 * c + 1]);
       } else {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) split3(v[2 * c], v[2 * c + 1], hp[c], mp[c], lp[c]);
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const float4 s4 = scl[c4];
+          split2h(v[4 * c4] * s4.x, v[4 * c4 + 1] * s4.y, hp[2 * c4], lp[2 * c4]);
+          split2h(v[4 * c4 + 2] * s4.z, v[4 * c4 + 3] * s4.w, hp[2 * c4 + 1], lp[2 * c4 + 1]);
+        }
       }
       // release the staging slot only once every lane's loads have returned:
       // an arrive right after the loads (lane 0, after __syncwarp) can
@@ -626,8 +404,6 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta), "r"(hp[0]),
                    "r"(hp[1]), "r"(hp[2]), "r"(hp[3]), "r"(hp[4]), "r"(hp[5]), "r"(hp[6]), "r"(hp[7]));
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta + 8u),
-                   "r"(mp[0]), "r"(mp[1]), "r"(mp[2]), "r"(mp[3]), "r"(mp[4]), "r"(mp[5]), "r"(mp[6]), "r"(mp[7]));
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta + 16u),
                    "r"(lp[0]), "r"(lp[1]), "r"(lp[2]), "r"(lp[3]), "r"(lp[4]), "r"(lp[5]), "r"(lp[6]), "r"(lp[7]));
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -636,6 +412,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     }
   } else if (warp < tm::kEpi0 + kEpiWarps) {
     const int q = warp & 3, e = (warp - tm::kEpi0) >> 2;
+    mbar_wait(w_full, 0);  // the column scales arrive with the W pieces
     int ab = 0;
     unsigned aph = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -656,17 +433,28 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         if (row_ok && !(kdbg & 2)) {
+          // U_j = acc_j 2^t_j (exact: a power of two)
+          const float4* us = reinterpret_cast<const float4*>(u_scl + c0);
+          float x[16];
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) {
+            const float4 s4 = us[j4];
+            x[4 * j4] = __uint_as_float(r[4 * j4]) * s4.x;
+            x[4 * j4 + 1] = __uint_as_float(r[4 * j4 + 1]) * s4.y;
+            x[4 * j4 + 2] = __uint_as_float(r[4 * j4 + 2]) * s4.z;
+            x[4 * j4 + 3] = __uint_as_float(r[4 * j4 + 3]) * s4.w;
+          }
           float* p = base + (long long)c0 * ldu;
           if (c0 + 16 <= n) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              *p = __uint_as_float(r[j]);
+              *p = x[j];
               p += ldu;
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              if (c0 + j < n) p[(long long)j * ldu] = __uint_as_float(r[j]);
+              if (c0 + j < n) p[(long long)j * ldu] = x[j];
           }
         }
       }
@@ -686,6 +474,7 @@ av_tc_tmem_f32(const float* __restrict__ a, long long lda, long long m, int n, i
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tcols));
 }
 
+
 // ---------------------------------------------------------------------------
 bool av_tc_supported(const float* a, long long lda, long long m, int n, long long ldu) {
   (void)ldu;
@@ -695,22 +484,23 @@ bool av_tc_supported(const float* a, long long lda, long long m, int n, long lon
   return true;
 }
 
+// the pieces + scales, then the saved Gram diagonal (np doubles)
 size_t av_tc_wplanes_bytes(int n) {
   const int np = (n + 15) / 16 * 16;
-  return 3ull * np * np * 2ull;
+  return tc::wplanes_bytes(np) + (size_t)np * 8;
 }
 
-// experiment switches of the shared-memory-plane variant (MPSVD_AV_PLANES=1,
-// or any MPSVD_AV_DBG bit selects it) — MPSVD_AV_DBG: bit 0 skips the U stores, bit 1 the
-// MMAs, bit 2 prints per-role cycle counts of CTA 0 (tools/av_probe.sh).
-// Findings (C2, n = 64): loads + conversion alone take 0.089 ms of the
-// 0.128 ms, and with loads, conversion, MMAs and stores all skipped the
-// barrier hand-offs alone still take ~0.065 ms: the ring of mbarrier
-// hand-offs (loader -> converter -> MMA -> epilogue, 8 slots deep, limited by
-// shared memory) bounds K7 at small n, not HBM. An XOR-swizzled staging
-// layout (conflict-free cp.async writes), 4 loader warps, packing the six
-// products into four MMAs (N = 2n) and test_wait spinning were all measured
-// slower or equal and not kept.
+cudaError_t launch_av_tc_save_diag(const double* gram, int n, void* wplanes, cudaStream_t st) {
+  const int np = (n + 15) / 16 * 16;
+  av_tc_save_diag<<<(n + 127) / 128, 128, 0, st>>>(
+      gram, n, reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(wplanes) + tc::wplanes_bytes(np)));
+  return cudaGetLastError();
+}
+
+// experiment switches (MPSVD_AV_DBG): bit 0 skips the MMAs, bit 1 the U
+// stores, bit 2 the split (c4, bf16x3 version: 14.8 ms; no MMA 11.1, no
+// stores 12.8, no split 13.2, none of the three 8.1); MPSVD_AV_STAGES caps
+// the staging ring (4-16 slots measured within 3%)
 static int g_av_dbg = [] {
   const char* e = getenv("MPSVD_AV_DBG");
   return e ? atoi(e) : 0;
@@ -722,57 +512,26 @@ cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, 
   using namespace tc;
   const int np = (n + 15) / 16 * 16;
   const int ldw = av_ldw(n);
-  const int prep_threads = 256;
   if (prep)
-    av_tc_prep_w<<<(np * np + prep_threads - 1) / prep_threads, prep_threads, 0, st>>>(
-        w, ldw, n, np, reinterpret_cast<__nv_bfloat16*>(wplanes), status);
-  const size_t wbytes = ((size_t)3 * np * np * 2 + 1023) & ~(size_t)1023;
-  static const bool planes = getenv("MPSVD_AV_PLANES") != nullptr;  // the shared-memory-plane variant
-  if (!planes && !(g_av_dbg & 7)) {
-    // TMEM variant: accumulators [0, 2 acc_stride), A slots after them
-    const int acc_stride = np <= 32 ? 32 : np <= 64 ? 64 : 128;
-    const int a_col0 = 2 * acc_stride;
-    const int need = a_col0 + tm::kASlots * tm::kACols;
-    const int tcols = need <= 128 ? 128 : need <= 256 ? 256 : 512;
-    int nstage = (int)((kSmemLimit - wbytes - 1024) / kStageBytes);
-    static const int stage_cap = getenv("MPSVD_AV_STAGES") ? atoi(getenv("MPSVD_AV_STAGES")) : 16;
-    if (nstage > stage_cap) nstage = stage_cap;
-    if (nstage < tm::kGroups) return cudaErrorInvalidConfiguration;
-    const size_t smem = wbytes + (size_t)nstage * kStageBytes + 1024;
-    cudaError_t e = cudaFuncSetAttribute(av_tc_tmem_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const long long ntiles = (m + kBM - 1) / kBM;
-    const int grid = (int)(ntiles < sm_count ? ntiles : sm_count);
-    av_tc_tmem_f32<<<grid, tm::kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const __nv_bfloat16*>(wplanes),
-                                                 u, ldu, status, nstage, acc_stride, a_col0,
-                                                 tcols | (((g_av_dbg >> 4) & 7) << 16));
-    return cudaGetLastError();
-  }
-  // one staging slot + one plane slot per active converter warp
-  int depth = kConvWarps;
-  auto smem_for = [&](int d) { return wbytes + (size_t)d * (3 * kPlaneBytes + kStageBytes) + 512; };
-  while (depth > 1 && smem_for(depth) > (size_t)kSmemLimit) depth /= 2;
-  const size_t smem = smem_for(depth);
-  if (smem > (size_t)kSmemLimit || depth < 2) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(av_tc_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    av_tc_prep_w<<<np, np < 32 ? 32 : np, 0, st>>>(w, ldw, n, np, reinterpret_cast<unsigned char*>(wplanes), status);
+  const size_t wbytes = (wplanes_bytes(np) + 1023) & ~(size_t)1023;
+  // accumulators [0, 2 acc_stride), A slots after them
+  const int acc_stride = np <= 32 ? 32 : np <= 64 ? 64 : 128;
+  const int a_col0 = 2 * acc_stride;
+  const int need = a_col0 + tm::kASlots * tm::kACols;
+  const int tcols = need <= 128 ? 128 : need <= 256 ? 256 : 512;
+  int nstage = (int)((kSmemLimit - wbytes - 1024) / kStageBytes);
+  static const int stage_cap = getenv("MPSVD_AV_STAGES") ? atoi(getenv("MPSVD_AV_STAGES")) : 16;
+  if (nstage > stage_cap) nstage = stage_cap;
+  if (nstage < tm::kGroups) return cudaErrorInvalidConfiguration;
+  const size_t smem = wbytes + (size_t)nstage * kStageBytes + 1024;
+  cudaError_t e = cudaFuncSetAttribute(av_tc_tmem_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (m + kBM - 1) / kBM;
   const int grid = (int)(ntiles < sm_count ? ntiles : sm_count);
-  if (g_av_dbg & 4) {
-    unsigned long long z[16] = {};
-    cudaMemcpyToSymbolAsync(g_av_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
-  }
-  av_tc_f32<<<grid, kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const __nv_bfloat16*>(wplanes), u, ldu,
-                                          status, depth, g_av_dbg);
-  if (g_av_dbg & 4) {
-    unsigned long long h[16];
-    cudaMemcpyFromSymbolAsync(h, g_av_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    fprintf(stderr,
-            "av_tc prof (cycles, CTA 0): mma: acc_empty %llu plane_full %llu | conv: data %llu split+issue %llu "
-            "plane_empty %llu store+fence %llu | epi: acc_full %llu ld+store %llu | total conv %llu epi %llu mma %llu\n",
-            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10]);
-  }
+  av_tc_tmem_f32<<<grid, tm::kThreads, smem, st>>>(a, lda, m, n, np, reinterpret_cast<const unsigned char*>(wplanes),
+                                               u, ldu, status, nstage, acc_stride, a_col0,
+                                               tcols | ((g_av_dbg & 7) << 16));
   return cudaGetLastError();
 }
 

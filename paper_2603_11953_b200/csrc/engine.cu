@@ -525,6 +525,11 @@ void Plan::gram(const void* d_a, long long lda, cudaStream_t st) {
     launches += 2 + (ndiag > 0 ? 1 : 0) + (ntp > ndiag ? 1 : 0);
   }
   if (nranks > 1) exchange(st);
+  // K7's column scales need ||a_k||^2 after the eigensolver has overwritten M
+  if (d_wplanes) {
+    check(dev::launch_av_tc_save_diag((const double*)d_m, (int)n, d_wplanes, st), "save Gram diagonal");
+    launches += 1;
+  }
 }
 
 // The one exchange of the multi-GPU path (north_star (4); the reference's
@@ -782,6 +787,10 @@ void Plan::execute_host(const void* h_a, void* d_a, void* h_u, void* d_u, double
                                        (double*)d_m, st),
           "gram_combine_f64");
   launches += k1z ? 1 : 2;
+  if (d_wplanes) {
+    check(dev::launch_av_tc_save_diag((const double*)d_m, (int)n, d_wplanes, st), "save Gram diagonal");
+    launches += 1;
+  }
   (void)esz;
   record_event(ev[1], st);
   eigen(st);

@@ -85,9 +85,12 @@ cudaError_t launch_finish(bool dd, int n, const JacobiWorkspace& ws, int* perm, 
 cudaError_t launch_av_f32(const float* a, long long lda, long long m, int n, const float* w,
                           float* u, long long ldu, const DevStatus* status, cudaStream_t st);
 // K7 on tcgen05 (compute_u_tc.cu): fp32, n <= 128, m % 4 == 0, lda % 4 == 0,
-// 16-byte aligned A. `wplanes` is av_tc_wplanes_bytes(n) of device scratch.
+// 16-byte aligned A. `wplanes` is av_tc_wplanes_bytes(n) of device scratch;
+// launch_av_tc_save_diag must have stored the Gram's diagonal in it (A's
+// column scales) before the Jacobi overwrites M.
 bool av_tc_supported(const float* a, long long lda, long long m, int n, long long ldu);
 size_t av_tc_wplanes_bytes(int n);
+cudaError_t launch_av_tc_save_diag(const double* gram, int n, void* wplanes, cudaStream_t st);
 cudaError_t launch_av_tc_f32(const float* a, long long lda, long long m, int n, const float* w, void* wplanes,
                              float* u, long long ldu, const DevStatus* status, int sm_count, cudaStream_t st,
                              bool prep = true);  // prep: split W into its bf16 pieces first
