@@ -899,6 +899,82 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
       }
   };
 
+  // Two off-diagonal blocks at once (the bulk update's common case): within a
+  // round the blocks touch disjoint entries, so both blocks' loads are
+  // issued before either block's stores and the two dependent chains
+  // (pair words -> entries -> two rotations -> stores) overlap; the
+  // arithmetic of each block is update_block's. Blocks that are diagonal,
+  // hold an odd n's bye or are fully inactive go through update_block.
+  auto full_block = [&](int aa, int bb, const int* pw) {
+    const int wa = pw[aa], wb = pw[bb];
+    return aa != bb && ((wa | wb) >> 30 & 1) && ((wa >> 15) & 0x7fff) < n && ((wb >> 15) & 0x7fff) < n;
+  };
+  auto update_pair = [&](int w1, int w2, const AT* rb, const int* pw) {
+    const int a1 = w1 & 0xffff, b1 = w1 >> 16, a2 = w2 & 0xffff, b2 = w2 >> 16;
+    if (!full_block(a1, b1, pw) || !full_block(a2, b2, pw)) {
+      update_block(a1, b1, rb, pw);
+      update_block(a2, b2, rb, pw);
+      return;
+    }
+    const AT* rcs = rb;
+    const AT* rss = rb + np;
+    const int wa1 = pw[a1], wb1 = pw[b1], wa2 = pw[a2], wb2 = pw[b2];
+    ST* const e00 = CE(wa1 & 0x7fff, wb1 & 0x7fff);
+    ST* const e01 = CE(wa1 & 0x7fff, (wb1 >> 15) & 0x7fff);
+    ST* const e10 = CE((wa1 >> 15) & 0x7fff, wb1 & 0x7fff);
+    ST* const e11 = CE((wa1 >> 15) & 0x7fff, (wb1 >> 15) & 0x7fff);
+    ST* const f00 = CE(wa2 & 0x7fff, wb2 & 0x7fff);
+    ST* const f01 = CE(wa2 & 0x7fff, (wb2 >> 15) & 0x7fff);
+    ST* const f10 = CE((wa2 >> 15) & 0x7fff, wb2 & 0x7fff);
+    ST* const f11 = CE((wa2 >> 15) & 0x7fff, (wb2 >> 15) & 0x7fff);
+    AT x00 = A_::lds(e00), x01 = A_::lds(e01), x10 = A_::lds(e10), x11 = A_::lds(e11);
+    AT z00 = A_::lds(f00), z01 = A_::lds(f01), z10 = A_::lds(f10), z11 = A_::lds(f11);
+    if ((wb1 >> 30) & 1) {
+      const AT cb = rcs[b1], sb = rss[b1];
+      const AT y00 = A_::rot_lo(cb, sb, x00, x01), y01 = A_::rot_hi(cb, sb, x00, x01);
+      const AT y10 = A_::rot_lo(cb, sb, x10, x11), y11 = A_::rot_hi(cb, sb, x10, x11);
+      x00 = y00;
+      x01 = y01;
+      x10 = y10;
+      x11 = y11;
+    }
+    if ((wb2 >> 30) & 1) {
+      const AT cb = rcs[b2], sb = rss[b2];
+      const AT y00 = A_::rot_lo(cb, sb, z00, z01), y01 = A_::rot_hi(cb, sb, z00, z01);
+      const AT y10 = A_::rot_lo(cb, sb, z10, z11), y11 = A_::rot_hi(cb, sb, z10, z11);
+      z00 = y00;
+      z01 = y01;
+      z10 = y10;
+      z11 = y11;
+    }
+    if ((wa1 >> 30) & 1) {
+      const AT ca = rcs[a1], sa = rss[a1];
+      const AT y00 = A_::rot_lo(ca, sa, x00, x10), y10 = A_::rot_hi(ca, sa, x00, x10);
+      const AT y01 = A_::rot_lo(ca, sa, x01, x11), y11 = A_::rot_hi(ca, sa, x01, x11);
+      x00 = y00;
+      x10 = y10;
+      x01 = y01;
+      x11 = y11;
+    }
+    if ((wa2 >> 30) & 1) {
+      const AT ca = rcs[a2], sa = rss[a2];
+      const AT y00 = A_::rot_lo(ca, sa, z00, z10), y10 = A_::rot_hi(ca, sa, z00, z10);
+      const AT y01 = A_::rot_lo(ca, sa, z01, z11), y11 = A_::rot_hi(ca, sa, z01, z11);
+      z00 = y00;
+      z10 = y10;
+      z01 = y01;
+      z11 = y11;
+    }
+    A_::st(e00, x00);
+    A_::st(e01, x01);
+    A_::st(e10, x10);
+    A_::st(e11, x11);
+    A_::st(f00, z00);
+    A_::st(f01, z01);
+    A_::st(f10, z10);
+    A_::st(f11, z11);
+  };
+
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     // sweep pre-check (see jacobi_kernel): nothing passes the stop test ->
     // this sweep is the rotation-free detection sweep
@@ -1053,7 +1129,10 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
         const int b = (int)((g + r) & 1);
         const AT* rb = RC(b);
         const int* pw = pwb + b * np;
-        for (int j = utid; j < nnon; j += n_upd) {
+        int j = utid;
+        if constexpr (sizeof(ST) == sizeof(double))  // fp64 only: the dd pair path spills
+          for (; j + n_upd < nnon; j += 2 * n_upd) update_pair(blk[j], blk[j + n_upd], rb, pw);
+        for (; j < nnon; j += n_upd) {
           const int w = blk[j];
           update_block(w & 0xffff, w >> 16, rb, pw);
         }
