@@ -84,7 +84,7 @@ NCU_NAME = {("gram", 0): "gram_f32_diag", ("gram", 1): "gram_f32_ozaki", ("gram"
             ("compute_u", 2): "av_dmma_f64"}
 GRAM_KERNELS = {0: "K1 gram_f32_diag/offdiag (DMMA)", 1: "K1z gram_f32_ozaki (tcgen05 kind::i8, TMA)",
                 2: "K2 gram_f64_dd (Dot2, fp64 pipe)", 3: "K2z gram_dd_ozaki (tcgen05 kind::i8) + ozaki_slice/colexp"}
-AV_KERNELS = {0: "av_kernel (fp32 SIMT)", 1: "av_tc_tmem_f32 (tcgen05 bf16x3)", 2: "av_dmma_f64 (DMMA)"}
+AV_KERNELS = {0: "av_kernel (fp32 SIMT)", 1: "av_tc_tmem_f32 (tcgen05, fp16 pieces: A x2, W x3)", 2: "av_dmma_f64 (DMMA)"}
 
 
 def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
