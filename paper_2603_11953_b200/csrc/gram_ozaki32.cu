@@ -18,7 +18,8 @@
 // A launch covers a chunk range; CTA pair p (a cluster of 2) takes an equal
 // share of it and both CTAs stream the same chunks (the second read is an L2
 // hit): CTA g of the pair owns accumulator group g (below). Per CTA:
-//   warp 0       TMA: 32 x 128 fp32 boxes (16 KB, 128B swizzle) into a ring
+//   warp 0       TMA: this CTA's 16 rows x 128 columns of each chunk (8 KB,
+//                64B swizzle) into a ring
 //   warp 1       MMA issue (one thread) + TMEM allocation (4 x 128 columns);
 //                in group 1 the warp also sums the D8 diagonal (below)
 //   warps 2-5    drain (TMEM lane quarter = tile rows): span totals -> dd
@@ -26,7 +27,9 @@
 //                thread = (column, 8 rows of this CTA's 16-row half): the
 //                6 signed digits of every entry as UMMA operand planes
 //                (K-major, no swizzle) in this CTA's half of a digit slot
-//   warps 22-25  scouts: lane = column; each chunk's column maxima -> the
+//   warps 22-25  scouts: lane = column; the column maxima of this CTA's
+//                half, exchanged with the peer's (st.async into its smem,
+//                completing on an mbarrier) -> the chunk's maxima -> the
 //                span decision (one 128-thread barrier-with-reduction) and
 //                the span's exponents, published per chunk by an mbarrier
 //   warp 26      copier: one DSMEM bulk copy moves this CTA's half of each
@@ -36,11 +39,11 @@
 // have returned (release_a: a plain lane-0 arrive after __syncwarp let the
 // TMA refill a slot under loads still in flight, tools/oz32_harness.cu).
 // Per role one warp polls an mbarrier and the role's other warps wait on a
-// named barrier. Measured (c4, ncu + harness stamps): ~1,300 cycles per
-// chunk; the SM's shared-memory bandwidth bounds it - the 6 MMAs read 48 KB
-// of operands per chunk (int8 M128 N128 K32 alone would need 128 B/clk),
-// plus 16 KB TMA, 16 KB scout and 8 KB converter reads, 12 KB digit writes
-// and 24 KB of DSMEM copies.
+// named barrier. The SM's shared-memory bandwidth bounds the kernel: per
+// chunk and CTA the 6 MMAs read 48 KB of operands (int8 M128 N128 K32 alone
+// would need 128 B/clk), plus 8 KB of TMA writes, 8 KB scout and 8 KB
+// converter reads, 12 KB of digit writes and 24 KB of DSMEM copies (each
+// CTA loading and scanning only its own half saved 16 KB per chunk).
 //
 // Digits. A span is a run of chunks with fixed column exponents E_c. A span
 // starts at the first chunk of the CTA's range, after kSpanMax chunks (the
@@ -92,7 +95,9 @@ constexpr int kDigits = 6;
 constexpr int kHead = 2;                      // exponent headroom (bits) of a new span
 constexpr int kSpanMax = 1024;                // chunks per span: int32 sums stay exact
 constexpr int kZeroE = -160;                  // exponent of an all-zero column
-constexpr int kAStageBytes = kKC * kCB * 4;   // 16384
+constexpr int kHalfRows = kKC / 2;            // each CTA of the pair loads and converts 16 rows of a chunk
+constexpr int kAStageBytes = kHalfRows * kCB * 4;  // 8192: 128 columns x 64 B, 64B-swizzled
+constexpr int kPmaxSlots = 16;                // ring of the peer's half-chunk column maxima (> A + digit slots)
 constexpr int kDStageBytes = kDigits * kPlane;
 constexpr int kConvGroups = 2;                // converter groups: group G converts the chunks j = G mod 2
 constexpr int kConvThreads = 256 * kConvGroups;
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begin, long long c_end, int npairs,
                double2* __restrict__ partials, int* __restrict__ bad_cols, int accumulate, int span_max, int wmode) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-aligned carve-up (the 128B swizzle needs 1024-byte aligned boxes);
+  // 1024-aligned carve-up (the swizzled TMA boxes want aligned bases);
   // offsets from smem_raw keep the pointers in the shared window (LDS/STS,
   // not generic loads and stores)
   unsigned char* base = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
@@ -434,10 +439,19 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   int* meta = desc + 2 * kCB;                            // [kAStages][2]: fresh, span
   int* sbad = meta + 2 * kAStages;                       // [128]
   int* dsq = sbad + kCB;                                 // [2][128] D8 diagonal sums per span (group 1's MMA warp)
+  uint32_t* pmax = reinterpret_cast<uint32_t*>(dsq + 2 * kCB);  // [kPmaxSlots][128] the peer half's column maxima
+  uint64_t* pmax_full = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(pmax + kPmaxSlots * kCB) + 7) & ~(uintptr_t)7);  // [kPmaxSlots]
+  static_assert(kPmaxSlots > kAStages + kDStages, "the peer's maxima ring must outrun both pipelines");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x >> 1, g = blockIdx.x & 1;
-  const uint32_t zmask = (uint32_t)wmode >> 8;  // 0 (wmode < 256), unknown to the compiler
+  // timing probes (MPSVD_OZ32_DBG, results wrong): bit 0 skips the MMAs,
+  // bit 1 the digit conversion (zeros are written), bit 2 the scouts' peer
+  // exchange and barrier reductions
+  const int kdbg = wmode >> 8;
+  wmode &= 0xFF;
+  const uint32_t zmask = (uint32_t)kdbg >> 16;  // 0, unknown to the compiler
   OZ32_DBG(const Oz32Dbg dbg = g_oz32_dbg;)
   const long long nch_all = c_end - c_begin;
   const long long c0 = c_begin + nch_all * pair / npairs, c1 = c_begin + nch_all * (pair + 1) / npairs;
@@ -459,6 +473,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     mbar_init(info_full, 1);
     mbar_init(&desc_empty[0], 4);
     mbar_init(&desc_empty[1], 4);
+    for (int i = 0; i < kPmaxSlots; ++i) mbar_init(&pmax_full[i], 1);  // one local expect_tx + 512 peer bytes
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (threadIdx.x < kCB) sbad[threadIdx.x] = 0;
@@ -482,7 +497,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         mbar_wait_m(&a_empty[s], ((unsigned)(j / kAStages) & 1u) ^ 1u, wmode, 64);
         OZ32_DBG(oz32_stamp(dbg, g, pair, j, 0);)
         mbar_expect_tx(&a_full[s], kAStageBytes);
-        tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + j) * kKC), 0, &a_full[s]);
+        tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + j) * kKC + g * kHalfRows), 0, &a_full[s]);
       }
     }
   } else if (warp == 1) {
@@ -526,9 +541,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const uint64_t sd = dbase + (uint64_t)((uint32_t)s * (kDStageBytes >> 4));
       uint32_t dep = 0;
       if (g == 0) {
-        issue_chunk<0>(tmem, sd, idesc, fresh, lead);
+        if (!(kdbg & 1)) issue_chunk<0>(tmem, sd, idesc, fresh, lead);
       } else {
-        issue_chunk<1>(tmem, sd, idesc, fresh, lead);
+        if (!(kdbg & 1)) issue_chunk<1>(tmem, sd, idesc, fresh, lead);
         const unsigned char* p4 = dstage + (size_t)s * kDStageBytes + 3 * 2048 + (lane >> 3) * 128 + (lane & 7) * 16;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -579,26 +594,46 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     // chunk, span_max chunks, or an entry >= 2^E_c: OR over the 128 scout
     // threads) and at a new span E_c = e(max) + kHead
     const int c = (warp - kScoutWarp0) * 32 + lane;
+    const uint32_t pmax_peer = mapa(saddr(pmax), (uint32_t)(g ^ 1));
+    const uint32_t pmax_full_peer = mapa(saddr(pmax_full), (uint32_t)(g ^ 1));
     int Ec = kZeroE;
     int span = -1, len = 0;
     for (int j = 0; j < nch; ++j) {
       const int sa = j % kAStages;
       if (warp == kScoutWarp0) mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
       nbar_sync(7, 128);
-      const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
-      // max of |x| as bit patterns over all entries: inf / NaN (exponent 255)
-      // lie above every finite value, so they force a new span and a huge
-      // E_c for their column, whose entries the converters then zero and flag
+      const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 64;
+      // max of |x| as bit patterns over this CTA's 16 rows: inf / NaN
+      // (exponent 255) lie above every finite value, so they force a new
+      // span and a huge E_c for their column, whose entries the converters
+      // then zero and flag
       uint32_t mx = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ (c & 7)) << 4));
+      for (int u = 0; u < 4; ++u) {
+        const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ ((c >> 1) & 3)) << 4));
         mx = max(mx, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
       }
       release_a(&a_empty[sa], lane, mx, zmask);
+      // exchange the half maxima with the peer (st.async, completing on its
+      // pmax_full), then take the chunk maximum: both CTAs of the pair make
+      // the same span decisions from the same 32 rows. The peer is never
+      // more than the A + digit ring depths ahead (kPmaxSlots > both), so a
+      // slot is never overwritten before this CTA has read it.
+      if (!(kdbg & 4)) {
+        const int ps = j % kPmaxSlots;
+        const unsigned pph = (unsigned)(j / kPmaxSlots) & 1u;
+        if (threadIdx.x == kScoutWarp0 * 32) mbar_expect_tx(&pmax_full[ps], kCB * 4);
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(
+                         pmax_peer + (uint32_t)((ps * kCB + c) * 4)),
+                     "r"(mx), "r"(pmax_full_peer + (uint32_t)(ps * 8))
+                     : "memory");
+        mbar_wait_cl(&pmax_full[ps], pph);
+        mx = max(mx, pmax[ps * kCB + c]);
+      }
       // bit 0: some column needs a new span; bit 1: some entry is inf / NaN
       const uint32_t mine = (fexp_bits(mx) > Ec ? 1u : 0u) | (mx >= 0x7F800000u ? 2u : 0u);
-      uint32_t any, anybad;
+      uint32_t any = 0, anybad = 0;
+      if (!(kdbg & 4)) {
       asm volatile(
           "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nbar.red.or.pred q, 1, 128, p;\nselp.u32 %0, 1, 0, q;\n}\n"
           : "=r"(any)
@@ -609,6 +644,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
           : "=r"(anybad)
           : "r"(mine & 2u)
           : "memory");
+      }
       const bool fresh = any != 0 || len == span_max || j == 0;
       if (fresh) {
         ++span;
@@ -723,12 +759,12 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const int mflags = meta[2 * sa];
       const bool fresh = (mflags & 1) != 0;
       const int mspan = meta[2 * sa + 1];
-      // 8 values: 16-byte units 4 g + 2 q, + 1 of column c, 128B-swizzled
-      const unsigned char* col = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
+      // 8 values: 16-byte units 2 q, 2 q + 1 of column c's 64 B (this CTA's 16 rows), 64B-swizzled
+      const unsigned char* col = astage + (size_t)sa * kAStageBytes + (size_t)c * 64;
       uint32_t b[8];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const uint4 w = *reinterpret_cast<const uint4*>(col + (((4 * g + 2 * q + u) ^ (c & 7)) << 4));
+        const uint4 w = *reinterpret_cast<const uint4*>(col + (((2 * q + u) ^ ((c >> 1) & 3)) << 4));
         b[4 * u] = w.x;
         b[4 * u + 1] = w.y;
         b[4 * u + 2] = w.z;
@@ -755,7 +791,10 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 2);)
       if (t == 0) d_meta[sd] = fresh ? 1 : 0;
       uint32_t ylo[8], yhi[8];
-      if (__all_sync(0xffffffffu, E >= -78 || E == kZeroE)) {
+      if (kdbg & 2) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) ylo[r] = yhi[r] = 0x80808080u;
+      } else if (__all_sync(0xffffffffu, E >= -78 || E == kZeroE)) {
         const uint32_t kc = (uint32_t)(942 - (E == kZeroE ? 0 : E)) << 20;
 #pragma unroll
         for (int r = 0; r < 8; ++r) fixed48_fast(b[r], kc, ylo[r], yhi[r]);
@@ -847,7 +886,7 @@ gram_f32_ozaki_combine(const double2* __restrict__ partials, int ncta, int n, co
 // ---------------------------------------------------------------------------
 static size_t ozaki32_smem(int astages, int dstages) {
   return 1024 + (size_t)astages * kAStageBytes + (size_t)dstages * kDStageBytes + 1024 + 4 * kCB * 4 + kCB * 4 +
-         4 * kCB * 4 + 64 * 4;
+         4 * kCB * 4 + 64 * 4 + (size_t)kPmaxSlots * kCB * 4 + kPmaxSlots * 8;
 }
 
 // pipeline shape (MPSVD_OZ32_STAGES: "8x3" or "7x4" A x digit slots) and
@@ -862,12 +901,14 @@ static const Oz32Cfg& oz32_cfg() {
   static std::once_flag once;
   std::call_once(once, [] {
     const char* st = getenv("MPSVD_OZ32_STAGES");
-    if (st && st[0] >= '4' && st[0] <= '8' && st[1] == 'x' && st[2] >= '2' && st[2] <= '9') {
+    if (st && st[0] >= '3' && st[0] <= '9' && st[1] == 'x' && st[2] >= '2' && st[2] <= '9') {
       c.astages = st[0] - '0';
       c.dstages = st[2] - '0';
     }
     const char* w = getenv("MPSVD_OZ32_WAIT");
     if (w && w[0] >= '0' && w[0] <= '2') c.wmode = w[0] - '0';
+    const char* d = getenv("MPSVD_OZ32_DBG");
+    if (d) c.wmode |= (atoi(d) & 7) << 8;
   });
   return c;
 }
@@ -898,13 +939,11 @@ using Oz32Kern = void (*)(CUtensorMap, int, long long, long long, int, double2*,
 static Oz32Kern oz32_kernel(const Oz32Cfg& c) {
   const int k = c.astages * 10 + c.dstages;
   switch (k) {
-    case 73: return gram_f32_ozaki<7, 3>;
-    case 46: return gram_f32_ozaki<4, 6>;
-    case 55: return gram_f32_ozaki<5, 5>;
-    case 45: return gram_f32_ozaki<4, 5>;
-    case 37: return gram_f32_ozaki<3, 7>;
-    case 36: return gram_f32_ozaki<3, 6>;
     case 83: return gram_f32_ozaki<8, 3>;
+    case 46: return gram_f32_ozaki<4, 6>;
+    case 85: return gram_f32_ozaki<8, 5>;
+    case 86: return gram_f32_ozaki<8, 6>;
+    case 66: return gram_f32_ozaki<6, 6>;
     default: return gram_f32_ozaki<7, 4>;
   }
 }
@@ -950,10 +989,10 @@ cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kCB};
+  const cuuint32_t box[2] = {(cuuint32_t)kHalfRows, (cuuint32_t)kCB};
   const cuuint32_t estr[2] = {1, 1};
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const Oz32Cfg& cfg = oz32_cfg();
