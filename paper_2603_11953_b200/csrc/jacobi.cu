@@ -627,7 +627,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 constexpr int kUpdateWarps = 12;
 constexpr int kRotWarps = 4;
 
-__device__ int g_jexp = 0;  // experiment switches (tracing only): 1 fake rotations, 2 skip pass 2
+__device__ int g_jexp = 0;  // experiment switches (MPSVD_JACOBI_EXP, timing only): 2 skip the bulk, 4 the priority blocks
 
 // partner of x in `round` (n itself for the bye of an odd n)
 __device__ __forceinline__ int rr_partner(int n, int round, int x) {
@@ -1094,7 +1094,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
             aborted = true;
             break;
           }
-          for (int j = rtid; j < npri; j += NPR) {
+          for (int j = (jexp & 4) ? npri : rtid; j < npri; j += NPR) {  // experiment: skip
             const int w = pri[j];
             update_block(w & 0xffff, w >> 16, rb, pw);
           }
@@ -1129,7 +1129,7 @@ jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol
         const int b = (int)((g + r) & 1);
         const AT* rb = RC(b);
         const int* pw = pwb + b * np;
-        int j = utid;
+        int j = (jexp & 2) ? nnon : utid;  // experiment: skip the bulk update
         if constexpr (sizeof(ST) == sizeof(double))  // fp64 only: the dd pair path spills
           for (; j + n_upd < nnon; j += 2 * n_upd) update_pair(blk[j], blk[j + n_upd], rb, pw);
         for (; j < nnon; j += n_upd) {
