@@ -1711,7 +1711,7 @@ static void* o32_worker(void* arg) {
   const int64_t m = J->m, n = J->n;
   const int g = J->g;
   int64_t* acc = (int64_t*)calloc((size_t)4 * 128 * 128, sizeof(int64_t));
-  int8_t* D = (int8_t*)malloc((size_t)6 * 32 * 128); /* [p][r][c] */
+  int8_t* D = (int8_t*)malloc((size_t)6 * 64 * 128); /* [p][r][c], one 64-row step */
   int E[128];
   int64_t s8[128];
   for (int c = 0; c < 128; ++c) {
@@ -1720,18 +1720,21 @@ static void* o32_worker(void* arg) {
   }
   int span = -1, len = 0;
   const int base = g ? 47 : 40;
-  for (int64_t ch = J->c0; ch <= J->c1; ++ch) {
-    const int end = ch == J->c1;
-    uint32_t b[32][128];
+  /* the device pipeline moves 64-row steps (two chunks; a range with an
+     odd chunk count ends on a half step whose second chunk is zero): span
+     decisions are per step */
+  uint32_t(*b)[128] = (uint32_t(*)[128])malloc(sizeof(uint32_t) * 64 * 128);
+  for (int64_t ch = J->c0;; ch += 2) {
+    const int end = ch >= J->c1;
     uint32_t mx[128];
     int fresh = 0;
     if (!end) {
       for (int c = 0; c < 128; ++c) {
         mx[c] = 0;
-        for (int r = 0; r < 32; ++r) {
+        for (int r = 0; r < 64; ++r) {
           const int64_t row = ch * 32 + r;
           uint32_t v = 0;
-          if (row < m && c < n) memcpy(&v, &J->a[c * m + row], 4);
+          if (ch + r / 32 < J->c1 && row < m && c < n) memcpy(&v, &J->a[c * m + row], 4);
           const uint32_t ab = v & 0x7FFFFFFFu;
           if (ab > mx[c]) mx[c] = ab; /* inf / NaN included: they force a new span */
           if ((ab >> 23) == 0xFFu) {  /* the column is flagged, the entry used as zero */
@@ -1771,20 +1774,20 @@ static void* o32_worker(void* arg) {
       memset(acc, 0, sizeof(int64_t) * 4 * 128 * 128);
     }
     ++len;
-    for (int r = 0; r < 32; ++r)
+    for (int r = 0; r < 64; ++r)
       for (int c = 0; c < 128; ++c) {
         const uint64_t y = o32_fixed48(b[r][c], E[c]);
-        for (int p = 1; p <= 6; ++p) D[((p - 1) * 32 + r) * 128 + c] = (int8_t)(((y >> (8 * (6 - p))) & 0xFFu) ^ 0x80u);
-        const int d4 = D[(3 * 32 + r) * 128 + c];
+        for (int p = 1; p <= 6; ++p) D[((p - 1) * 64 + r) * 128 + c] = (int8_t)(((y >> (8 * (6 - p))) & 0xFFu) ^ 0x80u);
+        const int d4 = D[(3 * 64 + r) * 128 + c];
         s8[c] += d4 * d4;
       }
     for (int k = 0; k < 6; ++k) {
       int p, q, ai;
       o32_product(g, k, &p, &q, &ai);
       int64_t* A = acc + (int64_t)ai * 16384;
-      for (int r = 0; r < 32; ++r) {
-        const int8_t* dp = D + ((p - 1) * 32 + r) * 128;
-        const int8_t* dq = D + ((q - 1) * 32 + r) * 128;
+      for (int r = 0; r < 64; ++r) {
+        const int8_t* dp = D + ((p - 1) * 64 + r) * 128;
+        const int8_t* dq = D + ((q - 1) * 64 + r) * 128;
         for (int i = 0; i < n; ++i) {
           const int64_t x = dp[i];
           if (!x) continue;
@@ -1798,6 +1801,7 @@ static void* o32_worker(void* arg) {
     for (int64_t e = 0; e < 128 * 128; ++e) J->P[e] = (dd){0.0, 0.0};
   free(acc);
   free(D);
+  free(b);
   return NULL;
 }
 

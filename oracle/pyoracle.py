@@ -422,7 +422,7 @@ class Port:
             raise OracleError(st)
         return hi, lo
 
-    def gram_f32_ozaki(self, a, npairs, bounds, span_max=1024, threads=8):
+    def gram_f32_ozaki(self, a, npairs, bounds, span_max=512, threads=8):
         """K1z's binary64 Gram of a binary32 A (csrc/gram_ozaki32.cu) on the
         plan's schedule (npairs, chunk-range bounds), bit for bit."""
         a = _fcol(a, np.float32)

@@ -14,41 +14,44 @@
 // analysis; tests/test_ozaki32.py pins it bitwise to the C restatement
 // (oracle/mpsvd_port.c port_gram_f32_ozaki) and to the reference criterion.
 //
-// Work split. The rows are cut into 32-row chunks (the kind::i8 UMMA K).
-// A launch covers a chunk range; CTA pair p (a cluster of 2) takes an equal
-// share of it and both CTAs stream the same chunks (the second read is an L2
-// hit): CTA g of the pair owns accumulator group g (below). Per CTA:
-//   warp 0       TMA: this CTA's 16 rows x 128 columns of each chunk (8 KB,
-//                64B swizzle) into a ring
-//   warp 1       MMA issue (one thread) + TMEM allocation (4 x 128 columns);
-//                in group 1 the warp also sums the D8 diagonal (below)
+// Work split. The rows are cut into 32-row chunks (the kind::i8 UMMA K) and
+// the pipeline moves 64-row steps (two chunks). A launch covers a chunk
+// range; CTA pair p (a cluster of 2) takes an equal share of it, CTA g of
+// the pair owns accumulator group g (below) and loads, scans and converts
+// chunk 2j + g of step j; the two chunks meet in both CTAs' digit slots.
+// Per CTA:
+//   warp 0       TMA: this CTA's chunk of each step (32 rows x 128 columns,
+//                16 KB, 128B swizzle) into a ring
+//   warp 1       MMA issue (one thread, 12 MMAs per step) + TMEM allocation
+//                (4 x 128 columns); in group 1 the warp also sums the D8
+//                diagonal (below)
 //   warps 2-5    drain (TMEM lane quarter = tile rows): span totals -> dd
-//   warps 6-21   convert, two groups of 8 warps taking alternate chunks;
-//                thread = (column, 8 rows of this CTA's 16-row half): the
-//                6 signed digits of every entry as UMMA operand planes
-//                (K-major, no swizzle) in this CTA's half of a digit slot
+//   warps 6-21   convert, two groups of 8 warps taking alternate steps;
+//                thread = (column, 16 rows): the 6 signed digits of every
+//                entry as UMMA operand planes (K-major, no swizzle) in this
+//                CTA's half (two 16-row K-core groups) of a digit slot
 //   warps 22-25  scouts: lane = column; the column maxima of this CTA's
-//                half, exchanged with the peer's (st.async into its smem,
-//                completing on an mbarrier) -> the chunk's maxima -> the
-//                span decision (one 128-thread barrier-with-reduction) and
-//                the span's exponents, published per chunk by an mbarrier
-//   warp 26      copier: one DSMEM bulk copy moves this CTA's half of each
-//                digit slot into the peer's slot (transaction bytes on the
-//                peer's slot barrier), so the pair converts each chunk once
+//                chunk, exchanged with the peer's (st.async into its smem,
+//                completing on an mbarrier) -> the step's maxima -> the span
+//                decision (one 128-thread barrier-with-reduction) and the
+//                span's exponents, published per step by an mbarrier
+//   warp 26      copier: one DSMEM bulk copy (24 KB) moves this CTA's half
+//                of each digit slot into the peer's slot (transaction bytes
+//                on the peer's slot barrier), so each row is converted once
 // A slot is released by the warps that read it only once every lane's loads
 // have returned (release_a: a plain lane-0 arrive after __syncwarp let the
 // TMA refill a slot under loads still in flight, tools/oz32_harness.cu).
 // Per role one warp polls an mbarrier and the role's other warps wait on a
-// named barrier. The SM's shared-memory bandwidth bounds the kernel: per
-// chunk and CTA the 6 MMAs read 48 KB of operands (int8 M128 N128 K32 alone
-// would need 128 B/clk), plus 8 KB of TMA writes, 8 KB scout and 8 KB
-// converter reads, 12 KB of digit writes and 24 KB of DSMEM copies (each
-// CTA loading and scanning only its own half saved 16 KB per chunk).
+// named barrier. The per-step hand-off chain (TMA -> scouts -> converter
+// group -> DSMEM copy -> MMA -> multicast release) paces the kernel: with
+// MMAs, conversion and the scouts' exchange all skipped (MPSVD_OZ32_DBG) a
+// 32-row step still took ~1,000 cycles, so the step was doubled to 64 rows
+// (c4 Gram 22.5 -> 17.3 ms).
 //
-// Digits. A span is a run of chunks with fixed column exponents E_c. A span
-// starts at the first chunk of the CTA's range, after kSpanMax chunks (the
-// int32 accumulators stay exact), or at a chunk holding an entry with
-// |x| >= 2^E_c; it sets E_c = e(colmax of that chunk) + kHead (frexp
+// Digits. A span is a run of steps with fixed column exponents E_c. A span
+// starts at the first step of the pair's range, after kSpanMax steps (the
+// int32 accumulators stay exact), or at a step holding an entry with
+// |x| >= 2^E_c; it sets E_c = e(colmax of that step) + kHead (frexp
 // exponent, colmax < 2^e), or kZeroE for an all-zero column. Within the span
 // every x of column c becomes X = sign(x) round(|x| 2^(46 - E_c)),
 // |X| < 2^46, written as 6 balanced digits X = sum_p d_p 2^(8 (6 - p)),
@@ -93,12 +96,14 @@ constexpr int kCB = 128;                      // tile columns = UMMA M = N
 constexpr int kPlane = kCB * kKC;             // 4096 bytes per digit plane
 constexpr int kDigits = 6;
 constexpr int kHead = 2;                      // exponent headroom (bits) of a new span
-constexpr int kSpanMax = 1024;                // chunks per span: int32 sums stay exact
+constexpr int kSpanMax = 512;                 // steps (2 chunks) per span: int32 sums stay exact
 constexpr int kZeroE = -160;                  // exponent of an all-zero column
-constexpr int kHalfRows = kKC / 2;            // each CTA of the pair loads and converts 16 rows of a chunk
-constexpr int kAStageBytes = kHalfRows * kCB * 4;  // 8192: 128 columns x 64 B, 64B-swizzled
+// The pipeline moves 64-row steps (two chunks): CTA g of the pair loads,
+// scans and converts chunk 2j + g of step j; the peer's chunk arrives by one
+// DSMEM copy; both CTAs run 12 MMAs per step.
+constexpr int kStep = 2;                          // chunks per step
+constexpr int kAStageBytes = kKC * kCB * 4;       // 16384: this CTA's chunk, 128 columns x 128 B, 128B-swizzled
 constexpr int kPmaxSlots = 16;                // ring of the peer's half-chunk column maxima (> A + digit slots)
-constexpr int kDStageBytes = kDigits * kPlane;
 constexpr int kConvGroups = 2;                // converter groups: group G converts the chunks j = G mod 2
 constexpr int kConvThreads = 256 * kConvGroups;
 constexpr int kConvWarp0 = 6;
@@ -106,7 +111,8 @@ constexpr int kScoutWarp0 = kConvWarp0 + kConvThreads / 32, kScoutWarps = 4;
 constexpr int kWarpCopy = kScoutWarp0 + kScoutWarps;  // DSMEM bulk copies of this CTA's digit half to the peer
 constexpr int kThreads = 32 * (kWarpCopy + 1);
 constexpr int kGroupWarps = 8;                // converter warps per group (one chunk half: 128 columns x 2)
-constexpr int kHalfBytes = kDigits * 2048;    // one CTA's 16-row half of a digit slot: 6 planes x 2 KB
+constexpr int kHalfBytes = kDigits * 2048;    // one 16-row K-core group of a digit slot: 6 planes x 2 KB
+constexpr int kDStageBytes = 2 * kStep * kHalfBytes;  // a step's 4 K-core groups (64 rows) x 6 planes
 constexpr unsigned long long kC48 = 0x808080808080ull;
 
 // products of group g, in issue order: (p, q, accumulator)
@@ -455,7 +461,8 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   OZ32_DBG(const Oz32Dbg dbg = g_oz32_dbg;)
   const long long nch_all = c_end - c_begin;
   const long long c0 = c_begin + nch_all * pair / npairs, c1 = c_begin + nch_all * (pair + 1) / npairs;
-  const int nch = (int)(c1 - c0);
+  const int nchunk = (int)(c1 - c0);
+  const int nch = (nchunk + kStep - 1) / kStep;  // steps; the last may hold one chunk (the other is zero)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kAStages; ++i) {
@@ -496,8 +503,12 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         const int s = j % kAStages;
         mbar_wait_m(&a_empty[s], ((unsigned)(j / kAStages) & 1u) ^ 1u, wmode, 64);
         OZ32_DBG(oz32_stamp(dbg, g, pair, j, 0);)
-        mbar_expect_tx(&a_full[s], kAStageBytes);
-        tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + j) * kKC + g * kHalfRows), 0, &a_full[s]);
+        if (2 * j + g < nchunk) {
+          mbar_expect_tx(&a_full[s], kAStageBytes);
+          tma_load_2d(astage + (size_t)s * kAStageBytes, &amap, (int)((c0 + 2 * j + g) * kKC), 0, &a_full[s]);
+        } else {
+          mbar_arrive(&a_full[s]);  // odd tail: this CTA's chunk of the last step is all zero
+        }
       }
     }
   } else if (warp == 1) {
@@ -526,7 +537,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         for (int k = 0; k < 4; ++k) s8[k] = 0;
       }
       OZ32_DBG(if (lead) oz32_stamp(dbg, g, pair, j, 5);)
-      OZ32_DBG(if (dbg.fresh && lead) dbg.fresh[(c0 + j) * 2 + g] = fresh ? 1 : 0;)
+      OZ32_DBG(if (dbg.fresh && lead) dbg.fresh[(c0 + 2 * j) * 2 + g] = fresh ? 1 : 0;)
       if (fresh) {
         if (span >= 0) {  // close the previous span: the drain may read it
           if (lead) span_last[span & 1] = 0;
@@ -540,15 +551,22 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint64_t sd = dbase + (uint64_t)((uint32_t)s * (kDStageBytes >> 4));
       uint32_t dep = 0;
+      const uint64_t sd1 = sd + (uint64_t)((2 * kHalfBytes) >> 4);  // the step's second chunk (K-core groups 2, 3)
       if (g == 0) {
-        if (!(kdbg & 1)) issue_chunk<0>(tmem, sd, idesc, fresh, lead);
+        if (!(kdbg & 1)) {
+          issue_chunk<0>(tmem, sd, idesc, fresh, lead);
+          issue_chunk<0>(tmem, sd1, idesc, false, lead);
+        }
       } else {
-        if (!(kdbg & 1)) issue_chunk<1>(tmem, sd, idesc, fresh, lead);
+        if (!(kdbg & 1)) {
+          issue_chunk<1>(tmem, sd, idesc, fresh, lead);
+          issue_chunk<1>(tmem, sd1, idesc, false, lead);
+        }
         const unsigned char* p4 = dstage + (size_t)s * kDStageBytes + 3 * 2048 + (lane >> 3) * 128 + (lane & 7) * 16;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < 2 * kStep; ++h) {
             const uint4 w = *reinterpret_cast<const uint4*>(p4 + h * kHalfBytes + k * 512);
             s8[k] = __dp4a((int)w.x, (int)w.x, s8[k]);
             s8[k] = __dp4a((int)w.y, (int)w.y, s8[k]);
@@ -576,10 +594,10 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     // so group 0 sends digits 1-5 only.
     if (lane == 0) {
       const uint32_t peer = (uint32_t)(g ^ 1);
-      const uint32_t src0 = saddr(dstage) + (uint32_t)(g * kHalfBytes);
+      const uint32_t src0 = saddr(dstage) + (uint32_t)(g * 2 * kHalfBytes);  // this CTA's chunk: K-core groups 2g, 2g+1
       const uint32_t dst0 = mapa(src0, peer);
       const uint32_t bar0 = mapa(saddr(d_full), peer);
-      const unsigned bytes = g == 0 ? 5u * 2048u : 6u * 2048u;
+      const unsigned bytes = 2u * kHalfBytes;
       for (int j = 0; j < nch; ++j) {
         const int s = j % kDStages;
         mbar_wait_m(&half_full[s], (unsigned)(j / kDStages) & 1u, wmode, 0);
@@ -602,17 +620,18 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const int sa = j % kAStages;
       if (warp == kScoutWarp0) mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
       nbar_sync(7, 128);
-      const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 64;
-      // max of |x| as bit patterns over this CTA's 16 rows: inf / NaN
-      // (exponent 255) lie above every finite value, so they force a new
+      const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
+      // max of |x| as bit patterns over this CTA's chunk of the step: inf /
+      // NaN (exponent 255) lie above every finite value, so they force a new
       // span and a huge E_c for their column, whose entries the converters
       // then zero and flag
       uint32_t mx = 0;
+      if (2 * j + g < nchunk)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ ((c >> 1) & 3)) << 4));
-        mx = max(mx, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
-      }
+        for (int u = 0; u < 8; ++u) {
+          const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ (c & 7)) << 4));
+          mx = max(mx, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
+        }
       release_a(&a_empty[sa], lane, mx, zmask);
       // exchange the half maxima with the peer (st.async, completing on its
       // pmax_full), then take the chunk maximum: both CTAs of the pair make
@@ -725,26 +744,27 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       if (last) break;
     }
   } else {
-    // ---- converters: thread = (column c, rows 16 g + 8 q .. + 7). Each CTA
-    // of the pair converts its own 16-row half of every chunk into its own
-    // digit slot; the copier moves that half into the peer's slot (one bulk
-    // copy through distributed shared memory), so the pair converts each
-    // chunk once. A slot is full when this CTA's converter warps have
-    // arrived and the peer's half has landed (transaction bytes), and free
-    // when both CTAs' MMAs have read it (multicast commit).
-    // Two groups of 8 warps alternate chunks (group G takes j = G mod 2), so
-    // the per-chunk hand-off latencies of one group overlap the other's work.
+    // ---- converters: thread = (column c, rows 16 q .. 16 q + 15 of this
+    // CTA's chunk of the step). Each CTA converts its own chunk (K-core
+    // groups 2g, 2g+1 of the step's digit slot); the copier moves it into the
+    // peer's slot (one bulk copy through distributed shared memory), so the
+    // pair converts each row once. A slot is full when this CTA's converter
+    // warps have arrived and the peer's chunk has landed (transaction
+    // bytes), and free when both CTAs' MMAs have read it (multicast commit).
+    // Two groups of 8 warps alternate steps (group G takes j = G mod 2), so
+    // the per-step hand-off latencies of one group overlap the other's work.
     const int grp = (threadIdx.x - kConvWarp0 * 32) >> 8;
     const int t = (threadIdx.x - kConvWarp0 * 32) & 255;
-    const int q = t & 1, c = t >> 1;  // lanes 2k, 2k + 1 store adjacent 8-byte pieces (no bank conflicts)
+    const int q = t & 1, c = t >> 1;  // adjacent lanes: the two 16-row K-core groups of a column
     const int gw = t >> 5;            // warp within the group
-    const uint32_t dloc = saddr(dstage) + (uint32_t)(g * kHalfBytes + (c >> 3) * 128 + (c & 7) * 16 + q * 8);
-    const unsigned in_bytes = g == 0 ? 6u * 2048u : 5u * 2048u;  // the peer's half (group 1 gets digits 1-5)
+    const uint32_t dloc = saddr(dstage) + (uint32_t)((2 * g + q) * kHalfBytes + (c >> 3) * 128 + (c & 7) * 16);
+    const unsigned in_bytes = 2u * kHalfBytes;  // the peer's chunk
     int E = kZeroE;
     int span = -1;
     int badc = 0;
     for (int j = grp; j < nch; j += kConvGroups) {
       const int sa = j % kAStages;
+      const bool valid = 2 * j + g < nchunk;
       OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 8);)  // iteration start
       // one warp of the group polls; the group's other warps block on a
       // named barrier (polling by all 16 converter warps took most of the
@@ -759,28 +779,33 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const int mflags = meta[2 * sa];
       const bool fresh = (mflags & 1) != 0;
       const int mspan = meta[2 * sa + 1];
-      // 8 values: 16-byte units 2 q, 2 q + 1 of column c's 64 B (this CTA's 16 rows), 64B-swizzled
-      const unsigned char* col = astage + (size_t)sa * kAStageBytes + (size_t)c * 64;
-      uint32_t b[8];
+      // 16 values: 16-byte units 4 q .. 4 q + 3 of column c's 128 B, 128B-swizzled
+      const unsigned char* col = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
+      uint32_t b[16];
+      if (valid) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const uint4 w = *reinterpret_cast<const uint4*>(col + (((2 * q + u) ^ ((c >> 1) & 3)) << 4));
-        b[4 * u] = w.x;
-        b[4 * u + 1] = w.y;
-        b[4 * u + 2] = w.z;
-        b[4 * u + 3] = w.w;
+        for (int u = 0; u < 4; ++u) {
+          const uint4 w = *reinterpret_cast<const uint4*>(col + (((4 * q + u) ^ (c & 7)) << 4));
+          b[4 * u] = w.x;
+          b[4 * u + 1] = w.y;
+          b[4 * u + 2] = w.z;
+          b[4 * u + 3] = w.w;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) b[r] = 0;  // odd tail: the chunk beyond the range is zero
       }
-      release_a(&a_empty[sa], lane, b[0] | b[4] | (uint32_t)mflags, zmask);
+      release_a(&a_empty[sa], lane, b[0] | b[4] | b[8] | b[12] | (uint32_t)mflags, zmask);
       OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 11);)
-      if (mflags & 2) {  // inf / NaN in this chunk (the scouts saw it): flag the column, use zeros
+      if (mflags & 2) {  // inf / NaN in this step (the scouts saw it): flag the column, use zeros
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 16; ++r)
           if ((b[r] & 0x7FFFFFFFu) >= 0x7F800000u) {
             b[r] = 0;
             badc = 1;
           }
       }
-      if (mspan != span) {  // this group's first chunk of a span (it may have skipped a short one)
+      if (mspan != span) {  // this group's first step of a span (it may have skipped a short one)
         span = mspan;
         E = desc[(span & 1) * kCB + c];
       }
@@ -790,17 +815,17 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       nbar_sync(3 + 2 * grp, 256);
       OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 2);)
       if (t == 0) d_meta[sd] = fresh ? 1 : 0;
-      uint32_t ylo[8], yhi[8];
+      uint32_t ylo[16], yhi[16];
       if (kdbg & 2) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) ylo[r] = yhi[r] = 0x80808080u;
+        for (int r = 0; r < 16; ++r) ylo[r] = yhi[r] = 0x80808080u;
       } else if (__all_sync(0xffffffffu, E >= -78 || E == kZeroE)) {
         const uint32_t kc = (uint32_t)(942 - (E == kZeroE ? 0 : E)) << 20;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) fixed48_fast(b[r], kc, ylo[r], yhi[r]);
+        for (int r = 0; r < 16; ++r) fixed48_fast(b[r], kc, ylo[r], yhi[r]);
       } else {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < 16; ++r) {
           const unsigned long long y = fixed48(b[r], E);
           ylo[r] = (uint32_t)y;
           yhi[r] = (uint32_t)(y >> 32);
@@ -809,9 +834,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       // 4 x 4 byte transposes: plane word w of digit p = byte (6 - p) of Y
       // for rows 4w .. 4w + 3 (8 PRMT for the low word's 4 digits, 4 for the
       // high word's 2, per 4 rows); then XOR 0x80 per byte (balanced digits)
-      uint32_t o[6][2];
+      uint32_t o[6][4];
 #pragma unroll
-      for (int w = 0; w < 2; ++w) {
+      for (int w = 0; w < 4; ++w) {
         const uint32_t a01 = __byte_perm(ylo[4 * w], ylo[4 * w + 1], 0x5140);
         const uint32_t b01 = __byte_perm(ylo[4 * w], ylo[4 * w + 1], 0x7362);
         const uint32_t a23 = __byte_perm(ylo[4 * w + 2], ylo[4 * w + 3], 0x5140);
@@ -827,13 +852,16 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       }
       const uint32_t so = dloc + (uint32_t)(sd * kDStageBytes);
 #pragma unroll
-      for (int p = 1; p <= kDigits; ++p) st_v2(so + (uint32_t)((p - 1) * 2048), o[p - 1][0], o[p - 1][1]);
-      OZ32_DBG(if (dbg.digits) {
-        const long long gc = c0 + j;
+      for (int p = 1; p <= kDigits; ++p)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(so + (uint32_t)((p - 1) * 2048)),
+                     "r"(o[p - 1][0]), "r"(o[p - 1][1]), "r"(o[p - 1][2]), "r"(o[p - 1][3])
+                     : "memory");
+      OZ32_DBG(if (dbg.digits && valid) {
+        const long long gc = c0 + 2 * j + g;
         for (int p = 1; p <= kDigits; ++p)
-          *reinterpret_cast<uint2*>(dbg.digits + ((gc * kDigits + p - 1) * kCB + c) * 32 + 16 * g + 8 * q) =
-              make_uint2(o[p - 1][0], o[p - 1][1]);
-        if (g == 0 && q == 0) dbg.E[gc * kCB + c] = (short)E;
+          *reinterpret_cast<uint4*>(dbg.digits + ((gc * kDigits + p - 1) * kCB + c) * 32 + 16 * q) =
+              make_uint4(o[p - 1][0], o[p - 1][1], o[p - 1][2], o[p - 1][3]);
+        if (q == 0) dbg.E[gc * kCB + c] = (short)E;
       })
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor core / bulk copy
       __syncwarp();
@@ -841,7 +869,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         mbar_arrive(&half_full[sd]);
         OZ32_DBG(if (t == 0) oz32_stamp(dbg, g, pair, j, 3);)
         if (t == 0)
-          mbar_expect_tx(&d_full[sd], in_bytes);  // one of the arrivals also expects the peer's half
+          mbar_expect_tx(&d_full[sd], in_bytes);  // one of the arrivals also expects the peer's chunk
         else
           mbar_arrive(&d_full[sd]);
       }
@@ -889,11 +917,11 @@ static size_t ozaki32_smem(int astages, int dstages) {
          4 * kCB * 4 + 64 * 4 + (size_t)kPmaxSlots * kCB * 4 + kPmaxSlots * 8;
 }
 
-// pipeline shape (MPSVD_OZ32_STAGES: "8x3" or "7x4" A x digit slots) and
+// pipeline shape (MPSVD_OZ32_STAGES: "4x3" (default), "3x3", "6x2", "5x2": A x digit slots) and
 // wait mode (MPSVD_OZ32_WAIT: 0 hinted try_wait, 1 plain try_wait, 2
 // back-off), read once
 struct Oz32Cfg {
-  int astages = 7, dstages = 4;  // A x digit slots (8x3, 7x4, 4x6 measured within 3% on c4)
+  int astages = 4, dstages = 3;  // A slots (16 KB) x digit slots (48 KB, a 64-row step)
   int wmode = 2;
 };
 static const Oz32Cfg& oz32_cfg() {
@@ -939,12 +967,10 @@ using Oz32Kern = void (*)(CUtensorMap, int, long long, long long, int, double2*,
 static Oz32Kern oz32_kernel(const Oz32Cfg& c) {
   const int k = c.astages * 10 + c.dstages;
   switch (k) {
-    case 83: return gram_f32_ozaki<8, 3>;
-    case 46: return gram_f32_ozaki<4, 6>;
-    case 85: return gram_f32_ozaki<8, 5>;
-    case 86: return gram_f32_ozaki<8, 6>;
-    case 66: return gram_f32_ozaki<6, 6>;
-    default: return gram_f32_ozaki<7, 4>;
+    case 33: return gram_f32_ozaki<3, 3>;
+    case 62: return gram_f32_ozaki<6, 2>;
+    case 52: return gram_f32_ozaki<5, 2>;
+    default: return gram_f32_ozaki<4, 3>;
   }
 }
 
@@ -989,10 +1015,10 @@ cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kHalfRows, (cuuint32_t)kCB};
+  const cuuint32_t box[2] = {(cuuint32_t)kKC, (cuuint32_t)kCB};
   const cuuint32_t estr[2] = {1, 1};
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const Oz32Cfg& cfg = oz32_cfg();
@@ -1000,7 +1026,7 @@ cudaError_t launch_gram_ozaki32_range(const float* a, long long lda, long long m
   const size_t smem = ozaki32_smem(cfg.astages, cfg.dstages);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // test hook: chunks per exact span (MPSVD_OZAKI32_SPAN, at most kSpanMax)
+  // test hook: steps (64 rows) per exact span (MPSVD_OZAKI32_SPAN, at most kSpanMax)
   const char* span_env = getenv("MPSVD_OZAKI32_SPAN");
   int span_max = span_env && atoi(span_env) > 0 ? atoi(span_env) : kSpanMax;
   if (span_max > kSpanMax) span_max = kSpanMax;

@@ -106,7 +106,7 @@ def test_gpu_ozaki32_bitwise_vs_restatement(port, monkeypatch, m, n, decades, sp
     oz, npairs, bounds = M.gram32_schedule(m, n)
     assert oz and npairs >= 1 and bounds[0] == 0 and bounds[-1] == (m + 31) // 32
     g = M.gram(a)
-    want = port.gram_f32_ozaki(a, npairs, bounds, span_max=span or 1024, threads=16)
+    want = port.gram_f32_ozaki(a, npairs, bounds, span_max=span or 512, threads=16)
     assert np.array_equal(g, want)
 
 
