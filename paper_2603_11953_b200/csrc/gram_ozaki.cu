@@ -60,7 +60,8 @@ constexpr int kCB = 128;               // columns per digit block = UMMA M
 constexpr int kPlane = kCB * kKC;      // 4096 bytes
 constexpr int kGroups = 6;              // weight-quad x step-range sub-groups (sub_group)
 constexpr int kBad = 1 << 20;          // E sentinel: the column holds inf/NaN
-constexpr int kRing = 24;              // step slots: A plane (4 KB) + B plane (4 KB) each
+constexpr int kCPS = 2;                // chunks per step: one slot, one wait and one release per kCPS MMAs
+constexpr int kRing = 12;              // step slots: kCPS A planes + kCPS B planes (4 KB each)
 constexpr int kThreads = 448;          // warps 0-1 loaders, 2-5 drain, 6-13 MMA issuers (weight k, parity)
 
 // Sub-group i: weight quad q ({12,11,10,9}, {8,7,6,5}, {4,3,2}: w_hi and
@@ -148,6 +149,15 @@ __device__ __forceinline__ void bulk_g2s_lead(void* dst, const void* src, unsign
   asm volatile(
       "{\n.reg .pred l;\nsetp.ne.b32 l, %4, 0;\n"
       "@l mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+      "@l cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar)), "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_nox_lead(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                  uint32_t lead) {
+  asm volatile(
+      "{\n.reg .pred l;\nsetp.ne.b32 l, %4, 0;\n"
       "@l cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
           saddr(dst)),
       "l"(src), "r"(bytes), "r"(saddr(bar)), "r"(lead)
@@ -348,8 +358,8 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
   using namespace oz;
   extern __shared__ __align__(1024) unsigned char smem_oz[];
   unsigned char* aring = smem_oz;
-  unsigned char* bring = aring + kRing * kPlane;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kRing * kPlane);
+  unsigned char* bring = aring + kRing * kCPS * kPlane;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + kRing * kCPS * kPlane);
   uint64_t* a_full = bars;  // one full barrier per step slot (A and B plane)
   uint64_t* a_empty = a_full + kRing;
   uint64_t* b_empty = a_empty + kRing;
@@ -422,24 +432,31 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
       const unsigned par = (unsigned)warp;
       unsigned t = 0;
       unsigned long long tw = 0;
-      for (long long ch = c0; ch < c1; ++ch) {
-        const unsigned char* chunk = digits + (ch * kL) * ncb2 * (long long)kPlane;
-        for (int j = 0; j < L; ++j, ++t) {
-          if ((t & 1u) != par) continue;
-          const int p = pa - npre + j;
-          const int sl = (int)(t % kRing);
-          const unsigned ph = ((t / kRing) & 1u) ^ 1u;
-          const unsigned long long t0 = prof ? clock64() : 0;
-          mbar_wait(&a_empty[sl], ph);
-          mbar_wait(&b_empty[sl], ph);
-          if (prof) tw += clock64() - t0;
-          if (p < pa)
-            bulk_g2s_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
-                          &a_full[sl], lead);
-          else
-            bulk_g2s2_lead(aring + (size_t)sl * kPlane, chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane,
-                           bring + (size_t)sl * kPlane,
-                           chunk + ((long long)(whi - p - 1) * ncb2 + ij.y) * kPlane, kPlane, &a_full[sl], lead);
+      // chunks grouped by kCPS inside each span (the issuers' grouping)
+      for (long long cs = c0; cs < c1; cs += span) {
+        const long long ce = cs + span < c1 ? cs + span : c1;
+        for (long long ch = cs; ch < ce; ch += kCPS) {
+          const int nc = (int)(ce - ch < kCPS ? ce - ch : kCPS);
+          for (int j = 0; j < L; ++j, ++t) {
+            if ((t & 1u) != par) continue;
+            const int p = pa - npre + j;
+            const int sl = (int)(t % kRing);
+            const unsigned ph = ((t / kRing) & 1u) ^ 1u;
+            const unsigned long long t0 = prof ? clock64() : 0;
+            mbar_wait(&a_empty[sl], ph);
+            mbar_wait(&b_empty[sl], ph);
+            if (prof) tw += clock64() - t0;
+            const unsigned bytes = (unsigned)nc * kPlane * (p < pa ? 1u : 2u);
+            if (lead) mbar_expect_tx(&a_full[sl], bytes);
+            for (int i = 0; i < nc; ++i) {
+              const unsigned char* chunk = digits + ((ch + i) * kL) * ncb2 * (long long)kPlane;
+              bulk_g2s_nox_lead(aring + ((size_t)sl * kCPS + i) * kPlane,
+                                chunk + ((long long)(p - 1) * ncb2 + ij.x) * kPlane, kPlane, &a_full[sl], lead);
+              if (p >= pa)
+                bulk_g2s_nox_lead(bring + ((size_t)sl * kCPS + i) * kPlane,
+                                  chunk + ((long long)(whi - p - 1) * ncb2 + ij.y) * kPlane, kPlane, &a_full[sl], lead);
+            }
+          }
         }
       }
       if (prof && lead && warp == 0) atomicAdd(&g_oz_prof[g][4], tw);
@@ -466,7 +483,8 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         long long ce = ch + span;
         if (ce > c1) ce = c1;
-        for (; ch < ce; ++ch) {
+        for (; ch < ce; ch += kCPS) {
+          const int nc = (int)(ce - ch < kCPS ? ce - ch : kCPS);
           for (int j = 0; j < L; ++j, ++t) {
             if ((t & 1u) != par) continue;
             const int p = pa - npre + j;
@@ -477,8 +495,9 @@ gram_dd_ozaki(const unsigned char* __restrict__ digits, int ncb2, const int* __r
             if (has_a && k > 0 && !(dbg & 1)) mbar_wait(&a_full[sla], ((t - (unsigned)k) / kRing) & 1u);
             if (p >= pa && p - k >= 1) {
               asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-              umma_i8_lead(dacc, kdesc(abase + (uint32_t)sla * kPlane), kdesc(bbase + (uint32_t)sl * kPlane), idesc,
-                           1u, lead && !(dbg & 2));
+              for (int i = 0; i < nc; ++i)  // the group's chunks: the same weight, summed exactly
+                umma_i8_lead(dacc, kdesc(abase + ((uint32_t)sla * kCPS + i) * kPlane),
+                             kdesc(bbase + ((uint32_t)sl * kCPS + i) * kPlane), idesc, 1u, lead && !(dbg & 2));
             }
             if (!(dbg & 8)) {
               if (has_a) umma_commit_lead(&a_empty[sla], lead);
@@ -613,7 +632,7 @@ void ozaki_tiles(int n, std::vector<int2>& tiles) {
 }
 
 static size_t ozaki_smem() {
-  return (size_t)oz::kRing * 2 * oz::kPlane + 3 * oz::kRing * 8 + 16 + 16 + 128 * 4 + 64;
+  return (size_t)oz::kRing * 2 * oz::kCPS * oz::kPlane + 3 * oz::kRing * 8 + 16 + 16 + 128 * 4 + 64;
 }
 
 cudaError_t launch_gram_ozaki(const double* a, long long lda, long long m, int n, const int* scb_dev,
