@@ -60,8 +60,12 @@ constexpr int kCB = 128;               // columns per digit block = UMMA M
 constexpr int kPlane = kCB * kKC;      // 4096 bytes
 constexpr int kGroups = 6;              // weight-quad x step-range sub-groups (sub_group)
 constexpr int kBad = 1 << 20;          // E sentinel: the column holds inf/NaN
-constexpr int kCPS = 2;                // chunks per step: one slot, one wait and one release per kCPS MMAs
-constexpr int kRing = 12;              // step slots: kCPS A planes + kCPS B planes (4 KB each)
+// Chunks per step: one slot, one wait and one release per kCPS MMAs (the
+// per-MMA wait/commit chain bounded the first version: c3 Gram 25.5 ms at
+// kCPS = 1, 20.6 at 2, 19.8 at 4; the issuers look back up to 3 slots, so
+// the 192 KB ring keeps kRing = 6 slots at kCPS = 4)
+constexpr int kCPS = 4;
+constexpr int kRing = 6;               // step slots: kCPS A planes + kCPS B planes (4 KB each)
 constexpr int kThreads = 448;          // warps 0-1 loaders, 2-5 drain, 6-13 MMA issuers (weight k, parity)
 
 // Sub-group i: weight quad q ({12,11,10,9}, {8,7,6,5}, {4,3,2}: w_hi and
