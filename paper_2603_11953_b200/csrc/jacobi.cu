@@ -706,8 +706,8 @@ __device__ void replay_consumer(const ST* __restrict__ rot_log, int n, DevStatus
   }
 }
 
-template <typename ST>
-__global__ void __launch_bounds__(512, 1)
+template <typename ST, int kNT = 512>
+__global__ void __launch_bounds__(kNT, 1)
 jacobi_smem(ST* __restrict__ a_glob, ST* __restrict__ rot_log, int n, double tol, int max_sweeps,
             DevStatus* __restrict__ status, ST* __restrict__ v_out, int cons_rows) {
   using A_ = Arith<ST>;
@@ -1457,7 +1457,10 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
                            (size_t)np * (8 * sizeof(typename Arith<ST>::AT) + 2 * sizeof(int)) +
                            ((size_t)np * (np + 1) / 2 + 2 * np) * sizeof(int);
   if (np <= 64 && smem_pipe <= smem_limit) {  // warp-specialised single-CTA solver
-    auto k = jacobi_smem<ST>;
+    // fp64 with 64 < n: 24 warps (8 more update warps; the n = 128 round is
+    // bound by the bulk update, 5 blocks per update thread with 16 warps)
+    const bool wide = sizeof(ST) == sizeof(double) && n > 64 && getenv("MPSVD_JACOBI_NARROW") == nullptr;
+    auto k = wide ? jacobi_smem<ST, 768> : jacobi_smem<ST, 512>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pipe);
     // 16 warps (__launch_bounds__(512): 128 registers, no spills); fewer via
     // MPSVD_JACOBI_WARPS (a multiple of 4, for experiments)
@@ -1465,7 +1468,7 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
       const int w = getenv("MPSVD_JACOBI_WARPS") ? atoi(getenv("MPSVD_JACOBI_WARPS")) : 16;
       return (w >= 8 && w <= 16 && w % 4 == 0) ? w : 16;
     }();
-    const int threads = 32 * warps_env;
+    const int threads = wide ? 768 : 32 * warps_env;
     static const bool trace = getenv("MPSVD_JACOBI_TRACE") != nullptr;
     unsigned long long* tbuf = nullptr;
     if (trace) {
