@@ -507,11 +507,44 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           A_::st(dnext + 3 * (w & 0xffff) + 2, v);
         }
       };
-      for (long long idx = gtid; idx < nblk; idx += gstride) {
-        int bb = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+      // The thread's blocks are processed with the next off-diagonal block's
+      // four entries already loaded (its L2 round trip overlaps this block's
+      // rotations); blocks of a round touch disjoint entries, so the early
+      // loads see the round's inputs. Same arithmetic per block.
+      auto decode = [&](long long idx, int& aa, int& bb) {
+        bb = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
         while ((long long)bb * (bb + 1) / 2 > idx) --bb;
         while ((long long)(bb + 1) * (bb + 2) / 2 <= idx) ++bb;
-        const int aa = (int)(idx - (long long)bb * (bb + 1) / 2);
+        aa = (int)(idx - (long long)bb * (bb + 1) / 2);
+      };
+      // entries of an off-diagonal block (zero outside an odd n's bye)
+      auto load_block = [&](int aa, int bb, AT (&x)[2][2]) {
+        const int wa = pw[aa], wb = pw[bb];
+        const int rows[2] = {wa & 0x7fff, (wa >> 15) & 0x7fff}, cols[2] = {wb & 0x7fff, (wb >> 15) & 0x7fff};
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            x[u][v] = (rows[u] < n && cols[v] < n) ? LD(CEg(rows[u], cols[v])) : A_::zero();
+      };
+      AT xn[2][2];
+      int an = 0, bn = 0;
+      long long idx = gtid;
+      if (idx < nblk) {
+        decode(idx, an, bn);
+        if (an != bn) load_block(an, bn, xn);
+      }
+      for (; idx < nblk; idx += gstride) {
+        const int aa = an, bb = bn;
+        AT x[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) x[u][v] = xn[u][v];
+        if (idx + gstride < nblk) {
+          decode(idx + gstride, an, bn);
+          if (an != bn) load_block(an, bn, xn);
+        }
         const int wa = pw[aa];
         const int p0 = wa & 0x7fff, q0 = (wa >> 15) & 0x7fff;
         const bool acta = (wa >> 30) & 1;
@@ -544,14 +577,10 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         const int rows[2] = {p0, q0}, cols[2] = {k0, l0};
         const int nr = q0 < n ? 2 : 1, nc = l0 < n ? 2 : 1;
         ST* e[2][2];
-        AT x[2][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            e[u][v] = CEg(rows[u], cols[v]);
-            x[u][v] = (u < nr && v < nc) ? LD(e[u][v]) : A_::zero();
-          }
+          for (int v = 0; v < 2; ++v) e[u][v] = CEg(rows[u], cols[v]);
         if (actb) {
           const AT cb = rc[bb], sb = rsn[bb];
 #pragma unroll
