@@ -185,7 +185,8 @@ __device__ unsigned long long* g_jtrace = nullptr;
 template <typename ST, bool kSmem>
 __global__ void __launch_bounds__(kSmem ? kJacobiThreads : kJacobiGridThreads)
 jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict__ rot_log, int n,
-              double tol, int max_sweeps, DevStatus* __restrict__ status) {
+              double tol, int max_sweeps, DevStatus* __restrict__ status, ST* __restrict__ v_out = nullptr,
+              int vrows = 0) {
   using A_ = Arith<ST>;
   using AT = typename A_::AT;
   extern __shared__ __align__(16) unsigned char jsm[];
@@ -211,6 +212,12 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   int* blk = pw + np;                            // aa | bb << 16 (smem variant)
   int* nsl = pw + np;                            // multi-CTA: next-round slot | (player is q) << 16
   int* npart = nsl + 2 * np;                     // multi-CTA: next-round partner (n for the bye)
+  // fused V (multi-CTA, vrows > 0): this CTA's rows [v0, v0 + vrows) of V,
+  // rotated by every round right after the round's rotations are known
+  // (rows of V never mix; the separate replay streamed the whole rotation
+  // log through every CTA: 259 ms of the c5 eigen phase)
+  ST* vsm = reinterpret_cast<ST*>((reinterpret_cast<uintptr_t>(npart + 2 * np) + 15) & ~(uintptr_t)15);
+  const int v0 = blockIdx.x * vrows, vn = vrows > 0 ? max(0, min(vrows, n - v0)) : 0;
   __shared__ int s_flag;
   __shared__ int w_cnt[32], w_bad[32];
   __shared__ double w_worst[32];
@@ -235,6 +242,17 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
     }
   }
   if (tid == 0) s_flag = 0x7fffffff;
+  for (int e = tid; e < vn * n; e += blockDim.x) {
+    const int rr = e / n, cc = e - rr * n;
+    A_::st(vsm + e, (v0 + rr == cc) ? A_::one() : A_::zero());
+  }
+  auto write_v = [&]() {
+    __syncthreads();
+    for (int e = tid; e < vn * n; e += blockDim.x) {
+      const int rr = e / n, cc = e - rr * n;
+      v_out[(size_t)cc * n + v0 + rr] = vsm[e];
+    }
+  };
   __syncthreads();
 
   // initial positive-definiteness check (jacobi.cpp:200-201): every CTA
@@ -250,6 +268,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
       status->sweeps = 0;
       status->rotations = 0;
     }
+    if (vn) write_v();
     return;
   }
 
@@ -404,6 +423,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           status->sweeps = sweeps;
           status->rotations = rotations;
         }
+        if (vn) write_v();
         return;
       }
       rot_sweep += cnt;
@@ -491,6 +511,22 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         }
         __syncthreads();
         continue;
+      }
+      // fused V: round r's rotations on this CTA's rows of V (the replay's
+      // arithmetic: identity rotations skipped, rot_lo / rot_hi per pair)
+      if (vn) {
+        const int items = vn * np;
+        for (int w = tid; w < items; w += bs) {
+          const int rr = w / np, k = w - rr * np;
+          const AT c = rc[k], sn = rsn[k];
+          if (A_::is_identity(c, sn)) continue;
+          const int wk = pw[k];
+          const int pp = wk & 0x7fff, qq = (wk >> 15) & 0x7fff;
+          ST* row = vsm + (size_t)rr * n;
+          const AT t1 = A_::lds(row + pp), t2 = A_::lds(row + qq);
+          A_::st(row + pp, A_::rot_lo(c, sn, t1, t2));
+          A_::st(row + qq, A_::rot_hi(c, sn, t1, t2));
+        }
       }
       // multi-CTA variant: every block is visited so that the entries the
       // next round's rotations read are published to the diag buffer.
@@ -624,6 +660,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
     __syncthreads();
     for (long long e = tid; e < (long long)n * n; e += bs) a_glob[e] = a[(e / n) * lda + e % n];
   }
+  if (vn) write_v();
   if (blockIdx.x == 0 && tid == 0) {
     status->status = converged ? kOk : kNoConvergence;
     status->index = converged ? 0 : max_sweeps;
@@ -1547,22 +1584,33 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   if (smem_a + smem_rot <= smem_limit) {
     auto k = jacobi_kernel<ST, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_a + smem_rot));
-    k<<<1, kJacobiThreads, smem_a + smem_rot, st>>>(a, d, lg, n, tol, max_sweeps, status);
+    k<<<1, kJacobiThreads, smem_a + smem_rot, st>>>(a, d, lg, n, tol, max_sweeps, status, nullptr, 0);
     return cudaGetLastError();
   }
   auto k = jacobi_kernel<ST, false>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rot);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kJacobiGridThreads, smem_rot);
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const long long nblk = (long long)np * (np + 1) / 2;
   long long want = (nblk + kJacobiGridThreads - 1) / kJacobiGridThreads;
   long long grid = (long long)sm_count;  // one CTA per SM (see kJacobiGridThreads)
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
+  // fused V: each CTA keeps ceil(n / grid) rows of V in shared memory
+  // (MPSVD_JACOBI_REPLAY=1 keeps the separate replay)
+  int vrows = (int)((n + grid - 1) / grid);
+  size_t smem_grid = smem_rot + 16 + (size_t)vrows * n * sizeof(ST);  // + alignment of the V rows
+  // fused only on a full grid: with few CTAs (n <= ~400) the extra work per
+  // round costs more than the short separate replay (c3: 9.0 vs 8.1 ms)
+  if (smem_grid > 200 * 1024 || 2 * grid < sm_count || getenv("MPSVD_JACOBI_REPLAY") != nullptr) {
+    vrows = 0;
+    smem_grid = smem_rot;
+  }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_grid);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kJacobiGridThreads, smem_grid);
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int nn = n, ms = max_sweeps;
   double tl = tol;
-  void* args[] = {&a, &d, &lg, &nn, &tl, &ms, &status};
+  ST* vout = (ST*)ws.v;
+  void* args[] = {&a, &d, &lg, &nn, &tl, &ms, &status, &vout, &vrows};
   static const bool trace = getenv("MPSVD_JACOBI_TRACE") != nullptr;
   unsigned long long* tbuf = nullptr;
   if (trace) {
@@ -1571,7 +1619,8 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
     cudaMemcpyToSymbol(g_jtrace, &tbuf, sizeof(tbuf));
   }
   const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(kJacobiGridThreads), args,
-                                                     smem_rot, st);
+                                                     smem_grid, st);
+  if (le == cudaSuccess && vrows > 0 && fused_replay) *fused_replay = true;
   if (trace) {
     unsigned long long h[64 * 16];
     cudaStreamSynchronize(st);
