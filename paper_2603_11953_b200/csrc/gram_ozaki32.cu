@@ -448,7 +448,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
   uint32_t* pmax = reinterpret_cast<uint32_t*>(dsq + 2 * kCB);  // [kPmaxSlots][128] the peer half's column maxima
   uint64_t* pmax_full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(pmax + kPmaxSlots * kCB) + 7) & ~(uintptr_t)7);  // [kPmaxSlots]
-  static_assert(kPmaxSlots > kAStages + kDStages, "the peer's maxima ring must outrun both pipelines");
+  static_assert(kPmaxSlots > kAStages + kDStages + 1, "the peer's maxima ring must outrun both pipelines");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = blockIdx.x >> 1, g = blockIdx.x & 1;
@@ -616,37 +616,49 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     const uint32_t pmax_full_peer = mapa(saddr(pmax_full), (uint32_t)(g ^ 1));
     int Ec = kZeroE;
     int span = -1, len = 0;
-    for (int j = 0; j < nch; ++j) {
-      const int sa = j % kAStages;
-      if (warp == kScoutWarp0) mbar_wait_m(&a_full[sa], (unsigned)(j / kAStages) & 1u, wmode, 0);
+    // the local part of step jj: this CTA's column maxima, the A slot
+    // released, the value sent to the peer. It runs one step ahead of the
+    // decision, so the exchange's round trip overlaps the next step's scan.
+    auto scan = [&](int jj) -> uint32_t {
+      const int sa = jj % kAStages;
+      if (warp == kScoutWarp0) mbar_wait_m(&a_full[sa], (unsigned)(jj / kAStages) & 1u, wmode, 0);
       nbar_sync(7, 128);
       const unsigned char* colp = astage + (size_t)sa * kAStageBytes + (size_t)c * 128;
       // max of |x| as bit patterns over this CTA's chunk of the step: inf /
       // NaN (exponent 255) lie above every finite value, so they force a new
       // span and a huge E_c for their column, whose entries the converters
       // then zero and flag
-      uint32_t mx = 0;
-      if (2 * j + g < nchunk)
+      uint32_t m = 0;
+      if (2 * jj + g < nchunk)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint4 w = *reinterpret_cast<const uint4*>(colp + ((u ^ (c & 7)) << 4));
-          mx = max(mx, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
+          m = max(m, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
         }
-      release_a(&a_empty[sa], lane, mx, zmask);
-      // exchange the half maxima with the peer (st.async, completing on its
-      // pmax_full), then take the chunk maximum: both CTAs of the pair make
-      // the same span decisions from the same 32 rows. The peer is never
-      // more than the A + digit ring depths ahead (kPmaxSlots > both), so a
-      // slot is never overwritten before this CTA has read it.
+      release_a(&a_empty[sa], lane, m, zmask);
+      // send the half maxima to the peer (st.async, completing on its
+      // pmax_full): both CTAs of the pair decide from the same 64 rows. The
+      // peer is never more than the A + digit ring depths (+1) ahead
+      // (kPmaxSlots exceeds that), so a slot is never overwritten before
+      // this CTA has read it.
       if (!(kdbg & 4)) {
-        const int ps = j % kPmaxSlots;
-        const unsigned pph = (unsigned)(j / kPmaxSlots) & 1u;
+        const int ps = jj % kPmaxSlots;
         if (threadIdx.x == kScoutWarp0 * 32) mbar_expect_tx(&pmax_full[ps], kCB * 4);
         asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(
                          pmax_peer + (uint32_t)((ps * kCB + c) * 4)),
-                     "r"(mx), "r"(pmax_full_peer + (uint32_t)(ps * 8))
+                     "r"(m), "r"(pmax_full_peer + (uint32_t)(ps * 8))
                      : "memory");
-        mbar_wait_cl(&pmax_full[ps], pph);
+      }
+      return m;
+    };
+    uint32_t mloc = nch > 0 ? scan(0) : 0u;
+    for (int j = 0; j < nch; ++j) {
+      const int sa = j % kAStages;
+      uint32_t mx = mloc;
+      if (j + 1 < nch) mloc = scan(j + 1);
+      if (!(kdbg & 4)) {
+        const int ps = j % kPmaxSlots;
+        mbar_wait_cl(&pmax_full[ps], (unsigned)(j / kPmaxSlots) & 1u);
         mx = max(mx, pmax[ps * kCB + c]);
       }
       // bit 0: some column needs a new span; bit 1: some entry is inf / NaN
