@@ -767,7 +767,10 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     // the per-step hand-off latencies of one group overlap the other's work.
     const int grp = (threadIdx.x - kConvWarp0 * 32) >> 8;
     const int t = (threadIdx.x - kConvWarp0 * 32) & 255;
-    const int q = t & 1, c = t >> 1;  // adjacent lanes: the two 16-row K-core groups of a column
+    // warp w of the group: K-core group q = w & 1, columns 32 (w >> 1) ..
+    // + 31, so a warp's 16-byte digit stores are 512 contiguous bytes and its
+    // A loads hit 8 distinct 16-byte units per 8 lanes (no bank conflicts)
+    const int q = (t >> 5) & 1, c = (t & 31) + 32 * (t >> 6);
     const int gw = t >> 5;            // warp within the group
     const uint32_t dloc = saddr(dstage) + (uint32_t)((2 * g + q) * kHalfBytes + (c >> 3) * 128 + (c & 7) * 16);
     const unsigned in_bytes = 2u * kHalfBytes;  // the peer's chunk
