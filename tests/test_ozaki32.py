@@ -169,6 +169,4 @@ def test_gpu_ozaki32_deterministic_at_scale(monkeypatch):
     g0 = M.gram(a)
     for _ in range(3):
         assert np.array_equal(M.gram(a), g0)
-    ex = _exact(a[: 1 << 16])  # the bound on a slice: the full exact Gram is costly on the host
     assert np.all(np.isfinite(g0)) and np.array_equal(g0, g0.T)
-    assert ex.shape == (128, 128)
