@@ -310,20 +310,21 @@ static int jacobi_rr_f64(double* A, double* V, int64_t n, double tol, int max_sw
           if (worst < ratio) worst = ratio;
         }
         if (fabs(aij) <= thresh) continue;
-        const double x = ajj - aii, y = 2.0 * aij, ax = fabs(x);
-        const double big = fmax(ax, fabs(y));
-        double r;
-        if (big < 0x1p500 && big > 0x1p-500) {
-          r = sqrt(fma(x, x, y * y));
-        } else {
+        double x = ajj - aii, y = 2.0 * aij;
+        const int xzero = x == 0.0, xpos = x > 0.0;
+        const double big = fmax(fabs(x), fabs(y));
+        if (!(big < 0x1p500 && big > 0x1p-500)) {
           int e;
           frexp(big, &e);
-          const double xs = ldexp(x, -e), ys = ldexp(y, -e);
-          r = ldexp(sqrt(fma(xs, xs, ys * ys)), e);
+          x = ldexp(x, -e);
+          y = ldexp(y, -e);
         }
+        const double ax = fabs(x);
+        const double q = fma(x, x, y * y);
+        const double r = sqrt(q), iq = 1.0 / q;
         const double den = ax + r;
-        const double t = x == 0.0 ? 1.0 : (x > 0.0 ? y : -y) / den;
-        const double c = sqrt(den / (2.0 * r));
+        const double t = xzero ? 1.0 : (xpos ? y : -y) / den;
+        const double c = sqrt(fma(0.5, ax * (r * iq), 0.5));
         C[k] = c;
         S[k] = c * t;
         T[k] = t;
@@ -1302,22 +1303,37 @@ static int dd_make_rotation_dev(dd aii, dd ajj, dd aij, double tol, double* wors
   r->s = dd_from(0.0);
   r->t = dd_from(0.0);
   if (fabs(aij.hi) <= thresh) return 0;
-  const dd x = dd_sub(ajj, aii), y = dd_scale2(aij), ax = dd_abs(x);
-  const double big = fmax(ax.hi, fabs(y.hi));
-  dd rr;
-  if (big < 0x1p250 && big > 0x1p-250) {
-    rr = dd_sqrt(dd_add(dd_mul(x, x), dd_mul(y, y)));
-  } else {
+  dd x = dd_sub(ajj, aii), y = dd_scale2(aij);
+  const int xzero = x.hi == 0.0, xpos = x.hi > 0.0;
+  const double big = fmax(fabs(x.hi), fabs(y.hi));
+  if (!(big < 0x1p250 && big > 0x1p-250)) {
     int e;
     frexp(big, &e);
-    const dd xs = {ldexp(x.hi, -e), ldexp(x.lo, -e)};
-    const dd ys = {ldexp(y.hi, -e), ldexp(y.lo, -e)};
-    const dd rs = dd_sqrt(dd_add(dd_mul(xs, xs), dd_mul(ys, ys)));
-    rr = (dd){ldexp(rs.hi, e), ldexp(rs.lo, e)};
+    x = (dd){ldexp(x.hi, -e), ldexp(x.lo, -e)};
+    y = (dd){ldexp(y.hi, -e), ldexp(y.lo, -e)};
   }
+  const dd ax = dd_abs(x);
+  const dd q = dd_add(dd_mul(x, x), dd_mul(y, y));
+  const double r0 = sqrt(q.hi), iq = 1.0 / q.hi;
+  const double ir = r0 * iq;
+  const double id = 1.0 / (ax.hi + r0);
+  const dd er = dd_sub(q, two_prod(r0, r0));
+  const dd rr = quick_two_sum(r0, er.hi * (0.5 * ir));
   const dd den = dd_add(ax, rr);
-  const dd t = x.hi == 0.0 ? dd_from(1.0) : dd_div(x.hi > 0.0 ? y : dd_neg(y), den);
-  const dd c = dd_sqrt(dd_div(den, dd_scale2(rr)));
+  dd t = dd_from(1.0);
+  if (!xzero) {
+    const dd ys = xpos ? y : dd_neg(y);
+    const double t0 = ys.hi * id;
+    const dd et = dd_sub(ys, dd_mul(dd_from(t0), den));
+    t = quick_two_sum(t0, et.hi * id);
+  }
+  const double u0 = ax.hi * ir;
+  const dd eu = dd_sub(ax, dd_mul(dd_from(u0), rr));
+  const dd u = quick_two_sum(u0, eu.hi * ir);
+  const dd c2 = dd_add(dd_from(0.5), (dd){0.5 * u.hi, 0.5 * u.lo});
+  const double c0 = sqrt(c2.hi), ic2 = 1.0 / c2.hi;
+  const dd ec = dd_sub(c2, two_prod(c0, c0));
+  const dd c = quick_two_sum(c0, ec.hi * (0.5 * (c0 * ic2)));
   r->c = c;
   r->s = dd_mul(c, t);
   r->t = t;

@@ -67,29 +67,39 @@ struct Arith<double> {
   }
   // normalised off-diagonal |a_pq| / sqrt(a_pp a_qq) (NoConvergence payload)
   static __device__ __forceinline__ double ratio(AT app, AT aqq, AT apq) { return fabs(apq) / sqrt(app * aqq); }
-  static __device__ __noinline__ double scaled_hypot(double x, double y, double big) {
-    int e;  // exact power-of-two rescaling keeps x^2 + y^2 finite and normal
-    frexp(big, &e);
-    const double xs = ldexp(x, -e), ys = ldexp(y, -e);
-    return ldexp(sqrt(fma(xs, xs, ys * ys)), e);
-  }
   // Annihilating rotation (jacobi.cpp:219-241). With x = a_qq - a_pp,
-  // y = 2 a_pq, r = sqrt(x^2 + y^2):
-  //   t = sign(x) y / (|x| + r)   (= sign(zeta)/(|zeta| + hypot(1, zeta))),
-  //   c = sqrt((|x| + r) / (2 r)) (= 1/sqrt(1 + t^2)),   s = c t,
-  // t = +1 at x == 0 (the reference's sign(0) = +1): three dependent
-  // square-root/division steps instead of five. Diagonal: a_pp - t a_pq,
-  // a_qq + t a_pq (fused).
+  // y = 2 a_pq, q = x^2 + y^2, r = sqrt(q):
+  //   t = sign(x) y / (|x| + r)        (= sign(zeta)/(|zeta| + hypot(1, zeta))),
+  //   c = sqrt(1/2 + 1/2 |x| / r)      (= 1/sqrt(1 + t^2)),   s = c t,
+  // t = +1 at x == 0 (the reference's sign(0) = +1). 1/r is formed as
+  // r (1/q) with the division next to the square root (both need only q), so
+  // the dependent chain holds two long operations (sqrt|div, then div|sqrt)
+  // instead of the reference's five; x and y are scaled by an exact power of
+  // two when q would leave the normal range (t, c, s are scale-free).
+  // Diagonal: a_pp - t a_pq, a_qq + t a_pq (fused).
   static __device__ __forceinline__ void rotate(AT app, AT aqq, AT apq, AT& c, AT& s, AT& npp, AT& nqq) {
-    const double x = aqq - app, y = 2.0 * apq, ax = fabs(x);
-    const double big = fmax(ax, fabs(y));
-    const double r = (big < 0x1p500 && big > 0x1p-500) ? sqrt(fma(x, x, y * y)) : scaled_hypot(x, y, big);
+    double x = aqq - app, y = 2.0 * apq;
+    const bool xzero = x == 0.0, xpos = x > 0.0;  // before any rescaling (it may flush a tiny x)
+    const double big = fmax(fabs(x), fabs(y));
+    if (!(big < 0x1p500 && big > 0x1p-500)) {
+      const double2 xy = rescale(x, y, big);
+      x = xy.x;
+      y = xy.y;
+    }
+    const double ax = fabs(x);
+    const double q = fma(x, x, y * y);
+    const double r = sqrt(q), iq = 1.0 / q;
     const double den = ax + r;
-    const double t = x == 0.0 ? 1.0 : (x > 0.0 ? y : -y) / den;
-    c = sqrt(den / (2.0 * r));
+    const double t = xzero ? 1.0 : (xpos ? y : -y) / den;
+    c = sqrt(fma(0.5, ax * (r * iq), 0.5));
     s = c * t;
     npp = fma(-t, apq, app);
     nqq = fma(t, apq, aqq);
+  }
+  static __device__ __noinline__ double2 rescale(double x, double y, double big) {
+    int e;  // exact power-of-two rescaling keeps x^2 + y^2 finite and normal
+    frexp(big, &e);
+    return make_double2(ldexp(x, -e), ldexp(y, -e));
   }
 };
 
@@ -128,22 +138,53 @@ struct Arith<double2> {
   static __device__ __forceinline__ double ratio(AT app, AT aqq, AT apq) {
     return fabs(apq.hi) / sqrt(app.hi * aqq.hi);
   }
-  static __device__ __noinline__ dd scaled_hypot(dd x, dd y, double big) {
+  static __device__ __noinline__ double4 rescale(dd x, dd y, double big) {
     int e;
     frexp(big, &e);
-    const dd xs = dd_make(ldexp(x.hi, -e), ldexp(x.lo, -e));
-    const dd ys = dd_make(ldexp(y.hi, -e), ldexp(y.lo, -e));
-    const dd rs = dd_sqrt(dd_add(dd_mul(xs, xs), dd_mul(ys, ys)));
-    return dd_make(ldexp(rs.hi, e), ldexp(rs.lo, e));
+    return make_double4(ldexp(x.hi, -e), ldexp(x.lo, -e), ldexp(y.hi, -e), ldexp(y.lo, -e));
   }
+  // The rotation of Arith<double>::rotate in double-double. Every quotient
+  // and root is one binary64 estimate plus one double-double residual
+  // correction (Newton), and each reciprocal is taken next to the square
+  // root it belongs to (1/sqrt(v) = sqrt(v) (1/v)), so the dependent chain
+  // holds two long operations; dd_sqrt / dd_div (two and three dependent
+  // divisions each) made it seven: 5.7 k cycles per rotation at n = 1024.
+  //   r = sqrt(q):      r0 = sqrt(q.hi), r = r0 + (q - r0^2) (ir / 2), ir = r0 / q.hi
+  //   u = |x| / r:      u0 = |x|.hi ir,  u = u0 + (|x| - u0 r) ir
+  //   c = sqrt(c2), c2 = (1 + u) / 2:    c0 = sqrt(c2.hi), c = c0 + (c2 - c0^2) (c0 / c2.hi) / 2
+  //   t = +-y / den, den = |x| + r:      id = 1 / (|x|.hi + r0), t0 = y.hi id, t = t0 + (y - t0 den) id
+  // Each result carries a relative error of a few 2^-102.
   static __device__ __forceinline__ void rotate(AT app, AT aqq, AT apq, AT& c, AT& s, AT& npp, AT& nqq) {
-    const dd x = dd_sub(aqq, app), y = dd_scale2(apq), ax = dd_abs(x);
-    const double big = fmax(ax.hi, fabs(y.hi));
-    const dd r = (big < 0x1p250 && big > 0x1p-250) ? dd_sqrt(dd_add(dd_mul(x, x), dd_mul(y, y)))
-                                                    : scaled_hypot(x, y, big);
+    dd x = dd_sub(aqq, app), y = dd_scale2(apq);
+    const bool xzero = x.hi == 0.0, xpos = x.hi > 0.0;  // before any rescaling
+    const double big = fmax(fabs(x.hi), fabs(y.hi));
+    if (!(big < 0x1p250 && big > 0x1p-250)) {
+      const double4 xy = rescale(x, y, big);
+      x = dd_make(xy.x, xy.y);
+      y = dd_make(xy.z, xy.w);
+    }
+    const dd ax = dd_abs(x);
+    const dd q = dd_add(dd_mul(x, x), dd_mul(y, y));
+    const double r0 = sqrt(q.hi), iq = 1.0 / q.hi;
+    const double ir = r0 * iq;
+    const double id = 1.0 / (ax.hi + r0);
+    const dd er = dd_sub(q, two_prod(r0, r0));
+    const dd r = quick_two_sum(r0, er.hi * (0.5 * ir));
     const dd den = dd_add(ax, r);
-    const dd t = x.hi == 0.0 ? dd_from(1.0) : dd_div(x.hi > 0.0 ? y : dd_neg(y), den);
-    c = dd_sqrt(dd_div(den, dd_scale2(r)));
+    dd t = dd_from(1.0);
+    if (!xzero) {
+      const dd ys = xpos ? y : dd_neg(y);
+      const double t0 = ys.hi * id;
+      const dd et = dd_sub(ys, dd_mul(dd_from(t0), den));
+      t = quick_two_sum(t0, et.hi * id);
+    }
+    const double u0 = ax.hi * ir;
+    const dd eu = dd_sub(ax, dd_mul(dd_from(u0), r));
+    const dd u = quick_two_sum(u0, eu.hi * ir);
+    const dd c2 = dd_add(dd_from(0.5), dd_make(0.5 * u.hi, 0.5 * u.lo));
+    const double c0 = sqrt(c2.hi), ic2 = 1.0 / c2.hi;
+    const dd ec = dd_sub(c2, two_prod(c0, c0));
+    c = quick_two_sum(c0, ec.hi * (0.5 * (c0 * ic2)));
     s = dd_mul(c, t);
     const dd tapq = dd_mul(t, apq);
     npp = dd_sub(app, tapq);
@@ -179,6 +220,17 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// stores into another CTA's shared memory (shared::cluster address from mapa)
+__device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, dd v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.hi), "d"(v.lo) : "memory");
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+
 // Optional per-round timestamps of the first sweep (MPSVD_JACOBI_TRACE=1).
 __device__ unsigned long long* g_jtrace = nullptr;
 
@@ -186,7 +238,7 @@ template <typename ST, bool kSmem>
 __global__ void __launch_bounds__(kSmem ? kJacobiThreads : kJacobiGridThreads)
 jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict__ rot_log, int n,
               double tol, int max_sweeps, DevStatus* __restrict__ status, ST* __restrict__ v_out = nullptr,
-              int vrows = 0) {
+              int vrows = 0, int vsplit = 0) {
   using A_ = Arith<ST>;
   using AT = typename A_::AT;
   extern __shared__ __align__(16) unsigned char jsm[];
@@ -194,7 +246,6 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   const int tid = threadIdx.x, bs = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const long long nblk = (long long)np * (np + 1) / 2;
   const int lda = kSmem ? n + 1 : n;  // odd smem pitch: row and column walks hit distinct banks
-  const int nw_rot = min(bs, (np + 31) / 32 * 32) / 32;  // warps that own rotation slots
   const unsigned FULL = 0xffffffffu;
 
   // shared memory: [A (smem variant)] [c][s][npp][nqq] [pair word] [block table (smem variant)]
@@ -222,14 +273,80 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   __shared__ int w_cnt[32], w_bad[32];
   __shared__ double w_worst[32];
   __shared__ unsigned s_sweep_flag;
-
-  auto LD = [&](const ST* q) -> AT { return kSmem ? A_::lds(q) : A_::ldg(q); };
-  auto gsync = [&]() {
-    if (kSmem)
-      __syncthreads();
-    else
-      cg::this_grid().sync();
+  // Multi-CTA variant launched as clusters of cs CTAs (n = 1024 dd: the 512
+  // double-double rotations of a round are ~6 k cycles of fp64 issue per SM
+  // when every CTA evaluates all of them): CTA rank cr evaluates the slots
+  // [cr * rchunk, (cr + 1) * rchunk) and stores the results into the shared
+  // memory of every CTA of its cluster (distributed shared memory), so each
+  // CTA still holds the whole round - same values, same decisions - after
+  // one cluster barrier. cs = 1 without a cluster launch.
+  constexpr int kMaxCs = 4;
+  int cs = 1, cr = 0;
+  if (!kSmem) {
+    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(cs));
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(cr));
+  }
+  const int rchunk = cs > 1 ? ((np + cs - 1) / cs + 31) / 32 * 32 : np;
+  const int nw_rot = min(bs, (rchunk + 31) / 32 * 32) / 32;  // warps that own rotation slots
+  // shared::cluster address offsets from this CTA's shared memory to the same
+  // location in the other CTAs of the cluster (mapa; one offset serves every
+  // array). The remote stores are explicit st.shared::cluster: a generic
+  // pointer built from a __shared__ one by adding an offset is still treated
+  // as CTA-local shared memory by the compiler.
+  uint32_t peer_off[kMaxCs - 1] = {0, 0, 0};
+  if (!kSmem && cs > 1) {
+    const uint32_t self = (uint32_t)__cvta_generic_to_shared(rc);
+#pragma unroll
+    for (int t = 1; t < kMaxCs; ++t)
+      if (t < cs) {
+        uint32_t rem;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rem) : "r"(self), "r"((uint32_t)((cr + t) % cs)));
+        peer_off[t - 1] = rem - self;
+      }
+  }
+  auto peer = [&](const void* q, int t) { return (uint32_t)__cvta_generic_to_shared(q) + peer_off[t]; };
+  // CTA barrier, cluster-wide when the round's rotations are shared
+  auto csync = [&]() {
+    __syncthreads();  // also reconverges every warp: the cluster barrier below is .aligned
+    if (!kSmem && cs > 1)
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   };
+
+  // Grid barrier of the multi-CTA variant (every CTA is resident: the launch
+  // is cooperative): a monotonic arrival counter behind the sweep flags,
+  // zeroed per launch. Split into arrive / wait so that CTA-local work can
+  // sit between the two; the wait ends in csync(). (cg::this_grid().sync()
+  // cost ~2.9 k cycles per round at 148 CTAs and is not valid under a
+  // cluster launch.)
+  unsigned* const gbar = reinterpret_cast<unsigned*>(diagbuf + 6 * np) + 2;
+  unsigned gseq = 0;
+  auto garrive = [&]() {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(gbar, 1u);
+    }
+    ++gseq;
+  };
+  auto gwait = [&]() {
+    if (tid == 0) {
+      const unsigned target = gseq * gridDim.x;
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(seen) : "l"(gbar) : "memory");
+      } while ((int)(seen - target) < 0);
+    }
+    csync();
+  };
+  auto gsync = [&]() {
+    if (kSmem) {
+      __syncthreads();
+    } else {
+      garrive();
+      gwait();
+    }
+  };
+  auto LD = [&](const ST* q) -> AT { return kSmem ? A_::lds(q) : A_::ldg(q); };
   auto AE = [&](int row, int col) -> ST* { return a + (long long)col * lda + row; };
 
   if (kSmem) {
@@ -345,10 +462,11 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
       if (warp < nw_rot) {
         int act_sum = 0, bad = 0x7fffffff;
         double wmax = 0.0;
-        for (int k0 = 0; k0 < np; k0 += bs) {  // uniform trip count within the warp
+        const int kend = min(np, (cr + 1) * rchunk);  // this CTA's slots (all of them without clusters)
+        for (int k0 = cr * rchunk; k0 < kend; k0 += bs) {  // uniform trip count within the warp
           const int k = k0 + tid;
           int pp = 0, qq = n;
-          if (k < np) rr_pair(n, r, k, pp, qq);
+          if (k < kend) rr_pair(n, r, k, pp, qq);
           AT app = A_::one(), aqq = A_::one(), apq = A_::zero();
           if (qq < n) {
             if (kSmem) {
@@ -378,21 +496,39 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
             }
           }
           act_sum += act ? 1 : 0;
-          if (k < np) {
+          if (k < kend) {
+            const int word = pp | (qq << 15) | ((act ? 1 : 0) << 30);
             rc[k] = c;
             rsn[k] = s;
             rnpp[k] = npp;
             rnqq[k] = nqq;
-            pw[k] = pp | (qq << 15) | ((act ? 1 : 0) << 30);
+            pw[k] = word;
+#pragma unroll
+            for (int t = 0; t < kMaxCs - 1; ++t)
+              if (t + 1 < cs) {
+                st_cluster(peer(rc + k, t), c);
+                st_cluster(peer(rsn + k, t), s);
+                st_cluster(peer(rnpp + k, t), npp);
+                st_cluster(peer(rnqq + k, t), nqq);
+                st_cluster(peer(pw + k, t), word);
+              }
           }
         }
         act_sum = warp_sum(act_sum);
         bad = warp_min(bad);
         if (want_ratio) wmax = warp_max(wmax);
         if (lane == 0) {
-          w_cnt[warp] = act_sum;
-          w_bad[warp] = bad;
-          w_worst[warp] = wmax;
+          const int wslot = cr * nw_rot + warp;
+          w_cnt[wslot] = act_sum;
+          w_bad[wslot] = bad;
+          w_worst[wslot] = wmax;
+#pragma unroll
+          for (int t = 0; t < kMaxCs - 1; ++t)
+            if (t + 1 < cs) {
+              st_cluster(peer(&w_cnt[wslot], t), act_sum);
+              st_cluster(peer(&w_bad[wslot], t), bad);
+              st_cluster(peer(&w_worst[wslot], t), wmax);
+            }
         }
       }
       if (!kSmem) {  // round rnext's slot and partner of every player, for emit()
@@ -404,10 +540,10 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           npart[x] = pp == x ? qq : pp;
         }
       }
-      __syncthreads();
+      csync();
       if (trace) g_jtrace[r * 16 + 1] = clock64();
       int cnt = 0, badx = 0x7fffffff;
-      for (int w = 0; w < nw_rot; ++w) {
+      for (int w = 0; w < cs * nw_rot; ++w) {
         cnt += w_cnt[w];
         badx = min(badx, w_bad[w]);
         worst = fmax(worst, w_worst[w]);
@@ -512,22 +648,6 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         __syncthreads();
         continue;
       }
-      // fused V: round r's rotations on this CTA's rows of V (the replay's
-      // arithmetic: identity rotations skipped, rot_lo / rot_hi per pair)
-      if (vn) {
-        const int items = vn * np;
-        for (int w = tid; w < items; w += bs) {
-          const int rr = w / np, k = w - rr * np;
-          const AT c = rc[k], sn = rsn[k];
-          if (A_::is_identity(c, sn)) continue;
-          const int wk = pw[k];
-          const int pp = wk & 0x7fff, qq = (wk >> 15) & 0x7fff;
-          ST* row = vsm + (size_t)rr * n;
-          const AT t1 = A_::lds(row + pp), t2 = A_::lds(row + qq);
-          A_::st(row + pp, A_::rot_lo(c, sn, t1, t2));
-          A_::st(row + qq, A_::rot_hi(c, sn, t1, t2));
-        }
-      }
       // multi-CTA variant: every block is visited so that the entries the
       // next round's rotations read are published to the diag buffer.
       // Store-once symmetric storage: entry (i, j) lives at its upper-triangle
@@ -563,6 +683,27 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           for (int v = 0; v < 2; ++v)
             x[u][v] = (rows[u] < n && cols[v] < n) ? LD(CEg(rows[u], cols[v])) : A_::zero();
       };
+      // fused V: round r's rotations on this CTA's rows of V (the replay's
+      // arithmetic: identity rotations skipped, rot_lo / rot_hi per pair),
+      // items [w0, w1) of vn * np
+      auto v_update = [&](int w0, int w1) {
+        for (int w = w0 + tid; w < w1; w += bs) {
+          const int rr = w / np, k = w - rr * np;
+          const AT c = rc[k], sn = rsn[k];
+          if (A_::is_identity(c, sn)) continue;
+          const int wk = pw[k];
+          const int pp = wk & 0x7fff, qq = (wk >> 15) & 0x7fff;
+          ST* row = vsm + (size_t)rr * n;
+          const AT t1 = A_::lds(row + pp), t2 = A_::lds(row + qq);
+          A_::st(row + pp, A_::rot_lo(c, sn, t1, t2));
+          A_::st(row + qq, A_::rot_hi(c, sn, t1, t2));
+        }
+      };
+      const int v_items = vn * np;
+      // the share of the V update done while the first block's loads are in
+      // flight (the block phase is bound by L2 traffic, not fp64 issue); the
+      // rest sits between the round barrier's arrive and wait
+      const int v_early = (int)((long long)v_items * vsplit / 100) / bs * bs;
       AT xn[2][2];
       int an = 0, bn = 0;
       long long idx = gtid;
@@ -570,6 +711,7 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
         decode(idx, an, bn);
         if (an != bn) load_block(an, bn, xn);
       }
+      if (vn) v_update(0, v_early);
       for (; idx < nblk; idx += gstride) {
         const int aa = an, bb = bn;
         AT x[2][2];
@@ -646,7 +788,17 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
           }
       }
       if (trace) g_jtrace[r * 16 + 2] = clock64();
-      gsync();
+      // ---- the round's grid barrier, split: arrive once this CTA's blocks
+      // are written, wait after the fused V update - the rows of V live in
+      // this CTA's shared memory and need only the round's rotations, so
+      // that work (as long as the block updates at n = 1024 dd) hides the
+      // barrier's latency (~2.9 k cycles through cg::grid.sync) and the
+      // stragglers instead of preceding them.
+      garrive();
+      if (vn) v_update(v_early, v_items);
+      // (cluster-wide at its end: the peer CTAs write the next round's
+      // rotations into this CTA's shared memory, which the V update reads)
+      gwait();
       if (trace) g_jtrace[r * 16 + 3] = clock64();
     }
     ++sweeps;
@@ -1584,12 +1736,28 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   if (smem_a + smem_rot <= smem_limit) {
     auto k = jacobi_kernel<ST, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_a + smem_rot));
-    k<<<1, kJacobiThreads, smem_a + smem_rot, st>>>(a, d, lg, n, tol, max_sweeps, status, nullptr, 0);
+    k<<<1, kJacobiThreads, smem_a + smem_rot, st>>>(a, d, lg, n, tol, max_sweeps, status, nullptr, 0, 0);
     return cudaGetLastError();
   }
   auto k = jacobi_kernel<ST, false>;
   const long long nblk = (long long)np * (np + 1) / 2;
-  long long want = (nblk + kJacobiGridThreads - 1) / kJacobiGridThreads;
+  // CTA size: 512 threads on a full grid; a mid-size matrix (fewer blocks
+  // than 512 x SMs) spreads over more, smaller CTAs - never fewer threads
+  // than rotation slots, so the rotations stay one pass
+  // (MPSVD_JACOBI_GRID_THREADS overrides, for experiments)
+  int gthreads = kJacobiGridThreads;
+  {
+    const char* te = getenv("MPSVD_JACOBI_GRID_THREADS");
+    const int tv = te ? atoi(te) : 0;
+    if (tv >= 64 && tv <= kJacobiGridThreads && tv % 32 == 0) {
+      gthreads = tv;
+    } else {
+      // c3 (n = 256 dd), eigen phase: 512 threads x 17 CTAs 8.2 ms, 256 x 33
+      // 7.4 (fused V 7.1), 128 x 65 7.2 (fused V 6.7)
+      while (gthreads > 128 && gthreads / 2 >= np && (nblk + gthreads - 1) / gthreads < sm_count) gthreads /= 2;
+    }
+  }
+  long long want = (nblk + gthreads - 1) / gthreads;
   long long grid = (long long)sm_count;  // one CTA per SM (see kJacobiGridThreads)
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
@@ -1597,20 +1765,28 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   // (MPSVD_JACOBI_REPLAY=1 keeps the separate replay)
   int vrows = (int)((n + grid - 1) / grid);
   size_t smem_grid = smem_rot + 16 + (size_t)vrows * n * sizeof(ST);  // + alignment of the V rows
-  // fused only on a full grid: with few CTAs (n <= ~400) the extra work per
-  // round costs more than the short separate replay (c3: 9.0 vs 8.1 ms)
-  if (smem_grid > 200 * 1024 || 2 * grid < sm_count || getenv("MPSVD_JACOBI_REPLAY") != nullptr) {
+  // fused unless the grid is small (few CTAs would each carry many rows of V
+  // per round; the V update sits between the round barrier's arrive and wait)
+  if (smem_grid > 200 * 1024 || (4 * grid < sm_count && getenv("MPSVD_JACOBI_FUSE") == nullptr) ||
+      getenv("MPSVD_JACOBI_REPLAY") != nullptr) {
     vrows = 0;
     smem_grid = smem_rot;
   }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_grid);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kJacobiGridThreads, smem_grid);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, gthreads, smem_grid);
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int nn = n, ms = max_sweeps;
   double tl = tol;
   ST* vout = (ST*)ws.v;
-  void* args[] = {&a, &d, &lg, &nn, &tl, &ms, &status, &vout, &vrows};
+  // percent of the fused V update done ahead of the block updates
+  // (MPSVD_JACOBI_VSPLIT, default below)
+  int vsplit = 50;
+  {
+    const char* ve = getenv("MPSVD_JACOBI_VSPLIT");
+    if (ve && atoi(ve) >= 0 && atoi(ve) <= 100) vsplit = atoi(ve);
+  }
+  void* args[] = {&a, &d, &lg, &nn, &tl, &ms, &status, &vout, &vrows, &vsplit};
   static const bool trace = getenv("MPSVD_JACOBI_TRACE") != nullptr;
   unsigned long long* tbuf = nullptr;
   if (trace) {
@@ -1618,8 +1794,55 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
     cudaMemset(tbuf, 0, 64 * 16 * sizeof(unsigned long long));
     cudaMemcpyToSymbol(g_jtrace, &tbuf, sizeof(tbuf));
   }
-  const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(kJacobiGridThreads), args,
-                                                     smem_grid, st);
+  // Experiment switch MPSVD_JACOBI_CLUSTER=2|4: clusters of CTAs share each
+  // round's rotations (see the kernel). Off by default: measured on c5
+  // (n = 1024 dd) the rotation phase is bound by the latency of one rotation
+  // chain, not by fp64 issue, so sharing did not shorten it (5.7 k -> 6.0 k
+  // cycles) and the cluster barriers cost more (eigen 570 -> 605 ms).
+  int csize = 1;
+  {
+    const char* ce = getenv("MPSVD_JACOBI_CLUSTER");
+    const int want_cs = ce ? atoi(ce) : 1;
+    if (np >= 256 && (want_cs == 2 || want_cs == 4) && grid % want_cs == 0) {
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3((unsigned)grid);
+      qc.blockDim = dim3(gthreads);
+      qc.dynamicSmemBytes = smem_grid;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = (unsigned)want_cs;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k, &qc) == cudaSuccess &&
+          (long long)nclusters * want_cs >= grid)
+        csize = want_cs;
+      else
+        cudaGetLastError();
+    }
+  }
+  cudaError_t le;
+  if (csize > 1) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3(gthreads);
+    lc.dynamicSmemBytes = smem_grid;
+    lc.stream = st;
+    cudaLaunchAttribute la[2];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = (unsigned)csize;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    la[1].id = cudaLaunchAttributeCooperative;
+    la[1].val.cooperative = 1;
+    lc.attrs = la;
+    lc.numAttrs = 2;
+    le = cudaLaunchKernelExC(&lc, (const void*)k, args);
+  } else {
+    le = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(gthreads), args, smem_grid, st);
+  }
   if (le == cudaSuccess && vrows > 0 && fused_replay) *fused_replay = true;
   if (trace) {
     unsigned long long h[64 * 16];
@@ -1639,9 +1862,9 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
     }
     if (cnt)
       fprintf(stderr,
-              "[jacobi multi-CTA trace n=%d grid=%lld] period %.0f | rotations %.0f, block updates %.0f, grid sync %.0f "
+              "[jacobi multi-CTA trace n=%d grid=%lld cluster=%d] period %.0f | rotations %.0f, block updates %.0f, grid sync %.0f "
               "(cycles/round, %d rounds)\n",
-              n, grid, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, cnt);
+              n, grid, csize, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, cnt);
   }
   return le;
 }

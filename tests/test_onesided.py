@@ -168,3 +168,36 @@ def test_gpu_plan_eigensolver_device_path_matches_host_path():
     assert np.array_equal(s_t.cpu().numpy(), host.sigma)
     assert np.array_equal(v_t.cpu().numpy().T, host.v)
     assert np.array_equal(u_t.cpu().numpy().T, host.u)
+
+
+def _huge_stacked(scale=3.0e38):
+    # A = scale * [e1; e1; e2; e2]: M = 2 scale^2 I, R = sqrt(2) scale I > FLT_MAX
+    a = np.zeros((4, 2), dtype=np.float32, order="F")
+    a[0, 0] = a[1, 0] = a[2, 1] = a[3, 1] = np.float32(scale)
+    return a
+
+
+def test_ref_gram_chol_cast_overflow():
+    """cast(R, Working) of the GramCholSvd branch (thinsvd.cpp:44, dense.cpp:172):
+    the reference reports CastOverflowError(1, 1, R_11)."""
+    if not pyoracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    with pytest.raises(pyoracle.OracleError) as er:
+        pyoracle.Ref().thin_svd(_huge_stacked(), choice=GRAM_CHOL)
+    assert er.value.status == 6  # MPSVD_ERR_CAST_OVERFLOW
+
+
+@pytest.mark.gpu
+def test_gpu_gram_chol_cast_overflow_like_reference(ref):
+    a = _huge_stacked()
+    with pytest.raises(pyoracle.OracleError) as er:
+        ref.thin_svd(a, choice=GRAM_CHOL)
+    with pytest.raises(M.CastOverflowError):
+        M.mp_thin_svd(a, choice=M.EigensolverChoice.GRAM_CHOL_SVD)
+    assert er.value.status == M.CastOverflowError.status
+    # the default branch has no checked cast (thinsvd.cpp:81-89): sigma = fl32(sqrt(lambda)) = inf
+    # passes check_sigma_normal, W = V / inf = 0, U = 0 - same on both sides
+    w = ref.thin_svd(a)
+    r = M.mp_thin_svd(a)
+    assert np.array_equal(np.asarray(r.sigma), np.asarray(w.sigma)) and np.all(np.isinf(np.asarray(r.sigma)))
+    assert np.array_equal(np.asarray(r.u), np.asarray(w.u))

@@ -4,11 +4,11 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
-__device__ __noinline__ double scaled_hypot(double x, double y, double big) {
+__device__ __noinline__ void rescale(double& x, double& y, double big) {
   int e;
   frexp(big, &e);
-  const double xs = ldexp(x, -e), ys = ldexp(y, -e);
-  return ldexp(sqrt(fma(xs, xs, ys * ys)), e);
+  x = ldexp(x, -e);
+  y = ldexp(y, -e);
 }
 
 __global__ void rot_chain(double* out, int iters, double tol) {
@@ -18,12 +18,16 @@ __global__ void rot_chain(double* out, int iters, double tol) {
     const double pr = app * aqq;
     const double thresh = (pr > 0x1p-1000 && pr < 0x1p1000) ? tol * sqrt(pr) : tol * sqrt(app) * sqrt(aqq);
     const bool act = !(fabs(apq) <= thresh);
-    const double x = aqq - app, y = 2.0 * apq, ax = fabs(x);
-    const double big = fmax(ax, fabs(y));
-    const double r = (big < 0x1p500 && big > 0x1p-500) ? sqrt(fma(x, x, y * y)) : scaled_hypot(x, y, big);
+    double x = aqq - app, y = 2.0 * apq;
+    const bool xzero = x == 0.0, xpos = x > 0.0;
+    const double big = fmax(fabs(x), fabs(y));
+    if (!(big < 0x1p500 && big > 0x1p-500)) rescale(x, y, big);
+    const double ax = fabs(x);
+    const double q = fma(x, x, y * y);
+    const double r = sqrt(q), iq = 1.0 / q;
     const double den = ax + r;
-    const double t = x == 0.0 ? 1.0 : (x > 0.0 ? y : -y) / den;
-    const double c = sqrt(den / (2.0 * r));
+    const double t = xzero ? 1.0 : (xpos ? y : -y) / den;
+    const double c = sqrt(fma(0.5, ax * (r * iq), 0.5));
     const double s = c * t;
     // feed back so iterations are dependent
     app = 2.0 + s * 1e-9 + (act ? 0.0 : 1e-300);
@@ -83,6 +87,33 @@ __global__ void grid_chain(double* out, int iters) {
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (double)(t1 - t0) / iters;
 }
 
+// the multi-CTA solver's own barrier (csrc/jacobi.cu garrive / gwait): a
+// monotonic arrival counter, one atomic per CTA, thread 0 polls with acquire
+__global__ void grid_chain_counter(double* out, int iters, unsigned* bar) {
+  unsigned seq = 0;
+  auto sync = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(bar, 1u);
+    }
+    ++seq;
+    if (threadIdx.x == 0) {
+      const unsigned target = seq * gridDim.x;
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(seen) : "l"(bar) : "memory");
+      } while ((int)(seen - target) < 0);
+    }
+    __syncthreads();
+  };
+  sync();
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) sync();
+  unsigned long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = (double)(t1 - t0) / iters;
+}
+
 int main() {
   double* d;
   cudaMalloc(&d, 16);
@@ -118,8 +149,19 @@ int main() {
   cudaLaunchCooperativeKernel((void*)grid_chain, sms, 512, args, 0, nullptr);
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
   const double gs = h[0];
-  printf("grid.sync (%d CTAs x 512): %.1f cycles\n", sms, gs);
+  printf("cg grid.sync (%d CTAs x 512): %.1f cycles\n", sms, gs);
+  unsigned* bar;
+  cudaMalloc(&bar, 4);
+  cudaMemset(bar, 0, 4);
+  void* cargs[] = {&d, &git, &bar};
+  cudaLaunchCooperativeKernel((void*)grid_chain_counter, sms, 512, cargs, 0, nullptr);
+  cudaMemset(bar, 0, 4);
+  cudaLaunchCooperativeKernel((void*)grid_chain_counter, sms, 512, cargs, 0, nullptr);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  const double gc = h[0];
+  printf("counter grid barrier (%d CTAs x 512): %.1f cycles\n", sms, gc);
   printf("JSON {\"rotation_chain_cycles\": %.1f, \"syncthreads_cycles\": %.1f, \"grid_sync_cycles\": %.1f, "
-         "\"sms\": %d, \"source\": \"tools/microbench/rot_latency.cu\"}\n", rot, syn, gs, sms);
+         "\"cg_grid_sync_cycles\": %.1f, \"sms\": %d, \"source\": \"tools/microbench/rot_latency.cu\"}\n",
+         rot, syn, gc, gs, sms);
   return 0;
 }
