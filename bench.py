@@ -169,7 +169,7 @@ def latency_probe():
     """Measured latency floors (tools/microbench/rot_latency.cu on the B200,
     committed as profiles/r02_latency_probe.json): cycles of one dependent
     fp64 rotation (stop test + rotation), one 512-thread __syncthreads
-    hand-off, one 148-CTA cooperative grid.sync."""
+    hand-off, one 148-CTA grid barrier (the solver's arrival counter)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r02_latency_probe.json")) as f:
             return json.load(f)

@@ -1781,7 +1781,7 @@ static cudaError_t launch_jacobi_t(int n, double tol, int max_sweeps, const Jaco
   ST* vout = (ST*)ws.v;
   // percent of the fused V update done ahead of the block updates
   // (MPSVD_JACOBI_VSPLIT, default below)
-  int vsplit = 50;
+  int vsplit = 0;  // measured on c5: 0, 30, 50, 70 within 1% of each other, 100 slower (the block phase grows by the V time)
   {
     const char* ve = getenv("MPSVD_JACOBI_VSPLIT");
     if (ve && atoi(ve) >= 0 && atoi(ve) <= 100) vsplit = atoi(ve);
