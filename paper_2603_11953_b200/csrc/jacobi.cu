@@ -267,8 +267,13 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
   // rotated by every round right after the round's rotations are known
   // (rows of V never mix; the separate replay streamed the whole rotation
   // log through every CTA: 259 ms of the c5 eigen phase)
-  ST* vsm = reinterpret_cast<ST*>((reinterpret_cast<uintptr_t>(npart + 2 * np) + 15) & ~(uintptr_t)15);
+  // (an offset from jsm, not a pointer rebuilt from an integer: the compiler
+  // then keeps the shared address space and emits LDS / STS - the rebuilt
+  // pointer made every access of the V update a generic LD.E / ST.E)
+  const size_t voff = ((size_t)(reinterpret_cast<unsigned char*>(npart + 2 * np) - jsm) + 15) & ~(size_t)15;
+  ST* vsm = reinterpret_cast<ST*>(jsm + voff);
   const int v0 = blockIdx.x * vrows, vn = vrows > 0 ? max(0, min(vrows, n - v0)) : 0;
+  const int vstep_r = bs / np, vstep_k = bs - vstep_r * np;  // bs = vstep_r * np + vstep_k
   __shared__ int s_flag;
   __shared__ int w_cnt[32], w_bad[32];
   __shared__ double w_worst[32];
@@ -687,8 +692,13 @@ jacobi_kernel(ST* __restrict__ a_glob, ST* __restrict__ diagbuf, ST* __restrict_
       // arithmetic: identity rotations skipped, rot_lo / rot_hi per pair),
       // items [w0, w1) of vn * np
       auto v_update = [&](int w0, int w1) {
-        for (int w = w0 + tid; w < w1; w += bs) {
-          const int rr = w / np, k = w - rr * np;
+        // item w = (row rr, slot k) = (w / np, w % np), stepped without divisions
+        int rr = (w0 + tid) / np, k = (w0 + tid) - rr * np;
+        for (int w = w0 + tid; w < w1; w += bs, rr += vstep_r, k += vstep_k) {
+          if (k >= np) {
+            k -= np;
+            ++rr;
+          }
           const AT c = rc[k], sn = rsn[k];
           if (A_::is_identity(c, sn)) continue;
           const int wk = pw[k];
