@@ -88,10 +88,22 @@ struct Arith<double> {
     }
     const double ax = fabs(x);
     const double q = fma(x, x, y * y);
-    const double r = sqrt(q), iq = 1.0 / q;
-    const double den = ax + r;
-    const double t = xzero ? 1.0 : (xpos ? y : -y) / den;
-    c = sqrt(fma(0.5, ax * (r * iq), 0.5));
+    const double ys = xpos ? y : -y;
+    double t;
+    // operands and results far inside the normal range: the branch-free
+    // forms of sqrt and / (common.cuh, the same bits), whose independent
+    // pairs (sqrt q | 1 / q, then y / den | sqrt c^2) overlap
+    if (big < 0x1p400 && big > 0x1p-400 && fabs(y) > big * 0x1p-200) {
+      const double r = fast_sqrt_normal(q), iq = fast_div_normal(1.0, q);
+      const double den = ax + r;
+      t = xzero ? 1.0 : fast_div_normal(ys, den);
+      c = fast_sqrt_normal(fma(0.5, ax * (r * iq), 0.5));
+    } else {
+      const double r = sqrt(q), iq = 1.0 / q;
+      const double den = ax + r;
+      t = xzero ? 1.0 : ys / den;
+      c = sqrt(fma(0.5, ax * (r * iq), 0.5));
+    }
     s = c * t;
     npp = fma(-t, apq, app);
     nqq = fma(t, apq, aqq);
@@ -165,9 +177,11 @@ struct Arith<double2> {
     }
     const dd ax = dd_abs(x);
     const dd q = dd_add(dd_mul(x, x), dd_mul(y, y));
-    const double r0 = sqrt(q.hi), iq = 1.0 / q.hi;
+    const bool fast = big < 0x1p250 && big > 0x1p-250;  // branch-free sqrt and / (common.cuh, the same bits)
+    const double r0 = fast ? fast_sqrt_normal(q.hi) : sqrt(q.hi);
+    const double iq = fast ? fast_div_normal(1.0, q.hi) : 1.0 / q.hi;
     const double ir = r0 * iq;
-    const double id = 1.0 / (ax.hi + r0);
+    const double id = fast ? fast_div_normal(1.0, ax.hi + r0) : 1.0 / (ax.hi + r0);
     const dd er = dd_sub(q, two_prod(r0, r0));
     const dd r = quick_two_sum(r0, er.hi * (0.5 * ir));
     const dd den = dd_add(ax, r);
@@ -182,7 +196,8 @@ struct Arith<double2> {
     const dd eu = dd_sub(ax, dd_mul(dd_from(u0), r));
     const dd u = quick_two_sum(u0, eu.hi * ir);
     const dd c2 = dd_add(dd_from(0.5), dd_make(0.5 * u.hi, 0.5 * u.lo));
-    const double c0 = sqrt(c2.hi), ic2 = 1.0 / c2.hi;
+    const double c0 = fast ? fast_sqrt_normal(c2.hi) : sqrt(c2.hi);
+    const double ic2 = fast ? fast_div_normal(1.0, c2.hi) : 1.0 / c2.hi;
     const dd ec = dd_sub(c2, two_prod(c0, c0));
     c = quick_two_sum(c0, ec.hi * (0.5 * (c0 * ic2)));
     s = dd_mul(c, t);

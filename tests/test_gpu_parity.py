@@ -71,7 +71,7 @@ def test_gram_dd_matches_oracle(port, m, n):
 
 # ---------------------------------------------------------------------------
 # K4: fp64 Jacobi — bitwise against the device-semantics restatement
-@pytest.mark.parametrize("n", [1, 2, 3, 5, 24, 64, 101, 128, 129, 200, 256])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 24, 64, 101, 128, 129, 200, 201, 256])
 def test_jacobi_f64_bitwise_vs_restatement(port, n):
     a = rng_matrix(3 * n + 5, n, seed=n, dtype=np.float64, scale_decades=3.0)
     g = a.T @ a
@@ -119,8 +119,40 @@ def test_jacobi_errors():
         M.twosided_jacobi_eig(g.T @ g, max_sweeps=1)
 
 
+def _indefinite(n, seed):
+    # positive diagonal, one slightly negative eigenvalue: the pivot check fails inside a round
+    rng = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.linspace(1.0, 2.0, n)
+    lam[-1] = -1e-3
+    g = (q * lam) @ q.T
+    return (g + g.T) / 2
+
+
+@pytest.mark.parametrize("n", [40, 200, 201])
+def test_jacobi_f64_error_paths_like_restatement(port, n):
+    """NotPositiveDefinite raised inside a round and NoConvergence, on the single-CTA
+    (n = 40) and multi-CTA solvers: same pivot / value / payload as the restatement."""
+    g = _indefinite(n, seed=n)
+    with pytest.raises(pyoracle.OracleError) as ep:
+        port.twosided_jacobi(g, sem=SEM_DEVICE)
+    with pytest.raises(M.NotPositiveDefiniteError) as eg:
+        M.twosided_jacobi_eig(g)
+    assert eg.value.index == ep.value.index
+    a = rng_matrix(2 * n, n, seed=7 + n, dtype=np.float64, scale_decades=3.0)
+    g = a.T @ a
+    g = (g + g.T) / 2
+    with pytest.raises(pyoracle.OracleError) as ep:
+        port.twosided_jacobi(g, max_sweeps=2, sem=SEM_DEVICE)
+    with pytest.raises(M.NoConvergenceError) as eg:
+        M.twosided_jacobi_eig(g, max_sweeps=2)
+    assert ep.value.index == 2 and "2 sweeps" in str(eg.value)
+    worst = float(str(eg.value).rsplit(" ", 1)[1])
+    assert abs(worst - ep.value.value) <= 1e-5 * ep.value.value
+
+
 # K5: double-double Jacobi — bitwise against the restatement
-@pytest.mark.parametrize("n", [2, 7, 32, 90, 120])
+@pytest.mark.parametrize("n", [2, 7, 32, 90, 111, 120])
 def test_jacobi_dd_bitwise_vs_restatement(port, n):
     a = rng_matrix(2 * n + 3, n, seed=100 + n, dtype=np.float64, scale_decades=8.0)
     hi, lo = port.dd_gram(a)

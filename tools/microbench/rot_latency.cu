@@ -4,6 +4,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 __device__ __noinline__ void rescale(double& x, double& y, double big) {
   int e;
   frexp(big, &e);
@@ -24,10 +26,19 @@ __global__ void rot_chain(double* out, int iters, double tol) {
     if (!(big < 0x1p500 && big > 0x1p-500)) rescale(x, y, big);
     const double ax = fabs(x);
     const double q = fma(x, x, y * y);
-    const double r = sqrt(q), iq = 1.0 / q;
-    const double den = ax + r;
-    const double t = xzero ? 1.0 : (xpos ? y : -y) / den;
-    const double c = sqrt(fma(0.5, ax * (r * iq), 0.5));
+    const double ys = xpos ? y : -y;
+    double t, c;
+    if (big < 0x1p400 && big > 0x1p-400 && fabs(y) > big * 0x1p-200) {
+      const double r = mpsvd::dev::fast_sqrt_normal(q), iq = mpsvd::dev::fast_div_normal(1.0, q);
+      const double den = ax + r;
+      t = xzero ? 1.0 : mpsvd::dev::fast_div_normal(ys, den);
+      c = mpsvd::dev::fast_sqrt_normal(fma(0.5, ax * (r * iq), 0.5));
+    } else {
+      const double r = sqrt(q), iq = 1.0 / q;
+      const double den = ax + r;
+      t = xzero ? 1.0 : ys / den;
+      c = sqrt(fma(0.5, ax * (r * iq), 0.5));
+    }
     const double s = c * t;
     // feed back so iterations are dependent
     app = 2.0 + s * 1e-9 + (act ? 0.0 : 1e-300);
