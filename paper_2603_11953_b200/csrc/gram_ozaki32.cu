@@ -115,17 +115,6 @@ constexpr int kHalfBytes = kDigits * 2048;    // one 16-row K-core group of a di
 constexpr int kDStageBytes = 2 * kStep * kHalfBytes;  // a step's 4 K-core groups (64 rows) x 6 planes
 constexpr unsigned long long kC48 = 0x808080808080ull;
 
-// products of group g, in issue order: (p, q, accumulator)
-__host__ __device__ __forceinline__ void product(int g, int k, int& p, int& q, int& acc) {
-  // group 0: T7 (1,6)(2,5)(3,4) -> acc 0, T4 (1,3) -> 1, T3 (1,2) -> 2, D2 (1,1) -> 3
-  // group 1: T6 (1,5)(2,4) -> 0, T5 (1,4)(2,3) -> 1, D4 (2,2) -> 2, D6 (3,3) -> 3
-  // nibble k of each word = product k (P: {1,2,3,1,1,1} / {1,2,1,2,2,3}, Q, accumulator)
-  const int sh = 4 * k;
-  p = (int)(((g ? 0x322121u : 0x111321u) >> sh) & 15u);
-  q = (int)(((g ? 0x323445u : 0x123456u) >> sh) & 15u);
-  acc = (int)(((g ? 0x321100u : 0x321000u) >> sh) & 15u);
-}
-
 // frexp exponent of a non-negative finite binary32 bit pattern (v < 2^e), or
 // -1000 for zero
 __host__ __device__ __forceinline__ int fexp_bits(uint32_t ab) {
@@ -358,20 +347,36 @@ __device__ __forceinline__ void arrive_lead(uint64_t* bar, uint32_t lead) {
       "r"(lead)
       : "memory");
 }
-// The 6 MMAs of one chunk for group G (compile-time products): operand
-// descriptors are the slot's base descriptor plus the plane offset >> 4.
+// The MMAs of one chunk for group G: operand descriptors are the slot's
+// base descriptor plus the plane offset >> 4. Digit planes q and q + 1 are
+// contiguous along N (16 + 16 eight-column groups, 128 B apart), so two
+// products with the same A plane and adjacent B planes are ONE N = 256 MMA
+// into two adjacent accumulators (the A plane is read once: 5 / 4 MMAs per
+// chunk instead of 6, 44 / 40 KB of operands instead of 48). Accumulator
+// columns (128 each):
+//   group 0: T7 (1,6)(2,5)(3,4) -> 0, [T3 | T4] = A_1^T [A_2 | A_3] -> 1, 2, D2 (1,1) -> 3
+//   group 1: [T5 | T6] = A_1^T [A_4 | A_5] + A_2^T [A_3 | A_4] -> 0, 1, D4 (2,2) -> 2, D6 (3,3) -> 3
+// idesc = N = 128, idesc2 = N = 256. The restatement (oracle/mpsvd_port.c
+// o32_product) lists the same twelve products one by one; the sums are exact
+// integers, so the grouping cannot change a bit.
 template <int G>
-__device__ __forceinline__ void issue_chunk(uint32_t tmem, uint64_t sd, uint32_t idesc, bool fresh, uint32_t lead) {
-  unsigned started = 0;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    int p, q, acc;
-    product(G, k, p, q, acc);
-    const uint32_t first = fresh && !(started & (1u << acc));
-    started |= 1u << acc;
-    umma_i8_lead(tmem + (uint32_t)(acc * kCB), sd + (uint64_t)((p - 1) * (2048 >> 4)),
-                 sd + (uint64_t)((q - 1) * (2048 >> 4)), idesc, first ? 0u : 1u, lead);
+__device__ __forceinline__ void issue_chunk(uint32_t tmem, uint64_t sd, uint32_t idesc, uint32_t idesc2, bool fresh,
+                                            uint32_t lead) {
+  const uint32_t acc0 = fresh ? 0u : 1u;
+#define OZ32_PL(p) (sd + (uint64_t)(((p) - 1) * (2048 >> 4)))
+  if (G == 0) {
+    umma_i8_lead(tmem, OZ32_PL(1), OZ32_PL(6), idesc, acc0, lead);
+    umma_i8_lead(tmem, OZ32_PL(2), OZ32_PL(5), idesc, 1u, lead);
+    umma_i8_lead(tmem, OZ32_PL(3), OZ32_PL(4), idesc, 1u, lead);
+    umma_i8_lead(tmem + (uint32_t)kCB, OZ32_PL(1), OZ32_PL(2), idesc2, acc0, lead);
+    umma_i8_lead(tmem + (uint32_t)(3 * kCB), OZ32_PL(1), OZ32_PL(1), idesc, acc0, lead);
+  } else {
+    umma_i8_lead(tmem, OZ32_PL(1), OZ32_PL(4), idesc2, acc0, lead);
+    umma_i8_lead(tmem, OZ32_PL(2), OZ32_PL(3), idesc2, 1u, lead);
+    umma_i8_lead(tmem + (uint32_t)(2 * kCB), OZ32_PL(2), OZ32_PL(2), idesc, acc0, lead);
+    umma_i8_lead(tmem + (uint32_t)(3 * kCB), OZ32_PL(3), OZ32_PL(3), idesc, acc0, lead);
   }
+#undef OZ32_PL
 }
 
 // Exact group total of one tile entry from the 4 accumulators, relative to
@@ -519,6 +524,7 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
     const uint32_t lead = lane == 0;
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kCB >> 3) << 17) |
                            ((uint32_t)(128 >> 4) << 24);  // D s32, A/B s8 K-major, N = M = 128
+    const uint32_t idesc2 = (idesc & ~(63u << 17)) | ((uint32_t)(256 >> 3) << 17);  // the same with N = 256
     const uint64_t dbase = kdesc(saddr(dstage));           // + (byte offset >> 4) per operand
     // D8 diagonal (group 1): sum over the chunk's 32 rows of d_4^2 per
     // column, from digit plane 4 of both halves of the slot; lane l owns
@@ -554,13 +560,13 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const uint64_t sd1 = sd + (uint64_t)((2 * kHalfBytes) >> 4);  // the step's second chunk (K-core groups 2, 3)
       if (g == 0) {
         if (!(kdbg & 1)) {
-          issue_chunk<0>(tmem, sd, idesc, fresh, lead);
-          issue_chunk<0>(tmem, sd1, idesc, false, lead);
+          issue_chunk<0>(tmem, sd, idesc, idesc2, fresh, lead);
+          issue_chunk<0>(tmem, sd1, idesc, idesc2, false, lead);
         }
       } else {
         if (!(kdbg & 1)) {
-          issue_chunk<1>(tmem, sd, idesc, fresh, lead);
-          issue_chunk<1>(tmem, sd1, idesc, false, lead);
+          issue_chunk<1>(tmem, sd, idesc, idesc2, fresh, lead);
+          issue_chunk<1>(tmem, sd1, idesc, idesc2, false, lead);
         }
         const unsigned char* p4 = dstage + (size_t)s * kDStageBytes + 3 * 2048 + (lane >> 3) * 128 + (lane & 7) * 16;
 #pragma unroll
@@ -737,7 +743,9 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
           for (int jj = 0; jj < 4; ++jj) {
             const int jc = j0 + jj;
             if (jc >= n) continue;
-            dd t0 = group_total(g, (int)v[0][jj], (int)v[1][jj], (int)v[2][jj], (int)v[3][jj]);
+            // accumulator columns: group 0 {T7, T3, T4, D2}, group 1 {T5, T6, D4, D6} (issue_chunk)
+            dd t0 = g == 0 ? group_total(0, (int)v[0][jj], (int)v[2][jj], (int)v[1][jj], (int)v[3][jj])
+                           : group_total(1, (int)v[1][jj], (int)v[0][jj], (int)v[2][jj], (int)v[3][jj]);
             if (g == 1 && jc == i)  // D8 diagonal: sum d_4^2 at 2^-16 of this frame (halved)
               t0 = dd_add(t0, dd_make((double)dsq[(span & 1) * kCB + i] * 0x1p-16, 0.0));
             const int sc = ei + E[jc] - 92 + basee;
