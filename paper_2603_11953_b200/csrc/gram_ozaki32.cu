@@ -722,6 +722,13 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
       const int basee = g ? 47 : 40;
       // 4 columns per step (4 x 4 TMEM words, 4 running partials in flight):
       // the kernel runs 27 warps, so the drain must fit in ~72 registers
+      // the partials of column group j0 + 4 are requested before group j0 is
+      // combined, so their L2 / HBM round trip overlaps the dd arithmetic
+      const bool rmw = accumulate || span > 0;
+      double2 nxt[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+        nxt[jj] = (rmw && i < n && jj < n) ? P[(size_t)jj * kCB + i] : make_double2(0.0, 0.0);
       for (int j0 = 0; j0 < kCB; j0 += 4) {
         uint32_t v[4][4];
         const uint32_t taddr = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)j0;
@@ -734,11 +741,12 @@ gram_f32_ozaki(const __grid_constant__ CUtensorMap amap, int n, long long c_begi
         if (i < n) {
           // the running partials of the step are loaded together (one
           // memory latency per group of columns, not per entry)
-          const bool rmw = accumulate || span > 0;
           double2 old[4];
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            old[jj] = (rmw && j0 + jj < n) ? P[(size_t)(j0 + jj) * kCB + i] : make_double2(0.0, 0.0);
+          for (int jj = 0; jj < 4; ++jj) {
+            old[jj] = nxt[jj];
+            nxt[jj] = (rmw && j0 + 4 + jj < n) ? P[(size_t)(j0 + 4 + jj) * kCB + i] : make_double2(0.0, 0.0);
+          }
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) {
             const int jc = j0 + jj;
