@@ -78,7 +78,7 @@ OZ_PRODUCTS = 66                               # digit products p + q <= 12 of 1
 I8_TOPS = 2 * 128 * 256 * 32 / 128 * 148 * 1.965e9 / 1e12  # 4.77 POPS (umma_i8 probe)
 
 
-K1Z_MMAS_PER_CHUNK = 12                        # 2 CTAs x 6 M128 N128 K32 int8 MMAs per 32-row chunk (gram_ozaki32.cu)
+K1Z_MMAS_PER_CHUNK = 12                        # 2 CTAs x 6 M128 N128 K32 int8 digit products per 32-row chunk (gram_ozaki32.cu; issued as 5 + 4 MMAs)
 NCU_NAME = {("gram", 0): "gram_f32_diag", ("gram", 1): "gram_f32_ozaki", ("gram", 2): "gram_f64_dd",
             ("gram", 3): "gram_dd_ozaki", ("compute_u", 0): "av_kernel", ("compute_u", 1): "av_tc_tmem_f32",
             ("compute_u", 2): "av_dmma_f64"}
@@ -93,8 +93,9 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
     info.av_kernel, reported by the library):
 
     gram K1 : m n (n+1) flops on the DMMA pipe
-    gram K1z: 12 int8 MMAs (M = N = 128, K = 32) per 32-row chunk = 12 x 2 x
-              128 x 128 ops per row, against the int8 tensor peak; also
+    gram K1z: 12 int8 digit products (M = N = 128, K = 32; issued as 9 MMAs,
+              three of them N = 256) per 32-row chunk = 12 x 2 x 128 x 128
+              ops per row, against the int8 tensor peak; also
               m n 4 bytes of A against HBM (hbm_frac)
     gram K2 : m n (n+1)/2 multiply-adds x 10 fp64 operations (c_dd = 10,
               SURVEY.md §8(d)) against the DFMA issue rate
@@ -117,8 +118,8 @@ def phase_rooflines(cfg, m_local, n, med, fp64_peak, hbm, info):
                        "unit": "TOPS", "frac": a / I8_TOPS,
                        "peak_source": "tcgen05 kind::i8 probe: one M128 N256 K32 MMA per 128 cycles per SM "
                                       "(tools/microbench/umma_i8.cu, profiles/r01_umma_i8.txt) x 148 SMs x 1965 MHz",
-                       "algorithmic": "12 x 2 x 128 x 128 int8 ops per row of A (2 CTA groups x 6 digit-product "
-                                      "MMAs per 32-row chunk)",
+                       "algorithmic": "12 x 2 x 128 x 128 int8 ops per row of A (2 CTA groups x 6 digit products "
+                                      "per 32-row chunk, issued as 5 + 4 MMAs)",
                        "hbm_achieved_gbs": bw, "hbm_frac": bw / hbm,
                        "fp64_equivalent_tflops": m_local * n * (n + 1) / t_g / 1e12}
     elif gk == 0:
