@@ -22,7 +22,8 @@
 // Per CTA:
 //   warp 0       TMA: this CTA's chunk of each step (32 rows x 128 columns,
 //                16 KB, 128B swizzle) into a ring
-//   warp 1       MMA issue (one thread, 12 MMAs per step) + TMEM allocation
+//   warp 1       MMA issue (one thread, 12 products per step as 10 / 8 MMAs)
+//                + TMEM allocation
 //                (4 x 128 columns); in group 1 the warp also sums the D8
 //                diagonal (below)
 //   warps 2-5    drain (TMEM lane quarter = tile rows): span totals -> dd
@@ -59,14 +60,15 @@
 // Products. x_ki x_kj ~ 2^(E_i + E_j - 92) sum_{p,q} d_p d_q 2^(8 (12 - p - q));
 // the weights s = p + q <= 7 are kept. The tile is diagonal (n <= 128), so
 // S_s = sum_{p+q=s} A_p^T A_q = T_s + T_s^T + D_s with T_s = sum_{p<q} and
-// D_s = A_{s/2}^T A_{s/2}: 12 MMAs per chunk instead of 21, in 8
+// D_s = A_{s/2}^T A_{s/2}: 12 products per chunk instead of 21, in 8
 // accumulators, which TMEM (512 columns) holds 4 at a time - hence the CTA
-// pair: group 0 = {T7: (1,6)(2,5)(3,4), T4: (1,3), T3: (1,2), D2: (1,1)},
-// group 1 = {T6: (1,5)(2,4), T5: (1,4)(2,3), D4: (2,2), D6: (3,3)},
-// 6 MMAs (M = N = 128, K = 32, 64 cycles each) per chunk per CTA. Of the
+// pair: group 0 = {T7: (1,6)(2,5)(3,4), T3: (1,2), T4: (1,3), D2: (1,1)},
+// group 1 = {T5: (1,4)(2,3), T6: (1,5)(2,4), D4: (2,2), D6: (3,3)},
+// 6 products (M = N = 128, K = 32, 64 cycles each) per chunk per CTA, issued
+// as 5 / 4 MMAs (adjacent B planes merged into N = 256, issue_chunk). Of the
 // dropped weights only D8 = A_4^T A_4 has a non-zero mean (on the diagonal,
 // sum_k d_4(x_ki)^2 >= 0); its diagonal is summed on the CUDA cores by the
-// converters (dp4a on plane 4) and added to M_ii by group 1's drain. Every
+// MMA warp of group 1 (dp4a on plane 4) and added to M_ii by its drain. Every
 // other dropped term is zero-mean noise of ~2^-39 colmax_i colmax_j per row.
 // Drain. At a span end every entry's group total is formed exactly
 // (int64 / double pieces), scaled by 2^(E_i + E_j - 92 + ...) - D terms
