@@ -587,6 +587,10 @@ def run_ours(args, cfg):
     roof = dict(phases[dom])
     roof["phase"] = dom
     roof["traffic"] = traffic_for(roof.get("ncu_kernel") or "", cfg.name)
+    if roof.get("ncu_kernel") == "gram_f32_ozaki" and roof["traffic"]:
+        # the ncu capture is one of the Gram's 16 range launches (one per logical block)
+        roof["traffic_note"] = ("DRAM bytes of ONE K1z range launch of c4 at N = 1 (2^22 rows, algorithmic 2^22 x 128 x 4 B = "
+                                "2.147e9); a Gram is 16 such launches")
     jac = jacobi_latency(n, info, med["eigen"], cfg.working != "f32")
     # north_star roofline for the whole Gram+AV pair
     t_hbm = 2.0 * m_global / world * n * esz / (hbm * 1e9)
